@@ -1,0 +1,144 @@
+"""Host-side polygon map model for the DET path.
+
+Mirrors the parts of ``cartomorph.geomodel`` that sit on or next to the hot
+path (``/root/reference/pkg/src/cartomorph/geomodel.py``):
+
+* :class:`Region` / :class:`MapModel` (geomodel.py:50-145) -- same field names,
+  same region -> ring -> vertex flattening order in :meth:`MapModel.vertex_array`
+  (geomodel.py:128-130), so vertex arrays are interchangeable with the
+  reference's.  Any object exposing ``regions`` whose items expose
+  ``region_id``, ``name``, ``rings`` and ``statistic`` (a reference
+  ``cartomorph.MapModel`` included) is accepted by the engine.
+* :func:`densify` (geomodel.py:353-377) -- one-time host pre-processing at
+  engine construction, float64, same formula as the reference so the vertex
+  rows fed to the GPU are identical.
+* :func:`shoelace_area` (geomodel.py:24-31) -- host convenience; the engine's
+  per-region area output is computed on the device (``det_get_areas``).
+
+Coordinates are y-down in the unit square; rings are open (no repeated
+closing vertex); outer rings have positive shoelace area.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, replace
+
+import numpy as np
+
+
+def shoelace_area(ring: np.ndarray) -> float:
+    """Signed area of an open (V, 2) ring (geomodel.py:24-31)."""
+    r = np.asarray(ring, dtype=float)
+    if r.shape[0] < 3:
+        return 0.0
+    xs, ys = r[:, 0], r[:, 1]
+    return 0.5 * float(np.sum(xs * np.roll(ys, -1) - np.roll(xs, -1) * ys))
+
+
+@dataclass(frozen=True)
+class Region:
+    """One statistical region (geomodel.py:50-80)."""
+
+    region_id: str
+    name: str
+    rings: tuple
+    statistic: float
+
+    def area(self) -> float:
+        return sum(shoelace_area(r) for r in self.rings)
+
+    def vertex_count(self) -> int:
+        return sum(int(np.asarray(r).shape[0]) for r in self.rings)
+
+
+@dataclass(frozen=True)
+class MapModel:
+    """Regions plus optional adjacency / normalisation metadata (geomodel.py:95-145)."""
+
+    regions: tuple
+    adjacency: frozenset = frozenset()
+    normalization: object = None
+
+    def region_ids(self) -> list:
+        return [r.region_id for r in self.regions]
+
+    def statistics(self) -> np.ndarray:
+        return np.array([r.statistic for r in self.regions], dtype=float)
+
+    def total_statistic(self) -> float:
+        return float(self.statistics().sum())
+
+    def bounds(self):
+        pts = self.vertex_array()
+        return (float(pts[:, 0].min()), float(pts[:, 1].min()),
+                float(pts[:, 0].max()), float(pts[:, 1].max()))
+
+    def with_statistics(self, values) -> "MapModel":
+        vals = np.asarray(values, dtype=float)
+        return replace(self, regions=tuple(replace(r, statistic=float(v))
+                                           for r, v in zip(self.regions, vals)))
+
+    def vertex_array(self) -> np.ndarray:
+        return np.vstack([np.asarray(ring, dtype=float) for reg in self.regions for ring in reg.rings])
+
+    def with_vertex_array(self, verts: np.ndarray) -> "MapModel":
+        return rebuild(self, verts)
+
+
+def ring_layout(mapmodel):
+    """Flatten a (duck-typed) map into index arrays.
+
+    Returns ``(xy, ring_start, ring_region, ids, stats)`` where ``xy`` is the
+    (N_rows, 2) float64 vertex array in region/ring order, ``ring_start`` the
+    (n_rings+1,) row offsets and ``ring_region`` the owning region index of
+    each ring.
+    """
+    ids, stats, rings, owner = [], [], [], []
+    for ridx, reg in enumerate(mapmodel.regions):
+        ids.append(str(reg.region_id))
+        stats.append(float(reg.statistic))
+        for ring in reg.rings:
+            rings.append(np.asarray(ring, dtype=float))
+            owner.append(ridx)
+    sizes = np.array([r.shape[0] for r in rings], dtype=np.int64)
+    ring_start = np.zeros(len(rings) + 1, dtype=np.int32)
+    ring_start[1:] = np.cumsum(sizes)
+    xy = np.ascontiguousarray(np.vstack(rings), dtype=np.float64)
+    return xy, ring_start, np.array(owner, dtype=np.int32), ids, np.array(stats, dtype=float)
+
+
+def rebuild(mapmodel, verts: np.ndarray):
+    """Rebuild a map (any dataclass-based MapModel) from stacked vertex rows."""
+    verts = np.asarray(verts, dtype=float)
+    out, pos = [], 0
+    for reg in mapmodel.regions:
+        rs = []
+        for ring in reg.rings:
+            q = np.asarray(ring).shape[0]
+            rs.append(np.array(verts[pos : pos + q], dtype=float))
+            pos += q
+        out.append(replace(reg, rings=tuple(rs)))
+    if pos != verts.shape[0]:
+        raise ValueError("vertex array length mismatch")
+    return replace(mapmodel, regions=tuple(out))
+
+
+def densify(mapmodel, max_edge: float):
+    """Split edges longer than ``max_edge`` into equal pieces (geomodel.py:353-377)."""
+    if max_edge <= 0:
+        raise ValueError("max_edge must be positive")
+    new_regions = []
+    for reg in mapmodel.regions:
+        rs = []
+        for ring in reg.rings:
+            ring = np.asarray(ring, dtype=float)
+            nxt = np.roll(ring, -1, axis=0)
+            ln = np.hypot(*(nxt - ring).T)
+            pieces = np.maximum(1, np.ceil(ln / max_edge).astype(int))
+            if pieces.max() == 1:
+                rs.append(ring)
+                continue
+            parts = [p0 + (np.arange(q) / q)[:, None] * (p1 - p0) for p0, p1, q in zip(ring, nxt, pieces)]
+            rs.append(np.vstack(parts))
+        new_regions.append(replace(reg, rings=tuple(rs)))
+    return replace(mapmodel, regions=tuple(new_regions))
