@@ -1,0 +1,144 @@
+/*
+ * det_api.h -- C-ABI of the B200-native DET (density-equalizing transformation)
+ * engine.  Plain pointers and sizes only; no torch types.  Host buffers are
+ * caller-owned; device buffers are owned by the context.  One context per host
+ * thread (a context owns one CUDA stream).
+ *
+ * The reference (cartomorph, pure Python) has no FFI; these entry points are
+ * the operations its Python API performs on the hot path, and each cites the
+ * reference code it replaces (paths under /root/reference/pkg/src/cartomorph).
+ * The Python drop-in (paper_2604_13880_b200) binds them with ctypes; see
+ * INTEGRATION.md for the binding a cartomorph maintainer would add.
+ *
+ * All functions return a status code (DET_OK on success).  On failure
+ * det_last_error(ctx) holds a message.  Status codes mirror cartomorph.errors.
+ */
+#ifndef DET_API_H
+#define DET_API_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct det_ctx det_ctx;
+
+/* status codes (errors.py:4-26) */
+#define DET_OK 0
+#define DET_E_ARG 1      /* ValueError from an argument check                      */
+#define DET_E_CUDA 2     /* CUDA runtime / launch failure                           */
+#define DET_E_RASTER 3   /* RasterizationError (raster.py:148-154)                  */
+#define DET_E_COLLAPSE 4 /* RegionCollapsedError (engine.py:148-150)                */
+#define DET_E_NUMERIC 5  /* NumericError (engine.py:125-126, displacement.py:110)   */
+#define DET_E_VALUE 6    /* ValueError raised inside the path (raster.py:168-169,
+                            bincount negative index raster.py:87-89)                */
+#define DET_E_STATE 7    /* call order / capacity problem                            */
+
+/* stop reasons (engine.py:196-211) */
+#define DET_STOP_RUNNING 0
+#define DET_STOP_CONVERGED 1
+#define DET_STOP_STAGNATION 2
+#define DET_STOP_MAXITER 3
+#define DET_STOP_COLLAPSED 4 /* RegionCollapsedError at evaluate()            */
+#define DET_STOP_BDV 5       /* build_density: bdv <= 0 -> ValueError          */
+#define DET_STOP_NEGINDEX 6  /* _submask bincount negative index -> ValueError */
+
+/* bdv policy (engine.py:91-96) */
+#define DET_BDV_FIXED_MASS 0
+#define DET_BDV_REDERIVE 1
+
+typedef struct {
+    double background_mass;   /* M_b (engine.py:131-136)                    */
+    double bdv_multiplier;    /* shape-preservation knob (engine.py:103)    */
+    double mean_density0;     /* S / N_map0 (engine.py:130)                 */
+    double total_statistic;   /* S (engine.py:123)                          */
+    int32_t bdv_mode;         /* DET_BDV_*                                  */
+    int32_t pad;
+} det_params;
+
+typedef struct {
+    double error_threshold;   /* StoppingCriteria (engine.py:27-35) */
+    int32_t stagnation_window;
+    int32_t max_iterations;
+} det_criteria;
+
+typedef struct {
+    int32_t stop_reason;      /* DET_STOP_*                                            */
+    int32_t iteration;        /* CartogramState.iteration of the returned state        */
+    int32_t best_iteration;
+    int32_t collapsed_region; /* region index for DET_STOP_COLLAPSED, else -1          */
+    int64_t clamp_events;     /* CartogramState.clamp_events (0 after stagnation)      */
+    double epsilon, xi;       /* errors of the returned state                          */
+    double bdv;               /* background density of the last step                   */
+    int32_t trace_len;        /* number of IterationRecord rows                        */
+    int32_t status;           /* DET_OK or the DET_E_* the reference would raise        */
+} det_result;
+
+int det_abi_version(void);
+const char *det_last_error(const det_ctx *ctx);
+/* device info string (name, SMs, L2) for reports */
+int det_device_info(int device, char *buf, int buflen);
+
+/* k in [4, 13] (raster.py:138-139); field_f64 selects the displacement-field
+ * storage precision (0: float32, 1: float64; accumulation is float64 always). */
+int det_ctx_create(int device, int k, int field_f64, det_ctx **out);
+void det_ctx_destroy(det_ctx *ctx);
+/* band height of the integral-image kernels (power of two, default 8) */
+int det_set_band_height(det_ctx *ctx, int h);
+
+/* Topology + initial vertices of one map: MapModel.vertex_array() rows
+ * (geomodel.py:128-130), ring row offsets, ring->region, region rank in
+ * ascending region_id order (raster.py:142).  Replaces the per-iteration
+ * vertex_array()/with_vertex_array() round trip (engine.py:176-178). */
+int det_load_map(det_ctx *ctx, const double *xy, int n_rows, const int32_t *ring_start, int n_rings,
+                 const int32_t *ring_region, const int32_t *region_rank, int n_regions);
+
+/* A batch of cartograms sharing the topology: per-cartogram start vertices
+ * (batch*n_rows*2, or NULL = the loaded vertices for all) and statistics
+ * (batch*n_regions; Region.statistic, geomodel.py:61). */
+int det_set_batch(det_ctx *ctx, int batch, const double *xy, const double *stats);
+
+/* rasterize_labels + pixel_counts/background_count (raster.py:110-155) of the
+ * batch's current start vertices for cartogram b.  labels_out: n*n int32 [j,i]
+ * (BACKGROUND=-1) or NULL; counts_out: n_regions+1 (last = background) or NULL. */
+int det_rasterize(det_ctx *ctx, int b, int32_t *labels_out, int64_t *counts_out);
+
+/* Per-cartogram engine constants (CartogramEngine.__init__, engine.py:98-141). */
+int det_set_params(det_ctx *ctx, const det_params *params, const double *weights_px);
+
+/* CartogramEngine.run (engine.py:182-219) for every cartogram of the batch,
+ * device-resident (no host round trip per iteration). */
+int det_run(det_ctx *ctx, const det_criteria *crit);
+/* Exactly `iters` DET iterations on every cartogram with no stopping test
+ * (benchmark helper; state continues from the last det_run/det_bench call). */
+int det_bench_iterations(det_ctx *ctx, int iters);
+int det_sync(det_ctx *ctx);
+/* Per-phase device time (CUDA events on the context stream) summed over `iters`
+ * eagerly launched iterations: ms_out[0]=integral images (k_sat1..3),
+ * [1]=advect+crossings (k_region), [2]=paint/labels/counts (k_row), [3]=control (k_ctrl). */
+int det_bench_kernel_times(det_ctx *ctx, int iters, float *ms_out);
+
+int det_get_result(det_ctx *ctx, int b, det_result *out);
+int det_get_vertices(det_ctx *ctx, int b, double *xy_out);       /* n_rows*2 */
+int det_get_labels(det_ctx *ctx, int b, int32_t *labels_out);    /* n*n      */
+int det_get_counts(det_ctx *ctx, int b, int64_t *counts_out);    /* R+1      */
+int det_get_region_error(det_ctx *ctx, int b, double *out);      /* R        */
+int det_get_trace(det_ctx *ctx, int b, double *out);             /* trace_len*4: iter, eps, xi, millis */
+int det_get_areas(det_ctx *ctx, int b, double *out);             /* R: Region.area() (geomodel.py:63-65) */
+
+/* Stage-level entry points (parity tests; integral.py:155, displacement.py:198-238). */
+/* u = t(d) - t(const) at pixel centres for a dense density d (n*n float64);
+ * optional 8 channels (alpha,beta,gamma,delta,alpha_t,beta_t,gamma_t,delta_t) */
+int det_field(det_ctx *ctx, const double *d, double *u_out, double *channels_out, double *total_out);
+/* t(d) itself at pixel centres (mapping_grid, displacement.py:102-131), n*n*2 */
+int det_mapping(det_ctx *ctx, const double *d, double *t_out);
+/* build_density (raster.py:166-184) of a label texture: d_out n*n, counts_out n_regions+1 */
+int det_density(det_ctx *ctx, const int32_t *labels, const double *stats, int n_regions, double bdv, double *d_out,
+                int64_t *counts_out);
+int det_advect(det_ctx *ctx, const double *u, const double *xy, int n_pts, double *xy_out, int64_t *clamps);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

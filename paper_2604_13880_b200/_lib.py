@@ -1,0 +1,264 @@
+"""ctypes binding of the C-ABI in ``include/det_api.h`` (library ``_det.so``).
+
+The product path has no fallback: if the CUDA library is missing or no CUDA
+device is usable, :func:`lib` raises.  Build with ``__graft_entry__.build()``
+or ``make -C paper_2604_13880_b200/csrc``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_det.so")
+
+DET_OK, DET_E_ARG, DET_E_CUDA, DET_E_RASTER, DET_E_COLLAPSE, DET_E_NUMERIC, DET_E_VALUE, DET_E_STATE = range(8)
+STOP_NAMES = {1: "converged", 2: "stagnation", 3: "max-iterations"}
+STOP_COLLAPSED, STOP_BDV, STOP_NEGINDEX = 4, 5, 6
+
+_c_double_p = ctypes.POINTER(ctypes.c_double)
+_c_int32_p = ctypes.POINTER(ctypes.c_int32)
+_c_int64_p = ctypes.POINTER(ctypes.c_int64)
+
+
+class DetParams(ctypes.Structure):
+    _fields_ = [("background_mass", ctypes.c_double), ("bdv_multiplier", ctypes.c_double),
+                ("mean_density0", ctypes.c_double), ("total_statistic", ctypes.c_double),
+                ("bdv_mode", ctypes.c_int32), ("pad", ctypes.c_int32)]
+
+
+class DetCriteria(ctypes.Structure):
+    _fields_ = [("error_threshold", ctypes.c_double), ("stagnation_window", ctypes.c_int32),
+                ("max_iterations", ctypes.c_int32)]
+
+
+class DetResult(ctypes.Structure):
+    _fields_ = [("stop_reason", ctypes.c_int32), ("iteration", ctypes.c_int32),
+                ("best_iteration", ctypes.c_int32), ("collapsed_region", ctypes.c_int32),
+                ("clamp_events", ctypes.c_int64), ("epsilon", ctypes.c_double), ("xi", ctypes.c_double),
+                ("bdv", ctypes.c_double), ("trace_len", ctypes.c_int32), ("status", ctypes.c_int32)]
+
+
+EXPORTS = {
+    "det_abi_version": (ctypes.c_int, []),
+    "det_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
+    "det_device_info": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.c_int]),
+    "det_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
+    "det_ctx_destroy": (None, [ctypes.c_void_p]),
+    "det_set_band_height": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "det_load_map": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, ctypes.c_int, _c_int32_p, ctypes.c_int,
+                                     _c_int32_p, _c_int32_p, ctypes.c_int]),
+    "det_set_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p, _c_double_p]),
+    "det_rasterize": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_int32_p, _c_int64_p]),
+    "det_set_params": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(DetParams), _c_double_p]),
+    "det_run": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(DetCriteria)]),
+    "det_bench_iterations": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "det_bench_kernel_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]),
+    "det_sync": (ctypes.c_int, [ctypes.c_void_p]),
+    "det_get_result": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(DetResult)]),
+    "det_get_vertices": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p]),
+    "det_get_labels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_int32_p]),
+    "det_get_counts": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_int64_p]),
+    "det_get_region_error": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p]),
+    "det_get_trace": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p]),
+    "det_get_areas": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p]),
+    "det_field": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p, _c_double_p, _c_double_p]),
+    "det_mapping": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p]),
+    "det_density": (ctypes.c_int, [ctypes.c_void_p, _c_int32_p, _c_double_p, ctypes.c_int, ctypes.c_double,
+                                    _c_double_p, _c_int64_p]),
+    "det_advect": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_int, _c_double_p, _c_int64_p]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load the shared library and declare every exported signature (no CUDA call)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise RuntimeError(f"DET CUDA library not built: {path} missing "
+                                   "(run __graft_entry__.build() or make -C paper_2604_13880_b200/csrc)")
+            lib = ctypes.CDLL(path)
+            for name, (res, args) in EXPORTS.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def _p(a, ctype):
+    return a.ctypes.data_as(ctypes.POINTER(ctype)) if a is not None else None
+
+
+class DetError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"det error {code}: {msg}")
+        self.code = code
+        self.msg = msg
+
+
+class Context:
+    """One device context (CUDA stream + buffers) of the DET engine."""
+
+    def __init__(self, k: int, device: int = 0, field_f64: bool = False):
+        self.lib = load_library()
+        self.k, self.n, self.device, self.field_f64 = k, 1 << k, device, bool(field_f64)
+        h = ctypes.c_void_p()
+        rc = self.lib.det_ctx_create(device, k, int(field_f64), ctypes.byref(h))
+        if rc != DET_OK:
+            raise DetError(rc, "det_ctx_create failed (no usable CUDA device?)")
+        self.h = h
+        self.B = 0
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.det_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, rc):
+        if rc != DET_OK:
+            raise DetError(rc, self.lib.det_last_error(self.h).decode(errors="replace"))
+
+    # --- topology / batch ---
+    def load_map(self, xy, ring_start, ring_region, region_rank):
+        xy = np.ascontiguousarray(xy, dtype=np.float64)
+        rs = np.ascontiguousarray(ring_start, dtype=np.int32)
+        rr = np.ascontiguousarray(ring_region, dtype=np.int32)
+        rk = np.ascontiguousarray(region_rank, dtype=np.int32)
+        self.n_rows, self.R = xy.shape[0], rk.shape[0]
+        self.check(self.lib.det_load_map(self.h, _p(xy, ctypes.c_double), xy.shape[0], _p(rs, ctypes.c_int32),
+                                         rs.shape[0] - 1, _p(rr, ctypes.c_int32), _p(rk, ctypes.c_int32), rk.shape[0]))
+        self.B = 0
+        self._owner_token = None  # engines re-load their map when they see another owner
+
+    def set_batch(self, stats, xy=None):
+        st = np.ascontiguousarray(np.atleast_2d(stats), dtype=np.float64)
+        b = st.shape[0]
+        x = None if xy is None else np.ascontiguousarray(xy, dtype=np.float64).reshape(b, self.n_rows, 2)
+        self.check(self.lib.det_set_batch(self.h, b, _p(x, ctypes.c_double), _p(st, ctypes.c_double)))
+        self.B = b
+
+    def set_band_height(self, h):
+        self.check(self.lib.det_set_band_height(self.h, int(h)))
+
+    def rasterize(self, b=0, want_labels=True):
+        lab = np.empty((self.n, self.n), dtype=np.int32) if want_labels else None
+        cnt = np.empty(self.R + 1, dtype=np.int64)
+        self.check(self.lib.det_rasterize(self.h, b, _p(lab, ctypes.c_int32), _p(cnt, ctypes.c_int64)))
+        return lab, cnt
+
+    def set_params(self, params, weights):
+        arr = (DetParams * len(params))()
+        for i, p in enumerate(params):
+            arr[i] = DetParams(p["background_mass"], p["bdv_multiplier"], p["mean_density0"],
+                               p["total_statistic"], p["bdv_mode"], 0)
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        self.check(self.lib.det_set_params(self.h, arr, _p(w, ctypes.c_double)))
+
+    def run(self, error_threshold, stagnation_window, max_iterations):
+        c = DetCriteria(float(error_threshold), int(stagnation_window), int(max_iterations))
+        self.check(self.lib.det_run(self.h, ctypes.byref(c)))
+
+    def bench_iterations(self, iters):
+        self.check(self.lib.det_bench_iterations(self.h, int(iters)))
+
+    def kernel_times(self, iters):
+        out = (ctypes.c_float * 4)()
+        self.check(self.lib.det_bench_kernel_times(self.h, int(iters), out))
+        return list(out)
+
+    def sync(self):
+        self.check(self.lib.det_sync(self.h))
+
+    # --- results ---
+    def result(self, b=0) -> DetResult:
+        r = DetResult()
+        self.check(self.lib.det_get_result(self.h, b, ctypes.byref(r)))
+        return r
+
+    def vertices(self, b=0):
+        out = np.empty((self.n_rows, 2), dtype=np.float64)
+        self.check(self.lib.det_get_vertices(self.h, b, _p(out, ctypes.c_double)))
+        return out
+
+    def labels(self, b=0):
+        out = np.empty((self.n, self.n), dtype=np.int32)
+        self.check(self.lib.det_get_labels(self.h, b, _p(out, ctypes.c_int32)))
+        return out
+
+    def counts(self, b=0):
+        out = np.empty(self.R + 1, dtype=np.int64)
+        self.check(self.lib.det_get_counts(self.h, b, _p(out, ctypes.c_int64)))
+        return out
+
+    def region_error(self, b=0):
+        out = np.empty(self.R, dtype=np.float64)
+        self.check(self.lib.det_get_region_error(self.h, b, _p(out, ctypes.c_double)))
+        return out
+
+    def trace(self, b=0, length=None):
+        if length is None:
+            length = self.result(b).trace_len
+        out = np.empty((max(length, 0), 4), dtype=np.float64)
+        if length > 0:
+            self.check(self.lib.det_get_trace(self.h, b, _p(out, ctypes.c_double)))
+        return out
+
+    def areas(self, b=0):
+        out = np.empty(self.R, dtype=np.float64)
+        self.check(self.lib.det_get_areas(self.h, b, _p(out, ctypes.c_double)))
+        return out
+
+    # --- stage level ---
+    def field(self, d, channels=False):
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        u = np.empty((self.n, self.n, 2), dtype=np.float64)
+        ch = np.empty((8, self.n, self.n), dtype=np.float64) if channels else None
+        tot = ctypes.c_double(0.0)
+        self.check(self.lib.det_field(self.h, _p(d, ctypes.c_double), _p(u, ctypes.c_double),
+                                      _p(ch, ctypes.c_double), ctypes.byref(tot)))
+        return u, ch, tot.value
+
+    def channels(self, d):
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        ch = np.empty((8, self.n, self.n), dtype=np.float64)
+        tot = ctypes.c_double(0.0)
+        self.check(self.lib.det_field(self.h, _p(d, ctypes.c_double), None, _p(ch, ctypes.c_double),
+                                      ctypes.byref(tot)))
+        return ch, tot.value
+
+    def mapping(self, d):
+        d = np.ascontiguousarray(d, dtype=np.float64)
+        t = np.empty((self.n, self.n, 2), dtype=np.float64)
+        self.check(self.lib.det_mapping(self.h, _p(d, ctypes.c_double), _p(t, ctypes.c_double)))
+        return t
+
+    def advect(self, u, xy):
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        xy = np.ascontiguousarray(xy, dtype=np.float64)
+        out = np.empty_like(xy)
+        cl = ctypes.c_int64(0)
+        self.check(self.lib.det_advect(self.h, _p(u, ctypes.c_double), _p(xy, ctypes.c_double), xy.shape[0],
+                                       _p(out, ctypes.c_double), ctypes.byref(cl)))
+        return out, int(cl.value)
+
+
+def device_info(device: int = 0) -> str:
+    lib = load_library()
+    buf = ctypes.create_string_buffer(256)
+    lib.det_device_info(device, buf, 256)
+    return buf.value.decode()

@@ -1,0 +1,892 @@
+// Host runtime and C-ABI of the DET engine.  See include/det_api.h.
+//
+// A context owns one CUDA stream, the map topology, a batch of cartograms and
+// all device buffers.  det_run() keeps the whole iteration loop on the device:
+// one iteration = k_sat1 -> k_sat2 -> k_sat3 -> k_region -> k_row -> k_ctrl,
+// captured G times into a CUDA graph; kernels of finished cartograms exit on
+// their device-side `active` flag, and the host only polls the flags once per
+// graph launch.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/det_api.h"
+#include "det_common.cuh"
+#include "det_ctrl.cuh"
+#include "det_raster.cuh"
+#include "det_sat.cuh"
+
+using namespace det;
+
+namespace {
+
+template <typename T>
+struct DVec {
+    T* p = nullptr;
+    size_t n = 0;
+    DVec() = default;
+    DVec(const DVec&) = delete;
+    DVec& operator=(const DVec&) = delete;
+    ~DVec() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    cudaError_t alloc(size_t count) {  // exact-or-larger, contents undefined
+        if (p && count <= n) return cudaSuccess;
+        release();
+        cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+        if (e == cudaSuccess) n = std::max<size_t>(count, 1);
+        return e;
+    }
+};
+
+constexpr int kGraphIters = 16;
+
+}  // namespace
+
+struct det_ctx {
+    int device = 0, k = 10, n = 1024, f64 = 0, H = 8;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    // topology
+    int R = 0, n_rows = 0, n_uniq = 0, n_rings = 0;
+    std::vector<int> h_row_uniq, h_ring_start, h_region_ring0;
+    std::vector<double> h_xy_uniq;
+    DVec<int> region_row0, row_uniq, row_next, region_rank, rank_region, ring_start, region_ring0;
+    DVec<uint8_t> row_owner;
+    // batch
+    int B = 0, cap = 64, nb = 0, trace_cap = 0;
+    DVec<double2> pos_init, pos0, pos1, best, rowpos;
+    DVec<int> labels, cnt_acc, cnt_state, rowcnt, maxspan;
+    DVec<unsigned long long> spans;
+    DVec<double> lut, stats, weights, rerr, cs, dgc, adc, rt, csX, dgXc, adSc, csT, dgT, adT, rowfull, trace;
+    DVec<char> uf;
+    DVec<Carto> st;
+    DVec<Params> prm;
+    std::vector<Params> h_prm;
+    std::vector<Carto> h_st;
+    bool params_set = false, ran = false, bench_mode = false;
+    // stage buffers
+    DVec<double> dense, ch8, uf64, pts_in, pts_out;
+    DVec<unsigned long long> clampbuf;
+    // graph
+    cudaGraphExec_t gexec = nullptr;
+    bool g_valid = false;
+};
+
+#define CK(expr)                                                                   \
+    do {                                                                           \
+        cudaError_t _e = (expr);                                                   \
+        if (_e != cudaSuccess) {                                                   \
+            ctx->err = std::string(#expr) + ": " + cudaGetErrorString(_e);         \
+            return DET_E_CUDA;                                                     \
+        }                                                                          \
+    } while (0)
+
+static int fail(det_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) ctx->err = msg;
+    return code;
+}
+
+static int cpt_for(int n) { return n <= 256 ? 2 : (n <= 4096 ? 4 : 8); }
+static int nthreads_for(int n) { return std::max(32, n / cpt_for(n)); }
+
+static Topo make_topo(det_ctx* c) {
+    Topo t;
+    t.n_rows = c->n_rows;
+    t.n_uniq = c->n_uniq;
+    t.R = c->R;
+    t.region_row0 = c->region_row0.p;
+    t.row_uniq = c->row_uniq.p;
+    t.row_next = c->row_next.p;
+    t.row_owner = c->row_owner.p;
+    t.region_rank = c->region_rank.p;
+    t.rank_region = c->rank_region.p;
+    return t;
+}
+
+static Bufs make_bufs(det_ctx* c) {
+    Bufs d;
+    memset(&d, 0, sizeof(d));
+    d.B = c->B; d.n = c->n; d.k = c->k; d.cap = c->cap; d.H = c->H; d.nb = c->nb;
+    d.nn = (size_t)c->n * c->n;
+    d.pos0 = c->pos0.p; d.pos1 = c->pos1.p; d.best = c->best.p; d.rowpos = c->rowpos.p;
+    d.labels = c->labels.p; d.cnt_acc = c->cnt_acc.p; d.cnt_state = c->cnt_state.p;
+    d.spans = c->spans.p; d.rowcnt = c->rowcnt.p; d.maxspan = c->maxspan.p;
+    d.lut = c->lut.p; d.stats = c->stats.p; d.weights = c->weights.p; d.rerr = c->rerr.p;
+    d.uf = c->uf.p;
+    d.cs = c->cs.p; d.dgc = c->dgc.p; d.adc = c->adc.p; d.rt = c->rt.p;
+    d.csX = c->csX.p; d.dgXc = c->dgXc.p; d.adSc = c->adSc.p;
+    d.csT = c->csT.p; d.dgT = c->dgT.p; d.adT = c->adT.p; d.rowfull = c->rowfull.p;
+    d.st = c->st.p; d.prm = c->prm.p; d.trace = c->trace.p; d.trace_cap = c->trace_cap;
+    return d;
+}
+
+// ----------------------------- launch helpers ---------------------------------
+template <int CPT>
+static void launch_sat_cpt(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S, int gate, int src, int out,
+                           bool u64, int B) {
+    const int n = c->n, nt = nthreads_for(n);
+    const dim3 gb(c->nb, B);
+    if (src == SRC_LABELS) k_sat1<CPT, SRC_LABELS><<<gb, nt, 0, c->stream>>>(T, D, S, gate);
+    else k_sat1<CPT, SRC_DENSE><<<gb, nt, 0, c->stream>>>(T, D, S, gate);
+    const int lanes = n + 2 * (2 * n - 1);
+    const int G = std::min(8, c->nb);
+    k_sat2<<<dim3((lanes + 31) / 32 + 1, B), 32 * G, 0, c->stream>>>(D, gate);
+    const size_t smem = (size_t)3 * (n + c->H) * sizeof(double);
+#define DET_SAT3(SRC_, UT_, OUT_)                                                                            \
+    do {                                                                                                     \
+        auto fn = k_sat3<CPT, SRC_, UT_, OUT_>;                                                              \
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                    \
+        fn<<<gb, nt, smem, c->stream>>>(T, D, S, gate);                                                      \
+    } while (0)
+    if (out == OUT_CH8) {
+        if (src == SRC_LABELS) DET_SAT3(SRC_LABELS, double, OUT_CH8);
+        else DET_SAT3(SRC_DENSE, double, OUT_CH8);
+    } else if (src == SRC_LABELS) {
+        if (u64) DET_SAT3(SRC_LABELS, double, OUT_U);
+        else DET_SAT3(SRC_LABELS, float, OUT_U);
+    } else {
+        if (u64) DET_SAT3(SRC_DENSE, double, OUT_U);
+        else DET_SAT3(SRC_DENSE, float, OUT_U);
+    }
+#undef DET_SAT3
+}
+
+static void launch_sat(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S, int gate, int src, int out, bool u64,
+                       int B) {
+    switch (cpt_for(c->n)) {
+        case 2: launch_sat_cpt<2>(c, T, D, S, gate, src, out, u64, B); break;
+        case 4: launch_sat_cpt<4>(c, T, D, S, gate, src, out, u64, B); break;
+        default: launch_sat_cpt<8>(c, T, D, S, gate, src, out, u64, B); break;
+    }
+}
+
+static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, int gate, int src) {
+    const dim3 g(c->R, c->B);
+    if (c->f64) k_region<double><<<g, REG_THREADS, 0, c->stream>>>(T, D, mode, gate, src);
+    else k_region<float><<<g, REG_THREADS, 0, c->stream>>>(T, D, mode, gate, src);
+}
+
+static void launch_row(det_ctx* c, const Topo& T, const Bufs& D, int gate) {
+    k_row<<<dim3(c->n, c->B), ROW_THREADS, (size_t)c->n * sizeof(uint32_t), c->stream>>>(T, D, gate);
+}
+
+static void enqueue_iteration(det_ctx* c) {
+    const Topo T = make_topo(c);
+    const Bufs D = make_bufs(c);
+    SatSrc S;
+    memset(&S, 0, sizeof(S));
+    launch_sat(c, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, c->f64 != 0, c->B);
+    launch_region(c, T, D, M_ADVECT | M_RASTER, G_ACTIVE, 0);
+    launch_row(c, T, D, G_ACTIVE);
+    k_ctrl<<<c->B, CTRL_THREADS, 0, c->stream>>>(T, D, 0, G_ACTIVE);
+}
+
+static void invalidate_graph(det_ctx* c) {
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+    c->g_valid = false;
+}
+
+static int ensure_graph(det_ctx* c) {
+    det_ctx* ctx = c;
+    if (c->g_valid) return DET_OK;
+    invalidate_graph(c);
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    for (int i = 0; i < kGraphIters; ++i) enqueue_iteration(c);
+    CK(cudaStreamEndCapture(c->stream, &g));
+    cudaError_t e = cudaGraphInstantiate(&c->gexec, g, 0);
+    cudaGraphDestroy(g);
+    CK(e);
+    c->g_valid = true;
+    return DET_OK;
+}
+
+// ------------------------------- allocation ----------------------------------
+static int alloc_spans(det_ctx* ctx) {
+    CK(ctx->spans.alloc((size_t)ctx->B * ctx->n * ctx->cap));
+    CK(ctx->rowcnt.alloc((size_t)ctx->B * ctx->n));
+    CK(cudaMemsetAsync(ctx->rowcnt.p, 0, (size_t)ctx->B * ctx->n * sizeof(int), ctx->stream));
+    invalidate_graph(ctx);  // the graph bakes in spans pointer and capacity
+    return DET_OK;
+}
+
+static int alloc_sat(det_ctx* ctx, int B) {
+    const size_t n = ctx->n, nb = ctx->nb, L = n + ctx->H - 1, M = 2 * n - 1;
+    CK(ctx->cs.alloc(B * nb * n));
+    CK(ctx->dgc.alloc(B * nb * L));
+    CK(ctx->adc.alloc(B * nb * L));
+    CK(ctx->rt.alloc(B * n));
+    CK(ctx->csX.alloc(B * nb * n));
+    CK(ctx->dgXc.alloc(B * nb * n));
+    CK(ctx->adSc.alloc(B * nb * L));
+    CK(ctx->csT.alloc(B * n));
+    CK(ctx->dgT.alloc(B * M));
+    CK(ctx->adT.alloc(B * M));
+    CK(ctx->rowfull.alloc(B * (n + 1)));
+    return DET_OK;
+}
+
+static int alloc_batch(det_ctx* ctx, int B) {
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    ctx->B = B;
+    CK(ctx->pos_init.alloc((size_t)B * ctx->n_uniq));
+    CK(ctx->pos0.alloc((size_t)B * ctx->n_uniq));
+    CK(ctx->pos1.alloc((size_t)B * ctx->n_uniq));
+    CK(ctx->best.alloc((size_t)B * ctx->n_uniq));
+    CK(ctx->rowpos.alloc((size_t)B * ctx->n_rows));
+    CK(ctx->labels.alloc((size_t)B * nn));
+    CK(ctx->cnt_acc.alloc((size_t)B * (ctx->R + 1)));
+    CK(ctx->cnt_state.alloc((size_t)B * (ctx->R + 1)));
+    CK(ctx->maxspan.alloc((size_t)B));
+    CK(ctx->lut.alloc((size_t)B * (ctx->R + 1)));
+    CK(ctx->stats.alloc((size_t)B * ctx->R));
+    CK(ctx->weights.alloc((size_t)B * ctx->R));
+    CK(ctx->rerr.alloc((size_t)B * ctx->R));
+    CK(ctx->uf.alloc((size_t)B * nn * 2 * (ctx->f64 ? 8 : 4)));
+    CK(ctx->st.alloc((size_t)B));
+    CK(ctx->prm.alloc((size_t)B));
+    CK(cudaMemsetAsync(ctx->cnt_acc.p, 0, (size_t)B * (ctx->R + 1) * sizeof(int), ctx->stream));
+    CK(cudaMemsetAsync(ctx->uf.p, 0, (size_t)B * nn * 2 * (ctx->f64 ? 8 : 4), ctx->stream));
+    int rc = alloc_sat(ctx, B);
+    if (rc) return rc;
+    rc = alloc_spans(ctx);
+    if (rc) return rc;
+    ctx->h_st.assign(B, Carto());
+    ctx->params_set = false;
+    ctx->ran = false;
+    invalidate_graph(ctx);
+    return DET_OK;
+}
+
+// Raster of the batch start vertices (pos_init) into labels/cnt_acc, growing the span
+// capacity until no row overflows.  Leaves the counts in cnt_acc.
+static int raster_start(det_ctx* ctx) {
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        CK(cudaMemcpyAsync(ctx->pos0.p, ctx->pos_init.p, (size_t)ctx->B * ctx->n_uniq * sizeof(double2),
+                           cudaMemcpyDeviceToDevice, ctx->stream));
+        const Topo T = make_topo(ctx);
+        const Bufs D = make_bufs(ctx);
+        k_init_state<<<(ctx->B + 127) / 128, 128, 0, ctx->stream>>>(D);
+        CK(cudaMemsetAsync(ctx->cnt_acc.p, 0, (size_t)ctx->B * (ctx->R + 1) * sizeof(int), ctx->stream));
+        launch_region(ctx, T, D, M_RASTER, G_ALWAYS, 0);
+        launch_row(ctx, T, D, G_ALWAYS);
+        CK(cudaGetLastError());
+        std::vector<Carto> hs(ctx->B);
+        std::vector<int> ms(ctx->B);
+        CK(cudaMemcpyAsync(hs.data(), ctx->st.p, ctx->B * sizeof(Carto), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(ms.data(), ctx->maxspan.p, ctx->B * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        int mx = 0;
+        bool ovf = false;
+        for (int b = 0; b < ctx->B; ++b) {
+            mx = std::max(mx, ms[b]);
+            if (hs[b].err & E_TOGGLE_OVF) return fail(ctx, DET_E_STATE, "more than 4096 crossings on one scanline of a region");
+            ovf |= (hs[b].err & E_SPAN_OVF) != 0;
+        }
+        const int want = std::max(64, 2 * mx + 32);  // headroom for deformation
+        if (!ovf) {
+            if (ctx->cap < want) {
+                ctx->cap = want;
+                int rc = alloc_spans(ctx);
+                if (rc) return rc;
+            }
+            return DET_OK;
+        }
+        ctx->cap = std::max(want, ctx->cap * 2);
+        int rc = alloc_spans(ctx);
+        if (rc) return rc;
+    }
+    return fail(ctx, DET_E_STATE, "span capacity did not converge");
+}
+
+// ================================ C-ABI ======================================
+extern "C" {
+
+int det_abi_version(void) { return 1; }
+
+const char* det_last_error(const det_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int det_device_info(int device, char* buf, int buflen) {
+    cudaDeviceProp p;
+    cudaError_t e = cudaGetDeviceProperties(&p, device);
+    if (e != cudaSuccess) {
+        snprintf(buf, buflen, "cuda error: %s", cudaGetErrorString(e));
+        return DET_E_CUDA;
+    }
+    snprintf(buf, buflen, "%s sm_%d%d SMs=%d L2=%dB smem/block=%zu", p.name, p.major, p.minor, p.multiProcessorCount,
+             p.l2CacheSize, p.sharedMemPerBlockOptin);
+    return DET_OK;
+}
+
+int det_ctx_create(int device, int k, int field_f64, det_ctx** out) {
+    if (!out) return DET_E_ARG;
+    *out = nullptr;
+    if (k < 4 || k > 13) return DET_E_ARG;
+    det_ctx* ctx = new det_ctx();
+    ctx->device = device;
+    ctx->k = k;
+    ctx->n = 1 << k;
+    ctx->f64 = field_f64 ? 1 : 0;
+    ctx->H = std::min(8, ctx->n);
+    ctx->nb = ctx->n / ctx->H;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        int rc = DET_E_CUDA;
+        delete ctx;
+        return rc;
+    }
+    *out = ctx;
+    return DET_OK;
+}
+
+void det_ctx_destroy(det_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    invalidate_graph(ctx);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int det_set_band_height(det_ctx* ctx, int h) {
+    if (!ctx || h < 1 || (h & (h - 1)) || h > ctx->n) return fail(ctx, DET_E_ARG, "band height must be a power of two <= n");
+    cudaSetDevice(ctx->device);
+    ctx->H = h;
+    ctx->nb = ctx->n / h;
+    invalidate_graph(ctx);
+    if (ctx->B > 0) return alloc_sat(ctx, ctx->B);
+    return DET_OK;
+}
+
+int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring_start, int n_rings,
+                 const int32_t* ring_region, const int32_t* region_rank, int n_regions) {
+    if (!ctx || !xy || !ring_start || !ring_region || !region_rank || n_rows <= 0 || n_rings <= 0 || n_regions <= 0)
+        return fail(ctx, DET_E_ARG, "invalid map arguments");
+    cudaSetDevice(ctx->device);
+    if (ring_start[0] != 0 || ring_start[n_rings] != n_rows) return fail(ctx, DET_E_ARG, "ring_start must span all rows");
+    std::vector<int> reg_row0(n_regions + 1, -1), reg_ring0(n_regions + 1, 0), next(n_rows), uniq(n_rows), rank_reg(n_regions, -1);
+    std::vector<uint8_t> owner(n_rows, 0);
+    int prev_region = -1;
+    for (int q = 0; q < n_rings; ++q) {
+        const int r = ring_region[q];
+        if (r < 0 || r >= n_regions || r < prev_region) return fail(ctx, DET_E_ARG, "rings must be grouped by region in order");
+        if (ring_start[q + 1] - ring_start[q] < 1) return fail(ctx, DET_E_ARG, "empty ring");
+        while (prev_region < r) {
+            ++prev_region;
+            reg_row0[prev_region] = ring_start[q];
+            reg_ring0[prev_region] = q;
+        }
+        for (int v = ring_start[q]; v < ring_start[q + 1]; ++v) next[v] = (v + 1 < ring_start[q + 1]) ? v + 1 : ring_start[q];
+    }
+    if (prev_region != n_regions - 1) return fail(ctx, DET_E_ARG, "every region needs at least one ring");
+    reg_row0[n_regions] = n_rows;
+    reg_ring0[n_regions] = n_rings;
+    for (int r = 0; r < n_regions; ++r) {
+        const int k = region_rank[r];
+        if (k < 0 || k >= n_regions || rank_reg[k] != -1) return fail(ctx, DET_E_ARG, "region_rank must be a permutation");
+        rank_reg[k] = r;
+    }
+    // exact (bitwise) de-duplication of vertex positions: duplicates evolve identically
+    struct KeyHash {
+        size_t operator()(const std::pair<uint64_t, uint64_t>& k) const {
+            return std::hash<uint64_t>()(k.first * 0x9E3779B97F4A7C15ull ^ k.second);
+        }
+    };
+    std::unordered_map<std::pair<uint64_t, uint64_t>, int, KeyHash> map;
+    map.reserve(n_rows * 2);
+    std::vector<double> xyu;
+    xyu.reserve(n_rows * 2);
+    for (int v = 0; v < n_rows; ++v) {
+        uint64_t a, b;
+        memcpy(&a, xy + 2 * v, 8);
+        memcpy(&b, xy + 2 * v + 1, 8);
+        auto it = map.find({a, b});
+        if (it == map.end()) {
+            const int id = (int)(xyu.size() / 2);
+            map.emplace(std::make_pair(a, b), id);
+            xyu.push_back(xy[2 * v]);
+            xyu.push_back(xy[2 * v + 1]);
+            uniq[v] = id;
+            owner[v] = 1;
+        } else {
+            uniq[v] = it->second;
+        }
+    }
+    ctx->R = n_regions;
+    ctx->n_rows = n_rows;
+    ctx->n_rings = n_rings;
+    ctx->n_uniq = (int)(xyu.size() / 2);
+    ctx->h_row_uniq = uniq;
+    ctx->h_xy_uniq = xyu;
+    ctx->h_ring_start.assign(ring_start, ring_start + n_rings + 1);
+    ctx->h_region_ring0 = reg_ring0;
+    CK(ctx->region_row0.alloc(n_regions + 1));
+    CK(ctx->region_ring0.alloc(n_regions + 1));
+    CK(ctx->ring_start.alloc(n_rings + 1));
+    CK(ctx->row_uniq.alloc(n_rows));
+    CK(ctx->row_next.alloc(n_rows));
+    CK(ctx->row_owner.alloc(n_rows));
+    CK(ctx->region_rank.alloc(n_regions));
+    CK(ctx->rank_region.alloc(n_regions));
+    CK(cudaMemcpy(ctx->region_row0.p, reg_row0.data(), (n_regions + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->region_ring0.p, reg_ring0.data(), (n_regions + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->ring_start.p, ring_start, (n_rings + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->row_uniq.p, uniq.data(), n_rows * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->row_next.p, next.data(), n_rows * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->row_owner.p, owner.data(), n_rows, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->region_rank.p, region_rank, n_regions * sizeof(int), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(ctx->rank_region.p, rank_reg.data(), n_regions * sizeof(int), cudaMemcpyHostToDevice));
+    ctx->B = 0;
+    ctx->params_set = false;
+    invalidate_graph(ctx);
+    return DET_OK;
+}
+
+int det_set_batch(det_ctx* ctx, int batch, const double* xy, const double* stats) {
+    if (!ctx || batch <= 0 || !stats) return fail(ctx, DET_E_ARG, "invalid batch arguments");
+    if (ctx->n_rows == 0) return fail(ctx, DET_E_STATE, "det_load_map first");
+    cudaSetDevice(ctx->device);
+    if (batch != ctx->B) {
+        int rc = alloc_batch(ctx, batch);
+        if (rc) return rc;
+    }
+    std::vector<double> pu((size_t)batch * ctx->n_uniq * 2);
+    for (int b = 0; b < batch; ++b) {
+        double* dst = pu.data() + (size_t)b * ctx->n_uniq * 2;
+        if (!xy) {
+            memcpy(dst, ctx->h_xy_uniq.data(), ctx->h_xy_uniq.size() * sizeof(double));
+            continue;
+        }
+        const double* src = xy + (size_t)b * ctx->n_rows * 2;
+        std::vector<uint8_t> seen(ctx->n_uniq, 0);
+        for (int v = 0; v < ctx->n_rows; ++v) {
+            const int u = ctx->h_row_uniq[v];
+            if (!seen[u]) {
+                dst[2 * u] = src[2 * v];
+                dst[2 * u + 1] = src[2 * v + 1];
+                seen[u] = 1;
+            } else if (memcmp(dst + 2 * u, src + 2 * v, 16) != 0) {
+                return fail(ctx, DET_E_ARG, "vertex rows break the loaded topology's shared vertices; reload the map");
+            }
+        }
+    }
+    CK(cudaMemcpyAsync(ctx->pos_init.p, pu.data(), pu.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->stats.p, stats, (size_t)batch * ctx->R * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->ran = false;
+    return DET_OK;
+}
+
+int det_rasterize(det_ctx* ctx, int b, int32_t* labels_out, int64_t* counts_out) {
+    if (!ctx || ctx->B == 0) return fail(ctx, DET_E_STATE, "det_set_batch first");
+    if (b < 0 || b >= ctx->B) return fail(ctx, DET_E_ARG, "cartogram index out of range");
+    cudaSetDevice(ctx->device);
+    int rc = raster_start(ctx);
+    if (rc) return rc;
+    Carto hs;
+    CK(cudaMemcpy(&hs, ctx->st.p + b, sizeof(Carto), cudaMemcpyDeviceToHost));
+    if (hs.err & E_NEGIDX) return fail(ctx, DET_E_VALUE, "'list' argument must have no negative elements");
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    if (labels_out) CK(cudaMemcpy(labels_out, ctx->labels.p + b * nn, nn * sizeof(int), cudaMemcpyDeviceToHost));
+    if (counts_out) {
+        std::vector<int> c(ctx->R + 1);
+        CK(cudaMemcpy(c.data(), ctx->cnt_acc.p + (size_t)b * (ctx->R + 1), (ctx->R + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+        for (int r = 0; r <= ctx->R; ++r) counts_out[r] = c[r];
+    }
+    CK(cudaMemset(ctx->cnt_acc.p, 0, (size_t)ctx->B * (ctx->R + 1) * sizeof(int)));
+    ctx->ran = false;
+    return DET_OK;
+}
+
+int det_set_params(det_ctx* ctx, const det_params* params, const double* weights_px) {
+    if (!ctx || ctx->B == 0 || !params || !weights_px) return fail(ctx, DET_E_ARG, "invalid params");
+    cudaSetDevice(ctx->device);
+    ctx->h_prm.resize(ctx->B);
+    for (int b = 0; b < ctx->B; ++b) {
+        Params& p = ctx->h_prm[b];
+        memset(&p, 0, sizeof(p));
+        p.background_mass = params[b].background_mass;
+        p.mult = params[b].bdv_multiplier;
+        p.mean_density0 = params[b].mean_density0;
+        p.S = params[b].total_statistic;
+        p.mode = params[b].bdv_mode;
+    }
+    CK(cudaMemcpyAsync(ctx->weights.p, weights_px, (size_t)ctx->B * ctx->R * sizeof(double), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->params_set = true;
+    return DET_OK;
+}
+
+static int run_once(det_ctx* ctx, const det_criteria* crit, bool* overflow) {
+    *overflow = false;
+    const int B = ctx->B;
+    const int tc = crit->max_iterations + 1;
+    if (tc > ctx->trace_cap || ctx->trace.n < (size_t)B * ctx->trace_cap * 4) {
+        ctx->trace_cap = std::max(tc, ctx->trace_cap);
+        CK(ctx->trace.alloc((size_t)B * ctx->trace_cap * 4));
+        invalidate_graph(ctx);
+    }
+    for (int b = 0; b < B; ++b) {
+        ctx->h_prm[b].thr = crit->error_threshold;
+        ctx->h_prm[b].window = crit->stagnation_window;
+        ctx->h_prm[b].max_iter = crit->max_iterations;
+    }
+    CK(cudaMemcpyAsync(ctx->prm.p, ctx->h_prm.data(), B * sizeof(Params), cudaMemcpyHostToDevice, ctx->stream));
+    int rc = raster_start(ctx);  // state 0 labels/counts (+ span capacity sizing)
+    if (rc) return rc;
+    {
+        Carto hs;
+        for (int b = 0; b < B; ++b) {
+            CK(cudaMemcpy(&hs, ctx->st.p + b, sizeof(Carto), cudaMemcpyDeviceToHost));
+            if (hs.err & E_NEGIDX) return fail(ctx, DET_E_VALUE, "'list' argument must have no negative elements");
+        }
+    }
+    rc = ensure_graph(ctx);
+    if (rc) return rc;
+    {
+        const Topo T = make_topo(ctx);
+        const Bufs D = make_bufs(ctx);
+        k_ctrl<<<B, CTRL_THREADS, 0, ctx->stream>>>(T, D, 0, G_ACTIVE);
+        CK(cudaGetLastError());
+    }
+    const int max_launches = crit->max_iterations / kGraphIters + 2;
+    for (int l = 0; l < max_launches; ++l) {
+        CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->h_st.data(), ctx->st.p, B * sizeof(Carto), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        bool any = false;
+        for (int b = 0; b < B; ++b) {
+            if (ctx->h_st[b].err & E_SPAN_OVF) { *overflow = true; return DET_OK; }
+            if (ctx->h_st[b].err & E_TOGGLE_OVF) return fail(ctx, DET_E_STATE, "more than 4096 crossings on one scanline of a region");
+            any |= ctx->h_st[b].active != 0;
+        }
+        if (!any) break;
+    }
+    bool fin = false;
+    for (int b = 0; b < B; ++b) fin |= ctx->h_st[b].final_pending != 0;
+    if (fin) {
+        const Topo T = make_topo(ctx);
+        const Bufs D = make_bufs(ctx);
+        launch_region(ctx, T, D, M_RASTER, G_FINAL, 2);
+        launch_row(ctx, T, D, G_FINAL);
+        k_ctrl<<<B, CTRL_THREADS, 0, ctx->stream>>>(T, D, 1, G_FINAL);
+        CK(cudaGetLastError());
+    }
+    CK(cudaMemcpyAsync(ctx->h_st.data(), ctx->st.p, B * sizeof(Carto), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int b = 0; b < B; ++b)
+        if (ctx->h_st[b].err & E_SPAN_OVF) *overflow = true;
+    return DET_OK;
+}
+
+int det_run(det_ctx* ctx, const det_criteria* crit) {
+    if (!ctx || !crit) return DET_E_ARG;
+    if (!ctx->params_set) return fail(ctx, DET_E_STATE, "det_set_params first");
+    if (crit->max_iterations <= 0 || crit->stagnation_window <= 0 || !(crit->error_threshold > 0))
+        return fail(ctx, DET_E_ARG, "stopping criteria must all be positive");
+    cudaSetDevice(ctx->device);
+    for (int attempt = 0; attempt < 6; ++attempt) {
+        bool ovf = false;
+        ctx->bench_mode = false;
+        int rc = run_once(ctx, crit, &ovf);
+        if (rc) return rc;
+        if (!ovf) {
+            ctx->ran = true;
+            return DET_OK;
+        }
+        ctx->cap *= 2;  // a row collected more spans than the buffer holds: grow and redo
+        rc = alloc_spans(ctx);
+        if (rc) return rc;
+    }
+    return fail(ctx, DET_E_STATE, "span capacity did not converge");
+}
+
+int det_bench_iterations(det_ctx* ctx, int iters) {
+    if (!ctx || !ctx->ran || !ctx->params_set) return fail(ctx, DET_E_STATE, "det_run first");
+    cudaSetDevice(ctx->device);
+    if (!ctx->bench_mode) {
+        // never-stopping criteria; every cartogram continues from its current state
+        for (int b = 0; b < ctx->B; ++b) {
+            ctx->h_prm[b].thr = 0.0;
+            ctx->h_prm[b].window = 0x3fffffff;
+            ctx->h_prm[b].max_iter = 0x3fffffff;
+        }
+        CK(cudaMemcpyAsync(ctx->prm.p, ctx->h_prm.data(), ctx->B * sizeof(Params), cudaMemcpyHostToDevice, ctx->stream));
+        k_reactivate<<<(ctx->B + 127) / 128, 128, 0, ctx->stream>>>(make_bufs(ctx));
+        CK(cudaGetLastError());
+        int rc = ensure_graph(ctx);
+        if (rc) return rc;
+        ctx->bench_mode = true;
+    }
+    int done = 0;
+    for (; done + kGraphIters <= iters; done += kGraphIters) CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
+    for (; done < iters; ++done) enqueue_iteration(ctx);
+    CK(cudaGetLastError());
+    return DET_OK;
+}
+
+int det_bench_kernel_times(det_ctx* ctx, int iters, float* ms_out) {
+    // Per-kernel device time of `iters` eagerly launched iterations, CUDA events on the
+    // context stream: ms_out[0..5] = sat1, sat2, sat3 (fused here as one launch_sat), region, row, ctrl
+    if (!ctx || !ms_out) return DET_E_ARG;
+    int rc = det_bench_iterations(ctx, 0);
+    if (rc) return rc;
+    cudaEvent_t ev[5];
+    for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&ev[i]));
+    for (int i = 0; i < 4; ++i) ms_out[i] = 0.f;
+    const Topo T = make_topo(ctx);
+    const Bufs D = make_bufs(ctx);
+    SatSrc S;
+    memset(&S, 0, sizeof(S));
+    for (int it = 0; it < iters; ++it) {
+        CK(cudaEventRecord(ev[0], ctx->stream));
+        launch_sat(ctx, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, ctx->f64 != 0, ctx->B);
+        CK(cudaEventRecord(ev[1], ctx->stream));
+        launch_region(ctx, T, D, M_ADVECT | M_RASTER, G_ACTIVE, 0);
+        CK(cudaEventRecord(ev[2], ctx->stream));
+        launch_row(ctx, T, D, G_ACTIVE);
+        CK(cudaEventRecord(ev[3], ctx->stream));
+        k_ctrl<<<ctx->B, CTRL_THREADS, 0, ctx->stream>>>(T, D, 0, G_ACTIVE);
+        CK(cudaEventRecord(ev[4], ctx->stream));
+        CK(cudaEventSynchronize(ev[4]));
+        for (int q = 0; q < 4; ++q) {
+            float t = 0.f;
+            CK(cudaEventElapsedTime(&t, ev[q], ev[q + 1]));
+            ms_out[q] += t;
+        }
+    }
+    for (int i = 0; i < 5; ++i) cudaEventDestroy(ev[i]);
+    return DET_OK;
+}
+
+int det_sync(det_ctx* ctx) {
+    if (!ctx) return DET_E_ARG;
+    CK(cudaStreamSynchronize(ctx->stream));
+    return DET_OK;
+}
+
+int det_get_result(det_ctx* ctx, int b, det_result* out) {
+    if (!ctx || !out || b < 0 || b >= ctx->B || !ctx->ran) return fail(ctx, DET_E_STATE, "no result");
+    const Carto& c = ctx->h_st[b];
+    memset(out, 0, sizeof(*out));
+    out->stop_reason = c.stop;
+    out->iteration = c.res_iter;
+    out->best_iteration = c.best_iter;
+    out->collapsed_region = c.stop == S_COLLAPSED ? c.collapsed : -1;
+    out->clamp_events = (int64_t)c.clamps;
+    out->epsilon = c.eps;
+    out->xi = c.xi;
+    out->bdv = c.bdv;
+    out->trace_len = c.trace_len;
+    out->status = c.stop == S_COLLAPSED ? DET_E_COLLAPSE : ((c.stop == S_BDV || c.stop == S_NEGINDEX) ? DET_E_VALUE : DET_OK);
+    return DET_OK;
+}
+
+static int result_src(det_ctx* ctx, int b) {
+    const Carto& c = ctx->h_st[b];
+    if (c.stop == S_STAGNATION) return 2;
+    return c.res_iter & 1;
+}
+
+static int gather_rows(det_ctx* ctx, int b) {
+    const int src = ctx->ran ? result_src(ctx, b) : 0;
+    if (!ctx->ran) {
+        CK(cudaMemcpyAsync(ctx->pos0.p + (size_t)b * ctx->n_uniq, ctx->pos_init.p + (size_t)b * ctx->n_uniq,
+                           ctx->n_uniq * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+    }
+    const Topo T = make_topo(ctx);
+    const Bufs D = make_bufs(ctx);
+    k_gather_rows<<<(ctx->n_rows + 255) / 256, 256, 0, ctx->stream>>>(T, D, b, src);
+    CK(cudaGetLastError());
+    return DET_OK;
+}
+
+int det_get_vertices(det_ctx* ctx, int b, double* xy_out) {
+    if (!ctx || !xy_out || b < 0 || b >= ctx->B) return fail(ctx, DET_E_ARG, "bad arguments");
+    cudaSetDevice(ctx->device);
+    int rc = gather_rows(ctx, b);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(xy_out, ctx->rowpos.p + (size_t)b * ctx->n_rows, ctx->n_rows * sizeof(double2),
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return DET_OK;
+}
+
+int det_get_labels(det_ctx* ctx, int b, int32_t* out) {
+    if (!ctx || !out || b < 0 || b >= ctx->B) return fail(ctx, DET_E_ARG, "bad arguments");
+    cudaSetDevice(ctx->device);
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    CK(cudaMemcpy(out, ctx->labels.p + b * nn, nn * sizeof(int), cudaMemcpyDeviceToHost));
+    return DET_OK;
+}
+
+int det_get_counts(det_ctx* ctx, int b, int64_t* out) {
+    if (!ctx || !out || b < 0 || b >= ctx->B || !ctx->ran) return fail(ctx, DET_E_STATE, "no result");
+    cudaSetDevice(ctx->device);
+    std::vector<int> c(ctx->R + 1);
+    CK(cudaMemcpy(c.data(), ctx->cnt_state.p + (size_t)b * (ctx->R + 1), (ctx->R + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int r = 0; r <= ctx->R; ++r) out[r] = c[r];
+    return DET_OK;
+}
+
+int det_get_region_error(det_ctx* ctx, int b, double* out) {
+    if (!ctx || !out || b < 0 || b >= ctx->B || !ctx->ran) return fail(ctx, DET_E_STATE, "no result");
+    cudaSetDevice(ctx->device);
+    CK(cudaMemcpy(out, ctx->rerr.p + (size_t)b * ctx->R, ctx->R * sizeof(double), cudaMemcpyDeviceToHost));
+    return DET_OK;
+}
+
+int det_get_trace(det_ctx* ctx, int b, double* out) {
+    if (!ctx || !out || b < 0 || b >= ctx->B || !ctx->ran) return fail(ctx, DET_E_STATE, "no result");
+    cudaSetDevice(ctx->device);
+    const int len = ctx->h_st[b].trace_len;
+    if (len > 0)
+        CK(cudaMemcpy(out, ctx->trace.p + (size_t)b * ctx->trace_cap * 4, (size_t)len * 4 * sizeof(double),
+                      cudaMemcpyDeviceToHost));
+    return DET_OK;
+}
+
+int det_get_areas(det_ctx* ctx, int b, double* out) {
+    if (!ctx || !out || b < 0 || b >= ctx->B) return fail(ctx, DET_E_ARG, "bad arguments");
+    cudaSetDevice(ctx->device);
+    int rc = gather_rows(ctx, b);
+    if (rc) return rc;
+    DVec<double> tmp;
+    CK(tmp.alloc(ctx->R));
+    const Topo T = make_topo(ctx);
+    const Bufs D = make_bufs(ctx);
+    k_areas<<<ctx->R, 128, 0, ctx->stream>>>(T, D, ctx->ring_start.p, ctx->region_ring0.p, b, tmp.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, tmp.p, ctx->R * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return DET_OK;
+}
+
+static int field_impl(det_ctx* ctx, const double* d, double* u_out, double* channels_out, double* total_out,
+                      bool full_mapping) {
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    int rc = alloc_sat(ctx, std::max(ctx->B, 1));
+    if (rc) return rc;
+    CK(ctx->dense.alloc(nn));
+    CK(ctx->uf64.alloc(nn * 2));
+    if (channels_out) CK(ctx->ch8.alloc(nn * 8));
+    CK(cudaMemcpyAsync(ctx->dense.p, d, nn * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    DVec<Carto> dummy;
+    CK(dummy.alloc(1));
+    CK(cudaMemsetAsync(dummy.p, 0, sizeof(Carto), ctx->stream));
+    const Topo T = make_topo(ctx);
+    Bufs D = make_bufs(ctx);
+    D.B = 1;
+    D.st = dummy.p;
+    D.uf = ctx->uf64.p;
+    SatSrc S;
+    memset(&S, 0, sizeof(S));
+    S.d = ctx->dense.p;
+    S.scale = 1.0;
+    S.offset = 0.0;
+    S.ch8 = ctx->ch8.p;
+    // pass 1: total mass C (and the 8 channels of d itself when requested)
+    launch_sat(ctx, T, D, S, G_ALWAYS, SRC_DENSE, channels_out ? OUT_CH8 : OUT_U, true, 1);
+    CK(cudaGetLastError());
+    double C = 0.0;
+    CK(cudaMemcpyAsync(&C, ctx->rowfull.p + ctx->n, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (total_out) *total_out = C;
+    if (channels_out) CK(cudaMemcpy(channels_out, ctx->ch8.p, nn * 8 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (u_out) {
+        if (!(C > 0)) return fail(ctx, DET_E_NUMERIC, "mapping undefined for zero total density");
+        if (full_mapping) {  // t(d) itself (displacement.py:102-131)
+            S.scale = 1.0;
+            S.offset = 0.0;
+            S.outscale = 0.5 / C;
+        } else {             // u = t(d) - t(const) via the residual density (displacement.py:198-206)
+            S.scale = (double)nn / C;
+            S.offset = -1.0;
+            S.outscale = 0.0;
+        }
+        launch_sat(ctx, T, D, S, G_ALWAYS, SRC_DENSE, OUT_U, true, 1);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(u_out, ctx->uf64.p, nn * 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return DET_OK;
+}
+
+int det_field(det_ctx* ctx, const double* d, double* u_out, double* channels_out, double* total_out) {
+    if (!ctx || !d) return fail(ctx, DET_E_ARG, "bad arguments");
+    cudaSetDevice(ctx->device);
+    return field_impl(ctx, d, u_out, channels_out, total_out, false);
+}
+
+int det_mapping(det_ctx* ctx, const double* d, double* t_out) {
+    if (!ctx || !d || !t_out) return fail(ctx, DET_E_ARG, "bad arguments");
+    cudaSetDevice(ctx->device);
+    return field_impl(ctx, d, t_out, nullptr, nullptr, true);
+}
+
+int det_density(det_ctx* ctx, const int32_t* labels, const double* stats, int n_regions, double bdv, double* d_out,
+                int64_t* counts_out) {
+    if (!ctx || !labels || !stats || n_regions <= 0) return fail(ctx, DET_E_ARG, "bad arguments");
+    if (!(bdv > 0)) return fail(ctx, DET_E_VALUE, "bdv must be positive");
+    cudaSetDevice(ctx->device);
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    DVec<int> lab, cnt;
+    DVec<double> st, d;
+    CK(lab.alloc(nn));
+    CK(cnt.alloc(n_regions + 1));
+    CK(st.alloc(n_regions));
+    CK(d.alloc(nn));
+    CK(cudaMemcpyAsync(lab.p, labels, nn * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(st.p, stats, n_regions * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(cnt.p, 0, (n_regions + 1) * sizeof(int), ctx->stream));
+    k_hist<<<592, 256, 0, ctx->stream>>>(lab.p, nn, n_regions, cnt.p);
+    std::vector<int> hc(n_regions + 1);
+    CK(cudaMemcpyAsync(hc.data(), cnt.p, (n_regions + 1) * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int r = 0; r < n_regions; ++r)
+        if (hc[r] == 0) return fail(ctx, DET_E_RASTER, "cannot build density with zero-pixel regions");
+    if (counts_out)
+        for (int r = 0; r <= n_regions; ++r) counts_out[r] = hc[r];
+    if (d_out) {
+        k_density<<<592, 256, 0, ctx->stream>>>(lab.p, nn, n_regions, st.p, cnt.p, bdv, d.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(d_out, d.p, nn * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return DET_OK;
+}
+
+int det_advect(det_ctx* ctx, const double* u, const double* xy, int n_pts, double* xy_out, int64_t* clamps) {
+    if (!ctx || !u || !xy || !xy_out || n_pts < 0) return fail(ctx, DET_E_ARG, "bad arguments");
+    cudaSetDevice(ctx->device);
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    CK(ctx->uf64.alloc(nn * 2));
+    CK(ctx->pts_in.alloc((size_t)n_pts * 2));
+    CK(ctx->pts_out.alloc((size_t)n_pts * 2));
+    CK(ctx->clampbuf.alloc(1));
+    CK(cudaMemcpyAsync(ctx->uf64.p, u, nn * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->pts_in.p, xy, (size_t)n_pts * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->clampbuf.p, 0, sizeof(unsigned long long), ctx->stream));
+    if (n_pts > 0)
+        k_advect_points<<<(n_pts + 255) / 256, 256, 0, ctx->stream>>>(ctx->uf64.p, ctx->n, (const double2*)ctx->pts_in.p,
+                                                                      n_pts, (double2*)ctx->pts_out.p, ctx->clampbuf.p);
+    CK(cudaGetLastError());
+    unsigned long long c = 0;
+    CK(cudaMemcpyAsync(xy_out, ctx->pts_out.p, (size_t)n_pts * 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(&c, ctx->clampbuf.p, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (clamps) *clamps = (int64_t)c;
+    return DET_OK;
+}
+
+}  // extern "C"

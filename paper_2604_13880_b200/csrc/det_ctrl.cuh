@@ -1,0 +1,167 @@
+// Per-cartogram control kernel (sm_100a): evaluate + stopping rule + next density LUT.
+//
+// One CTA per cartogram.  Reads the pixel counts accumulated by k_row and does,
+// on the device, what engine.py does on the host between two steps:
+//   * collapse check, first zero-count region (engine.py:147-150);
+//   * e_r = |o-w|/max(o,w), epsilon = mean, xi = max (engine.py:83-85,151);
+//   * trace row (iteration, epsilon, xi, millis) (engine.py:189-195);
+//   * best-state tracking with strict '<' and the three stop tests (engine.py:196-211);
+//   * background density (engine.py:162-168) and the residual density LUT
+//     rho_r = m*(s_r/o_r)/C - 1, rho_bg = m*bdv/C - 1 consumed by k_sat1/k_sat3
+//     (build_density, raster.py:166-184, fused with the residual form).
+#pragma once
+#include <limits.h>
+#include "det_common.cuh"
+
+namespace det {
+
+__global__ void k_init_state(Bufs D) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= D.B) return;
+    Carto c;
+    memset(&c, 0, sizeof(c));
+    c.active = 1;
+    c.best_xi = INFINITY;
+    c.collapsed = -1;
+    c.t_prev = globaltimer();
+    D.st[b] = c;
+    D.maxspan[b] = 0;
+}
+
+// Benchmark helper: continue every cartogram from its current state.
+__global__ void k_reactivate(Bufs D) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= D.B) return;
+    Carto* c = D.st + b;
+    if (c->stop == S_COLLAPSED || c->stop == S_BDV || c->stop == S_NEGINDEX) return;
+    if (c->stop != S_RUNNING) c->next_iter = c->res_iter + 1;  // its LUT was built by k_ctrl
+    c->active = 1;
+    c->stop = S_RUNNING;
+    c->final_pending = 0;
+}
+
+// cmode 0: loop evaluation of state next_iter; cmode 1: final re-evaluation of the best state.
+__global__ void __launch_bounds__(CTRL_THREADS) k_ctrl(Topo T, Bufs D, int cmode, int gate) {
+    __shared__ double s_red[33];
+    __shared__ int s_redi[33];
+    __shared__ int s_nbg, s_cont;
+    __shared__ double s_bdv;
+    const int b = blockIdx.x, t = threadIdx.x, R = T.R;
+    Carto* st = D.st + b;
+    if (!gate_open(st, gate)) return;
+    int* acc = D.cnt_acc + (size_t)b * (R + 1);
+    int* sc = D.cnt_state + (size_t)b * (R + 1);
+    const double* wt = D.weights + (size_t)b * R;
+    const double* s = D.stats + (size_t)b * R;
+    double* er = D.rerr + (size_t)b * R;
+    if (t == 0) {
+        s_nbg = acc[R];
+        sc[R] = s_nbg;
+        acc[R] = 0;
+    }
+    int fz = INT_MAX;
+    double es = 0.0, em = -INFINITY;
+    for (int r = t; r < R; r += blockDim.x) {
+        const int o = acc[r];
+        sc[r] = o;
+        acc[r] = 0;
+        if (o == 0) fz = min(fz, r);
+        const double od = (double)o, w = wt[r];
+        const double e = fabs(od - w) / fmax(od, w);
+        er[r] = e;
+        es += e;
+        em = fmax(em, e);
+    }
+    fz = block_reduce<1, int>(fz, INT_MAX, s_redi);
+    es = block_reduce<0, double>(es, 0.0, s_red);
+    em = block_reduce<2, double>(em, -INFINITY, s_red);
+    const int nbg = s_nbg;
+    const Params P = D.prm[b];
+    const int it = cmode == 0 ? st->next_iter : st->best_iter;
+    if (t == 0) {
+        s_cont = 0;
+        int stop = S_RUNNING;
+        if (st->err & E_NEGIDX) {
+            stop = S_NEGINDEX;
+            st->res_iter = it;
+        } else if (fz < R) {
+            stop = S_COLLAPSED;
+            st->collapsed = fz;
+            st->res_iter = it;
+        } else {
+            const double eps = es / (double)R, xi = em;
+            st->eps = eps;
+            st->xi = xi;
+            st->res_iter = it;
+            if (cmode == 1) {
+                st->final_pending = 0;
+                st->clamps = 0;  // evaluate() returns a fresh state (engine.py:204-208)
+            } else {
+                const unsigned long long now = globaltimer();
+                const double ms = (double)(now - st->t_prev) * 1e-6;
+                st->t_prev = now;
+                if (it < D.trace_cap) {
+                    double* tr = D.trace + ((size_t)b * D.trace_cap + it) * 4;
+                    tr[0] = (double)it; tr[1] = eps; tr[2] = xi; tr[3] = ms;
+                    st->trace_len = it + 1;
+                }
+                if (xi < st->best_xi) {
+                    st->best_xi = xi;
+                    st->best_iter = it;
+                    st->best_pending = 1;
+                } else {
+                    st->best_pending = 0;
+                }
+                if (xi < P.thr) {
+                    stop = S_CONVERGED;
+                } else if (it - st->best_iter >= P.window) {
+                    stop = S_STAGNATION;
+                    st->final_pending = 1;
+                } else if (it >= P.max_iter) {
+                    stop = S_MAXITER;
+                }
+                // background density of the next step (engine.py:162-168); also built for a
+                // stopped state so a benchmark can continue from it (det_bench_iterations)
+                const double m = (double)D.nn;
+                double bdv;
+                if (nbg == 0) bdv = P.mean_density0 * P.mult;
+                else if (P.mode == 0) bdv = P.background_mass / (double)nbg;
+                else bdv = P.mult * P.S / (m - (double)nbg);
+                if (!(bdv > 0.0)) {
+                    if (stop == S_RUNNING) stop = S_BDV;  // build_density raises ValueError (raster.py:168-169)
+                } else {
+                    s_cont = 1;
+                    s_bdv = bdv;
+                    st->bdv = bdv;
+                    if (stop == S_RUNNING) st->next_iter = it + 1;
+                }
+            }
+        }
+        if (stop != S_RUNNING) {
+            st->stop = stop;
+            st->active = 0;
+            if (stop != S_STAGNATION) st->final_pending = 0;
+        }
+    }
+    __syncthreads();
+    if (!s_cont) return;
+    const double bdv = s_bdv;
+    const double m = (double)D.nn;
+    double cpart = 0.0;
+    for (int r = t; r < R; r += blockDim.x) {
+        const double o = (double)sc[r];
+        cpart += (s[r] / o) * o;
+    }
+    const double C = block_reduce<0, double>(cpart, 0.0, s_red) + bdv * (double)nbg;
+    double* lut = D.lut + (size_t)b * (R + 1);
+    for (int r = t; r < R; r += blockDim.x) {
+        const double o = (double)sc[r];
+        lut[r] = m * (s[r] / o) / C - 1.0;
+    }
+    if (t == 0) {
+        lut[R] = m * bdv / C - 1.0;
+        st->C = C;
+    }
+}
+
+}  // namespace det

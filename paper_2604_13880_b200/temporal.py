@@ -1,0 +1,238 @@
+"""Time-varying cartogram sequences -- drop-in for cartomorph/temporal.py.
+
+Transition modes (temporal.py:162-290):
+
+* ``run_direct``: every frame starts from the densified base map.  Frames are
+  independent, so all T frames run as ONE batch on the GPU (``BatchEngine``:
+  every kernel launch covers all frames) -- the B200-native replacement for the
+  reference's frame-by-frame loop.
+* ``run_cumulative``: frame t starts from frame t-1's output; frames run one
+  after another, each fully device-resident.
+
+The background-mass schedule (temporal.py:83-102, 151-159) and the per-frame
+error capture (temporal.py:231-244) follow the reference.  The per-frame
+quality report (``full_report``, metrics.py:213-260) is outside this
+build's hot-path scope: ``Frame.report`` is None and the
+watchdog is not evaluated.
+"""
+
+from __future__ import annotations
+
+import logging
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .engine import DENSIFY_EDGE_PIXELS, BatchEngine, CartogramEngine, RunResult, StoppingCriteria
+from .errors import CartomorphError, IngestionError
+from .geomodel import densify, rebuild
+from .raster import rasterize_labels
+
+log = logging.getLogger(__name__)
+
+DEFAULT_WATCHDOG_CEILING = 0.5
+DEFAULT_FRAMES_PER_STEP = 10
+
+
+@dataclass(frozen=True)
+class TimeSeriesDataset:
+    """A map plus one positive statistic vector per time step (temporal.py:36-63)."""
+
+    mapmodel: object
+    times: tuple
+    statistics: np.ndarray
+
+    def __post_init__(self):
+        stats = np.asarray(self.statistics, dtype=float)
+        if stats.ndim != 2 or stats.shape[0] != len(self.times):
+            raise IngestionError("statistics must be (time, region) shaped")
+        if stats.shape[1] != len(self.mapmodel.regions):
+            raise IngestionError("statistics column count must match region count")
+        if (stats <= 0).any() or not np.isfinite(stats).all():
+            raise IngestionError("all statistics must be positive and finite")
+        object.__setattr__(self, "statistics", stats)
+
+    @property
+    def step_count(self) -> int:
+        return len(self.times)
+
+    def totals(self) -> np.ndarray:
+        return self.statistics.sum(axis=1)
+
+    def map_at(self, t: int):
+        return self.mapmodel.with_statistics(self.statistics[t])
+
+
+@dataclass(frozen=True)
+class AreaFractionPolicy:
+    a_min: float
+    a_max: float
+    window: tuple | None = None
+
+    def __post_init__(self):
+        if not (0.0 < self.a_min < self.a_max < 1.0):
+            raise ValueError("need 0 < a_min < a_max < 1")
+        if self.window is not None and self.window[0] > self.window[1]:
+            raise ValueError("window must be ordered")
+
+
+def background_mass_schedule(dataset: TimeSeriesDataset, policy: AreaFractionPolicy):
+    """Per-time (M_b, A_i) from the area-fraction schedule (temporal.py:83-102)."""
+    totals = dataset.totals()
+    t0, t1 = policy.window or (0, dataset.step_count - 1)
+    if not (0 <= t0 <= t1 < dataset.step_count):
+        raise ValueError("window outside dataset range")
+    m_min = float(totals[t0 : t1 + 1].min())
+    m_max = float(totals[t0 : t1 + 1].max())
+    if m_max == m_min:
+        log.info("constant mass over the window; using w = 1 for all time steps")
+        w = np.ones_like(totals)
+    else:
+        w = np.clip((totals - m_min) / (m_max - m_min), 0.0, 1.0)
+    area_fraction = (1.0 - w) * policy.a_min + w * policy.a_max
+    return totals * (1.0 - area_fraction) / area_fraction, area_fraction
+
+
+@dataclass
+class Frame:
+    time_index: int
+    time: str
+    mapmodel: object
+    result: RunResult | None
+    report: object
+    background_mass: float
+    area_fraction: float | None
+    wall_ms: float
+    watchdog: bool = False
+    error: str | None = None
+
+
+@dataclass
+class FrameSequence:
+    strategy: str
+    dataset: TimeSeriesDataset
+    base_map: object
+    frames: list = field(default_factory=list)
+
+    def series(self) -> dict:
+        totals = self.dataset.totals()
+        return {
+            "times": list(self.dataset.times),
+            "M_i": [float(v) for v in totals],
+            "M_b": [f.background_mass for f in self.frames],
+            "A_i": [f.area_fraction if f.area_fraction is not None else float(t / (t + f.background_mass))
+                    for f, t in zip(self.frames, totals)],
+            "epsilon": [f.result.state.epsilon if f.result else None for f in self.frames],
+            "xi": [f.result.state.xi if f.result else None for f in self.frames],
+            "wall_ms": [f.wall_ms for f in self.frames],
+            "watchdog": [f.watchdog for f in self.frames],
+            "errors": [f.error for f in self.frames],
+        }
+
+
+def _default_background_masses(dataset: TimeSeriesDataset, k: int, bdv_multiplier: float):
+    """temporal.py:151-159: the original map's pixel split, for both strategies (GPU raster)."""
+    labels = rasterize_labels(dataset.mapmodel, k)
+    n_map = labels.map_pixel_count()
+    n_bg = labels.background_count()
+    return bdv_multiplier * dataset.totals() / n_map * n_bg
+
+
+def _masses(dataset, policy, k, bdv_multiplier):
+    if policy is None:
+        return _default_background_masses(dataset, k, bdv_multiplier), [None] * dataset.step_count
+    return background_mass_schedule(dataset, policy)
+
+
+def run_direct(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None = None,
+               policy: AreaFractionPolicy | None = None, k: int = 10, bdv_multiplier: float = 1.0,
+               watchdog_ceiling: float = DEFAULT_WATCHDOG_CEILING, report_raster_k: int = 7, *,
+               device: int = 0, field_dtype: str = "float32") -> FrameSequence:
+    """Every frame deformed independently from the original map -- all frames in one GPU batch."""
+    criteria = criteria or StoppingCriteria()
+    masses, fractions = _masses(dataset, policy, k, bdv_multiplier)
+    base_map = densify(dataset.mapmodel, DENSIFY_EDGE_PIXELS / (1 << k))
+    seq = FrameSequence(strategy="direct", dataset=dataset, base_map=base_map)
+    began = time.perf_counter()
+    try:
+        # engines are built with the reference's per-frame arguments (temporal.py:190-196):
+        # bdv_multiplier defaults to 1.0 there, the masses carry the user's multiplier
+        be = BatchEngine(base_map, dataset.statistics, criteria=criteria, k=k,
+                         background_mass=np.asarray(masses, dtype=float), apply_densify=False,
+                         device=device, field_dtype=field_dtype)
+        results = be.run_all()
+    except CartomorphError as exc:  # a start-map problem fails every frame alike
+        results = [exc] * dataset.step_count
+    wall_ms = (time.perf_counter() - began) * 1e3 / max(dataset.step_count, 1)
+    for t, res in enumerate(results):
+        frac = None if fractions[t] is None else float(fractions[t])
+        if isinstance(res, CartomorphError):
+            log.error("direct frame %d failed: %s", t, res)
+            seq.frames.append(Frame(t, dataset.times[t], None, None, None, float(masses[t]), frac, wall_ms,
+                                    error=str(res)))
+        elif isinstance(res, Exception):
+            raise res
+        else:
+            seq.frames.append(Frame(t, dataset.times[t], res.state.mapmodel, res, None, float(masses[t]), frac,
+                                    wall_ms))
+    return seq
+
+
+def run_cumulative(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None = None,
+                   policy: AreaFractionPolicy | None = None, k: int = 10, bdv_multiplier: float = 1.0,
+                   watchdog_ceiling: float = DEFAULT_WATCHDOG_CEILING, report_raster_k: int = 7, *,
+                   device: int = 0, field_dtype: str = "float32") -> FrameSequence:
+    """Each frame starts from the previous frame's deformed map (temporal.py:271-290)."""
+    criteria = criteria or StoppingCriteria()
+    masses, fractions = _masses(dataset, policy, k, bdv_multiplier)
+    base_map = densify(dataset.mapmodel, DENSIFY_EDGE_PIXELS / (1 << k))
+    seq = FrameSequence(strategy="cumulative", dataset=dataset, base_map=base_map)
+    previous = base_map
+    for t in range(dataset.step_count):
+        start_map = previous.with_statistics(dataset.statistics[t])
+        frac = None if fractions[t] is None else float(fractions[t])
+        began = time.perf_counter()
+        try:
+            eng = CartogramEngine(start_map, criteria=criteria, k=k, background_mass=float(masses[t]),
+                                  apply_densify=False, device=device, field_dtype=field_dtype)
+            res = eng.run()
+            wall_ms = (time.perf_counter() - began) * 1e3
+            seq.frames.append(Frame(t, dataset.times[t], res.state.mapmodel, res, None, float(masses[t]), frac,
+                                    wall_ms))
+            previous = res.state.mapmodel
+        except CartomorphError as exc:
+            wall_ms = (time.perf_counter() - began) * 1e3
+            log.error("cumulative frame %d failed: %s", t, exc)
+            seq.frames.append(Frame(t, dataset.times[t], None, None, None, float(masses[t]), frac, wall_ms,
+                                    error=str(exc)))
+    return seq
+
+
+def interpolate_vertices(a, b, fraction: float):
+    """Linear per-vertex blend of two frames with identical vertex layout (temporal.py:293-302)."""
+    va, vb = a.vertex_array(), b.vertex_array()
+    if va.shape != vb.shape:
+        raise ValueError("vertex-count mismatch between frames")
+    sa = np.array([r.statistic for r in a.regions], dtype=float)
+    sb = np.array([r.statistic for r in b.regions], dtype=float)
+    return rebuild(a, va + fraction * (vb - va)).with_statistics(sa + fraction * (sb - sa))
+
+
+def interpolate_frames(seq: FrameSequence, frames_per_step: int = DEFAULT_FRAMES_PER_STEP):
+    """Dense animation frames (temporal.py:305-326)."""
+    if frames_per_step < 1:
+        raise ValueError("frames_per_step must be >= 1")
+    out = []
+    frames = list(seq.frames)
+    for idx, cur in enumerate(frames):
+        if cur.mapmodel is None:
+            continue
+        out.append((cur.time, cur.mapmodel))
+        if idx + 1 >= len(frames) or frames[idx + 1].mapmodel is None:
+            continue
+        nxt = frames[idx + 1]
+        for sub in range(1, frames_per_step):
+            u = sub / frames_per_step
+            out.append((f"{cur.time}+{u:.3f}", interpolate_vertices(cur.mapmodel, nxt.mapmodel, u)))
+    return out

@@ -1,0 +1,272 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the golden fixtures.
+
+Bars (BASELINE.json north_star): region-ID rasters bit-exact on identical vertex
+input; vertices within 1e-4 of the domain extent; per-region areas within 1e-3
+relative.  Float64-field runs are additionally held to trajectory identity with
+the reference where the fixtures allow it.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+import fixture_maps as fm
+from conftest import cuda_available
+from oracle import det_oracle as O
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
+
+VERT_TOL = 1e-4   # north_star: vertex positions within 1e-4 of the domain extent
+AREA_RTOL = 1e-3  # north_star: per-region area error within 1e-3 relative
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2604_13880_b200 as P
+
+    return P
+
+
+def _load(golden_dir, name):
+    return np.load(os.path.join(golden_dir, name))
+
+
+# ---------------------------------------------------------------- raster
+@pytest.mark.parametrize("case", ["overlap", "tie", "vor"])
+@pytest.mark.parametrize("q", [0, 1, 2])
+def test_raster_golden_bit_exact(P, golden_dir, case, q):
+    z = _load(golden_dir, "raster_cases.npz")
+    m = fm.unpack_map(z, prefix=f"{case}{q}_")
+    tex = P.rasterize_labels(m, int(z[f"{case}{q}_k"]), check_collapse=False)
+    assert np.array_equal(tex.labels, z[f"{case}{q}_labels"])
+    ref = z[f"{case}{q}_labels"]
+    assert np.array_equal(tex.pixel_counts(), np.bincount(ref[ref >= 0], minlength=len(m.regions)))
+    assert tex.background_count() == int((ref == -1).sum())
+
+
+@pytest.mark.parametrize("k", [4, 6, 8, 10])
+def test_raster_perturbed_vs_oracle(P, k):
+    m = fm.config1()
+    rng = np.random.default_rng(k)
+    base = m.vertex_array()
+    for q in range(4):
+        xy = base if q == 0 else np.clip(base + rng.normal(0, 0.5 / (1 << k), base.shape), 0, 1)
+        mq = m.with_vertex_array(xy)
+        tex = P.rasterize_labels(mq, k, check_collapse=False)
+        ref = O.FlatMap.from_mapmodel(mq).labels(k)
+        assert np.array_equal(tex.labels, ref), f"k={k} q={q}: {(tex.labels != ref).sum()} pixels differ"
+
+
+def test_raster_tie_and_edge_cases(P):
+    tex = P.rasterize_labels(fm.tie_partition(), 4)
+    assert tex.background_count() == 0 and tex.pixel_counts().tolist() == [128, 128]
+    full = P.MapModel(regions=(P.Region("A", "A", (np.array([[0., 0.], [1., 0.], [1., 1.], [0., 1.]]),), 1.0),))
+    assert P.rasterize_labels(full, 4).pixel_counts()[0] == 256
+    tiny = P.MapModel(regions=(P.Region("A", "A", (np.array([[.5, .5], [.501, .5], [.501, .501], [.5, .501]]),), 1.),))
+    with pytest.raises(P.RasterizationError, match="zero-pixel"):
+        P.rasterize_labels(tiny, 4)
+    with pytest.raises(ValueError):
+        P.rasterize_labels(full, 3)
+
+
+def test_raster_headline_size_vs_oracle(P):
+    from paper_2604_13880_b200.synthetic import voronoi_map
+
+    m = voronoi_map(3000, seed=3, target_unique=200_000, sigma=2.0)
+    tex = P.rasterize_labels(m, 10, check_collapse=False)
+    ref = O.FlatMap.from_mapmodel(m).labels(10)
+    assert np.array_equal(tex.labels, ref)
+    assert tex.pixel_counts().sum() + tex.background_count() == 1 << 20
+
+
+# ---------------------------------------------------------------- integral images / field / advect
+def test_channels_vs_oracle(P, golden_dir):
+    z = _load(golden_dir, "stage_k6.npz")
+    ii = P.integral_images(z["d"])
+    got = np.stack(ii.straight_channels() + ii.tilted_channels())
+    tol = 1e-9 * ii.total
+    assert np.abs(got - z["channels"]).max() <= tol
+    assert abs(ii.total - float(z["total"])) <= 1e-12 * ii.total
+
+
+@pytest.mark.parametrize("n", [16, 32, 128, 512])
+def test_channels_random_vs_oracle(P, n):
+    d = np.random.default_rng(n).uniform(0.0, 3.0, (n, n))
+    ii = P.integral_images(d)
+    ref = O.all_channels(d)
+    for a, b in zip(ii.straight_channels() + ii.tilted_channels(), ref[:8]):
+        assert np.abs(a - b).max() <= 1e-9 * ref[8]
+
+
+def test_field_and_advect_vs_golden(P, golden_dir):
+    z = _load(golden_dir, "stage_k6.npz")
+    fld = P.residual_field(P.integral_images(z["d"]))
+    assert np.abs(fld.u - z["u"]).max() <= 1e-12
+    moved, cl = P.advect(fm.unpack_map(z).vertex_array(), P.DisplacementField(64, z["u"]))
+    assert np.abs(moved - z["moved"]).max() <= 1e-15
+    assert cl == int(z["clamps"])
+    assert np.abs(P.base_mapping(64) - z["base"]).max() <= 1e-12
+
+
+@pytest.mark.parametrize("n", [256, 1024])
+def test_field_large_vs_oracle(P, n):
+    rng = np.random.default_rng(7)
+    d = np.repeat(np.repeat(rng.lognormal(0, 1, (n // 16, n // 16)), 16, 0), 16, 1)
+    from paper_2604_13880_b200._context import get_context
+
+    u, _, _ = get_context(n.bit_length() - 1).field(d)
+    ref = O.displacement(d)
+    assert np.abs(u - ref).max() <= 1e-12
+
+
+def test_density_vs_oracle(P, golden_dir):
+    z = _load(golden_dir, "stage_k6.npz")
+    lab = P.LabelTexture(64, z["labels"], tuple(str(i) for i in z["ids"]))
+    stats = z["stats"]
+    bdv = 0.8 * P.default_bdv(stats, lab)
+    dens = P.build_density(stats, lab, bdv)
+    assert np.array_equal(dens.d, O.density_texture(stats, z["labels"], bdv))
+
+
+# ---------------------------------------------------------------- engine runs
+_RUNS = ["c1", "two", "two_rederive", "vor_stag", "overlap"]
+
+
+def _golden_run_args(z, name):
+    kw, crit = {}, dict(error_threshold=1e-300, stagnation_window=10**9, max_iterations=int(z[f"{name}_trace"][-1, 0]))
+    if name == "c1":
+        kw = dict(bdv_multiplier=0.5)
+    elif name == "two_rederive":
+        kw = dict(bdv_mode="rederive")
+    elif name == "overlap":
+        kw = dict(bdv_multiplier=1.3)
+    elif name == "vor_stag":
+        crit = dict(error_threshold=1e-9, stagnation_window=5, max_iterations=200)
+    return kw, crit
+
+
+@pytest.mark.parametrize("field_dtype", ["float64", "float32"])
+@pytest.mark.parametrize("name", _RUNS)
+def test_engine_vs_golden(P, golden_dir, name, field_dtype):
+    z = _load(golden_dir, "engine_runs.npz")
+    m = fm.unpack_map(z, prefix=f"{name}_in_")
+    kw, crit = _golden_run_args(z, name)
+    res = P.run(m, P.StoppingCriteria(**crit), k=int(z[f"{name}_k"]), field_dtype=field_dtype, **kw)
+    verts = res.state.mapmodel.vertex_array()
+    dv = np.abs(verts - z[f"{name}_final_xy"]).max()
+    assert dv <= VERT_TOL, f"max vertex deviation {dv:.3e}"
+    np.testing.assert_array_equal(res.weights_px, z[f"{name}_weights_px"])
+    assert res.stop_reason == str(z[f"{name}_stop"])
+    cnt = res.state.pixel_counts
+    ref_cnt = z[f"{name}_counts"]
+    assert np.abs(cnt - ref_cnt).max() <= max(2, 1e-3 * ref_cnt.max())
+    areas = np.array([r.area() for r in res.state.mapmodel.regions])
+    assert np.allclose(areas, z[f"{name}_areas"], rtol=AREA_RTOL)
+    if field_dtype == "float64":
+        # trajectory identical to the reference: same integer pixel counts every iteration
+        assert res.state.iteration == int(z[f"{name}_iteration"])
+        assert np.array_equal(cnt, ref_cnt)
+        tr = np.array([[t.iteration, t.epsilon, t.xi] for t in res.trace])
+        np.testing.assert_allclose(tr, z[f"{name}_trace"], rtol=1e-12, atol=1e-15)
+        assert dv <= 1e-9
+
+
+def test_engine_rasterizes_its_own_state(P):
+    """Stage parity every iteration: the engine's labels equal the oracle raster of its own vertices."""
+    m = fm.config1()
+    for iters in (1, 3, 7):
+        res = P.run(m, P.StoppingCriteria(1e-300, 10**9, iters), k=8, bdv_multiplier=0.5)
+        ref = O.FlatMap.from_mapmodel(res.state.mapmodel).labels(8)
+        assert np.array_equal(res.state.labels.labels, ref)
+        assert np.array_equal(res.state.pixel_counts, O.label_counts(ref, len(m.regions)))
+
+
+def test_collapse_matches_golden(P, golden_dir):
+    z = _load(golden_dir, "collapse.npz")
+    with pytest.raises(P.RegionCollapsedError) as err:
+        P.run(fm.sliver(), P.StoppingCriteria(error_threshold=1e-6, max_iterations=400), k=5, field_dtype="float64")
+    assert err.value.region_id == str(z["region"])
+    assert err.value.iteration == int(z["iteration"])
+
+
+def test_determinism_bit_identical(P):
+    m = fm.two_region((1.0, 2.0))
+    r1 = P.run(m, P.StoppingCriteria(), k=6)
+    r2 = P.run(m, P.StoppingCriteria(), k=6)
+    assert (r1.state.mapmodel.vertex_array() == r2.state.mapmodel.vertex_array()).all()
+    assert [t.xi for t in r1.trace] == [t.xi for t in r2.trace]
+
+
+def test_analytic_ratio(P):
+    res = P.run(fm.two_region((1.0, 3.0)), P.StoppingCriteria(error_threshold=0.004), k=8)
+    assert res.stop_reason == "converged"
+    c = res.state.pixel_counts
+    assert c[1] / c[0] == pytest.approx(3.0, rel=0.01)
+
+
+def test_batch_equals_single(P):
+    m = fm.small_voronoi(seed=2, r=20, target=500)
+    stats = np.stack([m.statistics() * np.exp(np.random.default_rng(s).normal(0, 0.5, len(m.regions)))
+                      for s in range(4)])
+    mult = np.array([0.4, 0.8, 1.0, 1.6])
+    crit = P.StoppingCriteria(1e-300, 10**9, 25)
+    be = P.BatchEngine(m, stats, criteria=crit, k=7, bdv_multiplier=mult)
+    batch = be.run_all()
+    for b in range(4):
+        single = P.run(m.with_statistics(stats[b]), crit, k=7, bdv_multiplier=float(mult[b]))
+        assert np.array_equal(batch[b].state.mapmodel.vertex_array(), single.state.mapmodel.vertex_array())
+        assert np.array_equal(batch[b].state.pixel_counts, single.state.pixel_counts)
+
+
+def test_device_areas_match_shoelace(P):
+    m = fm.config1()
+    be = P.BatchEngine(m, m.statistics()[None], criteria=P.StoppingCriteria(1e-300, 10**9, 10), k=8)
+    res = be.run_all()[0]
+    host = np.array([r.area() for r in res.state.mapmodel.regions])
+    np.testing.assert_allclose(be.areas(0), host, rtol=1e-9, atol=1e-15)
+
+
+def test_step_and_evaluate_match_run(P):
+    m = fm.two_region((1.0, 3.0))
+    eng = P.CartogramEngine(m, P.StoppingCriteria(1e-300, 10**9, 3), k=6, field_dtype="float64")
+    st = eng.evaluate(eng.initial_map, 0, labels=eng._labels0)
+    for _ in range(3):
+        st = eng.step(st)
+    res = eng.run()
+    assert st.iteration == res.state.iteration == 3
+    assert np.abs(st.mapmodel.vertex_array() - res.state.mapmodel.vertex_array()).max() <= 1e-12
+    assert np.array_equal(st.pixel_counts, res.state.pixel_counts)
+
+
+# ---------------------------------------------------------------- temporal
+@pytest.mark.parametrize("strategy", ["direct", "cumulative"])
+def test_temporal_vs_golden(P, golden_dir, strategy):
+    z = _load(golden_dir, "temporal.npz")
+    m = fm.unpack_map(z)
+    ds = P.TimeSeriesDataset(m, ("t0", "t1", "t2"), z["walk"])
+    fn = P.run_direct if strategy == "direct" else P.run_cumulative
+    seq = fn(ds, P.StoppingCriteria(1e-300, 10**9, 8), k=6, field_dtype="float64")
+    for t, fr in enumerate(seq.frames):
+        assert fr.error is None
+        assert np.abs(fr.mapmodel.vertex_array() - z[f"{strategy}_{t}_xy"]).max() <= 1e-9
+        assert np.array_equal(fr.result.state.pixel_counts, z[f"{strategy}_{t}_counts"])
+        assert fr.background_mass == float(z[f"{strategy}_{t}_mb"])
+
+
+# ---------------------------------------------------------------- full-size properties
+def test_headline_size_properties(P):
+    """1024^2 / ~200k-vertex map: 20 iterations, size-independent invariants + oracle raster of the result."""
+    from paper_2604_13880_b200.synthetic import voronoi_map
+
+    m = voronoi_map(3000, seed=3, target_unique=200_000, sigma=2.0, lloyd=1)
+    res = P.run(m, P.StoppingCriteria(1e-300, 10**9, 20), k=10)
+    c = res.state.pixel_counts
+    assert c.sum() + res.state.labels.background_count() == 1 << 20
+    assert (c > 0).all()
+    eps = [t.epsilon for t in res.trace]
+    assert eps[-1] < eps[0]  # equalisation progresses
+    ref = O.FlatMap.from_mapmodel(res.state.mapmodel).labels(10)
+    assert np.array_equal(res.state.labels.labels, ref)
+    v = res.state.mapmodel.vertex_array()
+    assert v.min() >= 0.0 and v.max() <= 1.0
