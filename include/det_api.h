@@ -114,6 +114,10 @@ int det_run(det_ctx *ctx, const det_criteria *crit);
  * (benchmark helper; state continues from the last det_run/det_bench call). */
 int det_bench_iterations(det_ctx *ctx, int iters);
 int det_sync(det_ctx *ctx);
+/* Per-cartogram iteration counter (index of the next state to evaluate) and active flag. */
+int det_progress(det_ctx *ctx, int32_t *next_iter_out, int32_t *active_out);
+/* Device time of `iters` bench iterations (CUDA events on the context stream, synchronised both sides). */
+int det_time_iterations(det_ctx *ctx, int iters, float *ms_out);
 /* Per-phase device time (CUDA events on the context stream) summed over `iters`
  * eagerly launched iterations: ms_out[0]=integral images (k_sat1..3),
  * [1]=advect+crossings (k_region), [2]=paint/labels/counts (k_row), [3]=control (k_ctrl). */

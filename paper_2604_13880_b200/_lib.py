@@ -59,6 +59,8 @@ EXPORTS = {
     "det_bench_iterations": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "det_bench_kernel_times": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]),
     "det_sync": (ctypes.c_int, [ctypes.c_void_p]),
+    "det_progress": (ctypes.c_int, [ctypes.c_void_p, _c_int32_p, _c_int32_p]),
+    "det_time_iterations": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]),
     "det_get_result": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(DetResult)]),
     "det_get_vertices": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p]),
     "det_get_labels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_int32_p]),
@@ -180,6 +182,17 @@ class Context:
         out = (ctypes.c_float * 4)()
         self.check(self.lib.det_bench_kernel_times(self.h, int(iters), out))
         return list(out)
+
+    def time_iterations(self, iters):
+        ms = ctypes.c_float(0.0)
+        self.check(self.lib.det_time_iterations(self.h, int(iters), ctypes.byref(ms)))
+        return float(ms.value)
+
+    def progress(self):
+        it = np.empty(self.B, dtype=np.int32)
+        ac = np.empty(self.B, dtype=np.int32)
+        self.check(self.lib.det_progress(self.h, _p(it, ctypes.c_int32), _p(ac, ctypes.c_int32)))
+        return it, ac
 
     def sync(self):
         self.check(self.lib.det_sync(self.h))

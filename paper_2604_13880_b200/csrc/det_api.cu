@@ -532,7 +532,7 @@ static int run_once(det_ctx* ctx, const det_criteria* crit, bool* overflow) {
     const int B = ctx->B;
     const int tc = crit->max_iterations + 1;
     if (tc > ctx->trace_cap || ctx->trace.n < (size_t)B * ctx->trace_cap * 4) {
-        ctx->trace_cap = std::max(tc, ctx->trace_cap);
+        ctx->trace_cap = std::max(std::max(tc, ctx->trace_cap), 1024);
         CK(ctx->trace.alloc((size_t)B * ctx->trace_cap * 4));
         invalidate_graph(ctx);
     }
@@ -666,6 +666,39 @@ int det_bench_kernel_times(det_ctx* ctx, int iters, float* ms_out) {
         }
     }
     for (int i = 0; i < 5; ++i) cudaEventDestroy(ev[i]);
+    return DET_OK;
+}
+
+int det_time_iterations(det_ctx* ctx, int iters, float* ms_out) {
+    if (!ctx || !ms_out) return DET_E_ARG;
+    cudaSetDevice(ctx->device);
+    int rc = det_bench_iterations(ctx, 0);  // enter bench mode (criteria that never stop)
+    if (rc) return rc;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    CK(cudaStreamSynchronize(ctx->stream));
+    CK(cudaEventRecord(e0, ctx->stream));
+    rc = det_bench_iterations(ctx, iters);
+    if (rc) return rc;
+    CK(cudaEventRecord(e1, ctx->stream));
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(ms_out, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return DET_OK;
+}
+
+int det_progress(det_ctx* ctx, int32_t* next_iter_out, int32_t* active_out) {
+    if (!ctx || ctx->B == 0) return fail(ctx, DET_E_STATE, "no batch");
+    cudaSetDevice(ctx->device);
+    std::vector<Carto> hs(ctx->B);
+    CK(cudaMemcpyAsync(hs.data(), ctx->st.p, ctx->B * sizeof(Carto), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int b = 0; b < ctx->B; ++b) {
+        if (next_iter_out) next_iter_out[b] = hs[b].next_iter;
+        if (active_out) active_out[b] = hs[b].active;
+    }
     return DET_OK;
 }
 

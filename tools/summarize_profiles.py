@@ -1,0 +1,45 @@
+"""Summarise a gpurun ncu launch list (+ optional --set full reports) into profiles/<tag>.md."""
+import collections, csv, subprocess, sys, os
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hdr, agg = None, collections.defaultdict(list)
+    for r in rows:
+        if r and r[0] == "ID":
+            hdr = r
+            continue
+        if hdr and len(r) == len(hdr):
+            d = dict(zip(hdr, r))
+            if d["Metric Name"] == "gpu__time_duration.sum":
+                agg[d["Kernel Name"].split("(")[0]].append(float(d["Metric Value"]))
+    return agg
+
+WANT = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__grid_size",
+        "launch__block_size", "lts__t_sector_hit_rate.pct"]
+
+def full(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h, units = rows[0], rows[1]
+    res = []
+    for r in rows[2:]:
+        res.append({w: (r[h.index(w)], units[h.index(w)]) for w in WANT if w in h} | {"name": r[h.index("Kernel Name")]})
+    return res
+
+tag, launch_csv = sys.argv[1], sys.argv[2]
+reps = sys.argv[3:]
+lines = [f"# ncu summary {tag}", "", "## Launch list (gpu__time_duration.sum, --clock-control none, serialised)", "",
+         "| kernel | launches | mean (us) | share |", "|---|---|---|---|"]
+agg = launches(launch_csv)
+tot = sum(sum(v) for v in agg.values())
+for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
+    lines.append(f"| `{k}` | {len(v)} | {sum(v)/len(v)/1e3:.1f} | {sum(v)/tot:.3f} |")
+for rep in reps:
+    lines += ["", f"## `--set full`: {os.path.basename(rep)}", ""]
+    for d in full(rep):
+        lines.append(f"- **{d.pop('name')[:80]}**")
+        for k, (v, u) in d.items():
+            lines.append(f"  - {k}: {v} {u}")
+print("\n".join(lines))
