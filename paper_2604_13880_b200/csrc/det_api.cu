@@ -56,13 +56,13 @@ struct det_ctx {
     // topology
     int R = 0, n_rows = 0, n_uniq = 0, n_rings = 0;
     std::vector<int> h_row_uniq, h_ring_start, h_region_ring0;
-    std::vector<double> h_xy_uniq;
+    std::vector<double> h_xy_uniq, h_xy_rows;
     DVec<int> region_row0, row_uniq, row_next, region_rank, rank_region, ring_start, region_ring0;
     DVec<uint8_t> row_owner;
     // batch
     int B = 0, cap = 64, nb = 0, trace_cap = 0;
-    DVec<double2> pos_init, pos0, pos1, best, rowpos;
-    DVec<int> labels, cnt_acc, cnt_state, rowcnt, maxspan;
+    DVec<double2> pos_init, pos0, pos1, best;
+    DVec<int> labels, cnt_acc, cnt_state, rowcnt, maxspan, rowdone;
     DVec<unsigned long long> spans;
     DVec<double> lut, stats, weights, rerr, cs, dgc, adc, rt, csX, dgXc, adSc, csT, dgT, adT, rowfull, trace;
     DVec<char> uf;
@@ -70,7 +70,7 @@ struct det_ctx {
     DVec<Params> prm;
     std::vector<Params> h_prm;
     std::vector<Carto> h_st;
-    bool params_set = false, ran = false, bench_mode = false;
+    bool params_set = false, ran = false, bench_mode = false, h_fixed = false;
     // stage buffers
     DVec<double> dense, ch8, uf64, pts_in, pts_out;
     DVec<unsigned long long> clampbuf;
@@ -115,9 +115,9 @@ static Bufs make_bufs(det_ctx* c) {
     memset(&d, 0, sizeof(d));
     d.B = c->B; d.n = c->n; d.k = c->k; d.cap = c->cap; d.H = c->H; d.nb = c->nb;
     d.nn = (size_t)c->n * c->n;
-    d.pos0 = c->pos0.p; d.pos1 = c->pos1.p; d.best = c->best.p; d.rowpos = c->rowpos.p;
+    d.pos0 = c->pos0.p; d.pos1 = c->pos1.p; d.best = c->best.p;
     d.labels = c->labels.p; d.cnt_acc = c->cnt_acc.p; d.cnt_state = c->cnt_state.p;
-    d.spans = c->spans.p; d.rowcnt = c->rowcnt.p; d.maxspan = c->maxspan.p;
+    d.spans = c->spans.p; d.rowcnt = c->rowcnt.p; d.maxspan = c->maxspan.p; d.rowdone = c->rowdone.p;
     d.lut = c->lut.p; d.stats = c->stats.p; d.weights = c->weights.p; d.rerr = c->rerr.p;
     d.uf = c->uf.p;
     d.cs = c->cs.p; d.dgc = c->dgc.p; d.adc = c->adc.p; d.rt = c->rt.p;
@@ -133,8 +133,14 @@ static void launch_sat_cpt(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
                            bool u64, int B) {
     const int n = c->n, nt = nthreads_for(n);
     const dim3 gb(c->nb, B);
-    if (src == SRC_LABELS) k_sat1<CPT, SRC_LABELS><<<gb, nt, 0, c->stream>>>(T, D, S, gate);
-    else k_sat1<CPT, SRC_DENSE><<<gb, nt, 0, c->stream>>>(T, D, S, gate);
+    const size_t smem1 = (size_t)2 * (n + c->H - 1) * sizeof(double);
+    if (src == SRC_LABELS) {
+        cudaFuncSetAttribute(k_sat1<CPT, SRC_LABELS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+        k_sat1<CPT, SRC_LABELS><<<gb, nt, smem1, c->stream>>>(T, D, S, gate);
+    } else {
+        cudaFuncSetAttribute(k_sat1<CPT, SRC_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+        k_sat1<CPT, SRC_DENSE><<<gb, nt, smem1, c->stream>>>(T, D, S, gate);
+    }
     const int lanes = n + 2 * (2 * n - 1);
     const int G = std::min(8, c->nb);
     k_sat2<<<dim3((lanes + 31) / 32 + 1, B), 32 * G, 0, c->stream>>>(D, gate);
@@ -168,13 +174,20 @@ static void launch_sat(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S
 }
 
 static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, int gate, int src) {
-    const dim3 g(c->R, c->B);
-    if (c->f64) k_region<double><<<g, REG_THREADS, 0, c->stream>>>(T, D, mode, gate, src);
-    else k_region<float><<<g, REG_THREADS, 0, c->stream>>>(T, D, mode, gate, src);
+    const dim3 g((c->R + RW_WARPS - 1) / RW_WARPS, c->B);
+    if (c->f64) k_region<double><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
+    else k_region<float><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
 }
 
-static void launch_row(det_ctx* c, const Topo& T, const Bufs& D, int gate) {
-    k_row<<<dim3(c->n, c->B), ROW_THREADS, (size_t)c->n * sizeof(uint32_t), c->stream>>>(T, D, gate);
+// ctrl_mode: -1 raster only, 0 loop evaluation, 1 final (best-state) evaluation
+static void launch_row(det_ctx* c, const Topo& T, const Bufs& D, int gate, int ctrl_mode) {
+    // one warp per texture row; up to 8 rows per CTA within a 64 KB label-row budget
+    int rpc = 8;
+    while (rpc > 1 && (size_t)rpc * c->n * sizeof(uint32_t) > 64 * 1024) rpc >>= 1;
+    rpc = std::min(rpc, c->n);
+    const size_t smem = (size_t)rpc * c->n * sizeof(uint32_t);
+    cudaFuncSetAttribute(k_row, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_row<<<dim3((c->n + rpc - 1) / rpc, c->B), rpc * 32, smem, c->stream>>>(T, D, gate, ctrl_mode);
 }
 
 static void enqueue_iteration(det_ctx* c) {
@@ -184,8 +197,7 @@ static void enqueue_iteration(det_ctx* c) {
     memset(&S, 0, sizeof(S));
     launch_sat(c, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, c->f64 != 0, c->B);
     launch_region(c, T, D, M_ADVECT | M_RASTER, G_ACTIVE, 0);
-    launch_row(c, T, D, G_ACTIVE);
-    k_ctrl<<<c->B, CTRL_THREADS, 0, c->stream>>>(T, D, 0, G_ACTIVE);
+    launch_row(c, T, D, G_ACTIVE, 0);
 }
 
 static void invalidate_graph(det_ctx* c) {
@@ -226,7 +238,7 @@ static int alloc_sat(det_ctx* ctx, int B) {
     CK(ctx->rt.alloc(B * n));
     CK(ctx->csX.alloc(B * nb * n));
     CK(ctx->dgXc.alloc(B * nb * n));
-    CK(ctx->adSc.alloc(B * nb * L));
+    CK(ctx->adSc.alloc(B * nb * (L + 1)));
     CK(ctx->csT.alloc(B * n));
     CK(ctx->dgT.alloc(B * M));
     CK(ctx->adT.alloc(B * M));
@@ -234,18 +246,30 @@ static int alloc_sat(det_ctx* ctx, int B) {
     return DET_OK;
 }
 
+static int auto_band_height(int n, int B) {
+    // enough band CTAs to fill the 148 SMs twice over, but tall bands amortise the carries
+    int h = 8;
+    while (h < 64 && (long long)(n / (2 * h)) * B >= 2 * 148) h *= 2;
+    return std::min(h, n);
+}
+
 static int alloc_batch(det_ctx* ctx, int B) {
     const size_t nn = (size_t)ctx->n * ctx->n;
     ctx->B = B;
-    CK(ctx->pos_init.alloc((size_t)B * ctx->n_uniq));
-    CK(ctx->pos0.alloc((size_t)B * ctx->n_uniq));
-    CK(ctx->pos1.alloc((size_t)B * ctx->n_uniq));
-    CK(ctx->best.alloc((size_t)B * ctx->n_uniq));
-    CK(ctx->rowpos.alloc((size_t)B * ctx->n_rows));
+    if (!ctx->h_fixed) {
+        ctx->H = auto_band_height(ctx->n, B);
+        ctx->nb = ctx->n / ctx->H;
+    }
+    CK(ctx->pos_init.alloc((size_t)B * ctx->n_rows));
+    CK(ctx->pos0.alloc((size_t)B * ctx->n_rows));
+    CK(ctx->pos1.alloc((size_t)B * ctx->n_rows));
+    CK(ctx->best.alloc((size_t)B * ctx->n_rows));
     CK(ctx->labels.alloc((size_t)B * nn));
     CK(ctx->cnt_acc.alloc((size_t)B * (ctx->R + 1)));
     CK(ctx->cnt_state.alloc((size_t)B * (ctx->R + 1)));
     CK(ctx->maxspan.alloc((size_t)B));
+    CK(ctx->rowdone.alloc((size_t)B));
+    CK(cudaMemsetAsync(ctx->rowdone.p, 0, (size_t)B * sizeof(int), ctx->stream));
     CK(ctx->lut.alloc((size_t)B * (ctx->R + 1)));
     CK(ctx->stats.alloc((size_t)B * ctx->R));
     CK(ctx->weights.alloc((size_t)B * ctx->R));
@@ -270,14 +294,14 @@ static int alloc_batch(det_ctx* ctx, int B) {
 // capacity until no row overflows.  Leaves the counts in cnt_acc.
 static int raster_start(det_ctx* ctx) {
     for (int attempt = 0; attempt < 8; ++attempt) {
-        CK(cudaMemcpyAsync(ctx->pos0.p, ctx->pos_init.p, (size_t)ctx->B * ctx->n_uniq * sizeof(double2),
+        CK(cudaMemcpyAsync(ctx->pos0.p, ctx->pos_init.p, (size_t)ctx->B * ctx->n_rows * sizeof(double2),
                            cudaMemcpyDeviceToDevice, ctx->stream));
         const Topo T = make_topo(ctx);
         const Bufs D = make_bufs(ctx);
         k_init_state<<<(ctx->B + 127) / 128, 128, 0, ctx->stream>>>(D);
         CK(cudaMemsetAsync(ctx->cnt_acc.p, 0, (size_t)ctx->B * (ctx->R + 1) * sizeof(int), ctx->stream));
         launch_region(ctx, T, D, M_RASTER, G_ALWAYS, 0);
-        launch_row(ctx, T, D, G_ALWAYS);
+        launch_row(ctx, T, D, G_ALWAYS, -1);
         CK(cudaGetLastError());
         std::vector<Carto> hs(ctx->B);
         std::vector<int> ms(ctx->B);
@@ -362,6 +386,7 @@ int det_set_band_height(det_ctx* ctx, int h) {
     cudaSetDevice(ctx->device);
     ctx->H = h;
     ctx->nb = ctx->n / h;
+    ctx->h_fixed = true;
     invalidate_graph(ctx);
     if (ctx->B > 0) return alloc_sat(ctx, ctx->B);
     return DET_OK;
@@ -427,6 +452,7 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
     ctx->n_uniq = (int)(xyu.size() / 2);
     ctx->h_row_uniq = uniq;
     ctx->h_xy_uniq = xyu;
+    ctx->h_xy_rows.assign(xy, xy + (size_t)n_rows * 2);
     ctx->h_ring_start.assign(ring_start, ring_start + n_rings + 1);
     ctx->h_region_ring0 = reg_ring0;
     CK(ctx->region_row0.alloc(n_regions + 1));
@@ -459,25 +485,10 @@ int det_set_batch(det_ctx* ctx, int batch, const double* xy, const double* stats
         int rc = alloc_batch(ctx, batch);
         if (rc) return rc;
     }
-    std::vector<double> pu((size_t)batch * ctx->n_uniq * 2);
+    std::vector<double> pu((size_t)batch * ctx->n_rows * 2);
     for (int b = 0; b < batch; ++b) {
-        double* dst = pu.data() + (size_t)b * ctx->n_uniq * 2;
-        if (!xy) {
-            memcpy(dst, ctx->h_xy_uniq.data(), ctx->h_xy_uniq.size() * sizeof(double));
-            continue;
-        }
-        const double* src = xy + (size_t)b * ctx->n_rows * 2;
-        std::vector<uint8_t> seen(ctx->n_uniq, 0);
-        for (int v = 0; v < ctx->n_rows; ++v) {
-            const int u = ctx->h_row_uniq[v];
-            if (!seen[u]) {
-                dst[2 * u] = src[2 * v];
-                dst[2 * u + 1] = src[2 * v + 1];
-                seen[u] = 1;
-            } else if (memcmp(dst + 2 * u, src + 2 * v, 16) != 0) {
-                return fail(ctx, DET_E_ARG, "vertex rows break the loaded topology's shared vertices; reload the map");
-            }
-        }
+        double* dst = pu.data() + (size_t)b * ctx->n_rows * 2;
+        memcpy(dst, xy ? xy + (size_t)b * ctx->n_rows * 2 : ctx->h_xy_rows.data(), (size_t)ctx->n_rows * 2 * sizeof(double));
     }
     CK(cudaMemcpyAsync(ctx->pos_init.p, pu.data(), pu.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->stats.p, stats, (size_t)batch * ctx->R * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
@@ -578,8 +589,7 @@ static int run_once(det_ctx* ctx, const det_criteria* crit, bool* overflow) {
         const Topo T = make_topo(ctx);
         const Bufs D = make_bufs(ctx);
         launch_region(ctx, T, D, M_RASTER, G_FINAL, 2);
-        launch_row(ctx, T, D, G_FINAL);
-        k_ctrl<<<B, CTRL_THREADS, 0, ctx->stream>>>(T, D, 1, G_FINAL);
+        launch_row(ctx, T, D, G_FINAL, 1);
         CK(cudaGetLastError());
     }
     CK(cudaMemcpyAsync(ctx->h_st.data(), ctx->st.p, B * sizeof(Carto), cudaMemcpyDeviceToHost, ctx->stream));
@@ -654,9 +664,8 @@ int det_bench_kernel_times(det_ctx* ctx, int iters, float* ms_out) {
         CK(cudaEventRecord(ev[1], ctx->stream));
         launch_region(ctx, T, D, M_ADVECT | M_RASTER, G_ACTIVE, 0);
         CK(cudaEventRecord(ev[2], ctx->stream));
-        launch_row(ctx, T, D, G_ACTIVE);
+        launch_row(ctx, T, D, G_ACTIVE, 0);  // includes the control step (last CTA)
         CK(cudaEventRecord(ev[3], ctx->stream));
-        k_ctrl<<<ctx->B, CTRL_THREADS, 0, ctx->stream>>>(T, D, 0, G_ACTIVE);
         CK(cudaEventRecord(ev[4], ctx->stream));
         CK(cudaEventSynchronize(ev[4]));
         for (int q = 0; q < 4; ++q) {
@@ -731,26 +740,18 @@ static int result_src(det_ctx* ctx, int b) {
     return c.res_iter & 1;
 }
 
-static int gather_rows(det_ctx* ctx, int b) {
-    const int src = ctx->ran ? result_src(ctx, b) : 0;
-    if (!ctx->ran) {
-        CK(cudaMemcpyAsync(ctx->pos0.p + (size_t)b * ctx->n_uniq, ctx->pos_init.p + (size_t)b * ctx->n_uniq,
-                           ctx->n_uniq * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
-    }
-    const Topo T = make_topo(ctx);
-    const Bufs D = make_bufs(ctx);
-    k_gather_rows<<<(ctx->n_rows + 255) / 256, 256, 0, ctx->stream>>>(T, D, b, src);
-    CK(cudaGetLastError());
-    return DET_OK;
+// Device pointer to cartogram b's rows of the returned state (or the start rows before a run).
+static const double2* state_rows(det_ctx* ctx, int b) {
+    const size_t off = (size_t)b * ctx->n_rows;
+    if (!ctx->ran) return ctx->pos_init.p + off;
+    const int src = result_src(ctx, b);
+    return (src == 2 ? ctx->best.p : (src == 1 ? ctx->pos1.p : ctx->pos0.p)) + off;
 }
 
 int det_get_vertices(det_ctx* ctx, int b, double* xy_out) {
     if (!ctx || !xy_out || b < 0 || b >= ctx->B) return fail(ctx, DET_E_ARG, "bad arguments");
     cudaSetDevice(ctx->device);
-    int rc = gather_rows(ctx, b);
-    if (rc) return rc;
-    CK(cudaMemcpyAsync(xy_out, ctx->rowpos.p + (size_t)b * ctx->n_rows, ctx->n_rows * sizeof(double2),
-                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(xy_out, state_rows(ctx, b), ctx->n_rows * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     return DET_OK;
 }
@@ -792,13 +793,10 @@ int det_get_trace(det_ctx* ctx, int b, double* out) {
 int det_get_areas(det_ctx* ctx, int b, double* out) {
     if (!ctx || !out || b < 0 || b >= ctx->B) return fail(ctx, DET_E_ARG, "bad arguments");
     cudaSetDevice(ctx->device);
-    int rc = gather_rows(ctx, b);
-    if (rc) return rc;
     DVec<double> tmp;
     CK(tmp.alloc(ctx->R));
     const Topo T = make_topo(ctx);
-    const Bufs D = make_bufs(ctx);
-    k_areas<<<ctx->R, 128, 0, ctx->stream>>>(T, D, ctx->ring_start.p, ctx->region_ring0.p, b, tmp.p);
+    k_areas<<<ctx->R, 128, 0, ctx->stream>>>(T, state_rows(ctx, b), ctx->ring_start.p, ctx->region_ring0.p, tmp.p);
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(out, tmp.p, ctx->R * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));

@@ -63,13 +63,13 @@ struct Bufs {
     double2* pos0;
     double2* pos1;
     double2* best;
-    double2* rowpos;
     int* labels;
     int* cnt_acc;
     int* cnt_state;
     unsigned long long* spans;
     int* rowcnt;
     int* maxspan;
+    int* rowdone;     // B: k_row CTAs finished this iteration (last one runs the control step)
     double* lut;
     const double* stats;
     const double* weights;

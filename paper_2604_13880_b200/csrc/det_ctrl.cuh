@@ -1,7 +1,8 @@
-// Per-cartogram control kernel (sm_100a): evaluate + stopping rule + next density LUT.
+// Per-cartogram control step (sm_100a): evaluate + stopping rule + next density LUT.
 //
-// One CTA per cartogram.  Reads the pixel counts accumulated by k_row and does,
-// on the device, what engine.py does on the host between two steps:
+// Runs in the LAST k_row CTA of each cartogram (no separate launch).  It does, on
+// the device, what engine.py does on the host between two steps:
+//   * background count = n^2 - sum of region counts (raster.py:114-118);
 //   * collapse check, first zero-count region (engine.py:147-150);
 //   * e_r = |o-w|/max(o,w), epsilon = mean, xi = max (engine.py:83-85,151);
 //   * trace row (iteration, epsilon, xi, millis) (engine.py:189-195);
@@ -34,37 +35,36 @@ __global__ void k_reactivate(Bufs D) {
     if (b >= D.B) return;
     Carto* c = D.st + b;
     if (c->stop == S_COLLAPSED || c->stop == S_BDV || c->stop == S_NEGINDEX) return;
-    if (c->stop != S_RUNNING) c->next_iter = c->res_iter + 1;  // its LUT was built by k_ctrl
+    if (c->stop != S_RUNNING) c->next_iter = c->res_iter + 1;  // its LUT was built by the control step
     c->active = 1;
     c->stop = S_RUNNING;
     c->final_pending = 0;
 }
 
-// cmode 0: loop evaluation of state next_iter; cmode 1: final re-evaluation of the best state.
-__global__ void __launch_bounds__(CTRL_THREADS) k_ctrl(Topo T, Bufs D, int cmode, int gate) {
+// cmode -1: background count only; 0: loop evaluation of state next_iter; 1: final re-evaluation
+// of the best state.  Executed by one whole CTA (blockDim multiple of 32).
+__device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
     __shared__ double s_red[33];
+    __shared__ long long s_redl[33];
     __shared__ int s_redi[33];
-    __shared__ int s_nbg, s_cont;
+    __shared__ int s_cont;
     __shared__ double s_bdv;
-    const int b = blockIdx.x, t = threadIdx.x, R = T.R;
+    const int t = threadIdx.x, R = T.R;
     Carto* st = D.st + b;
-    if (!gate_open(st, gate)) return;
     int* acc = D.cnt_acc + (size_t)b * (R + 1);
     int* sc = D.cnt_state + (size_t)b * (R + 1);
     const double* wt = D.weights + (size_t)b * R;
     const double* s = D.stats + (size_t)b * R;
     double* er = D.rerr + (size_t)b * R;
-    if (t == 0) {
-        s_nbg = acc[R];
-        sc[R] = s_nbg;
-        acc[R] = 0;
-    }
+    const bool eval = cmode >= 0;
     int fz = INT_MAX;
+    long long osum = 0;
     double es = 0.0, em = -INFINITY;
     for (int r = t; r < R; r += blockDim.x) {
-        const int o = acc[r];
+        const int o = __ldcg(acc + r);
+        osum += o;
+        if (!eval) continue;
         sc[r] = o;
-        acc[r] = 0;
         if (o == 0) fz = min(fz, r);
         const double od = (double)o, w = wt[r];
         const double e = fabs(od - w) / fmax(od, w);
@@ -72,10 +72,16 @@ __global__ void __launch_bounds__(CTRL_THREADS) k_ctrl(Topo T, Bufs D, int cmode
         es += e;
         em = fmax(em, e);
     }
+    osum = block_reduce<0, long long>(osum, 0ll, s_redl);
+    const int nbg = (int)((long long)D.nn - osum);
+    if (t == 0) {
+        acc[R] = nbg;
+        if (eval) sc[R] = nbg;
+    }
+    if (!eval) return;
     fz = block_reduce<1, int>(fz, INT_MAX, s_redi);
     es = block_reduce<0, double>(es, 0.0, s_red);
     em = block_reduce<2, double>(em, -INFINITY, s_red);
-    const int nbg = s_nbg;
     const Params P = D.prm[b];
     const int it = cmode == 0 ? st->next_iter : st->best_iter;
     if (t == 0) {
@@ -162,6 +168,12 @@ __global__ void __launch_bounds__(CTRL_THREADS) k_ctrl(Topo T, Bufs D, int cmode
         lut[R] = m * bdv / C - 1.0;
         st->C = C;
     }
+}
+
+// Host-driven control step (evaluation of the start state): one CTA per cartogram.
+__global__ void __launch_bounds__(CTRL_THREADS) k_ctrl(Topo T, Bufs D, int cmode, int gate) {
+    if (!gate_open(D.st + blockIdx.x, gate)) return;
+    ctrl_body(T, D, blockIdx.x, cmode);
 }
 
 }  // namespace det

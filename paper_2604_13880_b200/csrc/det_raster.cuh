@@ -1,90 +1,122 @@
 // Advection + rasterisation kernels (sm_100a).
 //
-// k_region : one CTA per (region, cartogram).  Fuses
+// Vertex positions live per ring row (the order of MapModel.vertex_array(),
+// geomodel.py:128-130), so every region's rows are one contiguous, coalesced
+// range.  Rows that duplicate a shared vertex evolve bit-identically (same input,
+// same arithmetic), exactly as in the reference.
+//
+// k_region : one WARP per (region, cartogram), no CTA-wide barriers.  Fuses
 //            * advect (displacement.py:209-238): bilinear sample of the u field at
-//              every vertex row of the region, clamp to [0,1]^2, clamp count;
+//              every vertex row, clamp to [0,1]^2, clamp count;
 //            * the region's bounding-box crop (raster.py:70-78);
 //            * even-odd crossing toggles of every ring edge (raster.py:23-61) with the
 //              reference's exact float64 op order (explicit _rn intrinsics, no FMA);
 //            * the crop flattening of _submask incl. the absorber column and the
 //              negative-index case (raster.py:79-90);
-//            * per-row toggle sort (smem bitonic) and even-odd pairing into spans.
-//            Spans (start, end, rank) go to per-row buckets in HBM.
-// k_row    : one CTA per (texture row, cartogram).  Paints spans with smem atomicMin
-//            on the region rank (ascending-id first-writer-wins, raster.py:142-146),
-//            writes the label row (BACKGROUND=-1) and accumulates per-region pixel
-//            counts + background count from run ends (raster.py:110-118).
+//            * a counting sort of the toggles by row and even-odd pairing into spans
+//              (start, end, rank) appended to per-row buckets in HBM;
+//            * the region's provisional pixel count = sum of its span lengths.
+// k_row    : one WARP per (texture row, cartogram).  Paints spans with smem atomicMin
+//            on the region rank (ascending-id first-writer-wins, raster.py:142-146);
+//            every lost claim decrements the loser's count, so counts are exact
+//            (raster.py:110-118); writes the label row (BACKGROUND=-1).  The last CTA
+//            of a cartogram derives the background count and runs the control step
+//            (det_ctrl.cuh) -- no separate launch.
 #pragma once
 #include "det_common.cuh"
+#include "det_ctrl.cuh"
 
 namespace det {
 
-__device__ __forceinline__ void bitonic_sort_u32(uint32_t* a, int P) {
-    for (int k = 2; k <= P; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < P; i += blockDim.x) {
-                const int ixj = i ^ j;
-                if (ixj > i) {
-                    const uint32_t x = a[i], y = a[ixj];
-                    const bool up = (i & k) == 0;
-                    if ((x > y) == up) {
-                        a[i] = y;
-                        a[ixj] = x;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-
-__device__ __forceinline__ int lower_bound_u32(const uint32_t* a, int n, uint32_t key) {
-    int lo = 0, hi = n;
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (a[mid] < key) lo = mid + 1; else hi = mid;
-    }
-    return lo;
-}
+constexpr int RW_WARPS = 4;      // warps (regions) per k_region block
+constexpr int RW_ROWCAP = 384;   // vertex rows kept in smem per warp
+constexpr int RW_TCAP = 512;     // toggles per warp window
+constexpr int RW_WROWS = 128;    // texture rows per warp window
+constexpr int RW_UNROLL = 4;     // vertex rows in flight per lane (latency hiding)
 
 template <typename UT>
-__device__ __forceinline__ double2 sample_field(const UT* __restrict__ uf, int n, double px, double py) {
-    // displacement.py:211-226
+__device__ __forceinline__ void field_texels(const UT* __restrict__ uf, int n, double px, double py, double (&t)[8],
+                                             double& fx, double& fy) {
+    // displacement.py:211-219: g = p*n - 0.5, i0 = clip(floor(g), 0, n-2), f = clip(g - i0, 0, 1)
     const double nd = (double)n;
     const double gx = px * nd - 0.5, gy = py * nd - 0.5;
     const int ix = clampi((long long)floor(gx), 0, n - 2);
     const int iy = clampi((long long)floor(gy), 0, n - 2);
-    const double fx = fmin(fmax(gx - (double)ix, 0.0), 1.0);
-    const double fy = fmin(fmax(gy - (double)iy, 0.0), 1.0);
+    fx = fmin(fmax(gx - (double)ix, 0.0), 1.0);
+    fy = fmin(fmax(gy - (double)iy, 0.0), 1.0);
     const size_t o0 = ((size_t)iy * n + ix) * 2, o1 = o0 + (size_t)n * 2;
-    const double u00x = (double)uf[o0], u00y = (double)uf[o0 + 1];
-    const double u10x = (double)uf[o0 + 2], u10y = (double)uf[o0 + 3];
-    const double u01x = (double)uf[o1], u01y = (double)uf[o1 + 1];
-    const double u11x = (double)uf[o1 + 2], u11y = (double)uf[o1 + 3];
+    t[0] = (double)__ldg(uf + o0); t[1] = (double)__ldg(uf + o0 + 1);
+    t[2] = (double)__ldg(uf + o0 + 2); t[3] = (double)__ldg(uf + o0 + 3);
+    t[4] = (double)__ldg(uf + o1); t[5] = (double)__ldg(uf + o1 + 1);
+    t[6] = (double)__ldg(uf + o1 + 2); t[7] = (double)__ldg(uf + o1 + 3);
+}
+
+__device__ __forceinline__ double2 blend(const double (&t)[8], double fx, double fy) {
+    // displacement.py:220-226
     const double gxm = 1.0 - fx, gym = 1.0 - fy;
     double2 s;
-    s.x = u00x * gxm * gym + u10x * fx * gym + u01x * gxm * fy + u11x * fx * fy;
-    s.y = u00y * gxm * gym + u10y * fx * gym + u01y * gxm * fy + u11y * fx * fy;
+    s.x = t[0] * gxm * gym + t[2] * fx * gym + t[4] * gxm * fy + t[6] * fx * fy;
+    s.y = t[1] * gxm * gym + t[3] * fx * gym + t[5] * gxm * fy + t[7] * fx * fy;
     return s;
 }
 
 template <typename UT>
-__global__ void __launch_bounds__(REG_THREADS) k_region(Topo T, Bufs D, int mode, int gate, int src) {
-    __shared__ uint32_t s_keys[TOG_CAP];
-    __shared__ double s_red[33];
-    __shared__ unsigned long long s_redu[33];
-    __shared__ int s_tot;
+__device__ __forceinline__ double2 sample_field(const UT* __restrict__ uf, int n, double px, double py) {
+    double t[8], fx, fy;
+    field_texels<UT>(uf, n, px, py, t, fx, fy);
+    return blend(t, fx, fy);
+}
 
-    const int r = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+template <typename T>
+__device__ __forceinline__ T warp_allmin(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_allmax(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+    return v;
+}
+
+__device__ __forceinline__ int warp_excl_scan_int(int v, int lane, int* total) {
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, x, o);
+        if (lane >= o) x += y;
+    }
+    *total = __shfl_sync(FULL, x, 31);
+    return x - v;
+}
+
+template <typename UT>
+__global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mode, int gate, int src) {
+    __shared__ double2 s_pos[RW_WARPS][RW_ROWCAP];
+    __shared__ uint32_t s_key[RW_WARPS][RW_TCAP];
+    __shared__ uint16_t s_col[RW_WARPS][RW_TCAP];
+    __shared__ int s_rc[RW_WARPS][RW_WROWS + 1];
+    __shared__ int s_tot[RW_WARPS];
+
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int r = blockIdx.x * RW_WARPS + wid, b = blockIdx.y;
+    if (r >= T.R) return;
     Carto* st = D.st + b;
     if (!gate_open(st, gate)) return;
     const int n = D.n;
     const double nd = (double)n;
     const int row0 = T.region_row0[r], row1 = T.region_row0[r + 1];
-    const size_t ub = (size_t)b * T.n_uniq;
+    const int nrows = row1 - row0;
+    const size_t ub = (size_t)b * T.n_rows;
+    const bool in_smem = nrows <= RW_ROWCAP;
+    double2* spos = s_pos[wid];
+    uint32_t* keys = s_key[wid];
+    uint16_t* colb = s_col[wid];
+    int* rc = s_rc[wid];
 
-    const double2* pin;
-    double2* pout = nullptr;
+    const double2* __restrict__ pin;
+    double2* __restrict__ pout = nullptr;
     bool bestcopy = false;
     if (mode & M_ADVECT) {
         const int cur = st->next_iter - 1;
@@ -94,70 +126,97 @@ __global__ void __launch_bounds__(REG_THREADS) k_region(Topo T, Bufs D, int mode
     } else {
         pin = (src == 0 ? D.pos0 : (src == 1 ? D.pos1 : D.best)) + ub;
     }
-    double2* rowpos = D.rowpos + (size_t)b * T.n_rows;
+    const double2* gpos = (mode & M_ADVECT) ? pout : pin;  // row positions for huge regions
     const UT* uf = reinterpret_cast<const UT*>(D.uf) + (size_t)b * D.nn * 2;
 
-    // ---- phase A: advect every vertex row of the region, bbox, clamp count ----
+    // ---- phase A: advect every vertex row of the region (RW_UNROLL rows in flight per lane) ----
     double xmn = INFINITY, xmx = -INFINITY, ymn = INFINITY, ymx = -INFINITY;
-    unsigned long long ncl = 0;
-    for (int v = row0 + tid; v < row1; v += blockDim.x) {
-        const int u = T.row_uniq[v];
-        const double2 p = pin[u];
-        double2 q = p;
-        if (mode & M_ADVECT) {
-            const double2 s = sample_field<UT>(uf, n, p.x, p.y);
-            const double mx = p.x + s.x, my = p.y + s.y;
-            const double cx = fmin(fmax(mx, 0.0), 1.0), cy = fmin(fmax(my, 0.0), 1.0);
-            ncl += (cx != mx) + (cy != my);
-            q = make_double2(cx, cy);
-            if (T.row_owner[v]) {
-                pout[u] = q;
-                if (bestcopy) D.best[ub + u] = p;
-            }
+    int ncl = 0;
+    for (int base = row0; base < row1; base += 32 * RW_UNROLL) {
+        double2 p[RW_UNROLL];
+#pragma unroll
+        for (int q = 0; q < RW_UNROLL; ++q) {
+            const int v = base + q * 32 + lane;
+            p[q] = v < row1 ? pin[v] : make_double2(0.5, 0.5);
         }
-        rowpos[v] = q;
-        xmn = fmin(xmn, q.x); xmx = fmax(xmx, q.x);
-        ymn = fmin(ymn, q.y); ymx = fmax(ymx, q.y);
+        double2 nq[RW_UNROLL];
+        if (mode & M_ADVECT) {
+            double t[RW_UNROLL][8], fx[RW_UNROLL], fy[RW_UNROLL];
+#pragma unroll
+            for (int q = 0; q < RW_UNROLL; ++q) field_texels<UT>(uf, n, p[q].x, p[q].y, t[q], fx[q], fy[q]);
+#pragma unroll
+            for (int q = 0; q < RW_UNROLL; ++q) {
+                const double2 s = blend(t[q], fx[q], fy[q]);
+                const double mx = p[q].x + s.x, my = p[q].y + s.y;
+                const double cx = fmin(fmax(mx, 0.0), 1.0), cy = fmin(fmax(my, 0.0), 1.0);
+                const int v = base + q * 32 + lane;
+                if (v < row1) ncl += (cx != mx) + (cy != my);
+                nq[q] = make_double2(cx, cy);
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < RW_UNROLL; ++q) nq[q] = p[q];
+        }
+#pragma unroll
+        for (int q = 0; q < RW_UNROLL; ++q) {
+            const int v = base + q * 32 + lane;
+            if (v >= row1) continue;
+            if (mode & M_ADVECT) {
+                pout[v] = nq[q];
+                if (bestcopy) D.best[ub + v] = p[q];
+            }
+            if (in_smem) spos[v - row0] = nq[q];
+            xmn = fmin(xmn, nq[q].x); xmx = fmax(xmx, nq[q].x);
+            ymn = fmin(ymn, nq[q].y); ymx = fmax(ymx, nq[q].y);
+        }
     }
     if (mode & M_ADVECT) {
-        const unsigned long long tot = block_reduce<0, unsigned long long>(ncl, 0ull, s_redu);
-        if (tid == 0 && tot) atomicAdd(&st->clamps, tot);
+        ncl = warp_sum(ncl);
+        if (lane == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
     }
     if (!(mode & M_RASTER)) return;
-    xmn = block_reduce<1, double>(xmn, INFINITY, s_red);
-    xmx = block_reduce<2, double>(xmx, -INFINITY, s_red);
-    ymn = block_reduce<1, double>(ymn, INFINITY, s_red);
-    ymx = block_reduce<2, double>(ymx, -INFINITY, s_red);  // trailing __syncthreads also publishes rowpos
+    xmn = warp_allmin(xmn); xmx = warp_allmax(xmx);
+    ymn = warp_allmin(ymn); ymx = warp_allmax(ymx);
+    __syncwarp();  // row positions (smem, or this warp's global writes) visible to the warp
 
+    int* cnt = D.cnt_acc + (size_t)b * (T.R + 1);
     // ---- region crop (raster.py:70-78) ----
     const int j_off = clampi((long long)ceil(__dsub_rn(__dmul_rn(ymn, nd), 0.5)), 0, n);
     const int j_end = clampi((long long)ceil(__dsub_rn(__dmul_rn(ymx, nd), 0.5)), 0, n);
     const int i_off = clampi((long long)ceil(__dsub_rn(__dmul_rn(xmn, nd), 0.5)), 0, n);
     const int i_end = clampi((long long)ceil(__dsub_rn(__dmul_rn(xmx, nd), 0.5)), 0, n);
     const int rows = max(j_end - j_off, 0), cols = max(i_end - i_off, 0);
-    if (rows == 0 || cols == 0) return;
+    if (rows == 0 || cols == 0) {
+        if (lane == 0) cnt[r] = 0;
+        return;
+    }
     const long long width = (long long)cols + 1;
     const unsigned long long rank = (unsigned long long)T.region_rank[r];
-    const int back = (int)((long long)i_off / width) + 1;  // max rows a negative column can move a toggle up
+    const int back = (int)((long long)i_off / width) + 1;  // max rows a negative column moves a toggle up
+    int area = 0;
 
-    int w0 = j_off, wh = rows;
+    int w0 = j_off, wh = min(rows, RW_WROWS);
     while (w0 < j_end) {
         const int w1 = min(w0 + wh, j_end);
-        if (tid == 0) s_tot = 0;
-        __syncthreads();
+        const int W = w1 - w0;
+        if (lane == 0) s_tot[wid] = 0;
+        for (int q = lane; q <= W; q += 32) rc[q] = 0;
+        __syncwarp();
         // ---- crossings of every ring edge (raster.py:30-61, flattening :86-89) ----
-        for (int e = row0 + tid; e < row1; e += blockDim.x) {
-            const double2 a = rowpos[e], c = rowpos[T.row_next[e]];
+        for (int e = row0 + lane; e < row1; e += 32) {
+            const int en = T.row_next[e];
+            const double2 a = in_smem ? spos[e - row0] : gpos[e];
+            const double2 c = in_smem ? spos[en - row0] : gpos[en];
             const double x0 = __dmul_rn(a.x, nd), y0 = __dmul_rn(a.y, nd);
             const double x1 = __dmul_rn(c.x, nd), y1 = __dmul_rn(c.y, nd);
             if (y0 == y1) continue;
             const double ylo = fmin(y0, y1), yhi = fmax(y0, y1);
             const int jlo = clampi((long long)ceil(__dsub_rn(ylo, 0.5)), 0, n);
             const int jhi = clampi((long long)ceil(__dsub_rn(yhi, 0.5)), 0, n);
-            if (jhi <= jlo) continue;
-            const double slope = __ddiv_rn(__dsub_rn(x1, x0), __dsub_rn(y1, y0));
             const int js = max(jlo, w0);
             const int je = min(jhi, w1 + back);
+            if (je <= js) continue;
+            const double slope = __ddiv_rn(__dsub_rn(x1, x0), __dsub_rn(y1, y0));
             for (int j = js; j < je; ++j) {
                 const double yc = (double)j + 0.5;
                 const double xc = __dadd_rn(x0, __dmul_rn(__dsub_rn(yc, y0), slope));
@@ -172,84 +231,150 @@ __global__ void __launch_bounds__(REG_THREADS) k_region(Topo T, Bufs D, int mode
                 if (cc == cols) continue;  // absorber column
                 const int dest = j_off + (int)dr;
                 if (dest < w0 || dest >= w1) continue;
-                const int slot = atomicAdd(&s_tot, 1);
-                if (slot < TOG_CAP) s_keys[slot] = ((uint32_t)(dest - w0) << 14) | (uint32_t)(i_off + cc);
+                const int slot = atomicAdd(&s_tot[wid], 1);
+                if (slot < RW_TCAP) {
+                    keys[slot] = ((uint32_t)(dest - w0) << 16) | (uint32_t)(i_off + cc);
+                    atomicAdd(&rc[dest - w0], 1);
+                }
             }
         }
-        __syncthreads();
-        const int tot = s_tot;
-        if (tot > TOG_CAP) {
-            if (w1 - w0 == 1) {
-                if (tid == 0) atomicOr(&st->err, (int)E_TOGGLE_OVF);
+        __syncwarp();
+        const int tot = s_tot[wid];
+        if (tot > RW_TCAP) {
+            if (W == 1) {
+                if (lane == 0) atomicOr(&st->err, (int)E_TOGGLE_OVF);
                 return;
             }
-            wh = max(1, (w1 - w0) >> 1);
-            __syncthreads();
+            wh = max(1, W >> 1);
+            __syncwarp();
             continue;
         }
-        int P = 1;
-        while (P < tot) P <<= 1;
-        for (int i = tot + tid; i < P; i += blockDim.x) s_keys[i] = SENT;
-        __syncthreads();
-        bitonic_sort_u32(s_keys, P);
-        // ---- even-odd pairing within each row -> spans [start, end) clipped to the crop ----
-        for (int p = tid; p < tot; p += blockDim.x) {
-            const uint32_t key = s_keys[p];
-            const uint32_t lr = key >> 14;
-            const int s0 = lower_bound_u32(s_keys, tot, lr << 14);
-            if ((p - s0) & 1) continue;
-            const int col = (int)(key & 0x3FFFu);
-            const int end = (p + 1 < tot && (s_keys[p + 1] >> 14) == lr) ? (int)(s_keys[p + 1] & 0x3FFFu) : i_end;
-            if (end <= col) continue;
-            const int row = w0 + (int)lr;
-            const size_t rb = (size_t)b * n + row;
-            const int slot = atomicAdd(&D.rowcnt[rb], 1);
-            if (slot < D.cap)
-                D.spans[rb * D.cap + slot] = (rank << 32) | ((unsigned long long)end << 16) | (unsigned long long)col;
-            else
-                atomicOr(&st->err, (int)E_SPAN_OVF);
+        // ---- counting sort by row: rc -> exclusive offsets (rc[W] = total) ----
+        {
+            int carry = 0;
+            for (int q0 = 0; q0 < W; q0 += 32) {
+                const int q = q0 + lane;
+                const int v = q < W ? rc[q] : 0;
+                int chunk;
+                const int ex = warp_excl_scan_int(v, lane, &chunk);
+                __syncwarp();
+                if (q < W) rc[q] = carry + ex;
+                carry += chunk;
+            }
+            if (lane == 0) rc[W] = carry;
         }
-        __syncthreads();
+        __syncwarp();
+        // scatter columns into row buckets; a bucket's cursor runs from its start to the next start
+        for (int p = lane; p < tot; p += 32) {
+            const uint32_t key = keys[p];
+            const int pos = atomicAdd(&rc[key >> 16], 1);
+            colb[pos] = (uint16_t)(key & 0xFFFFu);
+        }
+        __syncwarp();
+        // after the scatter rc[q] = end of bucket q = start of bucket q+1
+        for (int q = lane; q < W; q += 32) {
+            const int s = q == 0 ? 0 : rc[q - 1], e = rc[q];
+            // insertion sort of the (few) crossings of this row, then even-odd pairing
+            for (int i = s + 1; i < e; ++i) {
+                const uint16_t x = colb[i];
+                int k = i - 1;
+                while (k >= s && colb[k] > x) { colb[k + 1] = colb[k]; --k; }
+                colb[k + 1] = x;
+            }
+            const int row = w0 + q;
+            for (int i = s; i < e; i += 2) {
+                const int col = colb[i];
+                const int end = i + 1 < e ? (int)colb[i + 1] : i_end;
+                if (end <= col) continue;
+                area += end - col;
+                const size_t rb = (size_t)b * n + row;
+                const int slot = atomicAdd(&D.rowcnt[rb], 1);
+                if (slot < D.cap)
+                    D.spans[rb * D.cap + slot] = (rank << 32) | ((unsigned long long)end << 16) | (unsigned long long)col;
+                else
+                    atomicOr(&st->err, (int)E_SPAN_OVF);
+            }
+        }
+        __syncwarp();
         w0 = w1;
-        if (tot < TOG_CAP / 4 && wh < rows) wh <<= 1;
+        if (tot < RW_TCAP / 4 && wh < RW_WROWS) wh = min(wh << 1, RW_WROWS);
     }
+    area = warp_sum(area);
+    if (lane == 0) cnt[r] = area;  // provisional; k_row subtracts pixels lost to lower ranks
 }
 
-__global__ void __launch_bounds__(ROW_THREADS) k_row(Topo T, Bufs D, int gate) {
-    extern __shared__ uint32_t s_lab[];
-    __shared__ int s_c;
-    const int j = blockIdx.x, b = blockIdx.y, tid = threadIdx.x, n = D.n;
+// One warp per texture row; rpc rows per CTA.  ctrl_mode: -1 raster only (background
+// count), 0 loop evaluation, 1 final re-evaluation.
+__global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_mode) {
+    extern __shared__ uint32_t s_lab[];  // [rows per CTA][n]
+    __shared__ int s_last;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, rpc = blockDim.x >> 5;
+    const int b = blockIdx.y, n = D.n;
+    const int j = blockIdx.x * rpc + wid;
     Carto* st = D.st + b;
     if (!gate_open(st, gate)) return;
-    for (int i = tid; i < n; i += blockDim.x) s_lab[i] = SENT;
+    uint32_t* lab_s = s_lab + (size_t)wid * n;
     const size_t rb = (size_t)b * n + j;
-    if (tid == 0) {
-        const int c = D.rowcnt[rb];
-        s_c = c;
-        D.rowcnt[rb] = 0;
-        if (c > D.cap) atomicOr(&st->err, (int)E_SPAN_OVF);
-        if (c > 0) atomicMax(&D.maxspan[b], c);
-    }
-    __syncthreads();
-    const int c = min(s_c, D.cap);
-    const unsigned long long* sp = D.spans + rb * D.cap;
-    for (int s = tid; s < c; s += blockDim.x) {
-        const unsigned long long v = sp[s];
-        const int lo = (int)(v & 0xFFFFull), hi = (int)((v >> 16) & 0xFFFFull);
-        const uint32_t rk = (uint32_t)(v >> 32);
-        for (int i = lo; i < hi; ++i) atomicMin(&s_lab[i], rk);
-    }
-    __syncthreads();
-    int* lab = D.labels + (size_t)b * D.nn + (size_t)j * n;
     int* cnt = D.cnt_acc + (size_t)b * (T.R + 1);
-    for (int i = tid; i < n; i += blockDim.x) {
-        const uint32_t rk = s_lab[i];
-        const int L = (rk == SENT) ? -1 : T.rank_region[rk];
-        lab[i] = L;
-        const int slot = L < 0 ? T.R : L;
-        if (i == n - 1 || s_lab[i + 1] != rk) atomicAdd(&cnt[slot], i + 1);
-        if (i == 0 || s_lab[i - 1] != rk) atomicAdd(&cnt[slot], -i);
+    if (j < n) {
+        for (int i = lane; i < n; i += 32) lab_s[i] = SENT;
+        const int c0 = D.rowcnt[rb];
+        __syncwarp();
+        if (lane == 0) {
+            D.rowcnt[rb] = 0;
+            if (c0 > D.cap) atomicOr(&st->err, (int)E_SPAN_OVF);
+            if (c0 > 0) atomicMax(&D.maxspan[b], c0);
+        }
+        const int c = min(c0, D.cap);
+        const unsigned long long* sp = D.spans + rb * D.cap;
+        bool lost = false;
+        for (int s0 = 0; s0 < c; s0 += 32) {
+            const unsigned long long v = s0 + lane < c ? sp[s0 + lane] : 0ull;
+            const int lo = (int)(v & 0xFFFFull), hi = (int)((v >> 16) & 0xFFFFull);
+            const uint32_t rk = (uint32_t)(v >> 32);
+            const bool longspan = hi - lo > 16;
+            if (!longspan) {  // lane paints its own short span
+                for (int i = lo; i < hi; ++i) {
+                    const uint32_t old = atomicMin(&lab_s[i], rk);
+                    if (old != SENT) {  // the higher rank loses the pixel
+                        atomicAdd(&cnt[T.rank_region[max(old, rk)]], -1);
+                        lost = true;
+                    }
+                }
+            }
+            unsigned lm = __ballot_sync(FULL, longspan);
+            while (lm) {  // the warp paints long spans together
+                const int q = __ffs(lm) - 1;
+                lm &= lm - 1;
+                const int qlo = __shfl_sync(FULL, lo, q), qhi = __shfl_sync(FULL, hi, q);
+                const uint32_t qrk = __shfl_sync(FULL, rk, q);
+                for (int i = qlo + lane; i < qhi; i += 32) {
+                    const uint32_t old = atomicMin(&lab_s[i], qrk);
+                    if (old != SENT) {
+                        atomicAdd(&cnt[T.rank_region[max(old, qrk)]], -1);
+                        lost = true;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        int* lab = D.labels + (size_t)b * D.nn + (size_t)j * n;
+        for (int i = lane; i < n; i += 32) {
+            const uint32_t rk = lab_s[i];
+            lab[i] = (rk == SENT) ? -1 : T.rank_region[rk];
+        }
+        if (lost) {  // order the (rare) count corrections before this CTA signs off
+            __threadfence();
+        }
     }
+    // ---- completion: the CTA that finishes the last row of this cartogram runs the control step ----
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&D.rowdone[b], 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) D.rowdone[b] = 0;
+    ctrl_body(T, D, b, ctrl_mode);
 }
 
 // Stage-level advect (displacement.py:229-238) on a float64 field.
@@ -284,21 +409,12 @@ __global__ void k_density(const int* __restrict__ lab, size_t nn, int R, const d
     }
 }
 
-// Vertex rows of the selected positions (src 0/1/2 = pos0/pos1/best) -> rowpos.
-__global__ void k_gather_rows(Topo T, Bufs D, int b, int src) {
-    const int v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= T.n_rows) return;
-    const size_t ub = (size_t)b * T.n_uniq;
-    const double2* p = (src == 0 ? D.pos0 : (src == 1 ? D.pos1 : D.best)) + ub;
-    D.rowpos[(size_t)b * T.n_rows + v] = p[T.row_uniq[v]];
-}
-
-// Region.area(): signed shoelace over the region's rings (geomodel.py:24-31, 63-65).
-__global__ void k_areas(Topo T, Bufs D, const int* __restrict__ ring_start, const int* __restrict__ region_ring0,
-                        int b, double* out) {
+// Region.area(): signed shoelace over the region's rings (geomodel.py:24-31, 63-65),
+// on the rows of the selected position buffer.
+__global__ void k_areas(Topo T, const double2* __restrict__ rp, const int* __restrict__ ring_start,
+                        const int* __restrict__ region_ring0, double* out) {
     __shared__ double s_red[33];
     const int r = blockIdx.x;
-    const double2* rp = D.rowpos + (size_t)b * T.n_rows;
     double acc = 0.0;
     for (int q = region_ring0[r]; q < region_ring0[r + 1]; ++q) {
         const int a = ring_start[q], e = ring_start[q + 1];

@@ -21,12 +21,14 @@
 // reference's sector tie rule (integral.py:9-14, oracle tests/oracles.py:30-54).
 //
 // The texture is cut into bands of H rows (one CTA per band and cartogram):
-//   k_sat1  per-band partial sums of rho along columns, diagonals, anti-diagonals,
-//           plus row totals -- streaming one row at a time, one barrier per row;
-//   k_sat2  band-direction exclusive prefixes / inclusive suffixes (carries) and totals;
-//   k_sat3  per band: x-prefix of the carries, then one top-down sweep computing
-//           A, alpha, UL and the in-band up-right ray URin (DL = DLtot - URin),
-//           and the displacement u at every pixel centre (or the 8 channels).
+//   k_sat1  per-band sums of rho along columns, diagonals and anti-diagonals
+//           (streamed one row at a time, one barrier per row), x-prefixed once at
+//           the band end, plus row totals;
+//   k_sat2  band-direction exclusive prefixes / inclusive suffixes (the carries)
+//           and image totals -- every value k_sat3 needs, ready to load;
+//   k_sat3  per band: load the carries, then one top-down sweep computing A,
+//           alpha, UL and the in-band up-right ray URin (DL = DLtot - URin), and
+//           the displacement u at every pixel centre (or the 8 channels).
 // All accumulation is float64; only the stored field may be float32.
 #pragma once
 #include "det_common.cuh"
@@ -65,20 +67,42 @@ __device__ __forceinline__ void load_rho(const Bufs& D, const SatSrc& S, int R, 
     }
 }
 
+// In-place inclusive prefix of a[0..len) in shared memory by the whole CTA.
+__device__ void block_prefix_smem(double* a, int len, double* sm) {
+    const int nt = blockDim.x;
+    const int per = (len + nt - 1) / nt;
+    const int s = min(len, threadIdx.x * per), e = min(len, s + per);
+    double loc = 0.0;
+    for (int i = s; i < e; ++i) loc += a[i];
+    double tot;
+    double run = block_excl_scan(loc, sm, &tot);
+    for (int i = s; i < e; ++i) {
+        run += a[i];
+        a[i] = run;
+    }
+    __syncthreads();
+}
+
 // ---------------------------------------------------------------------------------
+// Per-band sums, x-prefixed:  CS_b(x) = sum_{j in band, i<=x} rho,
+// DG_b(v) = sum_{j in band, i-j<=v} rho (compact index q = v + jb, q in [0, n+H-1)),
+// AD_b(w) = sum_{j in band, i+j<=w} rho (compact index q = w - jt).  Outside the
+// compact range the prefixes are 0 (below) or the band total (above).
 template <int CPT, int SRC>
 __global__ void k_sat1(Topo T, Bufs D, SatSrc S, int gate) {
+    extern __shared__ double s_part[];  // dg[L] | ad[L]
     __shared__ double s_w[3][32];
     __shared__ double s_bd[3][32];
     __shared__ double s_ba[3][32];
+    __shared__ double s_red[33];
     const int band = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
     const int lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
     if (!gate_open(D.st + b, gate)) return;
     const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, L = n + H - 1;
     const int x0 = t * CPT;
     const size_t bb = (size_t)b * D.nb + band;
-    double* dg = D.dgc + bb * L;
-    double* ad = D.adc + bb * L;
+    double* dg = s_part;
+    double* ad = s_part + L;
     double cs[CPT], pd[CPT], pa[CPT];
 #pragma unroll
     for (int k = 0; k < CPT; ++k) cs[k] = pd[k] = pa[k] = 0.0;
@@ -118,21 +142,41 @@ __global__ void k_sat1(Topo T, Bufs D, SatSrc S, int gate) {
 #pragma unroll
         for (int k = 0; k < CPT; ++k) { pd[k] = nd_[k]; pa[k] = na_[k]; }
     }
+    // band bottom: remaining diagonals / anti-diagonals end here; column sums -> x-prefix
+    double csum = 0.0;
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
         const int x = x0 + k;
         if (x < n) {
             dg[x] = pd[k];
             ad[jb - jt + x] = pa[k];
-            D.cs[bb * n + x] = cs[k];
         }
+        csum += x < n ? cs[k] : 0.0;
+    }
+    double tot;
+    double run = block_excl_scan(csum, s_red, &tot);
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int x = x0 + k;
+        run += cs[k];
+        if (x < n) D.cs[bb * n + x] = run;
+    }
+    block_prefix_smem(dg, L, s_red);
+    block_prefix_smem(ad, L, s_red);
+    for (int q = t; q < L; q += blockDim.x) {
+        D.dgc[bb * L + q] = dg[q];
+        D.adc[bb * L + q] = ad[q];
     }
 }
 
 // ---------------------------------------------------------------------------------
-// Band-direction carries.  Lanes: [0,n) columns, [n,3n-1) diagonals (idx=v+n-1),
-// [3n-1,5n-2) anti-diagonals (w).  blockDim = 32*G (G band groups).  The last
-// block column computes rowfull (row-total prefix) instead.
+// Band-direction carries.  Lanes: [0,n) columns x, [n,3n-1) diagonals (idx=v+n-1),
+// [3n-1,5n-2) anti-diagonals w.  blockDim = 32*G (G band groups).  The last block
+// column computes rowfull (row-total prefix) instead.  Outputs per band b:
+//   csX[b][x]   = sum_{b'<b} CS_b'(x)                 (alpha carry)
+//   dgXc[b][x]  = sum_{b'<b} DG_b'(x - jt + 1)        (UL carry, x in [0,n))
+//   adSc[b][q]  = sum_{b'>=b} AD_b'(jt - 1 + q)        (DLtot window, q in [0,n+H))
+// and totals csT[x] = colfull(x+1), dgT[idx] = Tv(v), adT[w] = Tu(w).
 __global__ void k_sat2(Bufs D, int gate) {
     __shared__ double s_g[32][33];
     __shared__ double s_red[33];
@@ -165,12 +209,17 @@ __global__ void k_sat2(Bufs D, int gate) {
     auto val = [&](int band) -> double {
         if (!valid) return 0.0;
         if (type == 0) return D.cs[(base + band) * n + idx];
+        int q;
+        const double* arr;
         if (type == 1) {
-            const int q = idx - (n - 1 - (band * H + H - 1));
-            return (q >= 0 && q < L) ? D.dgc[(base + band) * L + q] : 0.0;
+            q = idx - (n - 1) + (band * H + H - 1);  // v + jb
+            arr = D.dgc;
+        } else {
+            q = idx - band * H;                      // w - jt
+            arr = D.adc;
         }
-        const int q = idx - band * H;
-        return (q >= 0 && q < L) ? D.adc[(base + band) * L + q] : 0.0;
+        if (q < 0) return 0.0;
+        return arr[(base + band) * L + min(q, L - 1)];
     };
     double sum = 0.0;
     for (int band = bA; band < bE; ++band) sum += val(band);
@@ -190,8 +239,8 @@ __global__ void k_sat2(Bufs D, int gate) {
             if (type == 0) {
                 D.csX[(base + band) * n + idx] = run;
             } else {
-                const int q = idx - n + band * H;  // (v + jt - 1), v = idx - (n-1)
-                if (q >= 0 && q < n) D.dgXc[(base + band) * n + q] = run;
+                const int x = idx - n + band * H;  // v + jt - 1, v = idx - (n-1)
+                if (x >= 0 && x < n) D.dgXc[(base + band) * n + x] = run;
             }
             run += val(band);
         }
@@ -199,8 +248,8 @@ __global__ void k_sat2(Bufs D, int gate) {
         double run = after;
         for (int band = bE - 1; band >= bA; --band) {
             run += val(band);
-            const int q = idx - band * H;
-            if (q >= 0 && q < L) D.adSc[(base + band) * L + q] = run;
+            const int q = idx - band * H + 1;  // w - (jt - 1)
+            if (q >= 0 && q < L + 1) D.adSc[(base + band) * (L + 1) + q] = run;
         }
     }
     if (g == 0) {
@@ -214,64 +263,43 @@ __global__ void k_sat2(Bufs D, int gate) {
 template <int CPT, int SRC, typename UT, int OUT>
 __global__ void k_sat3(Topo T, Bufs D, SatSrc S, int gate) {
     extern __shared__ double sm[];
-    __shared__ double s_red[33];
     __shared__ double s_w[3][32];
     __shared__ double s_xa[3][32], s_xu1[3][32], s_xu2[3][32], s_xr[3][32];
     const int band = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
     const int lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
     if (!gate_open(D.st + b, gate)) return;
-    const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, L = n + H - 1, M = 2 * n - 1;
+    const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, M = 2 * n - 1;
     const int x0 = t * CPT;
     const size_t bb = (size_t)b * D.nb + band;
-    double* win_dl = sm;             // DLtot(w), w in [jt-1, jb+n-1]  -> [w-(jt-1)]
-    double* win_tu = sm + (n + H);   // Tu(w),    w in [jt-1, jb+n-2]  -> [w-(jt-1)]
-    double* win_tv = win_tu + (n + H);  // Tv(v), v in [-jb, n-1-jt]  -> [v+jb]; scratch first
+    const int WN = n + H;
+    double* win_dl = sm;            // DLtot(w), w in [jt-1, jb+n-1]  -> [w-(jt-1)]
+    double* win_tu = sm + WN;       // Tu(w),    w in [jt-1, jb+n-2]  -> [w-(jt-1)]
+    double* win_tv = sm + 2 * WN;   // Tv(v),    v in [-jb, n-1-jt]   -> [v+jb]
     const double* rowfull = D.rowfull + (size_t)b * (n + 1);
+    const double* adT = D.adT + (size_t)b * M;
+    const double* dgT = D.dgT + (size_t)b * M;
+    const double* csT = D.csT + (size_t)b * n;
 
-    // (a) UL carry: UL(jt-1, x) = inclusive prefix of dgXc at q = x
-    block_prefix_window(D.dgXc + bb * n, n, win_tv, 0, n, s_red);
-    __syncthreads();
+    // ---- carries (k_sat2) ----
+    for (int q = t; q < WN; q += blockDim.x) {
+        win_dl[q] = (jt == 0 && q == 0) ? 0.0 : D.adSc[bb * WN + q];  // DLtot(-1) = 0
+        const int wq = jt - 1 + q;
+        win_tu[q] = (wq >= 0 && wq < M) ? adT[wq] : 0.0;
+        const int iv = q - jb + n - 1;  // Tv index of v = q - jb
+        win_tv[q] = (iv >= 0 && iv < M) ? dgT[iv] : 0.0;
+    }
     double ul[CPT], al[CPT], cfe[CPT], cfi[CPT], ur[CPT];
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
         const int x = x0 + k;
-        ul[k] = x < n ? win_tv[x] : 0.0;
+        const bool in = x < n;
+        al[k] = in ? D.csX[bb * n + x] : 0.0;
+        ul[k] = in ? D.dgXc[bb * n + x] : 0.0;
+        cfi[k] = in ? csT[x] : 0.0;
+        cfe[k] = (in && x > 0) ? csT[x - 1] : 0.0;
         ur[k] = 0.0;
     }
-    __syncthreads();
-    // (b) alpha carry = x-prefix of csX; (c) column totals -> colfull(x), colfull(x+1)
-    {
-        double v[CPT], c[CPT], sv = 0.0, sc = 0.0;
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            const int x = x0 + k;
-            v[k] = x < n ? D.csX[bb * n + x] : 0.0;
-            c[k] = x < n ? D.csT[(size_t)b * n + x] : 0.0;
-            sv += v[k];
-            sc += c[k];
-        }
-        double tot;
-        double rv = block_excl_scan(sv, s_red, &tot);
-        double rc = block_excl_scan(sc, s_red, &tot);
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            rv += v[k];
-            al[k] = rv;
-            cfe[k] = rc;
-            rc += c[k];
-            cfi[k] = rc;
-        }
-    }
-    // (d) windows of Tv, Tu, DLtot
-    block_prefix_window(D.dgT + (size_t)b * M, M, win_tv, n - 1 - jb, M - jt, s_red);
-    block_prefix_window(D.adT + (size_t)b * M, M, win_tu + (jt == 0 ? 1 : 0), max(jt - 1, 0), jb + n - 1, s_red);
-    block_prefix_window(D.adSc + bb * L, L, win_dl + 1, 0, L, s_red);
-    if (t == 0) {
-        win_dl[0] = 0.0;
-        if (jt == 0) win_tu[0] = 0.0;
-    }
-    // boundary values of "row jt-1" = carries
-    if (lane == 31) {
+    if (lane == 31) {  // boundary values of "row jt-1" = carries
         s_xa[2][w] = al[CPT - 1];
         s_xu1[2][w] = ul[CPT - 1];
         s_xu2[2][w] = ul[CPT - 2];
