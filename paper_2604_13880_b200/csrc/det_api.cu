@@ -64,6 +64,7 @@ struct det_ctx {
     DVec<double2> pos_init, pos0, pos1, best;
     DVec<int> labels, cnt_acc, cnt_state, rowcnt, maxspan, rowdone;
     DVec<unsigned long long> spans;
+    DVec<float> lutf;
     DVec<double> lut, stats, weights, rerr, cs, dgc, adc, rt, csX, dgXc, adSc, csT, dgT, adT, rowfull, trace;
     DVec<char> uf;
     DVec<Carto> st;
@@ -93,8 +94,6 @@ static int fail(det_ctx* ctx, int code, const std::string& msg) {
     return code;
 }
 
-static int cpt_for(int n) { return n <= 256 ? 2 : (n <= 4096 ? 4 : 8); }
-static int nthreads_for(int n) { return std::max(32, n / cpt_for(n)); }
 
 static Topo make_topo(det_ctx* c) {
     Topo t;
@@ -118,7 +117,7 @@ static Bufs make_bufs(det_ctx* c) {
     d.pos0 = c->pos0.p; d.pos1 = c->pos1.p; d.best = c->best.p;
     d.labels = c->labels.p; d.cnt_acc = c->cnt_acc.p; d.cnt_state = c->cnt_state.p;
     d.spans = c->spans.p; d.rowcnt = c->rowcnt.p; d.maxspan = c->maxspan.p; d.rowdone = c->rowdone.p;
-    d.lut = c->lut.p; d.stats = c->stats.p; d.weights = c->weights.p; d.rerr = c->rerr.p;
+    d.lut = c->lut.p; d.lutf = c->lutf.p; d.stats = c->stats.p; d.weights = c->weights.p; d.rerr = c->rerr.p;
     d.uf = c->uf.p;
     d.cs = c->cs.p; d.dgc = c->dgc.p; d.adc = c->adc.p; d.rt = c->rt.p;
     d.csX = c->csX.p; d.dgXc = c->dgXc.p; d.adSc = c->adSc.p;
@@ -128,28 +127,35 @@ static Bufs make_bufs(det_ctx* c) {
 }
 
 // ----------------------------- launch helpers ---------------------------------
-template <int CPT>
-static void launch_sat_cpt(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S, int gate, int src, int out,
+template <int CPT, int NT>
+static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S, int gate, int src, int out,
                            bool u64, int B) {
-    const int n = c->n, nt = nthreads_for(n);
+    const int n = c->n;
     const dim3 gb(c->nb, B);
-    const size_t smem1 = (size_t)2 * (n + c->H - 1) * sizeof(double);
+    // float32 in-band arithmetic only for the float32 field from labels; float64 otherwise
+    const bool f32 = (src == SRC_LABELS && out == OUT_U && !u64);
+    const size_t smem1 = (size_t)2 * (n + c->H - 1) * (f32 ? sizeof(float) : sizeof(double));
     if (src == SRC_LABELS) {
-        cudaFuncSetAttribute(k_sat1<CPT, SRC_LABELS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-        k_sat1<CPT, SRC_LABELS><<<gb, nt, smem1, c->stream>>>(T, D, S, gate);
+        if (f32) {
+            cudaFuncSetAttribute(k_sat1<CPT, NT, SRC_LABELS, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+            k_sat1<CPT, NT, SRC_LABELS, float><<<gb, NT, smem1, c->stream>>>(T, D, S, gate);
+        } else {
+            cudaFuncSetAttribute(k_sat1<CPT, NT, SRC_LABELS, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+            k_sat1<CPT, NT, SRC_LABELS, double><<<gb, NT, smem1, c->stream>>>(T, D, S, gate);
+        }
     } else {
-        cudaFuncSetAttribute(k_sat1<CPT, SRC_DENSE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-        k_sat1<CPT, SRC_DENSE><<<gb, nt, smem1, c->stream>>>(T, D, S, gate);
+        cudaFuncSetAttribute(k_sat1<CPT, NT, SRC_DENSE, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+        k_sat1<CPT, NT, SRC_DENSE, double><<<gb, NT, smem1, c->stream>>>(T, D, S, gate);
     }
     const int lanes = n + 2 * (2 * n - 1);
     const int G = std::min(8, c->nb);
     k_sat2<<<dim3((lanes + 31) / 32 + 1, B), 32 * G, 0, c->stream>>>(D, gate);
-    const size_t smem = (size_t)3 * (n + c->H) * sizeof(double);
+    const size_t smem = (size_t)3 * (n + c->H) * (f32 ? sizeof(float) : sizeof(double));
 #define DET_SAT3(SRC_, UT_, OUT_)                                                                            \
     do {                                                                                                     \
-        auto fn = k_sat3<CPT, SRC_, UT_, OUT_>;                                                              \
+        auto fn = k_sat3<CPT, NT, SRC_, UT_, OUT_, UT_>;                                                     \
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                    \
-        fn<<<gb, nt, smem, c->stream>>>(T, D, S, gate);                                                      \
+        fn<<<gb, NT, smem, c->stream>>>(T, D, S, gate);                                                      \
     } while (0)
     if (out == OUT_CH8) {
         if (src == SRC_LABELS) DET_SAT3(SRC_LABELS, double, OUT_CH8);
@@ -164,12 +170,18 @@ static void launch_sat_cpt(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
 #undef DET_SAT3
 }
 
+// band kernels: one CTA per band row-set; CPT columns per thread, NT = n/CPT threads (>= 32)
 static void launch_sat(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S, int gate, int src, int out, bool u64,
                        int B) {
-    switch (cpt_for(c->n)) {
-        case 2: launch_sat_cpt<2>(c, T, D, S, gate, src, out, u64, B); break;
-        case 4: launch_sat_cpt<4>(c, T, D, S, gate, src, out, u64, B); break;
-        default: launch_sat_cpt<8>(c, T, D, S, gate, src, out, u64, B); break;
+    switch (c->n) {
+        case 16: case 32: case 64: launch_sat_cfg<2, 32>(c, T, D, S, gate, src, out, u64, B); break;
+        case 128: launch_sat_cfg<2, 64>(c, T, D, S, gate, src, out, u64, B); break;
+        case 256: launch_sat_cfg<2, 128>(c, T, D, S, gate, src, out, u64, B); break;
+        case 512: launch_sat_cfg<4, 128>(c, T, D, S, gate, src, out, u64, B); break;
+        case 1024: launch_sat_cfg<4, 256>(c, T, D, S, gate, src, out, u64, B); break;
+        case 2048: launch_sat_cfg<4, 512>(c, T, D, S, gate, src, out, u64, B); break;
+        case 4096: launch_sat_cfg<4, 1024>(c, T, D, S, gate, src, out, u64, B); break;
+        default: launch_sat_cfg<8, 1024>(c, T, D, S, gate, src, out, u64, B); break;
     }
 }
 
@@ -271,6 +283,7 @@ static int alloc_batch(det_ctx* ctx, int B) {
     CK(ctx->rowdone.alloc((size_t)B));
     CK(cudaMemsetAsync(ctx->rowdone.p, 0, (size_t)B * sizeof(int), ctx->stream));
     CK(ctx->lut.alloc((size_t)B * (ctx->R + 1)));
+    CK(ctx->lutf.alloc((size_t)B * (ctx->R + 1)));
     CK(ctx->stats.alloc((size_t)B * ctx->R));
     CK(ctx->weights.alloc((size_t)B * ctx->R));
     CK(ctx->rerr.alloc((size_t)B * ctx->R));

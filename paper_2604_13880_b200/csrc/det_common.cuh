@@ -71,6 +71,7 @@ struct Bufs {
     int* maxspan;
     int* rowdone;     // B: k_row CTAs finished this iteration (last one runs the control step)
     double* lut;
+    float* lutf;      // float copy of lut for the float32-field band kernels
     const double* stats;
     const double* weights;
     double* rerr;
@@ -102,6 +103,20 @@ struct SatSrc {
 
 __device__ __forceinline__ int clampi(long long v, int lo, int hi) {
     return (int)(v < lo ? lo : (v > hi ? hi : v));
+}
+
+// Exact ceil / floor of a double as int without the conversion (XU) pipe: adding
+// 1.5*2^52 in round-up / round-down mode leaves ceil(v) / floor(v) in the low mantissa
+// bits (valid for |v| < 2^31, the texture-coordinate range here).
+constexpr double ROUND_MAGIC = 6755399441055744.0;
+__device__ __forceinline__ int ceil_to_int(double v) {
+    return (int)(unsigned)__double_as_longlong(__dadd_ru(v, ROUND_MAGIC));
+}
+__device__ __forceinline__ int floor_to_int(double v) {
+    return (int)(unsigned)__double_as_longlong(__dadd_rd(v, ROUND_MAGIC));
+}
+__device__ __forceinline__ double floor_exact(double v) {  // floor(v) as a double, FP64 pipe only
+    return __dsub_rn(__dadd_rd(v, ROUND_MAGIC), ROUND_MAGIC);
 }
 
 __device__ __forceinline__ unsigned long long globaltimer() {

@@ -44,12 +44,12 @@ __global__ void k_reactivate(Bufs D) {
 // cmode -1: background count only; 0: loop evaluation of state next_iter; 1: final re-evaluation
 // of the best state.  Executed by one whole CTA (blockDim multiple of 32).
 __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
-    __shared__ double s_red[33];
-    __shared__ long long s_redl[33];
-    __shared__ int s_redi[33];
-    __shared__ int s_cont;
+    __shared__ double s_es[32], s_em[32];
+    __shared__ long long s_os[32];
+    __shared__ int s_fz[32];
+    __shared__ int s_cont, s_nbg;
     __shared__ double s_bdv;
-    const int t = threadIdx.x, R = T.R;
+    const int t = threadIdx.x, R = T.R, lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
     Carto* st = D.st + b;
     int* acc = D.cnt_acc + (size_t)b * (R + 1);
     int* sc = D.cnt_state + (size_t)b * (R + 1);
@@ -60,28 +60,54 @@ __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
     int fz = INT_MAX;
     long long osum = 0;
     double es = 0.0, em = -INFINITY;
-    for (int r = t; r < R; r += blockDim.x) {
-        const int o = __ldcg(acc + r);
-        osum += o;
-        if (!eval) continue;
-        sc[r] = o;
-        if (o == 0) fz = min(fz, r);
-        const double od = (double)o, w = wt[r];
-        const double e = fabs(od - w) / fmax(od, w);
-        er[r] = e;
-        es += e;
-        em = fmax(em, e);
+    for (int r0 = 0; r0 < R; r0 += 4 * blockDim.x) {
+        int o[4];
+        double wr[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // issue all loads first (latency hiding)
+            const int r = r0 + q * blockDim.x + t;
+            o[q] = r < R ? __ldcg(acc + r) : 0;
+            wr[q] = (eval && r < R) ? wt[r] : 1.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = r0 + q * blockDim.x + t;
+            if (r >= R) continue;
+            osum += o[q];
+            if (!eval) continue;
+            sc[r] = o[q];
+            if (o[q] == 0) fz = min(fz, r);
+            const double od = (double)o[q];
+            const double e = fabs(od - wr[q]) / fmax(od, wr[q]);  // engine.py:84
+            er[r] = e;
+            es += e;
+            em = fmax(em, e);
+        }
     }
-    osum = block_reduce<0, long long>(osum, 0ll, s_redl);
-    const int nbg = (int)((long long)D.nn - osum);
+    // one combined block reduction of (count sum, first zero, error sum, error max)
+    osum = warp_sum(osum);
+    es = warp_sum(es);
+    em = warp_max(em);
+    fz = warp_min(fz);
+    if (lane == 0) { s_os[w] = osum; s_es[w] = es; s_em[w] = em; s_fz[w] = fz; }
+    __syncthreads();
+    if (w == 0) {
+        long long o2 = lane < nw ? s_os[lane] : 0;
+        double e2 = lane < nw ? s_es[lane] : 0.0, m2 = lane < nw ? s_em[lane] : -INFINITY;
+        int f2 = lane < nw ? s_fz[lane] : INT_MAX;
+        o2 = warp_sum(o2); e2 = warp_sum(e2); m2 = warp_max(m2); f2 = warp_min(f2);
+        if (lane == 0) { s_os[0] = o2; s_es[0] = e2; s_em[0] = m2; s_fz[0] = f2; }
+    }
+    __syncthreads();
+    const int nbg = (int)((long long)D.nn - s_os[0]);
     if (t == 0) {
         acc[R] = nbg;
         if (eval) sc[R] = nbg;
     }
     if (!eval) return;
-    fz = block_reduce<1, int>(fz, INT_MAX, s_redi);
-    es = block_reduce<0, double>(es, 0.0, s_red);
-    em = block_reduce<2, double>(em, -INFINITY, s_red);
+    fz = s_fz[0];
+    es = s_es[0];
+    em = s_em[0];
     const Params P = D.prm[b];
     const int it = cmode == 0 ? st->next_iter : st->best_iter;
     if (t == 0) {
@@ -138,6 +164,7 @@ __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
                 } else {
                     s_cont = 1;
                     s_bdv = bdv;
+                    s_nbg = nbg;
                     st->bdv = bdv;
                     if (stop == S_RUNNING) st->next_iter = it + 1;
                 }
@@ -151,22 +178,35 @@ __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
     }
     __syncthreads();
     if (!s_cont) return;
+    // total mass C = sum_r (s_r/o_r) o_r + bdv n_bg = S + bdv n_bg (the reference's alpha[-1,-1],
+    // integral.py:58, agrees to rounding); residual LUT rho = m d / C - 1
     const double bdv = s_bdv;
     const double m = (double)D.nn;
-    double cpart = 0.0;
-    for (int r = t; r < R; r += blockDim.x) {
-        const double o = (double)sc[r];
-        cpart += (s[r] / o) * o;
-    }
-    const double C = block_reduce<0, double>(cpart, 0.0, s_red) + bdv * (double)nbg;
+    const double mc = m / (P.S + bdv * (double)s_nbg);
     double* lut = D.lut + (size_t)b * (R + 1);
-    for (int r = t; r < R; r += blockDim.x) {
-        const double o = (double)sc[r];
-        lut[r] = m * (s[r] / o) / C - 1.0;
+    float* lutf = D.lutf + (size_t)b * (R + 1);
+    for (int r0 = 0; r0 < R; r0 += 4 * blockDim.x) {
+        double sv[4], ov[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = r0 + q * blockDim.x + t;
+            sv[q] = r < R ? s[r] : 0.0;
+            ov[q] = r < R ? (double)sc[r] : 1.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = r0 + q * blockDim.x + t;
+            if (r < R) {
+                const double v = mc * (sv[q] / ov[q]) - 1.0;
+                lut[r] = v;
+                lutf[r] = (float)v;
+            }
+        }
     }
     if (t == 0) {
-        lut[R] = m * bdv / C - 1.0;
-        st->C = C;
+        lut[R] = mc * bdv - 1.0;
+        lutf[R] = (float)lut[R];
+        st->C = P.S + bdv * (double)s_nbg;
     }
 }
 

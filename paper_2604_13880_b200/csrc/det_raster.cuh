@@ -34,37 +34,62 @@ constexpr int RW_TCAP = 512;     // toggles per warp window
 constexpr int RW_WROWS = 128;    // texture rows per warp window
 constexpr int RW_UNROLL = 4;     // vertex rows in flight per lane (latency hiding)
 
-template <typename UT>
-__device__ __forceinline__ void field_texels(const UT* __restrict__ uf, int n, double px, double py, double (&t)[8],
-                                             double& fx, double& fy) {
-    // displacement.py:211-219: g = p*n - 0.5, i0 = clip(floor(g), 0, n-2), f = clip(g - i0, 0, 1)
+// Bilinear sample of the field (displacement.py:209-226): g = p*n - 0.5,
+// i0 = clip(floor(g), 0, n-2), f = clip(g - i0, 0, 1), 4-tap blend.  Index math in
+// float64; a float32 field is blended in float32 (its own precision), so the eight
+// texels need no float->double conversions.
+struct Tap {
+    int o0, o1;      // element offsets of the two texel pairs
+    double fx, fy;
+};
+
+__device__ __forceinline__ Tap field_tap(int n, double px, double py) {
     const double nd = (double)n;
     const double gx = px * nd - 0.5, gy = py * nd - 0.5;
-    const int ix = clampi((long long)floor(gx), 0, n - 2);
-    const int iy = clampi((long long)floor(gy), 0, n - 2);
-    fx = fmin(fmax(gx - (double)ix, 0.0), 1.0);
-    fy = fmin(fmax(gy - (double)iy, 0.0), 1.0);
-    const size_t o0 = ((size_t)iy * n + ix) * 2, o1 = o0 + (size_t)n * 2;
-    t[0] = (double)__ldg(uf + o0); t[1] = (double)__ldg(uf + o0 + 1);
-    t[2] = (double)__ldg(uf + o0 + 2); t[3] = (double)__ldg(uf + o0 + 3);
-    t[4] = (double)__ldg(uf + o1); t[5] = (double)__ldg(uf + o1 + 1);
-    t[6] = (double)__ldg(uf + o1 + 2); t[7] = (double)__ldg(uf + o1 + 3);
+    const double hi = (double)(n - 2);
+    double bx = floor_exact(gx), by = floor_exact(gy);
+    bx = bx < 0.0 ? 0.0 : (bx > hi ? hi : bx);
+    by = by < 0.0 ? 0.0 : (by > hi ? hi : by);
+    const int ix = floor_to_int(bx), iy = floor_to_int(by);
+    Tap t;
+    t.fx = gx - bx;
+    t.fy = gy - by;
+    t.fx = t.fx < 0.0 ? 0.0 : (t.fx > 1.0 ? 1.0 : t.fx);
+    t.fy = t.fy < 0.0 ? 0.0 : (t.fy > 1.0 ? 1.0 : t.fy);
+    t.o0 = (iy * n + ix) * 2;
+    t.o1 = t.o0 + n * 2;
+    return t;
 }
 
-__device__ __forceinline__ double2 blend(const double (&t)[8], double fx, double fy) {
-    // displacement.py:220-226
-    const double gxm = 1.0 - fx, gym = 1.0 - fy;
-    double2 s;
-    s.x = t[0] * gxm * gym + t[2] * fx * gym + t[4] * gxm * fy + t[6] * fx * fy;
-    s.y = t[1] * gxm * gym + t[3] * fx * gym + t[5] * gxm * fy + t[7] * fx * fy;
-    return s;
+template <typename UT>
+struct Texels {
+    UT v[8];
+};
+
+template <typename UT>
+__device__ __forceinline__ Texels<UT> field_load(const UT* __restrict__ uf, const Tap& t) {
+    Texels<UT> x;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        x.v[q] = __ldg(uf + t.o0 + q);
+        x.v[4 + q] = __ldg(uf + t.o1 + q);
+    }
+    return x;
+}
+
+template <typename UT>
+__device__ __forceinline__ double2 field_blend(const Texels<UT>& x, const Tap& t) {
+    const UT fx = (UT)t.fx, fy = (UT)t.fy;
+    const UT gxm = (UT)1 - fx, gym = (UT)1 - fy;
+    const UT sx = x.v[0] * gxm * gym + x.v[2] * fx * gym + x.v[4] * gxm * fy + x.v[6] * fx * fy;
+    const UT sy = x.v[1] * gxm * gym + x.v[3] * fx * gym + x.v[5] * gxm * fy + x.v[7] * fx * fy;
+    return make_double2((double)sx, (double)sy);
 }
 
 template <typename UT>
 __device__ __forceinline__ double2 sample_field(const UT* __restrict__ uf, int n, double px, double py) {
-    double t[8], fx, fy;
-    field_texels<UT>(uf, n, px, py, t, fx, fy);
-    return blend(t, fx, fy);
+    const Tap t = field_tap(n, px, py);
+    return field_blend<UT>(field_load<UT>(uf, t), t);
 }
 
 template <typename T>
@@ -141,14 +166,19 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
         }
         double2 nq[RW_UNROLL];
         if (mode & M_ADVECT) {
-            double t[RW_UNROLL][8], fx[RW_UNROLL], fy[RW_UNROLL];
-#pragma unroll
-            for (int q = 0; q < RW_UNROLL; ++q) field_texels<UT>(uf, n, p[q].x, p[q].y, t[q], fx[q], fy[q]);
+            Tap tp[RW_UNROLL];
+            Texels<UT> tx[RW_UNROLL];
 #pragma unroll
             for (int q = 0; q < RW_UNROLL; ++q) {
-                const double2 s = blend(t[q], fx[q], fy[q]);
+                tp[q] = field_tap(n, p[q].x, p[q].y);
+                tx[q] = field_load<UT>(uf, tp[q]);
+            }
+#pragma unroll
+            for (int q = 0; q < RW_UNROLL; ++q) {
+                const double2 s = field_blend<UT>(tx[q], tp[q]);
                 const double mx = p[q].x + s.x, my = p[q].y + s.y;
-                const double cx = fmin(fmax(mx, 0.0), 1.0), cy = fmin(fmax(my, 0.0), 1.0);
+                const double cx = mx < 0.0 ? 0.0 : (mx > 1.0 ? 1.0 : mx);  // np.clip (no NaNs here)
+                const double cy = my < 0.0 ? 0.0 : (my > 1.0 ? 1.0 : my);
                 const int v = base + q * 32 + lane;
                 if (v < row1) ncl += (cx != mx) + (cy != my);
                 nq[q] = make_double2(cx, cy);
@@ -166,8 +196,8 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
                 if (bestcopy) D.best[ub + v] = p[q];
             }
             if (in_smem) spos[v - row0] = nq[q];
-            xmn = fmin(xmn, nq[q].x); xmx = fmax(xmx, nq[q].x);
-            ymn = fmin(ymn, nq[q].y); ymx = fmax(ymx, nq[q].y);
+            xmn = nq[q].x < xmn ? nq[q].x : xmn; xmx = nq[q].x > xmx ? nq[q].x : xmx;
+            ymn = nq[q].y < ymn ? nq[q].y : ymn; ymx = nq[q].y > ymx ? nq[q].y : ymx;
         }
     }
     if (mode & M_ADVECT) {
@@ -181,18 +211,19 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
 
     int* cnt = D.cnt_acc + (size_t)b * (T.R + 1);
     // ---- region crop (raster.py:70-78) ----
-    const int j_off = clampi((long long)ceil(__dsub_rn(__dmul_rn(ymn, nd), 0.5)), 0, n);
-    const int j_end = clampi((long long)ceil(__dsub_rn(__dmul_rn(ymx, nd), 0.5)), 0, n);
-    const int i_off = clampi((long long)ceil(__dsub_rn(__dmul_rn(xmn, nd), 0.5)), 0, n);
-    const int i_end = clampi((long long)ceil(__dsub_rn(__dmul_rn(xmx, nd), 0.5)), 0, n);
+    // ceil then int cast == round-toward-+inf conversion (cvt.rpi), exact for |v| < 2^31
+    const int j_off = min(max(ceil_to_int(__dsub_rn(__dmul_rn(ymn, nd), 0.5)), 0), n);
+    const int j_end = min(max(ceil_to_int(__dsub_rn(__dmul_rn(ymx, nd), 0.5)), 0), n);
+    const int i_off = min(max(ceil_to_int(__dsub_rn(__dmul_rn(xmn, nd), 0.5)), 0), n);
+    const int i_end = min(max(ceil_to_int(__dsub_rn(__dmul_rn(xmx, nd), 0.5)), 0), n);
     const int rows = max(j_end - j_off, 0), cols = max(i_end - i_off, 0);
     if (rows == 0 || cols == 0) {
         if (lane == 0) cnt[r] = 0;
         return;
     }
-    const long long width = (long long)cols + 1;
+    const long long width = (long long)cols + 1;  // absorber column (raster.py:79-80)
     const unsigned long long rank = (unsigned long long)T.region_rank[r];
-    const int back = (int)((long long)i_off / width) + 1;  // max rows a negative column moves a toggle up
+    const int back = i_off / (cols + 1) + 1;  // max rows a negative column moves a toggle up
     int area = 0;
 
     int w0 = j_off, wh = min(rows, RW_WROWS);
@@ -210,26 +241,29 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
             const double x0 = __dmul_rn(a.x, nd), y0 = __dmul_rn(a.y, nd);
             const double x1 = __dmul_rn(c.x, nd), y1 = __dmul_rn(c.y, nd);
             if (y0 == y1) continue;
-            const double ylo = fmin(y0, y1), yhi = fmax(y0, y1);
-            const int jlo = clampi((long long)ceil(__dsub_rn(ylo, 0.5)), 0, n);
-            const int jhi = clampi((long long)ceil(__dsub_rn(yhi, 0.5)), 0, n);
+            const double ylo = y0 < y1 ? y0 : y1, yhi = y0 < y1 ? y1 : y0;
+            const int jlo = min(max(ceil_to_int(__dsub_rn(ylo, 0.5)), 0), n);
+            const int jhi = min(max(ceil_to_int(__dsub_rn(yhi, 0.5)), 0), n);
             const int js = max(jlo, w0);
             const int je = min(jhi, w1 + back);
             if (je <= js) continue;
             const double slope = __ddiv_rn(__dsub_rn(x1, x0), __dsub_rn(y1, y0));
-            for (int j = js; j < je; ++j) {
-                const double yc = (double)j + 0.5;
+            double yc = (double)js + 0.5;  // scanline centre j + 0.5 (exact, stepped by 1.0)
+            for (int j = js; j < je; ++j, yc += 1.0) {
                 const double xc = __dadd_rn(x0, __dmul_rn(__dsub_rn(yc, y0), slope));
-                const int i0 = clampi((long long)ceil(__dsub_rn(xc, 0.5)), 0, n);
-                const long long f = (long long)(j - j_off) * width + (long long)min(i0 - i_off, cols);
-                if (f < 0) {  // np.bincount raises on negative entries
-                    atomicOr(&st->err, (int)E_NEGIDX);
-                    continue;
+                const int i0 = min(max(ceil_to_int(__dsub_rn(xc, 0.5)), 0), n);
+                int dest = j, cc = min(i0 - i_off, cols);
+                if (cc < 0) {  // toggle left of the crop: the flat index lands in an earlier row
+                    const long long f = (long long)(j - j_off) * width + (long long)cc;
+                    if (f < 0) {  // np.bincount raises on negative entries
+                        atomicOr(&st->err, (int)E_NEGIDX);
+                        continue;
+                    }
+                    const long long dr = f / width;
+                    cc = (int)(f - dr * width);
+                    dest = j_off + (int)dr;
                 }
-                const long long dr = f / width;
-                const int cc = (int)(f - dr * width);
                 if (cc == cols) continue;  // absorber column
-                const int dest = j_off + (int)dr;
                 if (dest < w0 || dest >= w1) continue;
                 const int slot = atomicAdd(&s_tot[wid], 1);
                 if (slot < RW_TCAP) {

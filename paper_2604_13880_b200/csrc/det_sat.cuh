@@ -35,18 +35,18 @@
 
 namespace det {
 
-template <int CPT, int SRC>
-__device__ __forceinline__ void load_rho(const Bufs& D, const SatSrc& S, int R, int b, int j, int x0,
-                                         double (&rho)[CPT]) {
+// Residual density of CPT consecutive pixels of row j in the accumulator type A
+// (float32 in the float32-field mode, float64 otherwise).
+template <int CPT, int SRC, typename A>
+__device__ __forceinline__ void load_rho(const Bufs& D, const SatSrc& S, int R, int b, int j, int x0, A (&rho)[CPT]) {
     const int n = D.n;
     if (x0 >= n) {
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) rho[k] = 0.0;
+        for (int k = 0; k < CPT; ++k) rho[k] = (A)0;
         return;
     }
     if (SRC == SRC_LABELS) {
         const int* lab = D.labels + (size_t)b * D.nn + (size_t)j * n + x0;
-        const double* lut = D.lut + (size_t)b * (R + 1);
         int L[CPT];
         if (CPT == 2) {
             const int2 v = *reinterpret_cast<const int2*>(lab);
@@ -58,42 +58,61 @@ __device__ __forceinline__ void load_rho(const Bufs& D, const SatSrc& S, int R, 
                 L[q] = v.x; L[q + 1] = v.y; L[q + 2] = v.z; L[q + 3] = v.w;
             }
         }
+        if (sizeof(A) == 4) {
+            const float* lut = D.lutf + (size_t)b * (R + 1);
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) rho[k] = __ldg(lut + (L[k] < 0 ? R : L[k]));
+            for (int k = 0; k < CPT; ++k) rho[k] = (A)__ldg(lut + (L[k] < 0 ? R : L[k]));
+        } else {
+            const double* lut = D.lut + (size_t)b * (R + 1);
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) rho[k] = (A)__ldg(lut + (L[k] < 0 ? R : L[k]));
+        }
     } else {
         const double* d = S.d + (size_t)b * D.nn + (size_t)j * n + x0;
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) rho[k] = __dadd_rn(__dmul_rn(d[k], S.scale), S.offset);
+        for (int k = 0; k < CPT; ++k) rho[k] = (A)__dadd_rn(__dmul_rn(d[k], S.scale), S.offset);
     }
 }
 
-// In-place inclusive prefix of a[0..len) in shared memory by the whole CTA.
-__device__ void block_prefix_smem(double* a, int len, double* sm) {
+template <typename A>
+__device__ __forceinline__ A warp_incl_scan_t(A v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const A t = __shfl_up_sync(FULL, v, o);
+        if (lane >= o) v += t;
+    }
+    return v;
+}
+
+// In-place inclusive prefix of a[0..len) in shared memory by the whole CTA (float64 carry).
+template <typename A>
+__device__ void block_prefix_smem(A* a, double* out, int len, double* sm) {
     const int nt = blockDim.x;
     const int per = (len + nt - 1) / nt;
     const int s = min(len, threadIdx.x * per), e = min(len, s + per);
     double loc = 0.0;
-    for (int i = s; i < e; ++i) loc += a[i];
+    for (int i = s; i < e; ++i) loc += (double)a[i];
     double tot;
     double run = block_excl_scan(loc, sm, &tot);
     for (int i = s; i < e; ++i) {
-        run += a[i];
-        a[i] = run;
+        run += (double)a[i];
+        out[i] = run;
     }
-    __syncthreads();
 }
 
 // ---------------------------------------------------------------------------------
 // Per-band sums, x-prefixed:  CS_b(x) = sum_{j in band, i<=x} rho,
 // DG_b(v) = sum_{j in band, i-j<=v} rho (compact index q = v + jb, q in [0, n+H-1)),
 // AD_b(w) = sum_{j in band, i+j<=w} rho (compact index q = w - jt).  Outside the
-// compact range the prefixes are 0 (below) or the band total (above).
-template <int CPT, int SRC>
-__global__ void k_sat1(Topo T, Bufs D, SatSrc S, int gate) {
-    extern __shared__ double s_part[];  // dg[L] | ad[L]
-    __shared__ double s_w[3][32];
-    __shared__ double s_bd[3][32];
-    __shared__ double s_ba[3][32];
+// compact range the prefixes are 0 (below) or the band total (above).  In-band sums
+// in A; the x-prefixes and everything downstream in float64.
+template <int CPT, int NT, int SRC, typename A>
+__global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate) {
+    extern __shared__ unsigned char s_raw1[];  // dg[L] | ad[L] in A
+    __shared__ A s_w[3][32];
+    __shared__ A s_bd[3][32];
+    __shared__ A s_ba[3][32];
     __shared__ double s_red[33];
     const int band = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
     const int lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
@@ -101,27 +120,31 @@ __global__ void k_sat1(Topo T, Bufs D, SatSrc S, int gate) {
     const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, L = n + H - 1;
     const int x0 = t * CPT;
     const size_t bb = (size_t)b * D.nb + band;
-    double* dg = s_part;
-    double* ad = s_part + L;
-    double cs[CPT], pd[CPT], pa[CPT];
+    A* dg = reinterpret_cast<A*>(s_raw1);
+    A* ad = dg + L;
+    A cs[CPT], pd[CPT], pa[CPT];
 #pragma unroll
-    for (int k = 0; k < CPT; ++k) cs[k] = pd[k] = pa[k] = 0.0;
+    for (int k = 0; k < CPT; ++k) cs[k] = pd[k] = pa[k] = (A)0;
 
+    A rho_n[CPT];
+    load_rho<CPT, SRC, A>(D, S, T.R, b, jt, x0, rho_n);
     for (int j = jt; j <= jb; ++j) {
         const int slot = (j - jt) % 3, ps = (j - jt + 2) % 3;
-        double rho[CPT];
-        load_rho<CPT, SRC>(D, S, T.R, b, j, x0, rho);
-        double ts = 0.0;
+        A rho[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
+        if (j < jb) load_rho<CPT, SRC, A>(D, S, T.R, b, j + 1, x0, rho_n);  // prefetch the next row
+        A ts = (A)0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) ts += rho[k];
         ts = warp_sum(ts);
         if (lane == 0) s_w[slot][w] = ts;
         __syncthreads();
-        double left = __shfl_up_sync(FULL, pd[CPT - 1], 1);
-        double right = __shfl_down_sync(FULL, pa[0], 1);
-        if (lane == 0) left = (w == 0 || j == jt) ? 0.0 : s_bd[ps][w - 1];
-        if (lane == 31) right = (w == nw - 1 || j == jt) ? 0.0 : s_ba[ps][w + 1];
-        double nd_[CPT], na_[CPT];
+        A left = __shfl_up_sync(FULL, pd[CPT - 1], 1);
+        A right = __shfl_down_sync(FULL, pa[0], 1);
+        if (lane == 0) left = (w == 0 || j == jt) ? (A)0 : s_bd[ps][w - 1];
+        if (lane == 31) right = (w == nw - 1 || j == jt) ? (A)0 : s_ba[ps][w + 1];
+        A nd_[CPT], na_[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             nd_[k] = rho[k] + (k == 0 ? left : pd[k - 1]);
@@ -130,7 +153,7 @@ __global__ void k_sat1(Topo T, Bufs D, SatSrc S, int gate) {
         }
         if (t == 0) {
             double s = 0.0;
-            for (int q = 0; q < nw; ++q) s += s_w[slot][q];
+            for (int q = 0; q < nw; ++q) s += (double)s_w[slot][q];
             D.rt[(size_t)b * n + j] = s;
         }
         if (j < jb) {
@@ -151,22 +174,18 @@ __global__ void k_sat1(Topo T, Bufs D, SatSrc S, int gate) {
             dg[x] = pd[k];
             ad[jb - jt + x] = pa[k];
         }
-        csum += x < n ? cs[k] : 0.0;
+        csum += x < n ? (double)cs[k] : 0.0;
     }
     double tot;
-    double run = block_excl_scan(csum, s_red, &tot);
+    double run = block_excl_scan(csum, s_red, &tot);  // (its barriers also publish dg/ad)
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
         const int x = x0 + k;
-        run += cs[k];
+        run += (double)cs[k];
         if (x < n) D.cs[bb * n + x] = run;
     }
-    block_prefix_smem(dg, L, s_red);
-    block_prefix_smem(ad, L, s_red);
-    for (int q = t; q < L; q += blockDim.x) {
-        D.dgc[bb * L + q] = dg[q];
-        D.adc[bb * L + q] = ad[q];
-    }
+    block_prefix_smem<A>(dg, D.dgc + bb * L, L, s_red);
+    block_prefix_smem<A>(ad, D.adc + bb * L, L, s_red);
 }
 
 // ---------------------------------------------------------------------------------
@@ -260,11 +279,13 @@ __global__ void k_sat2(Bufs D, int gate) {
 }
 
 // ---------------------------------------------------------------------------------
-template <int CPT, int SRC, typename UT, int OUT>
-__global__ void k_sat3(Topo T, Bufs D, SatSrc S, int gate) {
-    extern __shared__ double sm[];
-    __shared__ double s_w[3][32];
-    __shared__ double s_xa[3][32], s_xu1[3][32], s_xu2[3][32], s_xr[3][32];
+// Per band: load the float64 carries, then one top-down sweep.  In-band arithmetic
+// in A (float32 when the field is stored as float32), carries rounded to A once.
+template <int CPT, int NT, int SRC, typename UT, int OUT, typename A>
+__global__ void __launch_bounds__(NT) k_sat3(Topo T, Bufs D, SatSrc S, int gate) {
+    extern __shared__ unsigned char s_raw3[];
+    __shared__ A s_w[3][32];
+    __shared__ A s_xa[3][32], s_xu1[3][32], s_xu2[3][32], s_xr[3][32];
     const int band = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
     const int lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
     if (!gate_open(D.st + b, gate)) return;
@@ -272,9 +293,9 @@ __global__ void k_sat3(Topo T, Bufs D, SatSrc S, int gate) {
     const int x0 = t * CPT;
     const size_t bb = (size_t)b * D.nb + band;
     const int WN = n + H;
-    double* win_dl = sm;            // DLtot(w), w in [jt-1, jb+n-1]  -> [w-(jt-1)]
-    double* win_tu = sm + WN;       // Tu(w),    w in [jt-1, jb+n-2]  -> [w-(jt-1)]
-    double* win_tv = sm + 2 * WN;   // Tv(v),    v in [-jb, n-1-jt]   -> [v+jb]
+    A* win_dl = reinterpret_cast<A*>(s_raw3);  // DLtot(w), w in [jt-1, jb+n-1]  -> [w-(jt-1)]
+    A* win_tu = win_dl + WN;                   // Tu(w),    w in [jt-1, jb+n-2]  -> [w-(jt-1)]
+    A* win_tv = win_dl + 2 * WN;               // Tv(v),    v in [-jb, n-1-jt]   -> [v+jb]
     const double* rowfull = D.rowfull + (size_t)b * (n + 1);
     const double* adT = D.adT + (size_t)b * M;
     const double* dgT = D.dgT + (size_t)b * M;
@@ -282,117 +303,131 @@ __global__ void k_sat3(Topo T, Bufs D, SatSrc S, int gate) {
 
     // ---- carries (k_sat2) ----
     for (int q = t; q < WN; q += blockDim.x) {
-        win_dl[q] = (jt == 0 && q == 0) ? 0.0 : D.adSc[bb * WN + q];  // DLtot(-1) = 0
+        win_dl[q] = (jt == 0 && q == 0) ? (A)0 : (A)D.adSc[bb * WN + q];  // DLtot(-1) = 0
         const int wq = jt - 1 + q;
-        win_tu[q] = (wq >= 0 && wq < M) ? adT[wq] : 0.0;
+        win_tu[q] = (wq >= 0 && wq < M) ? (A)adT[wq] : (A)0;
         const int iv = q - jb + n - 1;  // Tv index of v = q - jb
-        win_tv[q] = (iv >= 0 && iv < M) ? dgT[iv] : 0.0;
+        win_tv[q] = (iv >= 0 && iv < M) ? (A)dgT[iv] : (A)0;
     }
-    double ul[CPT], al[CPT], cfe[CPT], cfi[CPT], ur[CPT];
+    // cc[k]: column-total average cavg(x) = (colfull(x) + colfull(x+1))/2 for the field,
+    // colfull(x+1) for the channel dump
+    A ul[CPT], al[CPT], cc[CPT], ur[CPT];
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
         const int x = x0 + k;
         const bool in = x < n;
-        al[k] = in ? D.csX[bb * n + x] : 0.0;
-        ul[k] = in ? D.dgXc[bb * n + x] : 0.0;
-        cfi[k] = in ? csT[x] : 0.0;
-        cfe[k] = (in && x > 0) ? csT[x - 1] : 0.0;
-        ur[k] = 0.0;
+        al[k] = in ? (A)D.csX[bb * n + x] : (A)0;
+        ul[k] = in ? (A)D.dgXc[bb * n + x] : (A)0;
+        const double cfi = in ? csT[x] : 0.0, cfe = (in && x > 0) ? csT[x - 1] : 0.0;
+        cc[k] = (A)(OUT == OUT_CH8 ? cfi : 0.5 * (cfe + cfi));
+        ur[k] = (A)0;
     }
     if (lane == 31) {  // boundary values of "row jt-1" = carries
         s_xa[2][w] = al[CPT - 1];
         s_xu1[2][w] = ul[CPT - 1];
         s_xu2[2][w] = ul[CPT - 2];
     }
-    if (lane == 0) s_xr[2][w] = 0.0;
-    __syncthreads();
-
+    if (lane == 0) s_xr[2][w] = (A)0;
     const double rf_top = rowfull[jt];
-    const double Cr = rowfull[n];
-    const double nd = (double)n;
-    const double inv2m = S.outscale != 0.0 ? S.outscale : 0.5 / (nd * nd);
+    const A Cr = (A)rowfull[n];
+    const double inv_nd = 1.0 / (double)n;  // exact: n is a power of two
+    const A inv_n = (A)inv_nd;
+    const A inv2m = (A)(S.outscale != 0.0 ? S.outscale : 0.5 * inv_nd * inv_nd);
+    const A xc0 = (A)(((double)x0 + 0.5) * inv_nd);  // pixel-centre x of column x0 (displacement.py:59)
     UT* uf = reinterpret_cast<UT*>(D.uf) + (size_t)b * D.nn * 2;
+    A rho_n[CPT];
+    load_rho<CPT, SRC, A>(D, S, T.R, b, jt, x0, rho_n);
+    __syncthreads();
 
     for (int j = jt; j <= jb; ++j) {
         const int slot = (j - jt) % 3, ps = (j - jt + 2) % 3;
-        double rho[CPT];
-        load_rho<CPT, SRC>(D, S, T.R, b, j, x0, rho);
-        double loc[CPT];
-        double run = 0.0;
+        A rho[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
+        if (j < jb) load_rho<CPT, SRC, A>(D, S, T.R, b, j + 1, x0, rho_n);  // prefetch the next row
+        A loc[CPT];
+        A run = (A)0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) { run += rho[k]; loc[k] = run; }
-        const double tsum = run;
-        const double winc = warp_incl_scan(tsum);
+        const A tsum = run;
+        const A winc = warp_incl_scan_t<A>(tsum);
         if (lane == 31) s_w[slot][w] = winc;
         __syncthreads();
-        double off = 0.0;
+        A off = (A)0;
         for (int q = 0; q < w; ++q) off += s_w[slot][q];
-        const double excl = off + winc - tsum;  // A(j, x0-1)
-        double ap_m1 = __shfl_up_sync(FULL, al[CPT - 1], 1);
-        double ul_m1 = __shfl_up_sync(FULL, ul[CPT - 1], 1);
-        double ul_m2 = __shfl_up_sync(FULL, ul[CPT - 2], 1);
-        double ur_p = __shfl_down_sync(FULL, ur[0], 1);
+        const A excl = off + winc - tsum;  // A(j, x0-1)
+        A ap_m1 = __shfl_up_sync(FULL, al[CPT - 1], 1);
+        A ul_m1 = __shfl_up_sync(FULL, ul[CPT - 1], 1);
+        A ul_m2 = __shfl_up_sync(FULL, ul[CPT - 2], 1);
+        A ur_p = __shfl_down_sync(FULL, ur[0], 1);
         if (lane == 0) {
-            if (w == 0) { ap_m1 = 0.0; ul_m1 = 0.0; ul_m2 = 0.0; }
+            if (w == 0) { ap_m1 = (A)0; ul_m1 = (A)0; ul_m2 = (A)0; }
             else { ap_m1 = s_xa[ps][w - 1]; ul_m1 = s_xu1[ps][w - 1]; ul_m2 = s_xu2[ps][w - 1]; }
         }
-        if (lane == 31) ur_p = (w == nw - 1) ? (rowfull[j] - rf_top) : s_xr[ps][w + 1];
-        double A[CPT], an[CPT], uln[CPT], urn[CPT];
+        if (lane == 31) ur_p = (w == nw - 1) ? (A)(rowfull[j] - rf_top) : s_xr[ps][w + 1];
+        A Av[CPT], an[CPT], uln[CPT], urn[CPT];
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) A[k] = excl + loc[k];
+        for (int k = 0; k < CPT; ++k) Av[k] = excl + loc[k];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
-            an[k] = al[k] + A[k];
-            uln[k] = A[k] + (k == 0 ? ul_m1 : ul[k - 1]);
-            urn[k] = A[k] + (k == CPT - 1 ? ur_p : ur[k + 1]);
+            an[k] = al[k] + Av[k];
+            uln[k] = Av[k] + (k == 0 ? ul_m1 : ul[k - 1]);
+            urn[k] = Av[k] + (k == CPT - 1 ? ur_p : ur[k + 1]);
         }
-        const double rf0 = rowfull[j], rf1 = rowfull[j + 1];
-        const double yc = ((double)j + 0.5) / nd;
+        const double rf0d = rowfull[j], rf1d = rowfull[j + 1];
+        const A rf1 = (A)rf1d;
+        const A yc = (A)(((double)j + 0.5) * inv_nd);
+        const A ravg = (A)(0.5 * (rf0d + rf1d));
+        const int wi0 = j + x0 - (jt - 1);
+        A dlw[CPT + 1];  // DLtot(j + x - 1 + q), sliding window over this thread's columns
+#pragma unroll
+        for (int q = 0; q <= CPT; ++q) dlw[q] = win_dl[wi0 - 1 + q];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             const int x = x0 + k;
             if (x >= n) continue;
-            const double apm1 = k == 0 ? ap_m1 : al[k - 1];
-            const double anm1 = k == 0 ? (ap_m1 + excl) : an[k - 1];
-            const double ulnm1 = k == 0 ? (excl + ul_m2) : uln[k - 1];
-            const double ulpm1 = k == 0 ? ul_m1 : ul[k - 1];
-            const double ulpm2 = k == 0 ? ul_m2 : (k == 1 ? ul_m1 : ul[k - 2]);
-            const double urp1 = k == CPT - 1 ? ur_p : ur[k + 1];
-            const int wi = j + x - (jt - 1);
-            const double Dw = win_dl[wi], Dwm1 = win_dl[wi - 1];
-            const double Tu = win_tu[wi - 1];
-            const double Tv = win_tv[x - j + jb];
-            double R_UV = ulpm1 + (Dw - urp1);
-            double R_UVm1 = ulnm1 + (Dw - urn[k]);
-            double R_Um1Vm1 = ulpm2 + (Dwm1 - ur[k]);
-            if (x == 0) { R_UVm1 = 0.0; R_Um1Vm1 = 0.0; }
-            const double bt = R_UVm1;
-            const double at = Tu - R_Um1Vm1 + rho[k];
-            const double gt = Tv - R_UV;
-            const double dt = Cr - at - bt - gt;
+            const A apm1 = k == 0 ? ap_m1 : al[k - 1];
+            const A anm1 = k == 0 ? (ap_m1 + excl) : an[k - 1];
+            const A ulnm1 = k == 0 ? (excl + ul_m2) : uln[k - 1];
+            const A ulpm1 = k == 0 ? ul_m1 : ul[k - 1];
+            const A ulpm2 = k == 0 ? ul_m2 : (k == 1 ? ul_m1 : ul[k - 2]);
+            const A urp1 = k == CPT - 1 ? ur_p : ur[k + 1];
+            const A Dw = dlw[k + 1], Dwm1 = dlw[k];
+            const A Tu = win_tu[wi0 + k - 1];
+            const A Tv = win_tv[x - j + jb];
+            A R_UV = ulpm1 + (Dw - urp1);
+            A R_UVm1 = ulnm1 + (Dw - urn[k]);
+            A R_Um1Vm1 = ulpm2 + (Dwm1 - ur[k]);
+            if (x == 0) { R_UVm1 = (A)0; R_Um1Vm1 = (A)0; }
+            const A bt = R_UVm1;
+            const A at = Tu - R_Um1Vm1 + rho[k];
+            const A gt = Tv - R_UV;
             if (OUT == OUT_CH8) {
+                const A dt = Cr - at - bt - gt;
                 double* ch = S.ch8 + (size_t)b * 8 * D.nn + (size_t)j * n + x;
                 const size_t nn = D.nn;
                 ch[0] = an[k];
-                ch[nn] = cfi[k] - an[k];
-                ch[2 * nn] = Cr - cfi[k] - rf1 + an[k];
+                ch[nn] = cc[k] - an[k];
+                ch[2 * nn] = Cr - cc[k] - rf1 + an[k];
                 ch[3 * nn] = rf1 - an[k];
                 ch[4 * nn] = at;
                 ch[5 * nn] = bt;
                 ch[6 * nn] = gt;
                 ch[7 * nn] = dt;
             } else {
-                const double a = 0.25 * (apm1 + al[k] + anm1 + an[k]);
-                const double cavg = 0.5 * (cfe[k] + cfi[k]), ravg = 0.5 * (rf0 + rf1);
-                const double bS = cavg - a, dS = ravg - a, gS = Cr - cavg - ravg + a;
-                const double xc = ((double)x + 0.5) / nd;
-                double q1x, q1y, q3x, q3y, q2x, q2y, q4x, q4y;  // displacement.py:56-74
-                if (yc < xc) { q1x = 1.0; q1y = 1.0 + yc - xc; q3x = xc - yc; q3y = 0.0; }
-                else { q1x = 1.0 - yc + xc; q1y = 1.0; q3x = 0.0; q3y = yc - xc; }
-                if (xc + yc < 1.0) { q2x = xc + yc; q2y = 0.0; q4x = 0.0; q4y = xc + yc; }
-                else { q2x = 1.0; q2y = xc + yc - 1.0; q4x = xc + yc - 1.0; q4y = 1.0; }
-                const double ux = (a * q1x + bS * q2x + gS * q3x + dS * q4x + at * xc + bt + gt * xc) * inv2m;
-                const double uy = (a * q1y + bS * q2y + gS * q3y + dS * q4y + at + bt * yc + dt * yc) * inv2m;
+                // anchor combination (displacement.py:128-130) with b = cavg-a, d = ravg-a,
+                // g = C-cavg-ravg+a, delta_t = C-at-bt-gt; since q1+q3 = (1+x-y, 1-x+y) and
+                // q2+q4 = (x+y, x+y) in every case, a's coefficient is (1-2y, 1-2x).
+                const A a = (A)0.25 * (apm1 + al[k] + anm1 + an[k]);
+                const A cavg = cc[k];
+                const A K = cavg + ravg - Cr;
+                const A xc = xc0 + (A)k * inv_n, s2 = xc + yc;
+                const bool below = yc < xc, near = s2 < (A)1;  // displacement.py:62,67
+                const A q3x = below ? xc - yc : (A)0, q3y = below ? (A)0 : yc - xc;
+                const A q2x = near ? s2 : (A)1, q2y = near ? (A)0 : s2 - (A)1;
+                const A q4x = near ? (A)0 : s2 - (A)1, q4y = near ? s2 : (A)1;
+                const A ux = (a * ((A)1 - (A)2 * yc) + cavg * q2x + ravg * q4x - K * q3x + xc * (at + gt) + bt) * inv2m;
+                const A uy = (a * ((A)1 - (A)2 * xc) + cavg * q2y + ravg * q4y - K * q3y + at + yc * (Cr - at - gt)) * inv2m;
                 UT* o = uf + ((size_t)j * n + x) * 2;
                 o[0] = (UT)ux;
                 o[1] = (UT)uy;
