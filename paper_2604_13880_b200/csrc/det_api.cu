@@ -347,6 +347,9 @@ static int raster_start(det_ctx* ctx) {
 // ================================ C-ABI ======================================
 extern "C" {
 
+static int labels_to_host(det_ctx* ctx, int b, int32_t* out);
+
+
 int det_abi_version(void) { return 1; }
 
 const char* det_last_error(const det_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
@@ -519,8 +522,10 @@ int det_rasterize(det_ctx* ctx, int b, int32_t* labels_out, int64_t* counts_out)
     Carto hs;
     CK(cudaMemcpy(&hs, ctx->st.p + b, sizeof(Carto), cudaMemcpyDeviceToHost));
     if (hs.err & E_NEGIDX) return fail(ctx, DET_E_VALUE, "'list' argument must have no negative elements");
-    const size_t nn = (size_t)ctx->n * ctx->n;
-    if (labels_out) CK(cudaMemcpy(labels_out, ctx->labels.p + b * nn, nn * sizeof(int), cudaMemcpyDeviceToHost));
+    if (labels_out) {
+        const int rc2 = labels_to_host(ctx, b, labels_out);
+        if (rc2) return rc2;
+    }
     if (counts_out) {
         std::vector<int> c(ctx->R + 1);
         CK(cudaMemcpy(c.data(), ctx->cnt_acc.p + (size_t)b * (ctx->R + 1), (ctx->R + 1) * sizeof(int), cudaMemcpyDeviceToHost));
@@ -769,12 +774,21 @@ int det_get_vertices(det_ctx* ctx, int b, double* xy_out) {
     return DET_OK;
 }
 
+static int labels_to_host(det_ctx* ctx, int b, int32_t* out) {
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    DVec<int> tmp;
+    CK(tmp.alloc(nn));
+    k_rank_to_index<<<592, 256, 0, ctx->stream>>>(ctx->labels.p + b * nn, ctx->rank_region.p, nn, tmp.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, tmp.p, nn * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return DET_OK;
+}
+
 int det_get_labels(det_ctx* ctx, int b, int32_t* out) {
     if (!ctx || !out || b < 0 || b >= ctx->B) return fail(ctx, DET_E_ARG, "bad arguments");
     cudaSetDevice(ctx->device);
-    const size_t nn = (size_t)ctx->n * ctx->n;
-    CK(cudaMemcpy(out, ctx->labels.p + b * nn, nn * sizeof(int), cudaMemcpyDeviceToHost));
-    return DET_OK;
+    return labels_to_host(ctx, b, out);
 }
 
 int det_get_counts(det_ctx* ctx, int b, int64_t* out) {

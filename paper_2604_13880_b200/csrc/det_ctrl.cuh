@@ -196,10 +196,11 @@ __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int r = r0 + q * blockDim.x + t;
-            if (r < R) {
+            if (r < R) {  // the label texture holds ranks: LUT indexed by rank
                 const double v = mc * (sv[q] / ov[q]) - 1.0;
-                lut[r] = v;
-                lutf[r] = (float)v;
+                const int k = T.region_rank[r];
+                lut[k] = v;
+                lutf[k] = (float)v;
             }
         }
     }

@@ -30,7 +30,7 @@ namespace det {
 
 constexpr int RW_WARPS = 4;      // warps (regions) per k_region block
 constexpr int RW_ROWCAP = 384;   // vertex rows kept in smem per warp
-constexpr int RW_TCAP = 512;     // toggles per warp window
+constexpr int RW_TCAP = 256;     // toggles per warp window
 constexpr int RW_WROWS = 128;    // texture rows per warp window
 constexpr int RW_UNROLL = 4;     // vertex rows in flight per lane (latency hiding)
 
@@ -117,12 +117,13 @@ __device__ __forceinline__ int warp_excl_scan_int(int v, int lane, int* total) {
 }
 
 template <typename UT>
-__global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mode, int gate, int src) {
-    __shared__ double2 s_pos[RW_WARPS][RW_ROWCAP];
+__global__ void __launch_bounds__(RW_WARPS * 32, 8) k_region(Topo T, Bufs D, int mode, int gate, int src) {
+    __shared__ int s_jr[RW_WARPS][RW_ROWCAP];       // ceil(y*n - 0.5) clipped to [0, n]
+    __shared__ uint16_t s_nx[RW_WARPS][RW_ROWCAP];  // next row of the same ring (region-local index)
+    __shared__ int s_tot[RW_WARPS];
     __shared__ uint32_t s_key[RW_WARPS][RW_TCAP];
     __shared__ uint16_t s_col[RW_WARPS][RW_TCAP];
     __shared__ int s_rc[RW_WARPS][RW_WROWS + 1];
-    __shared__ int s_tot[RW_WARPS];
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int r = blockIdx.x * RW_WARPS + wid, b = blockIdx.y;
@@ -135,7 +136,8 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
     const int nrows = row1 - row0;
     const size_t ub = (size_t)b * T.n_rows;
     const bool in_smem = nrows <= RW_ROWCAP;
-    double2* spos = s_pos[wid];
+    int* sjr = s_jr[wid];
+    uint16_t* snx = s_nx[wid];
     uint32_t* keys = s_key[wid];
     uint16_t* colb = s_col[wid];
     int* rc = s_rc[wid];
@@ -154,8 +156,9 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
     const double2* gpos = (mode & M_ADVECT) ? pout : pin;  // row positions for huge regions
     const UT* uf = reinterpret_cast<const UT*>(D.uf) + (size_t)b * D.nn * 2;
 
-    // ---- phase A: advect every vertex row of the region (RW_UNROLL rows in flight per lane) ----
-    double xmn = INFINITY, xmx = -INFINITY, ymn = INFINITY, ymx = -INFINITY;
+    // ---- phase A: advect every vertex row (RW_UNROLL rows in flight per lane); per-row
+    //      scaled coordinates and scanline / column indices for the raster ----
+    int jmn = n, jmx = 0, imn = n, imx = 0;
     int ncl = 0;
     for (int base = row0; base < row1; base += 32 * RW_UNROLL) {
         double2 p[RW_UNROLL];
@@ -195,9 +198,18 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
                 pout[v] = nq[q];
                 if (bestcopy) D.best[ub + v] = p[q];
             }
-            if (in_smem) spos[v - row0] = nq[q];
-            xmn = nq[q].x < xmn ? nq[q].x : xmn; xmx = nq[q].x > xmx ? nq[q].x : xmx;
-            ymn = nq[q].y < ymn ? nq[q].y : ymn; ymx = nq[q].y > ymx ? nq[q].y : ymx;
+            // x*n, y*n are exact (n is a power of two); ceil is monotone, so the crop
+            // (raster.py:71-74) and each edge's scanline range (raster.py:45-46) are
+            // min/max of these per-row integers
+            const double xs = __dmul_rn(nq[q].x, nd), ys = __dmul_rn(nq[q].y, nd);
+            const int jr = min(max(ceil_to_int(__dsub_rn(ys, 0.5)), 0), n);
+            const int ir = min(max(ceil_to_int(__dsub_rn(xs, 0.5)), 0), n);
+            if (in_smem) {
+                sjr[v - row0] = jr;
+                snx[v - row0] = (uint16_t)(T.row_next[v] - row0);
+            }
+            jmn = min(jmn, jr); jmx = max(jmx, jr);
+            imn = min(imn, ir); imx = max(imx, ir);
         }
     }
     if (mode & M_ADVECT) {
@@ -205,17 +217,11 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
         if (lane == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
     }
     if (!(mode & M_RASTER)) return;
-    xmn = warp_allmin(xmn); xmx = warp_allmax(xmx);
-    ymn = warp_allmin(ymn); ymx = warp_allmax(ymx);
-    __syncwarp();  // row positions (smem, or this warp's global writes) visible to the warp
+    const int j_off = warp_allmin(jmn), j_end = warp_allmax(jmx);
+    const int i_off = warp_allmin(imn), i_end = warp_allmax(imx);
+    __syncwarp();  // row data (smem, or this warp's global writes) visible to the warp
 
     int* cnt = D.cnt_acc + (size_t)b * (T.R + 1);
-    // ---- region crop (raster.py:70-78) ----
-    // ceil then int cast == round-toward-+inf conversion (cvt.rpi), exact for |v| < 2^31
-    const int j_off = min(max(ceil_to_int(__dsub_rn(__dmul_rn(ymn, nd), 0.5)), 0), n);
-    const int j_end = min(max(ceil_to_int(__dsub_rn(__dmul_rn(ymx, nd), 0.5)), 0), n);
-    const int i_off = min(max(ceil_to_int(__dsub_rn(__dmul_rn(xmn, nd), 0.5)), 0), n);
-    const int i_end = min(max(ceil_to_int(__dsub_rn(__dmul_rn(xmx, nd), 0.5)), 0), n);
     const int rows = max(j_end - j_off, 0), cols = max(i_end - i_off, 0);
     if (rows == 0 || cols == 0) {
         if (lane == 0) cnt[r] = 0;
@@ -230,24 +236,36 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
     while (w0 < j_end) {
         const int w1 = min(w0 + wh, j_end);
         const int W = w1 - w0;
-        if (lane == 0) s_tot[wid] = 0;
         for (int q = lane; q <= W; q += 32) rc[q] = 0;
         __syncwarp();
         // ---- crossings of every ring edge (raster.py:30-61, flattening :86-89) ----
+        if (lane == 0) s_tot[wid] = 0;
+        __syncwarp();
         for (int e = row0 + lane; e < row1; e += 32) {
-            const int en = T.row_next[e];
-            const double2 a = in_smem ? spos[e - row0] : gpos[e];
-            const double2 c = in_smem ? spos[en - row0] : gpos[en];
-            const double x0 = __dmul_rn(a.x, nd), y0 = __dmul_rn(a.y, nd);
-            const double x1 = __dmul_rn(c.x, nd), y1 = __dmul_rn(c.y, nd);
-            if (y0 == y1) continue;
-            const double ylo = y0 < y1 ? y0 : y1, yhi = y0 < y1 ? y1 : y0;
-            const int jlo = min(max(ceil_to_int(__dsub_rn(ylo, 0.5)), 0), n);
-            const int jhi = min(max(ceil_to_int(__dsub_rn(yhi, 0.5)), 0), n);
-            const int js = max(jlo, w0);
-            const int je = min(jhi, w1 + back);
-            if (je <= js) continue;
-            const double slope = __ddiv_rn(__dsub_rn(x1, x0), __dsub_rn(y1, y0));
+            int ja, jb2, en;
+            double2 a, c;
+            if (in_smem) {
+                en = snx[e - row0];
+                ja = sjr[e - row0];
+                jb2 = sjr[en];
+            } else {
+                en = T.row_next[e] - row0;
+                a = gpos[e];
+                c = gpos[row0 + en];
+                ja = min(max(ceil_to_int(__dsub_rn(__dmul_rn(a.y, nd), 0.5)), 0), n);
+                jb2 = min(max(ceil_to_int(__dsub_rn(__dmul_rn(c.y, nd), 0.5)), 0), n);
+            }
+            const int js = max(min(ja, jb2), w0);  // scanlines j in [jlo, jhi) are crossed
+            const int je = min(max(ja, jb2), w1 + back);
+            if (je <= js) continue;  // most short edges cross no scanline centre
+            if (in_smem) {  // endpoints only for the edges that cross a scanline (L1/L2-resident)
+                a = gpos[e];
+                c = gpos[row0 + en];
+            }
+            a = make_double2(__dmul_rn(a.x, nd), __dmul_rn(a.y, nd));
+            c = make_double2(__dmul_rn(c.x, nd), __dmul_rn(c.y, nd));
+            const double x0 = a.x, y0 = a.y;
+            const double slope = __ddiv_rn(__dsub_rn(c.x, a.x), __dsub_rn(c.y, a.y));
             double yc = (double)js + 0.5;  // scanline centre j + 0.5 (exact, stepped by 1.0)
             for (int j = js; j < je; ++j, yc += 1.0) {
                 const double xc = __dadd_rn(x0, __dmul_rn(__dsub_rn(yc, y0), slope));
@@ -263,8 +281,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
                     cc = (int)(f - dr * width);
                     dest = j_off + (int)dr;
                 }
-                if (cc == cols) continue;  // absorber column
-                if (dest < w0 || dest >= w1) continue;
+                if (cc == cols || dest < w0 || dest >= w1) continue;  // absorber column / other window
                 const int slot = atomicAdd(&s_tot[wid], 1);
                 if (slot < RW_TCAP) {
                     keys[slot] = ((uint32_t)(dest - w0) << 16) | (uint32_t)(i_off + cc);
@@ -274,6 +291,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
         }
         __syncwarp();
         const int tot = s_tot[wid];
+        __syncwarp();
         if (tot > RW_TCAP) {
             if (W == 1) {
                 if (lane == 0) atomicOr(&st->err, (int)E_TOGGLE_OVF);
@@ -283,7 +301,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
             __syncwarp();
             continue;
         }
-        // ---- counting sort by row: rc -> exclusive offsets (rc[W] = total) ----
+        // ---- counting sort by row: rc -> exclusive offsets ----
         {
             int carry = 0;
             for (int q0 = 0; q0 < W; q0 += 32) {
@@ -295,7 +313,6 @@ __global__ void __launch_bounds__(RW_WARPS * 32) k_region(Topo T, Bufs D, int mo
                 if (q < W) rc[q] = carry + ex;
                 carry += chunk;
             }
-            if (lane == 0) rc[W] = carry;
         }
         __syncwarp();
         // scatter columns into row buckets; a bucket's cursor runs from its start to the next start
@@ -392,11 +409,11 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
             }
         }
         __syncwarp();
-        int* lab = D.labels + (size_t)b * D.nn + (size_t)j * n;
-        for (int i = lane; i < n; i += 32) {
-            const uint32_t rk = lab_s[i];
-            lab[i] = (rk == SENT) ? -1 : T.rank_region[rk];
-        }
+        // the label texture holds region RANKS (-1 = background); det_get_labels maps them
+        // back to region indices (raster.py:107 stores indices) -- saves a gather per pixel
+        int4* lab4 = reinterpret_cast<int4*>(D.labels + (size_t)b * D.nn + (size_t)j * n);
+        const int4* src4 = reinterpret_cast<const int4*>(lab_s);
+        for (int i = lane; i < (n >> 2); i += 32) lab4[i] = src4[i];  // SENT == -1 bitwise
         if (lost) {  // order the (rare) count corrections before this CTA signs off
             __threadfence();
         }
@@ -409,6 +426,15 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
     __threadfence();
     if (threadIdx.x == 0) D.rowdone[b] = 0;
     ctrl_body(T, D, b, ctrl_mode);
+}
+
+// Rank texture -> region-index texture (output format of rasterize_labels).
+__global__ void k_rank_to_index(const int* __restrict__ rk, const int* __restrict__ rank_region, size_t nn,
+                                int* __restrict__ out) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nn; i += (size_t)gridDim.x * blockDim.x) {
+        const int v = rk[i];
+        out[i] = v < 0 ? -1 : rank_region[v];
+    }
 }
 
 // Stage-level advect (displacement.py:229-238) on a float64 field.
