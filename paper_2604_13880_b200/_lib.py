@@ -50,6 +50,7 @@ EXPORTS = {
     "det_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
     "det_ctx_destroy": (None, [ctypes.c_void_p]),
     "det_set_band_height": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
+    "det_set_groups": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int]),
     "det_load_map": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, ctypes.c_int, _c_int32_p, ctypes.c_int,
                                      _c_int32_p, _c_int32_p, ctypes.c_int]),
     "det_set_batch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p, _c_double_p]),
@@ -153,6 +154,9 @@ class Context:
         x = None if xy is None else np.ascontiguousarray(xy, dtype=np.float64).reshape(b, self.n_rows, 2)
         self.check(self.lib.det_set_batch(self.h, b, _p(x, ctypes.c_double), _p(st, ctypes.c_double)))
         self.B = b
+
+    def set_groups(self, g):
+        self.check(self.lib.det_set_groups(self.h, int(g)))
 
     def set_band_height(self, h):
         self.check(self.lib.det_set_band_height(self.h, int(h)))

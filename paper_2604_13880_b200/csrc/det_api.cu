@@ -78,6 +78,8 @@ struct det_ctx {
     // graph
     cudaGraphExec_t gexec = nullptr;
     bool g_valid = false;
+    int groups = 2;
+    std::vector<cudaStream_t> gstreams;
 };
 
 #define CK(expr)                                                                   \
@@ -136,9 +138,10 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     const bool f32 = (src == SRC_LABELS && out == OUT_U && !u64);
     const size_t smem1 = (size_t)2 * (n + c->H - 1) * (f32 ? sizeof(float) : sizeof(double));
     if (src == SRC_LABELS) {
-        if (f32) {
-            cudaFuncSetAttribute(k_sat1<CPT, NT, SRC_LABELS, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-            k_sat1<CPT, NT, SRC_LABELS, float><<<gb, NT, smem1, c->stream>>>(T, D, S, gate);
+        if (f32) {  // smem-staged band
+            const size_t sm1s = ((size_t)c->H * n + 2 * (n + c->H - 1) + std::min(c->R + 1, LUT_SMEM_MAX)) * sizeof(float);
+            cudaFuncSetAttribute(k_sat1s<CPT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1s);
+            k_sat1s<CPT, NT><<<gb, NT, sm1s, c->stream>>>(T, D, gate);
         } else {
             cudaFuncSetAttribute(k_sat1<CPT, NT, SRC_LABELS, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
             k_sat1<CPT, NT, SRC_LABELS, double><<<gb, NT, smem1, c->stream>>>(T, D, S, gate);
@@ -150,7 +153,9 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     const int lanes = n + 2 * (2 * n - 1);
     const int G = std::min(8, c->nb);
     k_sat2<<<dim3((lanes + 31) / 32 + 1, B), 32 * G, 0, c->stream>>>(D, gate);
-    const size_t smem = (size_t)3 * (n + c->H) * (f32 ? sizeof(float) : sizeof(double));
+    const size_t smem = (size_t)3 * (n + c->H) * (f32 ? sizeof(float) : sizeof(double)) +
+                        (f32 ? ((size_t)c->H * n + (size_t)c->H * NT + std::min(c->R + 1, LUT_SMEM_MAX)) * sizeof(float)
+                             : 0);  // + staged band, row prefixes, LUT
 #define DET_SAT3(SRC_, UT_, OUT_)                                                                            \
     do {                                                                                                     \
         auto fn = k_sat3<CPT, NT, SRC_, UT_, OUT_, UT_>;                                                     \
@@ -202,14 +207,22 @@ static void launch_row(det_ctx* c, const Topo& T, const Bufs& D, int gate, int c
     k_row<<<dim3((c->n + rpc - 1) / rpc, c->B), rpc * 32, smem, c->stream>>>(T, D, gate, ctrl_mode);
 }
 
-static void enqueue_iteration(det_ctx* c) {
+static void enqueue_iteration(det_ctx* c, int b0 = 0, int Bg = -1, cudaStream_t s = nullptr) {
+    if (Bg < 0) Bg = c->B;
+    cudaStream_t keep = c->stream;
+    if (s) c->stream = s;
     const Topo T = make_topo(c);
-    const Bufs D = make_bufs(c);
+    Bufs D = make_bufs(c);
+    D.b0 = b0;
+    const int Bsave = c->B;
+    c->B = Bg;  // grid.y of every launch below
     SatSrc S;
     memset(&S, 0, sizeof(S));
-    launch_sat(c, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, c->f64 != 0, c->B);
+    launch_sat(c, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, c->f64 != 0, Bg);
     launch_region(c, T, D, M_ADVECT | M_RASTER, G_ACTIVE, 0);
     launch_row(c, T, D, G_ACTIVE, 0);
+    c->B = Bsave;
+    c->stream = keep;
 }
 
 static void invalidate_graph(det_ctx* c) {
@@ -218,16 +231,37 @@ static void invalidate_graph(det_ctx* c) {
     c->g_valid = false;
 }
 
+// Frame groups: the batch is split into up to kGroups contiguous groups whose iteration
+// chains are independent branches of one graph, so kernels of different groups overlap.
 static int ensure_graph(det_ctx* c) {
     det_ctx* ctx = c;
     if (c->g_valid) return DET_OK;
     invalidate_graph(c);
-    cudaGraph_t g;
+    const int G = std::max(1, std::min(c->groups, c->B));
+    while ((int)c->gstreams.size() < G) {
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        c->gstreams.push_back(s);
+    }
+    cudaEvent_t fork, join[16];
+    CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    for (int g = 0; g < G; ++g) CK(cudaEventCreateWithFlags(&join[g], cudaEventDisableTiming));
+    cudaGraph_t graph;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < kGraphIters; ++i) enqueue_iteration(c);
-    CK(cudaStreamEndCapture(c->stream, &g));
-    cudaError_t e = cudaGraphInstantiate(&c->gexec, g, 0);
-    cudaGraphDestroy(g);
+    CK(cudaEventRecord(fork, c->stream));
+    for (int g = 0; g < G; ++g) {
+        const int b0 = (int)((long long)c->B * g / G), b1 = (int)((long long)c->B * (g + 1) / G);
+        cudaStream_t s = c->gstreams[g];
+        CK(cudaStreamWaitEvent(s, fork, 0));
+        for (int i = 0; i < kGraphIters; ++i) enqueue_iteration(c, b0, b1 - b0, s);
+        CK(cudaEventRecord(join[g], s));
+        CK(cudaStreamWaitEvent(c->stream, join[g], 0));
+    }
+    CK(cudaStreamEndCapture(c->stream, &graph));
+    cudaError_t e = cudaGraphInstantiate(&c->gexec, graph, 0);
+    cudaGraphDestroy(graph);
+    cudaEventDestroy(fork);
+    for (int g = 0; g < G; ++g) cudaEventDestroy(join[g]);
     CK(e);
     c->g_valid = true;
     return DET_OK;
@@ -259,9 +293,11 @@ static int alloc_sat(det_ctx* ctx, int B) {
 }
 
 static int auto_band_height(int n, int B) {
-    // enough band CTAs to fill the 148 SMs twice over, but tall bands amortise the carries
+    // enough band CTAs to fill the 148 SMs twice over, but tall bands amortise the carries;
+    // the float path stages H x n floats in shared memory (<= 64 KB)
     int h = 8;
     while (h < 64 && (long long)(n / (2 * h)) * B >= 2 * 148) h *= 2;
+    while (h > 1 && (size_t)h * n * sizeof(float) > 64 * 1024) h >>= 1;
     return std::min(h, n);
 }
 
@@ -393,8 +429,16 @@ void det_ctx_destroy(det_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     invalidate_graph(ctx);
+    for (cudaStream_t s : ctx->gstreams) cudaStreamDestroy(s);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
+}
+
+int det_set_groups(det_ctx* ctx, int groups) {
+    if (!ctx || groups < 1 || groups > 16) return fail(ctx, DET_E_ARG, "groups must be in [1, 16]");
+    ctx->groups = groups;
+    invalidate_graph(ctx);
+    return DET_OK;
 }
 
 int det_set_band_height(det_ctx* ctx, int h) {

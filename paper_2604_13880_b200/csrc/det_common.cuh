@@ -59,6 +59,7 @@ struct Topo {
 
 struct Bufs {
     int B, n, k, cap, H, nb;
+    int b0;           // first cartogram of this launch (frame groups run as parallel graph branches)
     size_t nn;
     double2* pos0;
     double2* pos1;

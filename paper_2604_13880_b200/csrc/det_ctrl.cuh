@@ -213,8 +213,8 @@ __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
 
 // Host-driven control step (evaluation of the start state): one CTA per cartogram.
 __global__ void __launch_bounds__(CTRL_THREADS) k_ctrl(Topo T, Bufs D, int cmode, int gate) {
-    if (!gate_open(D.st + blockIdx.x, gate)) return;
-    ctrl_body(T, D, blockIdx.x, cmode);
+    if (!gate_open(D.st + blockIdx.x + D.b0, gate)) return;
+    ctrl_body(T, D, blockIdx.x + D.b0, cmode);
 }
 
 }  // namespace det

@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, 8) k_region(Topo T, Bufs D, int
     __shared__ int s_rc[RW_WARPS][RW_WROWS + 1];
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int r = blockIdx.x * RW_WARPS + wid, b = blockIdx.y;
+    const int r = blockIdx.x * RW_WARPS + wid, b = blockIdx.y + D.b0;
     if (r >= T.R) return;
     Carto* st = D.st + b;
     if (!gate_open(st, gate)) return;
@@ -360,7 +360,7 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
     extern __shared__ uint32_t s_lab[];  // [rows per CTA][n]
     __shared__ int s_last;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, rpc = blockDim.x >> 5;
-    const int b = blockIdx.y, n = D.n;
+    const int b = blockIdx.y + D.b0, n = D.n;
     const int j = blockIdx.x * rpc + wid;
     Carto* st = D.st + b;
     if (!gate_open(st, gate)) return;

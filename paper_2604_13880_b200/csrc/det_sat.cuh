@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
     __shared__ A s_bd[3][32];
     __shared__ A s_ba[3][32];
     __shared__ double s_red[33];
-    const int band = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
+    const int band = blockIdx.x, b = blockIdx.y + D.b0, t = threadIdx.x;
     const int lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
     if (!gate_open(D.st + b, gate)) return;
     const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, L = n + H - 1;
@@ -189,6 +189,104 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
 }
 
 // ---------------------------------------------------------------------------------
+// float32 path, smem-staged: the band's H x n residual densities are loaded once (all
+// label/LUT loads independent -> high memory-level parallelism) into shared memory.
+constexpr int LUT_SMEM_MAX = 16384;  // float LUT entries copied to shared memory per CTA
+
+// Copy the cartogram's float LUT (R+1 entries) into shared memory when it fits; returns the
+// table to gather from (smem copy or the global array).
+__device__ __forceinline__ const float* stage_lut(const Bufs& D, int R, int b, float* s_lut) {
+    const float* g = D.lutf + (size_t)b * (R + 1);
+    if (R + 1 > LUT_SMEM_MAX) return g;
+    for (int i = threadIdx.x; i <= R; i += blockDim.x) s_lut[i] = __ldg(g + i);
+    __syncthreads();
+    return s_lut;
+}
+
+template <int CPT>
+__device__ __forceinline__ void stage_rho_band(const Bufs& D, const float* lut, int R, int b, int jt, int H, int x0,
+                                               float* rho) {
+    const int n = D.n;
+    if (x0 >= n) return;
+    const int* lab = D.labels + (size_t)b * D.nn + (size_t)jt * n + x0;
+    for (int j0 = 0; j0 < H; j0 += 4) {
+        int L[4][CPT];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (j0 + q >= H) continue;
+#pragma unroll
+            for (int k = 0; k < CPT; k += 2) {
+                const int2 v = *reinterpret_cast<const int2*>(lab + (size_t)(j0 + q) * n + k);
+                L[q][k] = v.x;
+                L[q][k + 1] = v.y;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (j0 + q >= H) continue;
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) rho[(j0 + q) * n + x0 + k] = lut[L[q][k] < 0 ? R : L[q][k]];
+        }
+    }
+}
+
+// k_sat1 for the float32 path: band sums straight from the staged band, no per-row barriers.
+template <int CPT, int NT>
+__global__ void __launch_bounds__(NT) k_sat1s(Topo T, Bufs D, int gate) {
+    extern __shared__ float s_f1[];  // rho[H][n] | dg[L] | ad[L] | lut[R+1]
+    __shared__ double s_red[33];
+    const int band = blockIdx.x, b = blockIdx.y + D.b0, t = threadIdx.x;
+    const int lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+    if (!gate_open(D.st + b, gate)) return;
+    const int n = D.n, H = D.H, jt = band * H, L = n + H - 1;
+    const int x0 = t * CPT;
+    const size_t bb = (size_t)b * D.nb + band;
+    float* rho = s_f1;
+    float* dg = rho + H * n;
+    float* ad = dg + L;
+    const float* lut = stage_lut(D, T.R, b, ad + L);
+    stage_rho_band<CPT>(D, lut, T.R, b, jt, H, x0, rho);
+    __syncthreads();
+    for (int jj = w; jj < H; jj += nw) {  // row totals
+        float s = 0.f;
+        for (int x = lane; x < n; x += 32) s += rho[jj * n + x];
+        s = warp_sum(s);
+        if (lane == 0) D.rt[(size_t)b * n + jt + jj] = (double)s;
+    }
+    for (int q = t; q < L; q += blockDim.x) {
+        float sd = 0.f, sa = 0.f;
+        for (int jj = 0; jj < H; ++jj) {
+            const int xd = q - (H - 1) + jj;  // diagonal q = x - j + jb
+            const int xa = q - jj;            // anti-diagonal q = x + j - jt
+            if (xd >= 0 && xd < n) sd += rho[jj * n + xd];
+            if (xa >= 0 && xa < n) sa += rho[jj * n + xa];
+        }
+        dg[q] = sd;
+        ad[q] = sa;
+    }
+    double cs[CPT], csum = 0.0;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        float c = 0.f;
+        const int x = x0 + k;
+        if (x < n)
+            for (int jj = 0; jj < H; ++jj) c += rho[jj * n + x];
+        cs[k] = (double)c;
+        csum += cs[k];
+    }
+    double tot;
+    double run = block_excl_scan(csum, s_red, &tot);  // (its barriers also publish dg/ad)
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int x = x0 + k;
+        run += cs[k];
+        if (x < n) D.cs[bb * n + x] = run;
+    }
+    block_prefix_smem<float>(dg, D.dgc + bb * L, L, s_red);
+    block_prefix_smem<float>(ad, D.adc + bb * L, L, s_red);
+}
+
+// ---------------------------------------------------------------------------------
 // Band-direction carries.  Lanes: [0,n) columns x, [n,3n-1) diagonals (idx=v+n-1),
 // [3n-1,5n-2) anti-diagonals w.  blockDim = 32*G (G band groups).  The last block
 // column computes rowfull (row-total prefix) instead.  Outputs per band b:
@@ -199,7 +297,7 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
 __global__ void k_sat2(Bufs D, int gate) {
     __shared__ double s_g[32][33];
     __shared__ double s_red[33];
-    const int b = blockIdx.y, t = threadIdx.x, lx = t & 31, g = t >> 5, G = blockDim.x >> 5;
+    const int b = blockIdx.y + D.b0, t = threadIdx.x, lx = t & 31, g = t >> 5, G = blockDim.x >> 5;
     if (!gate_open(D.st + b, gate)) return;
     const int n = D.n, H = D.H, nb = D.nb, L = n + H - 1, M = 2 * n - 1;
     if (blockIdx.x == gridDim.x - 1) {
@@ -286,7 +384,7 @@ __global__ void __launch_bounds__(NT) k_sat3(Topo T, Bufs D, SatSrc S, int gate)
     extern __shared__ unsigned char s_raw3[];
     __shared__ A s_w[3][32];
     __shared__ A s_xa[3][32], s_xu1[3][32], s_xu2[3][32], s_xr[3][32];
-    const int band = blockIdx.x, b = blockIdx.y, t = threadIdx.x;
+    const int band = blockIdx.x, b = blockIdx.y + D.b0, t = threadIdx.x;
     const int lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
     if (!gate_open(D.st + b, gate)) return;
     const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, M = 2 * n - 1;
@@ -335,27 +433,85 @@ __global__ void __launch_bounds__(NT) k_sat3(Topo T, Bufs D, SatSrc S, int gate)
     const A inv2m = (A)(S.outscale != 0.0 ? S.outscale : 0.5 * inv_nd * inv_nd);
     const A xc0 = (A)(((double)x0 + 0.5) * inv_nd);  // pixel-centre x of column x0 (displacement.py:59)
     UT* uf = reinterpret_cast<UT*>(D.uf) + (size_t)b * D.nn * 2;
+    constexpr bool STAGED = (sizeof(A) == 4 && SRC == SRC_LABELS);
+    float* srho = reinterpret_cast<float*>(win_dl + 3 * WN);  // staged band (float path)
+    A* s_ex = reinterpret_cast<A*>(srho + (size_t)H * n);      // A(j, x0-1) per (row, thread)
+    __shared__ A s_wt[64][33];                                      // warp totals per row (H <= 64)
     A rho_n[CPT];
-    load_rho<CPT, SRC, A>(D, S, T.R, b, jt, x0, rho_n);
+    if (STAGED) {
+        const float* lut = stage_lut(D, T.R, b, reinterpret_cast<float*>(s_ex + (size_t)H * NT));
+        stage_rho_band<CPT>(D, lut, T.R, b, jt, H, x0, srho);
+        __syncthreads();
+        // all H row prefixes up front: the scans are independent across rows (ILP), so the
+        // sequential row loop below only carries the vertical/diagonal recurrences
+        for (int j0 = 0; j0 < H; j0 += 4) {
+            A ts[4], wi[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                ts[q] = (A)0;
+                if (j0 + q < H && x0 < n) {
+#pragma unroll
+                    for (int k = 0; k < CPT; ++k) ts[q] += (A)srho[(j0 + q) * n + x0 + k];
+                }
+                wi[q] = ts[q];
+            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const A y = __shfl_up_sync(FULL, wi[q], o);
+                    if (lane >= o) wi[q] += y;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (j0 + q >= H) continue;
+                if (lane == 31) s_wt[j0 + q][w] = wi[q];
+                s_ex[(j0 + q) * NT + t] = wi[q] - ts[q];
+            }
+        }
+        __syncthreads();
+        if (t < H) {  // exclusive prefix of the warp totals of row t, stored in place
+            A run = (A)0;
+            for (int q = 0; q < nw; ++q) {
+                const A v = s_wt[t][q];
+                s_wt[t][q] = run;
+                run += v;
+            }
+        }
+    } else {
+        load_rho<CPT, SRC, A>(D, S, T.R, b, jt, x0, rho_n);
+    }
     __syncthreads();
 
     for (int j = jt; j <= jb; ++j) {
         const int slot = (j - jt) % 3, ps = (j - jt + 2) % 3;
         A rho[CPT];
+        if (STAGED) {
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
-        if (j < jb) load_rho<CPT, SRC, A>(D, S, T.R, b, j + 1, x0, rho_n);  // prefetch the next row
+            for (int k = 0; k < CPT; ++k) rho[k] = x0 < n ? (A)srho[(j - jt) * n + x0 + k] : (A)0;
+        } else {
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
+            if (j < jb) load_rho<CPT, SRC, A>(D, S, T.R, b, j + 1, x0, rho_n);  // prefetch the next row
+        }
         A loc[CPT];
         A run = (A)0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) { run += rho[k]; loc[k] = run; }
-        const A tsum = run;
-        const A winc = warp_incl_scan_t<A>(tsum);
-        if (lane == 31) s_w[slot][w] = winc;
-        __syncthreads();
-        A off = (A)0;
-        for (int q = 0; q < w; ++q) off += s_w[slot][q];
-        const A excl = off + winc - tsum;  // A(j, x0-1)
+        A excl;  // A(j, x0-1)
+        if (STAGED) {
+            excl = s_ex[(j - jt) * NT + t] + s_wt[j - jt][w];
+            __syncthreads();  // boundary values of the previous row (s_x*) are published
+        } else {
+            const A tsum = run;
+            const A winc = warp_incl_scan_t<A>(tsum);
+            if (lane == 31) s_w[slot][w] = winc;
+            __syncthreads();
+            A off = (A)0;
+            for (int q = 0; q < w; ++q) off += s_w[slot][q];
+            excl = off + winc - tsum;
+        }
         A ap_m1 = __shfl_up_sync(FULL, al[CPT - 1], 1);
         A ul_m1 = __shfl_up_sync(FULL, ul[CPT - 1], 1);
         A ul_m2 = __shfl_up_sync(FULL, ul[CPT - 2], 1);

@@ -270,3 +270,33 @@ def test_headline_size_properties(P):
     assert np.array_equal(res.state.labels.labels, ref)
     v = res.state.mapmodel.vertex_array()
     assert v.min() >= 0.0 and v.max() <= 1.0
+
+
+# ---------------------------------------------------------------- other texture sizes / scales
+@pytest.mark.parametrize("k", [11, 12, 13])
+def test_large_textures_raster_and_field_precision(P, k):
+    """k = 11..13 (1024-thread band CTAs): raster bit-exact vs the oracle; float32 vs float64 field agree."""
+    from paper_2604_13880_b200.synthetic import voronoi_map
+
+    m = voronoi_map(40, seed=k, target_unique=4000 * (1 << (k - 11)), sigma=0.5)
+    tex = P.rasterize_labels(m, k, check_collapse=False)
+    ref = O.FlatMap.from_mapmodel(m).labels(k)
+    assert np.array_equal(tex.labels, ref)
+    crit = P.StoppingCriteria(1e-300, 10**9, 6)
+    r32 = P.run(m, crit, k=k, field_dtype="float32")
+    r64 = P.run(m, crit, k=k, field_dtype="float64")
+    dv = np.abs(r32.state.mapmodel.vertex_array() - r64.state.mapmodel.vertex_array()).max()
+    assert dv <= 1e-5, dv
+    assert np.array_equal(r64.state.labels.labels,
+                          O.FlatMap.from_mapmodel(r64.state.mapmodel).labels(k))
+
+
+def test_many_regions_control_step(P):
+    """R = 10,000 regions (config-5 scale region count) at 2048^2: counts partition the texture."""
+    from paper_2604_13880_b200.synthetic import voronoi_map
+
+    m = voronoi_map(10_000, seed=5, target_unique=150_000, sigma=0.5)
+    res = P.run(m, P.StoppingCriteria(1e-300, 10**9, 5), k=11)
+    c = res.state.pixel_counts
+    assert c.sum() + res.state.labels.background_count() == (1 << 11) ** 2
+    assert np.array_equal(res.state.labels.labels, O.FlatMap.from_mapmodel(res.state.mapmodel).labels(11))
