@@ -177,7 +177,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=64)
     ap.add_argument("--warmup", type=int, default=8)
-    ap.add_argument("--batch", type=int, default=8, help="frames per GPU")
+    ap.add_argument("--batch", type=int, default=16, help="frames per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--band", type=int, default=0, help="band height of the integral-image kernels (0 = auto)")
     ap.add_argument("--field", default="float32", choices=["float32", "float64"])

@@ -149,6 +149,7 @@ class Context:
         self._owner_token = None  # engines re-load their map when they see another owner
 
     def set_batch(self, stats, xy=None):
+        self.generation = getattr(self, "generation", 0) + 1
         st = np.ascontiguousarray(np.atleast_2d(stats), dtype=np.float64)
         b = st.shape[0]
         x = None if xy is None else np.ascontiguousarray(xy, dtype=np.float64).reshape(b, self.n_rows, 2)
@@ -162,6 +163,7 @@ class Context:
         self.check(self.lib.det_set_band_height(self.h, int(h)))
 
     def rasterize(self, b=0, want_labels=True):
+        self.generation = getattr(self, "generation", 0) + 1
         lab = np.empty((self.n, self.n), dtype=np.int32) if want_labels else None
         cnt = np.empty(self.R + 1, dtype=np.int64)
         self.check(self.lib.det_rasterize(self.h, b, _p(lab, ctypes.c_int32), _p(cnt, ctypes.c_int64)))
@@ -177,9 +179,11 @@ class Context:
 
     def run(self, error_threshold, stagnation_window, max_iterations):
         c = DetCriteria(float(error_threshold), int(stagnation_window), int(max_iterations))
+        self.generation = getattr(self, "generation", 0) + 1
         self.check(self.lib.det_run(self.h, ctypes.byref(c)))
 
     def bench_iterations(self, iters):
+        self.generation = getattr(self, "generation", 0) + 1
         self.check(self.lib.det_bench_iterations(self.h, int(iters)))
 
     def kernel_times(self, iters):

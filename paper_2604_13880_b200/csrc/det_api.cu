@@ -8,6 +8,7 @@
 // graph launch.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <unordered_map>
@@ -79,6 +80,10 @@ struct det_ctx {
     cudaGraphExec_t gexec = nullptr;
     bool g_valid = false;
     int groups = 2;
+    Topo g_topo;  // launch signature the graph was captured with
+    Bufs g_bufs;
+    int g_groups = 0;
+    bool stage_band = false;  // smem-staged float band kernels (DET_STAGE_BAND=1)
     std::vector<cudaStream_t> gstreams;
 };
 
@@ -99,6 +104,7 @@ static int fail(det_ctx* ctx, int code, const std::string& msg) {
 
 static Topo make_topo(det_ctx* c) {
     Topo t;
+    memset(&t, 0, sizeof(t));
     t.n_rows = c->n_rows;
     t.n_uniq = c->n_uniq;
     t.R = c->R;
@@ -136,12 +142,16 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     const dim3 gb(c->nb, B);
     // float32 in-band arithmetic only for the float32 field from labels; float64 otherwise
     const bool f32 = (src == SRC_LABELS && out == OUT_U && !u64);
+    const bool staged = f32 && c->stage_band;
     const size_t smem1 = (size_t)2 * (n + c->H - 1) * (f32 ? sizeof(float) : sizeof(double));
     if (src == SRC_LABELS) {
-        if (f32) {  // smem-staged band
+        if (staged) {  // smem-staged band
             const size_t sm1s = ((size_t)c->H * n + 2 * (n + c->H - 1) + std::min(c->R + 1, LUT_SMEM_MAX)) * sizeof(float);
             cudaFuncSetAttribute(k_sat1s<CPT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1s);
             k_sat1s<CPT, NT><<<gb, NT, sm1s, c->stream>>>(T, D, gate);
+        } else if (f32) {
+            cudaFuncSetAttribute(k_sat1<CPT, NT, SRC_LABELS, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+            k_sat1<CPT, NT, SRC_LABELS, float><<<gb, NT, smem1, c->stream>>>(T, D, S, gate);
         } else {
             cudaFuncSetAttribute(k_sat1<CPT, NT, SRC_LABELS, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
             k_sat1<CPT, NT, SRC_LABELS, double><<<gb, NT, smem1, c->stream>>>(T, D, S, gate);
@@ -154,23 +164,24 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     const int G = std::min(8, c->nb);
     k_sat2<<<dim3((lanes + 31) / 32 + 1, B), 32 * G, 0, c->stream>>>(D, gate);
     const size_t smem = (size_t)3 * (n + c->H) * (f32 ? sizeof(float) : sizeof(double)) +
-                        (f32 ? ((size_t)c->H * n + (size_t)c->H * NT + std::min(c->R + 1, LUT_SMEM_MAX)) * sizeof(float)
-                             : 0);  // + staged band, row prefixes, LUT
-#define DET_SAT3(SRC_, UT_, OUT_)                                                                            \
+                        (staged ? ((size_t)c->H * n + (size_t)c->H * NT + std::min(c->R + 1, LUT_SMEM_MAX)) * sizeof(float)
+                                : 0);  // + staged band, row prefixes, LUT
+#define DET_SAT3(SRC_, UT_, OUT_, STG_)                                                                            \
     do {                                                                                                     \
-        auto fn = k_sat3<CPT, NT, SRC_, UT_, OUT_, UT_>;                                                     \
+        auto fn = k_sat3<CPT, NT, SRC_, UT_, OUT_, UT_, STG_>;                                               \
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                    \
         fn<<<gb, NT, smem, c->stream>>>(T, D, S, gate);                                                      \
     } while (0)
     if (out == OUT_CH8) {
-        if (src == SRC_LABELS) DET_SAT3(SRC_LABELS, double, OUT_CH8);
-        else DET_SAT3(SRC_DENSE, double, OUT_CH8);
+        if (src == SRC_LABELS) DET_SAT3(SRC_LABELS, double, OUT_CH8, false);
+        else DET_SAT3(SRC_DENSE, double, OUT_CH8, false);
     } else if (src == SRC_LABELS) {
-        if (u64) DET_SAT3(SRC_LABELS, double, OUT_U);
-        else DET_SAT3(SRC_LABELS, float, OUT_U);
+        if (u64) DET_SAT3(SRC_LABELS, double, OUT_U, false);
+        else if (staged) DET_SAT3(SRC_LABELS, float, OUT_U, true);
+        else DET_SAT3(SRC_LABELS, float, OUT_U, false);
     } else {
-        if (u64) DET_SAT3(SRC_DENSE, double, OUT_U);
-        else DET_SAT3(SRC_DENSE, float, OUT_U);
+        if (u64) DET_SAT3(SRC_DENSE, double, OUT_U, false);
+        else DET_SAT3(SRC_DENSE, float, OUT_U, false);
     }
 #undef DET_SAT3
 }
@@ -235,7 +246,17 @@ static void invalidate_graph(det_ctx* c) {
 // chains are independent branches of one graph, so kernels of different groups overlap.
 static int ensure_graph(det_ctx* c) {
     det_ctx* ctx = c;
-    if (c->g_valid) return DET_OK;
+    {
+        // re-capture only when a pointer, shape or the grouping the graph bakes in changed
+        const Topo t = make_topo(c);
+        const Bufs d = make_bufs(c);
+        if (c->g_valid && c->g_groups == c->groups && !memcmp(&t, &c->g_topo, sizeof(t)) &&
+            !memcmp(&d, &c->g_bufs, sizeof(d)))
+            return DET_OK;
+        c->g_topo = t;
+        c->g_bufs = d;
+        c->g_groups = c->groups;
+    }
     invalidate_graph(c);
     const int G = std::max(1, std::min(c->groups, c->B));
     while ((int)c->gstreams.size() < G) {
@@ -272,7 +293,6 @@ static int alloc_spans(det_ctx* ctx) {
     CK(ctx->spans.alloc((size_t)ctx->B * ctx->n * ctx->cap));
     CK(ctx->rowcnt.alloc((size_t)ctx->B * ctx->n));
     CK(cudaMemsetAsync(ctx->rowcnt.p, 0, (size_t)ctx->B * ctx->n * sizeof(int), ctx->stream));
-    invalidate_graph(ctx);  // the graph bakes in spans pointer and capacity
     return DET_OK;
 }
 
@@ -412,6 +432,7 @@ int det_ctx_create(int device, int k, int field_f64, det_ctx** out) {
     ctx->n = 1 << k;
     ctx->f64 = field_f64 ? 1 : 0;
     ctx->H = std::min(8, ctx->n);
+    if (const char* e = getenv("DET_STAGE_BAND")) ctx->stage_band = atoi(e) != 0;
     ctx->nb = ctx->n / ctx->H;
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
@@ -480,38 +501,16 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
         if (k < 0 || k >= n_regions || rank_reg[k] != -1) return fail(ctx, DET_E_ARG, "region_rank must be a permutation");
         rank_reg[k] = r;
     }
-    // exact (bitwise) de-duplication of vertex positions: duplicates evolve identically
-    struct KeyHash {
-        size_t operator()(const std::pair<uint64_t, uint64_t>& k) const {
-            return std::hash<uint64_t>()(k.first * 0x9E3779B97F4A7C15ull ^ k.second);
-        }
-    };
-    std::unordered_map<std::pair<uint64_t, uint64_t>, int, KeyHash> map;
-    map.reserve(n_rows * 2);
-    std::vector<double> xyu;
-    xyu.reserve(n_rows * 2);
+    // vertex rows are stored per ring row (coalesced); rows duplicating a shared vertex
+    // evolve bit-identically, so no de-duplication is needed
     for (int v = 0; v < n_rows; ++v) {
-        uint64_t a, b;
-        memcpy(&a, xy + 2 * v, 8);
-        memcpy(&b, xy + 2 * v + 1, 8);
-        auto it = map.find({a, b});
-        if (it == map.end()) {
-            const int id = (int)(xyu.size() / 2);
-            map.emplace(std::make_pair(a, b), id);
-            xyu.push_back(xy[2 * v]);
-            xyu.push_back(xy[2 * v + 1]);
-            uniq[v] = id;
-            owner[v] = 1;
-        } else {
-            uniq[v] = it->second;
-        }
+        uniq[v] = v;
+        owner[v] = 1;
     }
     ctx->R = n_regions;
     ctx->n_rows = n_rows;
     ctx->n_rings = n_rings;
-    ctx->n_uniq = (int)(xyu.size() / 2);
-    ctx->h_row_uniq = uniq;
-    ctx->h_xy_uniq = xyu;
+    ctx->n_uniq = n_rows;
     ctx->h_xy_rows.assign(xy, xy + (size_t)n_rows * 2);
     ctx->h_ring_start.assign(ring_start, ring_start + n_rings + 1);
     ctx->h_region_ring0 = reg_ring0;
@@ -533,7 +532,6 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
     CK(cudaMemcpy(ctx->rank_region.p, rank_reg.data(), n_regions * sizeof(int), cudaMemcpyHostToDevice));
     ctx->B = 0;
     ctx->params_set = false;
-    invalidate_graph(ctx);
     return DET_OK;
 }
 
@@ -545,12 +543,15 @@ int det_set_batch(det_ctx* ctx, int batch, const double* xy, const double* stats
         int rc = alloc_batch(ctx, batch);
         if (rc) return rc;
     }
-    std::vector<double> pu((size_t)batch * ctx->n_rows * 2);
-    for (int b = 0; b < batch; ++b) {
-        double* dst = pu.data() + (size_t)b * ctx->n_rows * 2;
-        memcpy(dst, xy ? xy + (size_t)b * ctx->n_rows * 2 : ctx->h_xy_rows.data(), (size_t)ctx->n_rows * 2 * sizeof(double));
+    const size_t rowb = (size_t)ctx->n_rows * sizeof(double2);
+    if (xy) {
+        CK(cudaMemcpyAsync(ctx->pos_init.p, xy, (size_t)batch * rowb, cudaMemcpyHostToDevice, ctx->stream));
+    } else {  // one upload of the loaded rows, replicated on the device
+        CK(cudaMemcpyAsync(ctx->pos_init.p, ctx->h_xy_rows.data(), rowb, cudaMemcpyHostToDevice, ctx->stream));
+        for (int b = 1; b < batch; ++b)
+            CK(cudaMemcpyAsync(ctx->pos_init.p + (size_t)b * ctx->n_rows, ctx->pos_init.p, rowb, cudaMemcpyDeviceToDevice,
+                               ctx->stream));
     }
-    CK(cudaMemcpyAsync(ctx->pos_init.p, pu.data(), pu.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->stats.p, stats, (size_t)batch * ctx->R * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->ran = false;

@@ -379,7 +379,7 @@ __global__ void k_sat2(Bufs D, int gate) {
 // ---------------------------------------------------------------------------------
 // Per band: load the float64 carries, then one top-down sweep.  In-band arithmetic
 // in A (float32 when the field is stored as float32), carries rounded to A once.
-template <int CPT, int NT, int SRC, typename UT, int OUT, typename A>
+template <int CPT, int NT, int SRC, typename UT, int OUT, typename A, bool STAGE>
 __global__ void __launch_bounds__(NT) k_sat3(Topo T, Bufs D, SatSrc S, int gate) {
     extern __shared__ unsigned char s_raw3[];
     __shared__ A s_w[3][32];
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(NT) k_sat3(Topo T, Bufs D, SatSrc S, int gate)
     const A inv2m = (A)(S.outscale != 0.0 ? S.outscale : 0.5 * inv_nd * inv_nd);
     const A xc0 = (A)(((double)x0 + 0.5) * inv_nd);  // pixel-centre x of column x0 (displacement.py:59)
     UT* uf = reinterpret_cast<UT*>(D.uf) + (size_t)b * D.nn * 2;
-    constexpr bool STAGED = (sizeof(A) == 4 && SRC == SRC_LABELS);
+    constexpr bool STAGED = STAGE && (sizeof(A) == 4 && SRC == SRC_LABELS);
     float* srho = reinterpret_cast<float*>(win_dl + 3 * WN);  // staged band (float path)
     A* s_ex = reinterpret_cast<A*>(srho + (size_t)H * n);      // A(j, x0-1) per (row, thread)
     __shared__ A s_wt[64][33];                                      // warp totals per row (H <= 64)

@@ -27,8 +27,8 @@ import numpy as np
 from ._context import get_context, region_ranks
 from ._lib import STOP_BDV, STOP_COLLAPSED, STOP_NAMES, STOP_NEGINDEX
 from .errors import NumericError, RasterizationError, RegionCollapsedError
-from .geomodel import densify, rebuild, ring_layout
-from .raster import LabelTexture, rasterize_labels
+from .geomodel import densify, rebuild, rebuild_fast, ring_layout, ring_sizes
+from .raster import LabelTexture, _LazyLabels, rasterize_labels
 
 DENSIFY_EDGE_PIXELS = 4.0
 
@@ -132,6 +132,7 @@ class BatchEngine:
         if stats.shape[1] != len(ids):
             raise ValueError("statistics column count must match region count")
         self._xy, self._rs, self._rr, self.region_ids = xy, rs, rr, ids
+        self._sizes = np.diff(rs).astype(np.int64)
         self._rank = region_ranks(ids)
         self.B = B
         self.statistics = stats
@@ -214,15 +215,11 @@ class BatchEngine:
         records = tuple(IterationRecord(int(t[0]) + it_off, float(t[1]), float(t[2]), float(t[3])) for t in tr)
         verts = ctx.vertices(b)
         counts = ctx.counts(b)
-        labels = LabelTexture(size=self.n, labels=ctx.labels(b), region_ids=tuple(self.region_ids), _counts=counts)
-        base_map = self.initial_map
-        if self.B > 1 or hasattr(base_map, "with_statistics"):
-            try:
-                base_map = base_map.with_statistics(self.statistics[b])
-            except AttributeError:
-                pass
         clamps = int(r.clamp_events) + (cl_off if r.stop_reason != 2 else 0)
-        state = CartogramState(mapmodel=rebuild(base_map, verts), iteration=int(r.iteration) + it_off,
+        result_map = rebuild_fast(self.initial_map, verts, self.statistics[b], self._sizes)
+        lazy = _LazyLabels(ctx, b, getattr(ctx, "generation", None), lambda: result_map, self.k, self.device)
+        labels = LabelTexture(size=self.n, labels=lazy, region_ids=tuple(self.region_ids), _counts=counts)
+        state = CartogramState(mapmodel=result_map, iteration=int(r.iteration) + it_off,
                                labels=labels, pixel_counts=counts[:-1].copy(),
                                per_region_error=ctx.region_error(b), epsilon=float(r.epsilon), xi=float(r.xi),
                                clamp_events=clamps)

@@ -50,6 +50,13 @@ class Region:
     def vertex_count(self) -> int:
         return sum(int(np.asarray(r).shape[0]) for r in self.rings)
 
+    @classmethod
+    def _make(cls, region_id, name, rings, statistic):
+        """Fast constructor (skips the frozen-dataclass __setattr__ path)."""
+        obj = object.__new__(cls)
+        obj.__dict__.update(region_id=region_id, name=name, rings=rings, statistic=statistic)
+        return obj
+
 
 @dataclass(frozen=True)
 class MapModel:
@@ -120,6 +127,41 @@ def rebuild(mapmodel, verts: np.ndarray):
         out.append(replace(reg, rings=tuple(rs)))
     if pos != verts.shape[0]:
         raise ValueError("vertex array length mismatch")
+    return replace(mapmodel, regions=tuple(out))
+
+
+def ring_sizes(mapmodel) -> np.ndarray:
+    """Number of vertex rows of every ring, region/ring order."""
+    return np.array([np.asarray(r).shape[0] for reg in mapmodel.regions for r in reg.rings], dtype=np.int64)
+
+
+def rebuild_fast(mapmodel, verts: np.ndarray, statistics=None, sizes=None):
+    """``rebuild`` (+ optional new statistics) in one pass; rings are views of ``verts``.
+
+    For this package's own ``Region``/``MapModel`` the objects are constructed
+    directly; other (reference) dataclasses go through ``dataclasses.replace``.
+    """
+    verts = np.asarray(verts, dtype=float)
+    if sizes is None:
+        sizes = ring_sizes(mapmodel)
+    if int(sizes.sum()) != verts.shape[0]:
+        raise ValueError("vertex array length mismatch")
+    offs = np.concatenate([[0], np.cumsum(sizes)]).tolist()
+    pieces = [verts[a:e] for a, e in zip(offs[:-1], offs[1:])]
+    out, q = [], 0
+    own = isinstance(mapmodel, MapModel)
+    stats_l = None if statistics is None else np.asarray(statistics, dtype=float).tolist()
+    for i, reg in enumerate(mapmodel.regions):
+        nr = len(reg.rings)
+        rings = tuple(pieces[q : q + nr])
+        q += nr
+        stat = reg.statistic if statistics is None else stats_l[i]
+        if own and type(reg) is Region:
+            out.append(Region._make(reg.region_id, reg.name, rings, stat))
+        else:
+            out.append(replace(reg, rings=rings, statistic=stat))
+    if own:
+        return MapModel(tuple(out), mapmodel.adjacency, mapmodel.normalization)
     return replace(mapmodel, regions=tuple(out))
 
 

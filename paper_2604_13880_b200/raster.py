@@ -20,14 +20,43 @@ from .geomodel import ring_layout
 BACKGROUND = -1
 
 
+class _LazyLabels:
+    """Deferred label texture of a run result: read back from the device while the context
+    still holds it, otherwise re-rasterised from the result's own vertices (the raster is
+    deterministic, so both give the same array)."""
+
+    def __init__(self, ctx, b, generation, mapmodel_fn, k, device):
+        self.ctx, self.b, self.gen, self.mapmodel_fn, self.k, self.device = ctx, b, generation, mapmodel_fn, k, device
+
+    def materialize(self) -> np.ndarray:
+        if getattr(self.ctx, "generation", None) == self.gen:
+            return self.ctx.labels(self.b)
+        return rasterize_labels(self.mapmodel_fn(), self.k, check_collapse=False, device=self.device).labels
+
+
 @dataclass(frozen=True)
 class LabelTexture:
-    """Per-pixel region index; BACKGROUND (-1) marks unclaimed pixels (raster.py:102-118)."""
+    """Per-pixel region index; BACKGROUND (-1) marks unclaimed pixels (raster.py:102-118).
+
+    ``labels`` may be backed by a device buffer and materialised on first access.
+    """
 
     size: int
-    labels: np.ndarray
+    _labels: object
     region_ids: tuple
     _counts: np.ndarray | None = field(default=None, repr=False, compare=False)
+
+    def __init__(self, size, labels, region_ids, _counts=None):
+        object.__setattr__(self, "size", size)
+        object.__setattr__(self, "_labels", labels)
+        object.__setattr__(self, "region_ids", tuple(region_ids))
+        object.__setattr__(self, "_counts", _counts)
+
+    @property
+    def labels(self) -> np.ndarray:
+        if isinstance(self._labels, _LazyLabels):
+            object.__setattr__(self, "_labels", self._labels.materialize())
+        return self._labels
 
     def pixel_counts(self) -> np.ndarray:
         if self._counts is not None:

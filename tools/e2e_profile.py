@@ -1,0 +1,26 @@
+"""Phase timing of the end-to-end public-API call (BatchEngine.run_all) on the headline workload."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_2604_13880_b200 as P
+from paper_2604_13880_b200 import engine as E
+from paper_2604_13880_b200.synthetic import config_map, random_walk
+
+m, prm = config_map("headline")
+walk = random_walk(m.statistics(), 16, 0.15, seed=7)
+crit = P.StoppingCriteria(1e-300, 10**9, 200)
+t0 = time.perf_counter()
+be = P.BatchEngine(m, walk, criteria=crit, k=10)
+print(f"BatchEngine init  {1e3*(time.perf_counter()-t0):8.1f} ms")
+be.run_all()  # warm (graph capture, allocation)
+for rep in range(2):
+    be._token = None
+    T = {}
+    t = time.perf_counter(); ctx = be._ctx(); T["load_map+set_batch (H2D)"] = time.perf_counter() - t
+    t = time.perf_counter(); ctx.set_params(be._params(), be.weights_px); T["set_params"] = time.perf_counter() - t
+    t = time.perf_counter(); ctx.run(crit.error_threshold, crit.stagnation_window, crit.max_iterations); T["det_run (200 it x 16)"] = time.perf_counter() - t
+    t = time.perf_counter(); res = [be._collect(ctx, b) for b in range(be.B)]; T["collect (D2H + rebuild)"] = time.perf_counter() - t
+    tot = sum(T.values())
+    for k, v in T.items():
+        print(f"  {k:28s} {1e3*v:8.1f} ms")
+    print(f"  total {1e3*tot:.1f} ms -> e2e {16*200/tot:.0f} it/s")
