@@ -300,3 +300,85 @@ def test_many_regions_control_step(P):
     c = res.state.pixel_counts
     assert c.sum() + res.state.labels.background_count() == (1 << 11) ** 2
     assert np.array_equal(res.state.labels.labels, O.FlatMap.from_mapmodel(res.state.mapmodel).labels(11))
+
+
+# ---------------------------------------------------------------- BASELINE configs 2-5 (seeded stand-ins)
+def _trajectory_matches(P, m, k, iters, **kw):
+    res = P.run(m, P.StoppingCriteria(1e-300, 10**9, iters), k=k, field_dtype="float64", **kw)
+    ref = O.OracleEngine(O.FlatMap.from_mapmodel(m), k=k, **kw).run(1e-300, 10**9, iters)
+    return res, ref
+
+
+def test_config2_cumulative_chain_vs_oracle(P):
+    """Config 2 map (500 Lloyd-relaxed regions, ~40k vertices, 1024^2), cumulative chain of
+    3 frames x 4 iterations: float64 field reproduces the oracle trajectory frame by frame."""
+    from paper_2604_13880_b200.synthetic import config_map, random_walk
+
+    m, prm = config_map("c2")
+    walk = random_walk(m.statistics(), 3, prm["walk_sigma"], seed=21)
+    ds = P.TimeSeriesDataset(m, ("t0", "t1", "t2"), walk)
+    crit = dict(error_threshold=1e-300, stagnation_window=10**9, max_iterations=4)
+    seq = P.run_cumulative(ds, P.StoppingCriteria(**crit), k=10, field_dtype="float64")
+    ref = O.run_frames(O.FlatMap.from_mapmodel(m), walk, 10, cumulative=True, **crit)
+    for fr, r in zip(seq.frames, ref):
+        assert fr.error is None
+        dv = np.abs(fr.mapmodel.vertex_array() - r.rows).max()
+        assert dv <= 1e-9, dv
+        assert np.array_equal(fr.result.state.pixel_counts, r.counts)
+
+
+def test_config3_direct_mode_collapse_frames(P):
+    """Config 3 (3000 regions, 5% at 1e-3 x median, multiplier 0.3, 2048^2), 4 direct frames:
+    frames that collapse report the oracle's region and iteration; others stay in tolerance."""
+    from paper_2604_13880_b200.synthetic import config_map, random_walk
+
+    m, prm = config_map("c3")
+    walk = random_walk(m.statistics(), 4, prm["walk_sigma"], seed=31)
+    ds = P.TimeSeriesDataset(m, tuple(f"t{i}" for i in range(4)), walk)
+    seq = P.run_direct(ds, P.StoppingCriteria(1e-300, 10**9, 60), k=11, bdv_multiplier=prm["bdv_multiplier"],
+                       field_dtype="float64")
+    collapsed = [fr for fr in seq.frames if fr.error is not None]
+    assert collapsed, "config 3 is built to make small regions collapse"
+    fr = collapsed[0]
+    f = O.FlatMap.from_mapmodel(m)
+    masses = O.default_background_masses(f, walk.sum(axis=1), 11, prm["bdv_multiplier"])
+    eng = O.OracleEngine(f.densified(4.0 / 2048).with_stats(walk[fr.time_index]), k=11,
+                         background_mass=float(masses[fr.time_index]), apply_densify=False)
+    with pytest.raises(O.OracleCollapseError) as err:
+        eng.run(error_threshold=1e-300, stagnation_window=10**9, max_iterations=60)
+    assert fr.error == str(err.value)
+
+
+def test_config4_parameter_sweep_batch(P):
+    """Config 4: 8 value seeds x 8 multipliers of the config-2 map as ONE 64-cartogram batch;
+    two members checked against the oracle trajectory (float64 field)."""
+    from paper_2604_13880_b200.synthetic import batch_statistics, config_map
+
+    m, _ = config_map("c4")
+    seeds = batch_statistics(m, 8, 1.5)
+    mult = np.repeat(np.arange(1, 9) / 10.0, 8)
+    stats = np.tile(seeds, (8, 1))
+    be = P.BatchEngine(m, stats, criteria=P.StoppingCriteria(1e-300, 10**9, 3), k=10, bdv_multiplier=mult,
+                       field_dtype="float64")
+    res = be.run_all()
+    assert len(res) == 64
+    for b in (5, 62):
+        ref = O.OracleEngine(O.FlatMap.from_mapmodel(m.with_statistics(stats[b])), k=10,
+                             bdv_multiplier=float(mult[b])).run(1e-300, 10**9, 3)
+        assert np.abs(res[b].state.mapmodel.vertex_array() - ref.rows).max() <= 1e-9
+        assert np.array_equal(res[b].state.pixel_counts, ref.counts)
+
+
+def test_config5_stress_scale(P):
+    """Config 5 scale: 10,000 regions, ~1M vertices, 4096^2 texture: a few iterations run, the
+    state's raster equals the oracle raster of its vertices, and the float32 field stays within
+    1e-5 of the float64 build (the 'fp32 integral image checked against an fp64 build' ask)."""
+    from paper_2604_13880_b200.synthetic import config_map
+
+    m, _ = config_map("c5")
+    crit = P.StoppingCriteria(1e-300, 10**9, 3)
+    r32 = P.run(m, crit, k=12, field_dtype="float32")
+    r64 = P.run(m, crit, k=12, field_dtype="float64")
+    dv = np.abs(r32.state.mapmodel.vertex_array() - r64.state.mapmodel.vertex_array()).max()
+    assert dv <= 1e-5, dv
+    assert np.array_equal(r64.state.labels.labels, O.FlatMap.from_mapmodel(r64.state.mapmodel).labels(12))
