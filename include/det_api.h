@@ -125,6 +125,13 @@ int det_time_iterations(det_ctx *ctx, int iters, float *ms_out);
  * [1]=advect+crossings (k_region), [2]=paint/labels/counts (k_row), [3]=control (k_ctrl). */
 int det_bench_kernel_times(det_ctx *ctx, int iters, float *ms_out);
 
+/* Cumulative chain of T time steps (temporal.py:162-246, cumulative=True), device resident:
+ * frame t starts from frame t-1's result.  stats: T*R; S: T statistic totals; masses: T
+ * background masses; out: xy_out T*n_rows*2, res_out T, counts_out T*(R+1) (a failed frame's
+ * start-raster counts), trace_out T*(max_iterations+1)*4.  Requires det_set_batch(ctx, 1, ...). */
+int det_run_chain(det_ctx *ctx, int T, const double *stats, const double *S, const double *masses,
+                  const det_criteria *crit, double *xy_out, det_result *res_out, int64_t *counts_out,
+                  double *trace_out);
 int det_get_result(det_ctx *ctx, int b, det_result *out);
 int det_get_vertices(det_ctx *ctx, int b, double *xy_out);       /* n_rows*2 */
 int det_get_labels(det_ctx *ctx, int b, int32_t *labels_out);    /* n*n      */

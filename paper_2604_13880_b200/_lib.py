@@ -63,6 +63,9 @@ EXPORTS = {
     "det_progress": (ctypes.c_int, [ctypes.c_void_p, _c_int32_p, _c_int32_p]),
     "det_time_iterations": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]),
     "det_get_result": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(DetResult)]),
+    "det_run_chain": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p, _c_double_p, _c_double_p,
+                                      ctypes.POINTER(DetCriteria), _c_double_p, ctypes.POINTER(DetResult),
+                                      _c_int64_p, _c_double_p]),
     "det_get_vertices": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p]),
     "det_get_labels": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_int32_p]),
     "det_get_counts": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_int64_p]),
@@ -181,6 +184,23 @@ class Context:
         c = DetCriteria(float(error_threshold), int(stagnation_window), int(max_iterations))
         self.generation = getattr(self, "generation", 0) + 1
         self.check(self.lib.det_run(self.h, ctypes.byref(c)))
+
+    def run_chain(self, stats, totals, masses, error_threshold, stagnation_window, max_iterations):
+        """Cumulative chain of T frames on the device (see det_run_chain)."""
+        stats = np.ascontiguousarray(stats, dtype=np.float64)
+        T = stats.shape[0]
+        tot = np.ascontiguousarray(totals, dtype=np.float64)
+        mb = np.ascontiguousarray(masses, dtype=np.float64)
+        c = DetCriteria(float(error_threshold), int(stagnation_window), int(max_iterations))
+        xy = np.zeros((T, self.n_rows, 2), dtype=np.float64)
+        res = (DetResult * T)()
+        cnt = np.zeros((T, self.R + 1), dtype=np.int64)
+        tr = np.zeros((T, int(max_iterations) + 1, 4), dtype=np.float64)
+        self.generation = getattr(self, "generation", 0) + 1
+        self.check(self.lib.det_run_chain(self.h, T, _p(stats, ctypes.c_double), _p(tot, ctypes.c_double),
+                                          _p(mb, ctypes.c_double), ctypes.byref(c), _p(xy, ctypes.c_double), res,
+                                          _p(cnt, ctypes.c_int64), _p(tr, ctypes.c_double)))
+        return xy, list(res), cnt, tr
 
     def bench_iterations(self, iters):
         self.generation = getattr(self, "generation", 0) + 1

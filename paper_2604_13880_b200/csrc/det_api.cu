@@ -404,6 +404,7 @@ static int raster_start(det_ctx* ctx) {
 extern "C" {
 
 static int labels_to_host(det_ctx* ctx, int b, int32_t* out);
+static const double2* state_rows(det_ctx* ctx, int b);
 
 
 int det_abi_version(void) { return 1; }
@@ -682,6 +683,79 @@ int det_run(det_ctx* ctx, const det_criteria* crit) {
         if (rc) return rc;
     }
     return fail(ctx, DET_E_STATE, "span capacity did not converge");
+}
+
+// Cumulative time-step chain (temporal.py:162-246 with cumulative=True), device resident:
+// frame t starts from frame t-1's deformed vertices without leaving the GPU.  Per frame the
+// engine constants (engine.py:122-139) are derived from the frame's initial raster with the
+// reference's float64 expressions; S[t] is the statistic total as the caller computed it.
+int det_run_chain(det_ctx* ctx, int T, const double* stats, const double* S, const double* masses,
+                  const det_criteria* crit, double* xy_out, det_result* res_out, int64_t* counts_out,
+                  double* trace_out) {
+    if (!ctx || T <= 0 || !stats || !S || !masses || !crit || !xy_out || !res_out || !counts_out || !trace_out)
+        return fail(ctx, DET_E_ARG, "bad arguments");
+    if (ctx->B != 1) return fail(ctx, DET_E_STATE, "det_set_batch(ctx, 1, ...) first");
+    cudaSetDevice(ctx->device);
+    const int R = ctx->R, nr = ctx->n_rows;
+    const double m = (double)ctx->n * ctx->n;
+    const int tstride = (crit->max_iterations + 1) * 4;
+    std::vector<int> c0(R + 1);
+    std::vector<double> w(R);
+    for (int t = 0; t < T; ++t) {
+        const double* s = stats + (size_t)t * R;
+        det_result& res = res_out[t];
+        memset(&res, 0, sizeof(res));
+        res.collapsed_region = -1;
+        CK(cudaMemcpyAsync(ctx->stats.p, s, R * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        int rc = raster_start(ctx);  // frame start raster (engine.py:128, check_collapse=True)
+        if (rc) return rc;
+        Carto hs;
+        CK(cudaMemcpy(&hs, ctx->st.p, sizeof(Carto), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(c0.data(), ctx->cnt_acc.p, (R + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+        for (int r = 0; r <= R; ++r) counts_out[(size_t)t * (R + 1) + r] = c0[r];
+        if (hs.err & E_NEGIDX) {
+            res.status = DET_E_VALUE;
+            res.stop_reason = DET_STOP_NEGINDEX;
+            continue;
+        }
+        bool empty = false;
+        for (int r = 0; r < R; ++r) empty |= c0[r] == 0;
+        if (empty) {  // RasterizationError at engine construction: frame fails, chain keeps its geometry
+            res.status = DET_E_RASTER;
+            continue;
+        }
+        const double total_mass = S[t] + masses[t];
+        for (int r = 0; r < R; ++r) w[r] = s[r] / total_mass * m;  // engine.py:138-139
+        const double map0 = m - (double)c0[R];
+        det_params p;
+        memset(&p, 0, sizeof(p));
+        p.background_mass = masses[t];
+        p.bdv_multiplier = 1.0;  // temporal.py:190-196 leaves the engine's multiplier at its default
+        p.mean_density0 = S[t] / map0;
+        p.total_statistic = S[t];
+        p.bdv_mode = DET_BDV_FIXED_MASS;
+        rc = det_set_params(ctx, &p, w.data());
+        if (rc) return rc;
+        rc = det_run(ctx, crit);
+        if (rc) return rc;
+        rc = det_get_result(ctx, 0, &res);
+        if (rc) return rc;
+        if (res.stop_reason == DET_STOP_COLLAPSED || res.stop_reason == DET_STOP_BDV ||
+            res.stop_reason == DET_STOP_NEGINDEX)
+            continue;  // the frame failed; the next frame starts from the same geometry
+        rc = det_get_counts(ctx, 0, counts_out + (size_t)t * (R + 1));
+        if (rc) return rc;
+        if (res.trace_len > 0) {
+            rc = det_get_trace(ctx, 0, trace_out + (size_t)t * tstride);
+            if (rc) return rc;
+        }
+        const double2* rows = state_rows(ctx, 0);
+        CK(cudaMemcpyAsync(xy_out + (size_t)t * nr * 2, rows, nr * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->pos_init.p, rows, nr * sizeof(double2), cudaMemcpyDeviceToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    ctx->ran = false;  // per-frame results were returned; the context now holds the chain's last start
+    return DET_OK;
 }
 
 int det_bench_iterations(det_ctx* ctx, int iters) {

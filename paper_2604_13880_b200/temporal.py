@@ -24,10 +24,13 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .engine import DENSIFY_EDGE_PIXELS, BatchEngine, CartogramEngine, RunResult, StoppingCriteria
-from .errors import CartomorphError, IngestionError
-from .geomodel import densify, rebuild
-from .raster import rasterize_labels
+from ._context import get_context, region_ranks
+from ._lib import DET_E_RASTER, STOP_BDV, STOP_COLLAPSED, STOP_NAMES, STOP_NEGINDEX
+from .engine import (DENSIFY_EDGE_PIXELS, BatchEngine, CartogramEngine, CartogramState, IterationRecord, RunResult,
+                     StoppingCriteria)
+from .errors import CartomorphError, IngestionError, RasterizationError, RegionCollapsedError
+from .geomodel import densify, rebuild, rebuild_fast, ring_layout
+from .raster import LabelTexture, _LazyLabels, rasterize_labels
 
 log = logging.getLogger(__name__)
 
@@ -183,29 +186,60 @@ def run_cumulative(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None
                    policy: AreaFractionPolicy | None = None, k: int = 10, bdv_multiplier: float = 1.0,
                    watchdog_ceiling: float = DEFAULT_WATCHDOG_CEILING, report_raster_k: int = 7, *,
                    device: int = 0, field_dtype: str = "float32") -> FrameSequence:
-    """Each frame starts from the previous frame's deformed map (temporal.py:271-290)."""
+    """Each frame starts from the previous frame's deformed map (temporal.py:271-290).
+
+    The whole chain stays on the GPU (``det_run_chain``): frame t+1 starts from frame t's
+    device-resident vertices; per frame only the results come back.
+    """
     criteria = criteria or StoppingCriteria()
     masses, fractions = _masses(dataset, policy, k, bdv_multiplier)
     base_map = densify(dataset.mapmodel, DENSIFY_EDGE_PIXELS / (1 << k))
     seq = FrameSequence(strategy="cumulative", dataset=dataset, base_map=base_map)
-    previous = base_map
+    xy, rs, rr, ids, _ = ring_layout(base_map)
+    ctx = get_context(k, device, field_dtype == "float64")
+    ctx.load_map(xy, rs, rr, region_ranks(ids))
+    ctx.set_batch(dataset.statistics[:1])
+    totals = np.array([float(s.sum()) for s in dataset.statistics])  # engine.py:123 (numpy sum)
+    began = time.perf_counter()
+    out_xy, res, cnt, trace = ctx.run_chain(dataset.statistics, totals, np.asarray(masses, dtype=float),
+                                            criteria.error_threshold, criteria.stagnation_window,
+                                            criteria.max_iterations)
+    wall_ms = (time.perf_counter() - began) * 1e3 / max(dataset.step_count, 1)
+    n = 1 << k
+    sizes = np.diff(rs).astype(np.int64)
     for t in range(dataset.step_count):
-        start_map = previous.with_statistics(dataset.statistics[t])
+        r = res[t]
         frac = None if fractions[t] is None else float(fractions[t])
-        began = time.perf_counter()
-        try:
-            eng = CartogramEngine(start_map, criteria=criteria, k=k, background_mass=float(masses[t]),
-                                  apply_densify=False, device=device, field_dtype=field_dtype)
-            res = eng.run()
-            wall_ms = (time.perf_counter() - began) * 1e3
-            seq.frames.append(Frame(t, dataset.times[t], res.state.mapmodel, res, None, float(masses[t]), frac,
-                                    wall_ms))
-            previous = res.state.mapmodel
-        except CartomorphError as exc:
-            wall_ms = (time.perf_counter() - began) * 1e3
-            log.error("cumulative frame %d failed: %s", t, exc)
-            seq.frames.append(Frame(t, dataset.times[t], None, None, None, float(masses[t]), frac, wall_ms,
-                                    error=str(exc)))
+        mb = float(masses[t])
+        err = None
+        if r.status == DET_E_RASTER:
+            empty = [rid for rid, c in zip(ids, cnt[t, :-1]) if c == 0]
+            err = RasterizationError(f"zero-pixel region(s) at resolution {n}x{n}: {empty} (resolution too low)")
+        elif r.stop_reason == STOP_COLLAPSED:
+            err = RegionCollapsedError(ids[r.collapsed_region], r.iteration)
+        elif r.stop_reason in (STOP_BDV, STOP_NEGINDEX):
+            raise ValueError("bdv must be positive" if r.stop_reason == STOP_BDV
+                             else "'list' argument must have no negative elements")
+        if err is not None:
+            log.error("cumulative frame %d failed: %s", t, err)
+            seq.frames.append(Frame(t, dataset.times[t], None, None, None, mb, frac, wall_ms, error=str(err)))
+            continue
+        stats_t = dataset.statistics[t]
+        carto = rebuild_fast(base_map, out_xy[t], stats_t, sizes)
+        total_mass = float(totals[t]) + mb
+        weights = stats_t / total_mass * (n * n)
+        counts = cnt[t]
+        records = tuple(IterationRecord(int(q[0]), float(q[1]), float(q[2]), float(q[3]))
+                        for q in trace[t, : r.trace_len])
+        labels = LabelTexture(size=n, labels=_LazyLabels(ctx, 0, -1, (lambda c=carto: c), k, device),
+                              region_ids=tuple(ids), _counts=counts)
+        per_region = np.abs(counts[:-1] - weights) / np.maximum(counts[:-1].astype(float), weights)
+        state = CartogramState(mapmodel=carto, iteration=int(r.iteration), labels=labels,
+                               pixel_counts=counts[:-1].copy(), per_region_error=per_region,
+                               epsilon=float(r.epsilon), xi=float(r.xi), clamp_events=int(r.clamp_events))
+        result = RunResult(state=state, trace=records, stop_reason=STOP_NAMES[r.stop_reason], weights_px=weights,
+                           background_mass=mb)
+        seq.frames.append(Frame(t, dataset.times[t], carto, result, None, mb, frac, wall_ms))
     return seq
 
 
