@@ -149,6 +149,10 @@ int det_mapping(det_ctx *ctx, const double *d, double *t_out);
 /* build_density (raster.py:166-184) of a label texture: d_out n*n, counts_out n_regions+1 */
 int det_density(det_ctx *ctx, const int32_t *labels, const double *stats, int n_regions, double bdv, double *d_out,
                 int64_t *counts_out);
+/* interpolate_vertices (temporal.py:293-302): out[f][i] = a[i] + fracs[f]*(b[i]-a[i]), float64,
+ * reference op order; len doubles per frame (vertex rows*2 followed by R statistics). */
+int det_interpolate(det_ctx *ctx, const double *a, const double *b, long long len, const double *fracs, int n_frac,
+                    double *out);
 int det_advect(det_ctx *ctx, const double *u, const double *xy, int n_pts, double *xy_out, int64_t *clamps);
 
 #ifdef __cplusplus

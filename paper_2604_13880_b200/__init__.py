@@ -12,7 +12,7 @@ library and a CUDA device.
 from .engine import (BatchEngine, CartogramEngine, CartogramState, IterationRecord, RunResult, StoppingCriteria,
                      cartographic_error_arrays, run, target_weights)
 from .errors import CartomorphError, IngestionError, NumericError, RasterizationError, RegionCollapsedError
-from .geomodel import MapModel, Region, densify, shoelace_area
+from .geomodel import MapModel, Region, densify, shoelace_area, to_geojson
 from .integral import IntegralImageSet, integral_images, straight_inims, tilted_inims
 from .displacement import (AnchorSet, DisplacementField, advect, anchors, base_mapping, mapping_grid,
                            residual_field)

@@ -76,6 +76,8 @@ EXPORTS = {
     "det_mapping": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p]),
     "det_density": (ctypes.c_int, [ctypes.c_void_p, _c_int32_p, _c_double_p, ctypes.c_int, ctypes.c_double,
                                     _c_double_p, _c_int64_p]),
+    "det_interpolate": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_longlong, _c_double_p,
+                                        ctypes.c_int, _c_double_p]),
     "det_advect": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_int, _c_double_p, _c_int64_p]),
 }
 
@@ -287,6 +289,15 @@ class Context:
         t = np.empty((self.n, self.n, 2), dtype=np.float64)
         self.check(self.lib.det_mapping(self.h, _p(d, ctypes.c_double), _p(t, ctypes.c_double)))
         return t
+
+    def interpolate(self, a, b, fracs):
+        a = np.ascontiguousarray(a, dtype=np.float64).ravel()
+        b = np.ascontiguousarray(b, dtype=np.float64).ravel()
+        fr = np.ascontiguousarray(fracs, dtype=np.float64)
+        out = np.empty((fr.shape[0], a.shape[0]), dtype=np.float64)
+        self.check(self.lib.det_interpolate(self.h, _p(a, ctypes.c_double), _p(b, ctypes.c_double), a.shape[0],
+                                            _p(fr, ctypes.c_double), fr.shape[0], _p(out, ctypes.c_double)))
+        return out
 
     def advect(self, u, xy):
         u = np.ascontiguousarray(u, dtype=np.float64)

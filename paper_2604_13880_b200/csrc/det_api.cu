@@ -1043,6 +1043,26 @@ int det_density(det_ctx* ctx, const int32_t* labels, const double* stats, int n_
     return DET_OK;
 }
 
+int det_interpolate(det_ctx* ctx, const double* a, const double* b, long long len, const double* fracs, int n_frac,
+                    double* out) {
+    if (!ctx || !a || !b || !fracs || !out || len < 0 || n_frac < 0) return fail(ctx, DET_E_ARG, "bad arguments");
+    cudaSetDevice(ctx->device);
+    if (len == 0 || n_frac == 0) return DET_OK;
+    DVec<double> da, db, df, dout;
+    CK(da.alloc(len));
+    CK(db.alloc(len));
+    CK(df.alloc(n_frac));
+    CK(dout.alloc((size_t)len * n_frac));
+    CK(cudaMemcpyAsync(da.p, a, len * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(db.p, b, len * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(df.p, fracs, n_frac * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    k_interpolate<<<592, 256, 0, ctx->stream>>>(da.p, db.p, len, df.p, n_frac, dout.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, dout.p, (size_t)len * n_frac * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return DET_OK;
+}
+
 int det_advect(det_ctx* ctx, const double* u, const double* xy, int n_pts, double* xy_out, int64_t* clamps) {
     if (!ctx || !u || !xy || !xy_out || n_pts < 0) return fail(ctx, DET_E_ARG, "bad arguments");
     cudaSetDevice(ctx->device);

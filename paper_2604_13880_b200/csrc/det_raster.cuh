@@ -428,6 +428,18 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
     ctrl_body(T, D, b, ctrl_mode);
 }
 
+// interpolate_vertices (temporal.py:293-302): out[f] = a + frac[f] * (b - a), same float64
+// op order (no FMA); rows first, then the R statistics.
+__global__ void k_interpolate(const double* __restrict__ a, const double* __restrict__ b, long long len,
+                              const double* __restrict__ fr, int nf, double* __restrict__ out) {
+    const long long total = len * nf;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+        const int f = (int)(i / len);
+        const long long e = i - (long long)f * len;
+        out[i] = __dadd_rn(a[e], __dmul_rn(fr[f], __dsub_rn(b[e], a[e])));
+    }
+}
+
 // Rank texture -> region-index texture (output format of rasterize_labels).
 __global__ void k_rank_to_index(const int* __restrict__ rk, const int* __restrict__ rank_region, size_t nn,
                                 int* __restrict__ out) {

@@ -184,3 +184,46 @@ def densify(mapmodel, max_edge: float):
             rs.append(np.vstack(parts))
         new_regions.append(replace(reg, rings=tuple(rs)))
     return replace(mapmodel, regions=tuple(new_regions))
+
+
+def _inside_ring(pt, ring) -> bool:
+    """Even-odd point-in-ring test used to attach holes (geomodel.py:466-477)."""
+    x, y = float(pt[0]), float(pt[1])
+    inside = False
+    r = np.asarray(ring, dtype=float)
+    for (x0, y0), (x1, y1) in zip(r, np.roll(r, -1, axis=0)):
+        if (y0 <= y) != (y1 <= y) and x0 + (y - y0) * (x1 - x0) / (y1 - y0) > x:
+            inside = not inside
+    return inside
+
+
+def to_geojson(mapmodel, extra_properties: dict | None = None) -> bytes:
+    """GeoJSON FeatureCollection of a (deformed) map, y-up (geomodel.py:422-463).
+
+    Output format of cartogram runs: outer rings are the positively oriented ones, each
+    hole goes to the first outer ring containing its first vertex, rings are closed and
+    y is emitted as 1 - y; keys are sorted and separators compact, so the bytes match the
+    reference's emitter.
+    """
+    import json
+
+    feats = []
+    for reg in mapmodel.regions:
+        rings = [np.asarray(r, dtype=float) for r in reg.rings]
+        outer = [r for r in rings if shoelace_area(r) >= 0]
+        holes = [r for r in rings if shoelace_area(r) < 0]
+        if not outer:
+            raise ValueError(f"region {reg.region_id!r} has no positively oriented ring")
+        polys = [[r] for r in outer]
+        for h in holes:
+            dest = next((i for i, o in enumerate(outer) if _inside_ring(h[0], o)), 0)
+            polys[dest].append(h)
+        coords = [[[[float(x), float(1.0 - y)] for x, y in np.vstack([r, r[:1]])] for r in poly] for poly in polys]
+        geom = ({"type": "Polygon", "coordinates": coords[0]} if len(coords) == 1
+                else {"type": "MultiPolygon", "coordinates": coords})
+        props = {"name": reg.name, "statistic": reg.statistic}
+        if extra_properties and reg.region_id in extra_properties:
+            props.update(extra_properties[reg.region_id])
+        feats.append({"type": "Feature", "id": reg.region_id, "properties": props, "geometry": geom})
+    return json.dumps({"type": "FeatureCollection", "features": feats}, sort_keys=True,
+                      separators=(",", ":")).encode()

@@ -243,18 +243,27 @@ def run_cumulative(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None
     return seq
 
 
-def interpolate_vertices(a, b, fraction: float):
-    """Linear per-vertex blend of two frames with identical vertex layout (temporal.py:293-302)."""
+def _blend(a, b, fracs, device=0):
+    """Per-vertex + per-statistic linear blends of two frames on the GPU (k_interpolate)."""
     va, vb = a.vertex_array(), b.vertex_array()
     if va.shape != vb.shape:
         raise ValueError("vertex-count mismatch between frames")
     sa = np.array([r.statistic for r in a.regions], dtype=float)
     sb = np.array([r.statistic for r in b.regions], dtype=float)
-    return rebuild(a, va + fraction * (vb - va)).with_statistics(sa + fraction * (sb - sa))
+    ctx = get_context(4, device)
+    out = ctx.interpolate(np.concatenate([va.ravel(), sa]), np.concatenate([vb.ravel(), sb]), fracs)
+    nv = va.size
+    sizes = np.array([np.asarray(r).shape[0] for reg in a.regions for r in reg.rings], dtype=np.int64)
+    return [rebuild_fast(a, o[:nv].reshape(-1, 2), o[nv:], sizes) for o in out]
 
 
-def interpolate_frames(seq: FrameSequence, frames_per_step: int = DEFAULT_FRAMES_PER_STEP):
-    """Dense animation frames (temporal.py:305-326)."""
+def interpolate_vertices(a, b, fraction: float, device: int = 0):
+    """Linear per-vertex blend of two frames with identical vertex layout (temporal.py:293-302)."""
+    return _blend(a, b, np.array([float(fraction)]), device)[0]
+
+
+def interpolate_frames(seq: FrameSequence, frames_per_step: int = DEFAULT_FRAMES_PER_STEP, device: int = 0):
+    """Dense animation frames (temporal.py:305-326); all blends of a step pair in one GPU launch."""
     if frames_per_step < 1:
         raise ValueError("frames_per_step must be >= 1")
     out = []
@@ -263,10 +272,10 @@ def interpolate_frames(seq: FrameSequence, frames_per_step: int = DEFAULT_FRAMES
         if cur.mapmodel is None:
             continue
         out.append((cur.time, cur.mapmodel))
-        if idx + 1 >= len(frames) or frames[idx + 1].mapmodel is None:
+        if idx + 1 >= len(frames) or frames[idx + 1].mapmodel is None or frames_per_step == 1:
             continue
         nxt = frames[idx + 1]
-        for sub in range(1, frames_per_step):
-            u = sub / frames_per_step
-            out.append((f"{cur.time}+{u:.3f}", interpolate_vertices(cur.mapmodel, nxt.mapmodel, u)))
+        us = [sub / frames_per_step for sub in range(1, frames_per_step)]
+        for u, mm in zip(us, _blend(cur.mapmodel, nxt.mapmodel, np.array(us), device)):
+            out.append((f"{cur.time}+{u:.3f}", mm))
     return out

@@ -68,7 +68,8 @@ def pack_map(m) -> dict:
     from paper_2604_13880_b200.geomodel import ring_layout
 
     xy, rs, rr, ids, stats = ring_layout(m)
-    return dict(xy=xy, ring_start=rs, ring_region=rr, ids=np.array(ids), stats=stats)
+    return dict(xy=xy, ring_start=rs, ring_region=rr, ids=np.array(ids), stats=stats,
+                names=np.array([str(r.name) for r in m.regions]))
 
 
 def unpack_map(z, prefix="") -> MapModel:
@@ -80,4 +81,5 @@ def unpack_map(z, prefix="") -> MapModel:
     rings = [[] for _ in ids]
     for q in range(len(rr)):
         rings[int(rr[q])].append(np.array(xy[rs[q] : rs[q + 1]], dtype=float))
-    return MapModel(regions=tuple(Region(i, i, tuple(rg), float(s)) for i, rg, s in zip(ids, rings, stats)))
+    names = [str(s) for s in z[prefix + "names"]] if (prefix + "names") in z else ids
+    return MapModel(regions=tuple(Region(i, nm, tuple(rg), float(s)) for i, nm, rg, s in zip(ids, names, rings, stats)))

@@ -127,6 +127,19 @@ def main():
             tem[f"{strat}_{t}_counts"] = fr.result.state.pixel_counts
             tem[f"{strat}_{t}_mb"] = np.array(fr.background_mass)
     np.savez_compressed(os.path.join(OUT, "temporal.npz"), **tem)
+    # 6. output format: GeoJSON bytes of a holed/multi-ring map and of a deformed config-1 frame
+    from cartomorph.geomodel import to_geojson
+
+    gj = {}
+    for name, mm in [("overlap", fm.overlap_holes_multi()), ("c1", fm.config1())]:
+        rm = to_reference_map(cm, mm)
+        if name == "c1":
+            rm = rm.with_vertex_array(runs["c1_final_xy"])
+        gj[name] = np.frombuffer(to_geojson(rm, extra_properties={rm.regions[0].region_id: {"x": 1}}), dtype=np.uint8)
+        for key, val in fm.pack_map(mm).items():
+            gj[f"{name}_{key}"] = val
+    gj["c1_final_xy"] = runs["c1_final_xy"]
+    np.savez_compressed(os.path.join(OUT, "geojson.npz"), **gj)
     print("golden fixtures written to", OUT)
 
 

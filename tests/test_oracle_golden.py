@@ -102,3 +102,15 @@ def test_temporal(golden_dir):
             assert np.array_equal(res.rows, z[f"{strat}_{t}_xy"])
             assert np.array_equal(res.counts, z[f"{strat}_{t}_counts"])
             assert res.background_mass == float(z[f"{strat}_{t}_mb"])
+
+
+@pytest.mark.parametrize("name", ["overlap", "c1"])
+def test_geojson_output_matches_reference_bytes(golden_dir, name):
+    from paper_2604_13880_b200.geomodel import to_geojson
+
+    z = _load(golden_dir, "geojson.npz")
+    m = fm.unpack_map(z, prefix=f"{name}_")
+    if name == "c1":
+        m = m.with_vertex_array(z["c1_final_xy"])
+    got = to_geojson(m, extra_properties={m.regions[0].region_id: {"x": 1}})
+    assert got == z[name].tobytes()
