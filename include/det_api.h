@@ -155,6 +155,32 @@ int det_interpolate(det_ctx *ctx, const double *a, const double *b, long long le
                     double *out);
 int det_advect(det_ctx *ctx, const double *u, const double *xy, int n_pts, double *xy_out, int64_t *clamps);
 
+/* Frame quality metrics (the per-frame report of temporal.py:203-209).  They
+ * need no loaded map: each call carries its layouts (ring_start: n_rings+1 row offsets, ring_region:
+ * owning region of every ring, grouped in region order).
+ * det_shape_metrics replaces metrics.py:82-135 (hamming_distance / shape_distortion) plus
+ * Region.area / Region.centroid (geomodel.py:63-77): map a (one vertex set) against `frames` vertex
+ * sets of map b (frames*rows_b*2 doubles, one layout).  Per (frame, region): hamming (NaN unless
+ * status is 0), area_b, cent_b (2 doubles) and status (0 ok; 1/2 non-positive area of map a/b ->
+ * NumericError; 3 a shape rasterised to zero pixels -> RasterizationError; 4/5 negative toggle index
+ * in map a/b -> ValueError, as np.bincount raises).  cent_a is R*2.  raster_k in [1, 8]; raster_k = 0
+ * computes areas and centroids only (status 0, hamming NaN). */
+int det_shape_metrics(det_ctx *ctx, int n_regions, const double *xy_a, int rows_a, const int32_t *ring_start_a,
+                      int rings_a, const int32_t *ring_region_a, const double *xy_b, int rows_b,
+                      const int32_t *ring_start_b, int rings_b, const int32_t *ring_region_b, int frames,
+                      int raster_k, int rescale, double *hamming, double *area_b, double *cent_a, double *cent_b,
+                      int32_t *status);
+/* detect_adjacencies (geomodel.py:380-415) of one vertex set: row_region is the owning region of
+ * every row.  Region index pairs (a < b) sharing >= 2 epsilon-cells; min(count, cap) pairs are
+ * written (2 int32 each) and *n_pairs = count. */
+int det_adjacency(det_ctx *ctx, const double *xy, int n_rows, const int32_t *row_region, int n_regions,
+                  double epsilon, int32_t *pairs, long long cap, long long *n_pairs);
+/* relative_position_error numerator (metrics.py:138-162): per frame, the sum over ordered pairs
+ * u != v of |atan2(cross, dot)| between barycenter vectors of cent_m (R*2) and cent_c[f] (R*2),
+ * plus the count of degenerate pairs. */
+int det_position_error(det_ctx *ctx, const double *cent_m, const double *cent_c, int frames, int n_regions,
+                       double *sums_out, long long *degenerate_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,15 @@ EXPORTS = {
     "det_interpolate": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_longlong, _c_double_p,
                                         ctypes.c_int, _c_double_p]),
     "det_advect": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_int, _c_double_p, _c_int64_p]),
+    "det_shape_metrics": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p, ctypes.c_int, _c_int32_p,
+                                          ctypes.c_int, _c_int32_p, _c_double_p, ctypes.c_int, _c_int32_p,
+                                          ctypes.c_int, _c_int32_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                          _c_double_p, _c_double_p, _c_double_p, _c_double_p, _c_int32_p]),
+    "det_adjacency": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, ctypes.c_int, _c_int32_p, ctypes.c_int,
+                                      ctypes.c_double, _c_int32_p, ctypes.c_longlong,
+                                      ctypes.POINTER(ctypes.c_longlong)]),
+    "det_position_error": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_int, ctypes.c_int,
+                                           _c_double_p, ctypes.POINTER(ctypes.c_longlong)]),
 }
 
 _lock = threading.Lock()
@@ -298,6 +307,63 @@ class Context:
         self.check(self.lib.det_interpolate(self.h, _p(a, ctypes.c_double), _p(b, ctypes.c_double), a.shape[0],
                                             _p(fr, ctypes.c_double), fr.shape[0], _p(out, ctypes.c_double)))
         return out
+
+    def shape_metrics(self, layout_a, layout_b, raster_k, rescale=True):
+        """Per (frame, region) Hamming distortion, carto area/centroid and status (k_shape).
+
+        ``layout_*`` = (xy, ring_start, ring_region, n_regions); layout_b's xy may stack frames.
+        """
+        xa, rsa, rra, r = layout_a
+        xb, rsb, rrb, rb = layout_b
+        if r != rb:
+            raise ValueError("region count mismatch")
+        xa = np.ascontiguousarray(xa, dtype=np.float64)
+        rsa = np.ascontiguousarray(rsa, dtype=np.int32)
+        rra = np.ascontiguousarray(rra, dtype=np.int32)
+        rsb = np.ascontiguousarray(rsb, dtype=np.int32)
+        rrb = np.ascontiguousarray(rrb, dtype=np.int32)
+        rows_a, rows_b = int(rsa[-1]), int(rsb[-1])
+        xb = np.ascontiguousarray(xb, dtype=np.float64).reshape(-1, rows_b, 2)
+        f = xb.shape[0]
+        ham = np.empty((f, r))
+        area = np.empty((f, r))
+        ca = np.empty((r, 2))
+        cb = np.empty((f, r, 2))
+        st = np.empty((f, r), dtype=np.int32)
+        self.check(self.lib.det_shape_metrics(
+            self.h, r, _p(xa, ctypes.c_double), rows_a, _p(rsa, ctypes.c_int32), rsa.shape[0] - 1,
+            _p(rra, ctypes.c_int32), _p(xb, ctypes.c_double), rows_b, _p(rsb, ctypes.c_int32), rsb.shape[0] - 1,
+            _p(rrb, ctypes.c_int32), f, int(raster_k), int(bool(rescale)), _p(ham, ctypes.c_double),
+            _p(area, ctypes.c_double), _p(ca, ctypes.c_double), _p(cb, ctypes.c_double), _p(st, ctypes.c_int32)))
+        return ham, area, ca, cb, st
+
+    def adjacency(self, xy, row_region, n_regions, epsilon):
+        """Region index pairs (a < b) sharing >= 2 epsilon-cells (k_adj_*)."""
+        x = np.ascontiguousarray(xy, dtype=np.float64).reshape(-1, 2)
+        rr = np.ascontiguousarray(row_region, dtype=np.int32)
+        cap = 4 * int(n_regions) + 64
+        for _ in range(2):
+            out = np.empty((cap, 2), dtype=np.int32)
+            cnt = ctypes.c_longlong(0)
+            self.check(self.lib.det_adjacency(self.h, _p(x, ctypes.c_double), x.shape[0], _p(rr, ctypes.c_int32),
+                                              int(n_regions), float(epsilon), _p(out, ctypes.c_int32), cap,
+                                              ctypes.byref(cnt)))
+            if cnt.value <= cap:
+                return out[: cnt.value]
+            cap = int(cnt.value)
+        raise RuntimeError("adjacency pair count changed between calls")
+
+    def position_error(self, cent_m, cent_c):
+        """Sum of |angle change| over ordered barycenter pairs, and degenerate pair counts (k_poserr)."""
+        cm = np.ascontiguousarray(cent_m, dtype=np.float64).reshape(-1, 2)
+        r = cm.shape[0]
+        cc = np.ascontiguousarray(cent_c, dtype=np.float64).reshape(-1, r, 2)
+        f = cc.shape[0]
+        sums = np.empty(f)
+        dg = (ctypes.c_longlong * f)()
+        self.check(self.lib.det_position_error(self.h, _p(cm, ctypes.c_double), _p(cc, ctypes.c_double), f, r,
+                                               _p(sums, ctypes.c_double), dg))
+        return sums, np.array(list(dg), dtype=np.int64)
 
     def advect(self, u, xy):
         u = np.ascontiguousarray(u, dtype=np.float64)

@@ -19,6 +19,12 @@
 #include "det_ctrl.cuh"
 #include "det_raster.cuh"
 #include "det_sat.cuh"
+#include "det_metrics.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_reduce.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_select.cuh>
 
 using namespace det;
 
@@ -1083,6 +1089,205 @@ int det_advect(det_ctx* ctx, const double* u, const double* xy, int n_pts, doubl
     CK(cudaMemcpyAsync(&c, ctx->clampbuf.p, sizeof(c), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (clamps) *clamps = (int64_t)c;
+    return DET_OK;
+}
+
+
+// ---------------- frame quality metrics (metrics.py:82-162, geomodel.py:380-415) ----------------
+
+static int upload_layout(det_ctx* ctx, const double* xy, int n_rows, int frames, const int32_t* ring_start,
+                         int n_rings, const int32_t* ring_region, int n_regions, DVec<double2>& dxy,
+                         DVec<int>& drs, DVec<int>& drr0) {
+    if (!xy || !ring_start || !ring_region || n_rows <= 0 || n_rings <= 0)
+        return fail(ctx, DET_E_ARG, "invalid map layout");
+    if (ring_start[0] != 0 || ring_start[n_rings] != n_rows) return fail(ctx, DET_E_ARG, "ring_start must span all rows");
+    std::vector<int> r0(n_regions + 1, 0);
+    int prev = -1;
+    for (int q = 0; q < n_rings; ++q) {
+        const int r = ring_region[q];
+        if (r < 0 || r >= n_regions || r < prev) return fail(ctx, DET_E_ARG, "rings must be grouped by region in order");
+        if (ring_start[q + 1] - ring_start[q] < 1) return fail(ctx, DET_E_ARG, "empty ring");
+        while (prev < r) r0[++prev] = q;
+    }
+    if (prev != n_regions - 1) return fail(ctx, DET_E_ARG, "every region needs at least one ring");
+    r0[n_regions] = n_rings;
+    CK(dxy.alloc((size_t)n_rows * frames));
+    CK(drs.alloc(n_rings + 1));
+    CK(drr0.alloc(n_regions + 1));
+    CK(cudaMemcpyAsync(dxy.p, xy, (size_t)n_rows * frames * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(drs.p, ring_start, (n_rings + 1) * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(drr0.p, r0.data(), (n_regions + 1) * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));  // r0 is a host temporary
+    return DET_OK;
+}
+
+int det_shape_metrics(det_ctx* ctx, int n_regions, const double* xy_a, int rows_a, const int32_t* ring_start_a,
+                      int rings_a, const int32_t* ring_region_a, const double* xy_b, int rows_b,
+                      const int32_t* ring_start_b, int rings_b, const int32_t* ring_region_b, int frames,
+                      int raster_k, int rescale, double* hamming, double* area_b, double* cent_a, double* cent_b,
+                      int32_t* status) {
+    if (!ctx || n_regions <= 0 || frames <= 0 || !hamming || !area_b || !cent_a || !cent_b || !status)
+        return fail(ctx, DET_E_ARG, "bad arguments");
+    if (raster_k < 0 || raster_k > 8) return fail(ctx, DET_E_ARG, "raster_k must be in [0, 8]");
+    cudaSetDevice(ctx->device);
+    const size_t R = (size_t)n_regions, F = (size_t)frames;
+    DVec<double2> da, db, dca, dcb;
+    DVec<int> rsa, r0a, rsb, r0b, dst;
+    DVec<double> dh, dar;
+    int rc = upload_layout(ctx, xy_a, rows_a, 1, ring_start_a, rings_a, ring_region_a, n_regions, da, rsa, r0a);
+    if (rc) return rc;
+    rc = upload_layout(ctx, xy_b, rows_b, frames, ring_start_b, rings_b, ring_region_b, n_regions, db, rsb, r0b);
+    if (rc) return rc;
+    CK(dh.alloc(R * F));
+    CK(dar.alloc(R * F));
+    CK(dca.alloc(R));
+    CK(dcb.alloc(R * F));
+    CK(dst.alloc(R * F));
+    const ShapeLayout La{da.p, rsa.p, r0a.p, rows_a}, Lb{db.p, rsb.p, r0b.p, rows_b};
+    k_shape<<<dim3((unsigned)R, (unsigned)F), MK_THREADS, 0, ctx->stream>>>(La, Lb, n_regions, raster_k, rescale, dh.p,
+                                                                            dar.p, dca.p, dcb.p, dst.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(hamming, dh.p, R * F * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(area_b, dar.p, R * F * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(cent_a, dca.p, R * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(cent_b, dcb.p, R * F * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(status, dst.p, R * F * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return DET_OK;
+}
+
+int det_adjacency(det_ctx* ctx, const double* xy, int n_rows, const int32_t* row_region, int n_regions,
+                  double epsilon, int32_t* pairs, long long cap, long long* n_pairs) {
+    if (!ctx || !xy || !row_region || n_rows <= 0 || n_regions <= 0 || !n_pairs || cap < 0 || (cap > 0 && !pairs))
+        return fail(ctx, DET_E_ARG, "bad arguments");
+    if (!(epsilon > 0.0)) return fail(ctx, DET_E_ARG, "epsilon must be positive");
+    for (int v = 0; v < n_rows; ++v)
+        if (row_region[v] < 0 || row_region[v] >= n_regions) return fail(ctx, DET_E_ARG, "row_region out of range");
+    cudaSetDevice(ctx->device);
+    const int nr = n_rows;
+    const int R_ = n_regions;
+    cudaStream_t s = ctx->stream;
+    DVec<double2> dxy;
+    DVec<long long> cx, cy, mm;
+    DVec<unsigned long long> keys, skeys, uk, pk, spk, rk;
+    DVec<int> nuk, rc, nrun, dreg;
+    DVec<unsigned long long> npair;
+    DVec<char> tmp;
+    CK(dxy.alloc(nr));
+    CK(dreg.alloc(nr));
+    CK(cudaMemcpyAsync(dreg.p, row_region, (size_t)nr * sizeof(int), cudaMemcpyHostToDevice, s));
+    CK(cx.alloc(nr));
+    CK(cy.alloc(nr));
+    CK(mm.alloc(4));
+    CK(cudaMemcpyAsync(dxy.p, xy, (size_t)nr * sizeof(double2), cudaMemcpyHostToDevice, s));
+    k_adj_cells<<<(nr + 255) / 256, 256, 0, s>>>(dxy.p, nr, epsilon, cx.p, cy.p);
+    CK(cudaGetLastError());
+    auto run_cub = [&](auto&& fn) -> cudaError_t {  // size query, then the call
+        size_t bytes = 0;
+        cudaError_t e = fn((void*)nullptr, bytes);
+        if (e != cudaSuccess) return e;
+        e = tmp.alloc(bytes);
+        if (e != cudaSuccess) return e;
+        return fn((void*)tmp.p, bytes);
+    };
+    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceReduce::Min(t, b, cx.p, mm.p + 0, nr, s); }));
+    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceReduce::Max(t, b, cx.p, mm.p + 1, nr, s); }));
+    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceReduce::Min(t, b, cy.p, mm.p + 2, nr, s); }));
+    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceReduce::Max(t, b, cy.p, mm.p + 3, nr, s); }));
+    long long h_mm[4];
+    CK(cudaMemcpyAsync(h_mm, mm.p, sizeof(h_mm), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    AdjGrid g;
+    g.mx = h_mm[0] - 1;
+    g.my = h_mm[2] - 1;
+    g.sy = h_mm[3] - h_mm[2] + 3;
+    g.R = R_;
+    const long double span = (long double)(h_mm[1] - h_mm[0] + 3) * (long double)g.sy * (long double)R_;
+    if (span >= 9.0e18L) return fail(ctx, DET_E_ARG, "vertex extent too large for the adjacency cell grid");
+    const unsigned long long maxkey = (unsigned long long)span;
+    int end_bit = 1;
+    while (end_bit < 64 && (maxkey >> end_bit)) ++end_bit;
+    CK(keys.alloc(nr));
+    CK(skeys.alloc(nr));
+    CK(uk.alloc(nr));
+    CK(nuk.alloc(1));
+    k_adj_keys<<<(nr + 255) / 256, 256, 0, s>>>(cx.p, cy.p, dreg.p, nr, g, keys.p);
+    CK(cudaGetLastError());
+    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceRadixSort::SortKeys(t, b, keys.p, skeys.p, nr, 0, end_bit, s); }));
+    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceSelect::Unique(t, b, skeys.p, uk.p, nuk.p, nr, s); }));
+    unsigned long long pcap = (unsigned long long)nr * 4 + 1024, h_np = 0;
+    CK(npair.alloc(1));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        CK(pk.alloc(pcap));
+        CK(cudaMemsetAsync(npair.p, 0, sizeof(unsigned long long), s));
+        k_adj_pairs<<<(nr + 255) / 256, 256, 0, s>>>(uk.p, nuk.p, g, pk.p, pcap, npair.p);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(&h_np, npair.p, sizeof(h_np), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (h_np <= pcap) break;
+        pcap = h_np;
+    }
+    const int np_ = (int)h_np;
+    std::vector<unsigned long long> h_keys;
+    std::vector<int> h_cnt;
+    int h_runs = 0;
+    if (np_ > 0) {
+        CK(spk.alloc(np_));
+        CK(rk.alloc(np_));
+        CK(rc.alloc(np_));
+        CK(nrun.alloc(1));
+        int pbits = 1;
+        const unsigned long long pmax = (unsigned long long)R_ * (unsigned long long)R_;
+        while (pbits < 64 && (pmax >> pbits)) ++pbits;
+        CK(run_cub([&](void* t, size_t& b) { return cub::DeviceRadixSort::SortKeys(t, b, pk.p, spk.p, np_, 0, pbits, s); }));
+        CK(run_cub([&](void* t, size_t& b) {
+            return cub::DeviceRunLengthEncode::Encode(t, b, spk.p, rk.p, rc.p, nrun.p, np_, s);
+        }));
+        CK(cudaMemcpyAsync(&h_runs, nrun.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        h_keys.resize(h_runs);
+        h_cnt.resize(h_runs);
+        CK(cudaMemcpyAsync(h_keys.data(), rk.p, h_runs * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(h_cnt.data(), rc.p, h_runs * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    long long cnt = 0;
+    for (int i = 0; i < h_runs; ++i) {
+        if (h_cnt[i] < 2) continue;  // one shared corner is not an adjacency (geomodel.py:411-414)
+        if (cnt < cap) {
+            pairs[2 * cnt] = (int32_t)(h_keys[i] / (unsigned long long)R_);
+            pairs[2 * cnt + 1] = (int32_t)(h_keys[i] % (unsigned long long)R_);
+        }
+        ++cnt;
+    }
+    *n_pairs = cnt;
+    return DET_OK;
+}
+
+int det_position_error(det_ctx* ctx, const double* cent_m, const double* cent_c, int frames, int n_regions,
+                       double* sums_out, long long* degenerate_out) {
+    if (!ctx || !cent_m || !cent_c || frames <= 0 || n_regions < 2 || !sums_out || !degenerate_out)
+        return fail(ctx, DET_E_ARG, "bad arguments");
+    cudaSetDevice(ctx->device);
+    const size_t R = (size_t)n_regions, F = (size_t)frames;
+    DVec<double2> bm, bc;
+    DVec<double> part, out;
+    DVec<long long> dg, dout;
+    CK(bm.alloc(R));
+    CK(bc.alloc(R * F));
+    CK(part.alloc(R * F));
+    CK(dg.alloc(R * F));
+    CK(out.alloc(F));
+    CK(dout.alloc(F));
+    CK(cudaMemcpyAsync(bm.p, cent_m, R * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(bc.p, cent_c, R * F * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+    k_poserr<<<dim3((unsigned)R, (unsigned)F), 128, 0, ctx->stream>>>(bm.p, bc.p, n_regions, part.p, dg.p);
+    CK(cudaGetLastError());
+    k_poserr_final<<<(unsigned)F, 256, 0, ctx->stream>>>(part.p, dg.p, n_regions, out.p, dout.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(sums_out, out.p, F * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaMemcpyAsync(degenerate_out, dout.p, F * sizeof(long long), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
     return DET_OK;
 }
 

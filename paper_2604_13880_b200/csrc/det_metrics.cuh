@@ -1,0 +1,584 @@
+// Frame quality metrics on the device: cartomorph/metrics.py:82-162 and
+// geomodel.py:380-415, the per-frame report of temporal.py:203-209.
+//
+//  k_shape      one CTA per (region, frame): the Hamming shape distortion of metrics.py:82-118.
+//               Both ring sets are rescaled about their centroid (metrics.py:48-59), put on one
+//               shared 2^k grid (metrics.py:62-77) and rasterised as bit rows in shared memory with
+//               the crossing/toggle rules of raster.py:23-91.  The best overlap over the shift
+//               window is an exact integer correlation (popc of AND-ed, funnel-shifted bit rows):
+//               the same integers the reference recovers by rounding its FFT correlation, so the
+//               distortion is bit-identical.  Shifts whose row- or column-count upper bound cannot
+//               beat the running best are skipped.
+//               The centroid/area moments reproduce numpy's pairwise summation order
+//               (np.add.reduce on contiguous float64: 8 accumulators, 128-element leaves), so the
+//               rescaled vertices, and hence every mask bit, match the reference exactly.
+//  k_adj_*      detect_adjacencies: cell keys -> radix sort -> unique (cell, region) -> 3x3 probes
+//               -> sorted pair keys -> run lengths >= 2.
+//  k_poserr     relative_position_error: |atan2(cross, dot)| over ordered barycenter pairs
+//               (the pair (v,u) repeats (u,v) bit for bit, so each unordered pair is done once).
+#pragma once
+#include "det_common.cuh"
+
+namespace det {
+
+constexpr int MK_NMAX = 256;  // raster_k <= 8
+constexpr int MK_WMAX = MK_NMAX / 32;
+constexpr int MK_THREADS = 256;
+
+enum MetricStatus : int { MS_OK = 0, MS_AREA_A = 1, MS_AREA_B = 2, MS_EMPTY = 3, MS_NEGIDX_A = 4, MS_NEGIDX_B = 5 };
+
+struct Mom3 {
+    double s, sx, sy;
+};
+
+__device__ __forceinline__ Mom3 mom_add(Mom3 a, Mom3 b) {
+    return Mom3{__dadd_rn(a.s, b.s), __dadd_rn(a.sx, b.sx), __dadd_rn(a.sy, b.sy)};
+}
+
+// element k of a ring: cross = x*yn - xn*y, (x+xn)*cross, (y+yn)*cross (geomodel.py:24-47)
+__device__ __forceinline__ Mom3 ring_term(const double2* __restrict__ p, int a, int V, int k) {
+    const double2 P = p[a + k];
+    const double2 Q = p[a + (k + 1 == V ? 0 : k + 1)];
+    const double c = __dsub_rn(__dmul_rn(P.x, Q.y), __dmul_rn(Q.x, P.y));
+    return Mom3{c, __dmul_rn(__dadd_rn(P.x, Q.x), c), __dmul_rn(__dadd_rn(P.y, Q.y), c)};
+}
+
+// numpy pairwise_sum (loops_utils.h): n < 8 sequential from 0; n <= 128 eight accumulators;
+// larger n split at n/2 rounded down to a multiple of 8.
+__device__ Mom3 pw_moments(const double2* __restrict__ p, int a, int V, int lo, int cnt) {
+    if (cnt < 8) {
+        Mom3 r{0.0, 0.0, 0.0};
+        for (int i = 0; i < cnt; ++i) r = mom_add(r, ring_term(p, a, V, lo + i));
+        return r;
+    }
+    if (cnt <= 128) {
+        Mom3 acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = ring_term(p, a, V, lo + j);
+        int i = 8;
+        for (; i < cnt - (cnt % 8); i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = mom_add(acc[j], ring_term(p, a, V, lo + i + j));
+        }
+        Mom3 r = mom_add(mom_add(mom_add(acc[0], acc[1]), mom_add(acc[2], acc[3])),
+                         mom_add(mom_add(acc[4], acc[5]), mom_add(acc[6], acc[7])));
+        for (; i < cnt; ++i) r = mom_add(r, ring_term(p, a, V, lo + i));
+        return r;
+    }
+    int n2 = cnt / 2;
+    n2 -= n2 % 8;
+    const Mom3 l = pw_moments(p, a, V, lo, n2);
+    const Mom3 h = pw_moments(p, a, V, lo + n2, cnt - n2);
+    return mom_add(l, h);
+}
+
+struct ShapeMap {
+    double cx, cy, f;     // rescale: (p - c) * f
+    double total;         // Region.area() (geomodel.py:63-65)
+    double gx, gy;        // Region.centroid() (geomodel.py:67-77)
+    int status;
+    double mn[2], mx[2];  // bbox of the rescaled vertices
+    int j0, j1, i0, i1;   // crop (raster.py:71-76) on the Hamming grid
+};
+
+// Region moments of one map (single thread; regions are a few short rings).
+__device__ void region_moments(const double2* __restrict__ p, const int* __restrict__ ring_start, int q0, int q1,
+                               ShapeMap& M) {
+    double total = 0.0, ax = 0.0, ay = 0.0;
+    for (int q = q0; q < q1; ++q) {
+        const int a = ring_start[q], V = ring_start[q + 1] - a;
+        const Mom3 m = pw_moments(p, a, V, 0, V);
+        const double area = __dmul_rn(0.5, m.s);
+        double cx, cy;
+        if (area == 0.0) {  // ring.mean(axis=0): sequential over rows
+            double sx = 0.0, sy = 0.0;
+            for (int v = 0; v < V; ++v) {
+                sx = __dadd_rn(sx, p[a + v].x);
+                sy = __dadd_rn(sy, p[a + v].y);
+            }
+            cx = __ddiv_rn(sx, (double)V);
+            cy = __ddiv_rn(sy, (double)V);
+        } else {
+            const double six = __dmul_rn(6.0, area);
+            cx = __ddiv_rn(m.sx, six);
+            cy = __ddiv_rn(m.sy, six);
+        }
+        const double sa = V < 3 ? 0.0 : area;  // shoelace_area returns 0 below 3 vertices
+        ax = __dadd_rn(ax, __dmul_rn(sa, cx));
+        ay = __dadd_rn(ay, __dmul_rn(sa, cy));
+        total = __dadd_rn(total, sa);
+    }
+    M.total = total;
+    if (total == 0.0) {  // np.vstack(rings).mean(axis=0)
+        double sx = 0.0, sy = 0.0;
+        const int a = ring_start[q0], e = ring_start[q1];
+        for (int v = a; v < e; ++v) {
+            sx = __dadd_rn(sx, p[v].x);
+            sy = __dadd_rn(sy, p[v].y);
+        }
+        M.gx = __ddiv_rn(sx, (double)(e - a));
+        M.gy = __ddiv_rn(sy, (double)(e - a));
+    } else {
+        M.gx = __ddiv_rn(ax, total);
+        M.gy = __ddiv_rn(ay, total);
+    }
+}
+
+__device__ __forceinline__ double2 shape_xf(double2 p, const ShapeMap& M, bool rescale) {
+    if (!rescale) return p;
+    return make_double2(__dmul_rn(__dsub_rn(p.x, M.cx), M.f), __dmul_rn(__dsub_rn(p.y, M.cy), M.f));
+}
+
+// overlap |A & (B shifted by (sy, sx))| over the rows/words both occupy; one warp
+__device__ __forceinline__ int shape_overlap(const uint32_t (*A)[MK_WMAX], const uint32_t (*Bm)[MK_WMAX], int W,
+                                             int sy, int sx, int ra0, int ra1, int rb0, int rb1, int ca0, int ca1,
+                                             int cb0, int cb1, int lane) {
+    const int j0 = max(ra0, rb0 + sy), j1 = min(ra1, rb1 + sy);
+    const int c0 = max(ca0, cb0 + sx), c1 = min(ca1, cb1 + sx);
+    if (j0 > j1 || c0 > c1) return 0;
+    const int w0 = c0 >> 5, w1 = c1 >> 5;
+    const int q = sx >> 5, r = sx & 31;  // floor division for negative shifts
+    int acc = 0;
+    for (int j = j0 + lane; j <= j1; j += 32) {
+        const uint32_t* br = Bm[j - sy];
+        for (int w = w0; w <= w1; ++w) {
+            const int hi = w - q, lo = hi - 1;
+            const uint32_t h = (hi >= 0 && hi < W) ? br[hi] : 0u;
+            const uint32_t l = (lo >= 0 && lo < W) ? br[lo] : 0u;
+            acc += __popc(A[j][w] & __funnelshift_l(l, h, r));
+        }
+    }
+    return __reduce_add_sync(0xffffffffu, acc);
+}
+
+struct ShapeLayout {  // one map's vertex layout: region r owns rings [region_ring0[r], region_ring0[r+1])
+    const double2* xy;
+    const int* ring_start;
+    const int* region_ring0;
+    int n_rows;
+};
+
+__global__ void __launch_bounds__(MK_THREADS) k_shape(ShapeLayout La, ShapeLayout Lb, int R, int k, int rescale,
+                                                      double* __restrict__ ham, double* __restrict__ area_b,
+                                                      double2* __restrict__ cent_a, double2* __restrict__ cent_b,
+                                                      int* __restrict__ status) {
+    __shared__ uint32_t s_mask[2][MK_NMAX][MK_WMAX];
+    __shared__ int s_rowc[2][MK_NMAX], s_colc[2][MK_NMAX];
+    __shared__ int s_urow[2 * MK_NMAX], s_ucol[2 * MK_NMAX];
+    __shared__ ShapeMap s_m[2];
+    __shared__ double s_red[8][8];
+    __shared__ int s_ext[2][4];
+    __shared__ int s_best, s_err[2];
+    const int r = blockIdx.x, f = blockIdx.y;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = 1 << k, W = (n + 31) >> 5;
+    const double nd = (double)n;
+    const ShapeLayout L[2] = {La, Lb};
+    const double2* P[2] = {La.xy, Lb.xy + (size_t)f * Lb.n_rows};
+    const bool resc = rescale != 0;
+
+    // ---- moments, centroids, rescale factors (metrics.py:48-59, geomodel.py:67-77) ----
+    if (tid == 0 || tid == 32) {
+        const int m = tid >> 5;
+        ShapeMap& M = s_m[m];
+        region_moments(P[m], L[m].ring_start, L[m].region_ring0[r], L[m].region_ring0[r + 1], M);
+        M.status = MS_OK;
+        M.cx = M.cy = 0.0;
+        M.f = 1.0;
+        if (resc) {
+            if (M.total <= 0.0) {
+                M.status = m == 0 ? MS_AREA_A : MS_AREA_B;
+            } else {
+                M.cx = M.gx;
+                M.cy = M.gy;
+                M.f = __dsqrt_rn(__ddiv_rn(1.0, M.total));
+            }
+        }
+    }
+    for (int i = tid; i < 2 * MK_NMAX * MK_WMAX; i += MK_THREADS) (&s_mask[0][0][0])[i] = 0u;
+    if (tid < 2) s_err[tid] = 0;
+    if (tid == 0) s_best = 0;
+    __syncthreads();
+    const int st0 = k == 0 ? MS_OK : (s_m[0].status != MS_OK ? s_m[0].status : s_m[1].status);
+    if (st0 != MS_OK || k == 0) {  // k == 0: areas and centroids only
+        if (tid == 0) {
+            const size_t o = (size_t)f * R + r;
+            ham[o] = __longlong_as_double(0x7ff8000000000000LL);
+            area_b[o] = s_m[1].total;
+            if (f == 0) cent_a[r] = make_double2(s_m[0].gx, s_m[0].gy);
+            cent_b[o] = make_double2(s_m[1].gx, s_m[1].gy);
+            status[o] = st0;
+        }
+        return;
+    }
+
+    // ---- bbox of the rescaled vertices of both maps (metrics.py:64-69) ----
+    {
+        double mn[2][2] = {{INFINITY, INFINITY}, {INFINITY, INFINITY}}, mx[2][2] = {{-INFINITY, -INFINITY}, {-INFINITY, -INFINITY}};
+        for (int m = 0; m < 2; ++m) {
+            const int v0 = L[m].ring_start[L[m].region_ring0[r]], v1 = L[m].ring_start[L[m].region_ring0[r + 1]];
+            for (int v = v0 + tid; v < v1; v += MK_THREADS) {
+                const double2 t = shape_xf(P[m][v], s_m[m], resc);
+                mn[m][0] = fmin(mn[m][0], t.x);
+                mn[m][1] = fmin(mn[m][1], t.y);
+                mx[m][0] = fmax(mx[m][0], t.x);
+                mx[m][1] = fmax(mx[m][1], t.y);
+            }
+        }
+        double vals[8] = {mn[0][0], mn[0][1], mn[1][0], mn[1][1], mx[0][0], mx[0][1], mx[1][0], mx[1][1]};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) vals[i] = i < 4 ? warp_min(vals[i]) : warp_max(vals[i]);
+        if (lane == 0)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s_red[warp][i] = vals[i];
+        __syncthreads();
+        if (tid < 8) {
+            double v = s_red[0][tid];
+            for (int w = 1; w < MK_THREADS / 32; ++w) v = tid < 4 ? fmin(v, s_red[w][tid]) : fmax(v, s_red[w][tid]);
+            const int m = (tid >> 1) & 1, ax = tid & 1;
+            if (tid < 4) s_m[m].mn[ax] = v;
+            else s_m[m].mx[ax] = v;
+        }
+        __syncthreads();
+    }
+    // shared grid: centre, half-width, corner; per-map crops (metrics.py:66-77, raster.py:71-76)
+    double cornx, corny, twoh;
+    {
+        const double lox = fmin(s_m[0].mn[0], s_m[1].mn[0]), loy = fmin(s_m[0].mn[1], s_m[1].mn[1]);
+        const double hix = fmax(s_m[0].mx[0], s_m[1].mx[0]), hiy = fmax(s_m[0].mx[1], s_m[1].mx[1]);
+        const double ex = __dsub_rn(hix, lox), ey = __dsub_rn(hiy, loy);
+        const double half = __dadd_rn(__dmul_rn(0.55, ey > ex ? ey : ex), 1e-12);
+        cornx = __dsub_rn(__dmul_rn(0.5, __dadd_rn(lox, hix)), half);
+        corny = __dsub_rn(__dmul_rn(0.5, __dadd_rn(loy, hiy)), half);
+        twoh = __dmul_rn(2.0, half);
+    }
+    if (tid < 2) {
+        ShapeMap& M = s_m[tid];
+        auto crop = [&](double t, double corner) {
+            const double g = __dmul_rn(__ddiv_rn(__dsub_rn(t, corner), twoh), nd);
+            return min(max(ceil_to_int(__dsub_rn(g, 0.5)), 0), n);
+        };
+        M.j0 = crop(M.mn[1], corny);
+        M.j1 = crop(M.mx[1], corny);
+        M.i0 = crop(M.mn[0], cornx);
+        M.i1 = crop(M.mx[0], cornx);
+    }
+    __syncthreads();
+
+    // ---- crossings -> toggles (raster.py:23-91): XOR straight into the bit rows ----
+    for (int m = 0; m < 2; ++m)
+    for (int q = L[m].region_ring0[r]; q < L[m].region_ring0[r + 1]; ++q) {
+        const int a = L[m].ring_start[q], V = L[m].ring_start[q + 1] - a;
+        for (int e = tid; e < V; e += MK_THREADS) {
+            const ShapeMap& M = s_m[m];
+            const int rows = max(M.j1 - M.j0, 0), cols = max(M.i1 - M.i0, 0);
+            if (rows == 0 || cols == 0) continue;
+            const int width = cols + 1;
+            const double2 ta = shape_xf(P[m][a + e], M, resc);
+            const double2 tc = shape_xf(P[m][a + (e + 1 == V ? 0 : e + 1)], M, resc);
+            const double ax = __dmul_rn(__ddiv_rn(__dsub_rn(ta.x, cornx), twoh), nd);
+            const double ay = __dmul_rn(__ddiv_rn(__dsub_rn(ta.y, corny), twoh), nd);
+            const double cx = __dmul_rn(__ddiv_rn(__dsub_rn(tc.x, cornx), twoh), nd);
+            const double cy = __dmul_rn(__ddiv_rn(__dsub_rn(tc.y, corny), twoh), nd);
+            if (ay == cy) continue;
+            const int ja = min(max(ceil_to_int(__dsub_rn(ay, 0.5)), 0), n);
+            const int jc = min(max(ceil_to_int(__dsub_rn(cy, 0.5)), 0), n);
+            const int js = min(ja, jc), je = max(ja, jc);
+            if (je <= js) continue;
+            const double slope = __ddiv_rn(__dsub_rn(cx, ax), __dsub_rn(cy, ay));
+            double yc = (double)js + 0.5;
+            for (int j = js; j < je; ++j, yc += 1.0) {
+                const double xc = __dadd_rn(ax, __dmul_rn(__dsub_rn(yc, ay), slope));
+                const int i0 = min(max(ceil_to_int(__dsub_rn(xc, 0.5)), 0), n);
+                int dest = j, cc = min(i0 - M.i0, cols);
+                if (cc < 0) {  // lands in an earlier row of the flattened crop
+                    const long long fl = (long long)(j - M.j0) * width + (long long)cc;
+                    if (fl < 0) {  // np.bincount raises on negative entries
+                        s_err[m] = 1;
+                        continue;
+                    }
+                    const long long dr = fl / width;
+                    cc = (int)(fl - dr * width);
+                    dest = M.j0 + (int)dr;
+                }
+                if (cc >= cols) continue;  // absorber column
+                const int col = M.i0 + cc;
+                atomicXor(&s_mask[m][dest][col >> 5], 1u << (col & 31));
+            }
+        }
+    }
+    __syncthreads();
+    if (s_err[0] | s_err[1]) {
+        if (tid == 0) {
+            const size_t o = (size_t)f * R + r;
+            ham[o] = __longlong_as_double(0x7ff8000000000000LL);
+            area_b[o] = s_m[1].total;
+            if (f == 0) cent_a[r] = make_double2(s_m[0].gx, s_m[0].gy);
+            cent_b[o] = make_double2(s_m[1].gx, s_m[1].gy);
+            status[o] = s_err[0] ? MS_NEGIDX_A : MS_NEGIDX_B;
+        }
+        return;
+    }
+
+    // ---- even-odd fill: prefix XOR along each row, clipped to the crop columns ----
+    for (int t = tid; t < 2 * n; t += MK_THREADS) {
+        const int m = t >= n ? 1 : 0, j = t - m * n;
+        const ShapeMap& M = s_m[m];
+        uint32_t carry = 0u;
+        int cnt = 0;
+        for (int w = 0; w < W; ++w) {
+            uint32_t x = s_mask[m][j][w];
+            x ^= x << 1;
+            x ^= x << 2;
+            x ^= x << 4;
+            x ^= x << 8;
+            x ^= x << 16;
+            x ^= carry;
+            carry = (x & 0x80000000u) ? 0xffffffffu : 0u;
+            const int b0 = w * 32;  // keep columns [i0, i1)
+            const int lo = min(max(M.i0 - b0, 0), 32), hi = min(max(M.i1 - b0, 0), 32);
+            const uint32_t keep = (hi >= 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~(lo >= 32 ? 0xffffffffu : ((1u << lo) - 1u));
+            x &= keep;
+            s_mask[m][j][w] = x;
+            cnt += __popc(x);
+        }
+        s_rowc[m][j] = cnt;
+    }
+    __syncthreads();
+    for (int t = tid; t < 2 * n; t += MK_THREADS) {
+        const int m = t >= n ? 1 : 0, i = t - m * n;
+        int cnt = 0;
+        for (int j = 0; j < n; ++j) cnt += (s_mask[m][j][i >> 5] >> (i & 31)) & 1u;
+        s_colc[m][i] = cnt;
+    }
+    __syncthreads();
+    // extents (row/col first..last occupied) and areas, warp 0 for map A, warp 1 for map B
+    if (warp < 2) {
+        const int m = warp;
+        int rmin = n, rmax = -1, cmin = n, cmax = -1, tot = 0;
+        for (int j = lane; j < n; j += 32) {
+            if (s_rowc[m][j]) {
+                rmin = min(rmin, j);
+                rmax = max(rmax, j);
+                tot += s_rowc[m][j];
+            }
+            if (s_colc[m][j]) {
+                cmin = min(cmin, j);
+                cmax = max(cmax, j);
+            }
+        }
+        rmin = warp_min(rmin);
+        rmax = warp_max(rmax);
+        cmin = warp_min(cmin);
+        cmax = warp_max(cmax);
+        tot = __reduce_add_sync(0xffffffffu, tot);
+        if (lane == 0) {
+            s_ext[m][0] = rmin;
+            s_ext[m][1] = rmax;
+            s_ext[m][2] = cmin;
+            s_ext[m][3] = cmax;
+            s_red[m][0] = (double)tot;
+        }
+    }
+    __syncthreads();
+    const int na = (int)s_red[0][0], nb = (int)s_red[1][0];
+    if (na == 0 || nb == 0) {
+        if (tid == 0) {
+            const size_t o = (size_t)f * R + r;
+            ham[o] = __longlong_as_double(0x7ff8000000000000LL);
+            area_b[o] = s_m[1].total;
+            if (f == 0) cent_a[r] = make_double2(s_m[0].gx, s_m[0].gy);
+            cent_b[o] = make_double2(s_m[1].gx, s_m[1].gy);
+            status[o] = MS_EMPTY;
+        }
+        return;
+    }
+    const int ra0 = s_ext[0][0], ra1 = s_ext[0][1], ca0 = s_ext[0][2], ca1 = s_ext[0][3];
+    const int rb0 = s_ext[1][0], rb1 = s_ext[1][1], cb0 = s_ext[1][2], cb1 = s_ext[1][3];
+    // search window (metrics.py:101-112): |s| <= max bbox extent per axis, within +-(n-1)
+    const int wy = min(max(ra1 - ra0, rb1 - rb0) + 1, n - 1);
+    const int wx = min(max(ca1 - ca0, cb1 - cb0) + 1, n - 1);
+    // upper bounds: sum over rows (cols) of min(count_A, count_B shifted)
+    for (int t = tid; t < 2 * wy + 1; t += MK_THREADS) {
+        const int sy = t - wy;
+        int u = 0;
+        for (int j = max(ra0, rb0 + sy); j <= min(ra1, rb1 + sy); ++j) u += min(s_rowc[0][j], s_rowc[1][j - sy]);
+        s_urow[t] = u;
+    }
+    for (int t = tid; t < 2 * wx + 1; t += MK_THREADS) {
+        const int sx = t - wx;
+        int u = 0;
+        for (int i = max(ca0, cb0 + sx); i <= min(ca1, cb1 + sx); ++i) u += min(s_colc[0][i], s_colc[1][i - sx]);
+        s_ucol[t] = u;
+    }
+    __syncthreads();
+    const uint32_t(*A)[MK_WMAX] = s_mask[0];
+    const uint32_t(*Bm)[MK_WMAX] = s_mask[1];
+    // seed the running best with the 3x3 shifts around zero (the centroids coincide)
+    for (int t = warp; t < 9; t += MK_THREADS / 32) {
+        const int sy = t / 3 - 1, sx = t % 3 - 1;
+        if (sy < -wy || sy > wy || sx < -wx || sx > wx) continue;
+        const int v = shape_overlap(A, Bm, W, sy, sx, ra0, ra1, rb0, rb1, ca0, ca1, cb0, cb1, lane);
+        if (lane == 0) atomicMax(&s_best, v);
+    }
+    __syncthreads();
+    volatile int* vbest = &s_best;
+    for (int t = warp; t < 2 * wy + 1; t += MK_THREADS / 32) {
+        const int sy = (t & 1) ? (t + 1) / 2 : -(t / 2);  // 0, 1, -1, 2, -2, ...
+        const int ur = s_urow[sy + wy];
+        if (ur <= *vbest) continue;
+        for (int u = 0; u < 2 * wx + 1; ++u) {
+            const int sx = (u & 1) ? (u + 1) / 2 : -(u / 2);
+            if (sy >= -1 && sy <= 1 && sx >= -1 && sx <= 1) continue;
+            int skip = 0;
+            if (lane == 0) skip = min(ur, s_ucol[sx + wx]) <= *vbest;
+            if (__shfl_sync(0xffffffffu, skip, 0)) continue;
+            const int v = shape_overlap(A, Bm, W, sy, sx, ra0, ra1, rb0, rb1, ca0, ca1, cb0, cb1, lane);
+            if (lane == 0) atomicMax(&s_best, v);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const size_t o = (size_t)f * R + r;
+        const double best = (double)s_best;
+        const double sum = (double)na + (double)nb;
+        const double uni = __dsub_rn(sum, best);
+        ham[o] = uni <= 0.0 ? 0.0 : __ddiv_rn(__dsub_rn(sum, __dmul_rn(2.0, best)), uni);
+        area_b[o] = s_m[1].total;
+        if (f == 0) cent_a[r] = make_double2(s_m[0].gx, s_m[0].gy);
+        cent_b[o] = make_double2(s_m[1].gx, s_m[1].gy);
+        status[o] = MS_OK;
+    }
+}
+
+// ---------------- adjacency (geomodel.py:380-415) ----------------
+__global__ void k_adj_cells(const double2* __restrict__ xy, int n_rows, double eps, long long* __restrict__ cx,
+                            long long* __restrict__ cy) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n_rows) return;
+    const double2 p = xy[v];
+    cx[v] = (long long)rint(__ddiv_rn(p.x, eps));  // np.round: half to even
+    cy[v] = (long long)rint(__ddiv_rn(p.y, eps));
+}
+
+struct AdjGrid {
+    long long mx, my, sy;  // key = ((cx - mx) * sy + (cy - my)) * R + region
+    int R;
+};
+
+__global__ void k_adj_keys(const long long* __restrict__ cx, const long long* __restrict__ cy,
+                           const int* __restrict__ row_region, int n_rows, AdjGrid g,
+                           unsigned long long* __restrict__ keys) {
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n_rows) return;
+    keys[v] = (unsigned long long)(((cx[v] - g.mx) * g.sy + (cy[v] - g.my)) * g.R + row_region[v]);
+}
+
+__device__ __forceinline__ int lower_bound_u64(const unsigned long long* __restrict__ a, int n, unsigned long long x) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// one thread per unique (cell, region a): partners b > a owning any of the 3x3 neighbour cells,
+// each counted once per cell of a (geomodel.py:398-408)
+__global__ void k_adj_pairs(const unsigned long long* __restrict__ uk, const int* __restrict__ n_uk_p, AdjGrid g,
+                            unsigned long long* __restrict__ out, unsigned long long cap,
+                            unsigned long long* __restrict__ n_out) {
+    const int n_uk = *n_uk_p;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n_uk) return;
+    const unsigned long long key = uk[e];
+    const unsigned long long R = (unsigned long long)g.R;
+    const unsigned long long cell = key / R;
+    const int a = (int)(key - cell * R);
+    const long long ccx = (long long)cell / g.sy, ccy = (long long)cell - ccx * g.sy;
+    constexpr int CAP = 48;
+    int part[CAP];
+    int np = 0;
+    for (int dx = -1; dx <= 1; ++dx)
+        for (int dy = -1; dy <= 1; ++dy) {
+            const long long nx = ccx + dx, ny = ccy + dy;
+            if (nx < 0 || ny < 0 || ny >= g.sy) continue;
+            const unsigned long long c2 = (unsigned long long)(nx * g.sy + ny);
+            int i = lower_bound_u64(uk, n_uk, c2 * R + (unsigned long long)(a + 1));
+            for (; i < n_uk && uk[i] < (c2 + 1) * R; ++i) {
+                const int b = (int)(uk[i] - c2 * R);
+                bool seen = false;
+                for (int t = 0; t < np && t < CAP; ++t) seen |= part[t] == b;
+                if (seen) continue;
+                if (np < CAP) part[np] = b;
+                ++np;
+                const unsigned long long slot = atomicAdd(n_out, 1ull);
+                if (slot < cap) out[slot] = (unsigned long long)a * R + (unsigned long long)b;
+            }
+        }
+}
+
+// ---------------- relative position error (metrics.py:138-162) ----------------
+// block per (u, frame): sum over v > u of |atan2(cross, dot)|, degenerate pairs counted
+__global__ void k_poserr(const double2* __restrict__ bm, const double2* __restrict__ bc, int R,
+                         double* __restrict__ part, long long* __restrict__ degen) {
+    __shared__ double s_red[33];
+    __shared__ long long s_cnt[32];
+    const int u = blockIdx.x, f = blockIdx.y;
+    const double2* c = bc + (size_t)f * R;
+    const double2 mu = bm[u], cu = c[u];
+    double acc = 0.0;
+    long long dg = 0;
+    for (int v = u + 1 + threadIdx.x; v < R; v += blockDim.x) {
+        const double2 mv = bm[v], cv = c[v];
+        const double vmx = __dsub_rn(mv.x, mu.x), vmy = __dsub_rn(mv.y, mu.y);
+        const double vcx = __dsub_rn(cv.x, cu.x), vcy = __dsub_rn(cv.y, cu.y);
+        // np.allclose(v, 0): |v| <= 1e-8 componentwise
+        if ((fabs(vmx) <= 1e-8 && fabs(vmy) <= 1e-8) || (fabs(vcx) <= 1e-8 && fabs(vcy) <= 1e-8)) {
+            ++dg;
+            continue;
+        }
+        const double cr = __dsub_rn(__dmul_rn(vmx, vcy), __dmul_rn(vmy, vcx));
+        const double dt = __dadd_rn(__dmul_rn(vmx, vcx), __dmul_rn(vmy, vcy));
+        acc += fabs(atan2(cr, dt));
+    }
+    const double s = block_reduce<0, double>(acc, 0.0, s_red);
+    long long d = dg;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+    if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = d;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_cnt[w];
+        part[(size_t)f * R + u] = s;
+        degen[(size_t)f * R + u] = t;
+    }
+}
+
+__global__ void k_poserr_final(const double* __restrict__ part, const long long* __restrict__ degen, int R,
+                               double* __restrict__ out, long long* __restrict__ dout) {
+    __shared__ double s_red[33];
+    __shared__ long long s_cnt[32];
+    const int f = blockIdx.x;
+    double acc = 0.0;
+    long long dg = 0;
+    for (int u = threadIdx.x; u < R; u += blockDim.x) {
+        acc += part[(size_t)f * R + u];
+        dg += degen[(size_t)f * R + u];
+    }
+    const double s = block_reduce<0, double>(acc, 0.0, s_red);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) dg += __shfl_xor_sync(0xffffffffu, dg, o);
+    if ((threadIdx.x & 31) == 0) s_cnt[threadIdx.x >> 5] = dg;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_cnt[w];
+        out[f] = 2.0 * s;  // (u, v) and (v, u) contribute the same term
+        dout[f] = 2 * t;
+    }
+}
+
+}  // namespace det

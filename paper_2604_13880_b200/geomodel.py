@@ -186,6 +186,18 @@ def densify(mapmodel, max_edge: float):
     return replace(mapmodel, regions=tuple(new_regions))
 
 
+def detect_adjacencies(mapmodel, epsilon: float, *, device: int = 0) -> frozenset:
+    """Region pairs sharing >= 2 coincident vertex cells (geomodel.py:380-415), on the GPU."""
+    from .metrics import detect_adjacencies as _detect
+
+    return _detect(mapmodel, epsilon, device=device)
+
+
+def with_adjacency(mapmodel, epsilon: float, *, device: int = 0):
+    """The map with its adjacency set filled in (geomodel.py:418-419)."""
+    return replace(mapmodel, adjacency=detect_adjacencies(mapmodel, epsilon, device=device))
+
+
 def _inside_ring(pt, ring) -> bool:
     """Even-odd point-in-ring test used to attach holes (geomodel.py:466-477)."""
     x, y = float(pt[0]), float(pt[1])

@@ -10,10 +10,11 @@ Transition modes (temporal.py:162-290):
   after another, each fully device-resident.
 
 The background-mass schedule (temporal.py:83-102, 151-159) and the per-frame
-error capture (temporal.py:231-244) follow the reference.  The per-frame
-quality report (``full_report``, metrics.py:213-260) is outside this
-build's hot-path scope: ``Frame.report`` is None and the
-watchdog is not evaluated.
+error capture (temporal.py:231-244) follow the reference.  Every successful
+frame carries its quality report (``full_report``, metrics.py:213-260,
+temporal.py:203-209) computed on the GPU for all frames at once
+(``metrics.frame_reports``), and the shape-distortion watchdog
+(temporal.py:219-228) is evaluated from it.
 """
 
 from __future__ import annotations
@@ -30,6 +31,7 @@ from .engine import (DENSIFY_EDGE_PIXELS, BatchEngine, CartogramEngine, Cartogra
                      StoppingCriteria)
 from .errors import CartomorphError, IngestionError, RasterizationError, RegionCollapsedError
 from .geomodel import densify, rebuild, rebuild_fast, ring_layout
+from .metrics import frame_reports
 from .raster import LabelTexture, _LazyLabels, rasterize_labels
 
 log = logging.getLogger(__name__)
@@ -126,8 +128,10 @@ class FrameSequence:
             "M_b": [f.background_mass for f in self.frames],
             "A_i": [f.area_fraction if f.area_fraction is not None else float(t / (t + f.background_mass))
                     for f, t in zip(self.frames, totals)],
-            "epsilon": [f.result.state.epsilon if f.result else None for f in self.frames],
-            "xi": [f.result.state.xi if f.result else None for f in self.frames],
+            "epsilon": [f.report.epsilon if f.report else None for f in self.frames],
+            "xi": [f.report.xi if f.report else None for f in self.frames],
+            "hamming_avg": [f.report.hamming_avg if f.report else None for f in self.frames],
+            "position_error": [f.report.position_error if f.report else None for f in self.frames],
             "wall_ms": [f.wall_ms for f in self.frames],
             "watchdog": [f.watchdog for f in self.frames],
             "errors": [f.error for f in self.frames],
@@ -168,6 +172,10 @@ def run_direct(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None = N
     except CartomorphError as exc:  # a start-map problem fails every frame alike
         results = [exc] * dataset.step_count
     wall_ms = (time.perf_counter() - began) * 1e3 / max(dataset.step_count, 1)
+    ok = [t for t, res in enumerate(results) if not isinstance(res, Exception)]
+    reports = _reports(base_map, dataset, masses, [results[t].state.mapmodel for t in ok], ok, report_raster_k,
+                       wall_ms, device)
+    rep_of = dict(zip(ok, reports))
     for t, res in enumerate(results):
         frac = None if fractions[t] is None else float(fractions[t])
         if isinstance(res, CartomorphError):
@@ -177,9 +185,34 @@ def run_direct(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None = N
         elif isinstance(res, Exception):
             raise res
         else:
-            seq.frames.append(Frame(t, dataset.times[t], res.state.mapmodel, res, None, float(masses[t]), frac,
-                                    wall_ms))
+            seq.frames.append(_frame(seq, t, dataset, res, rep_of[t], float(masses[t]), frac, wall_ms,
+                                     watchdog_ceiling))
     return seq
+
+
+def _reports(base_map, dataset, masses, cartos, times, raster_k, wall_ms, device):
+    """full_report of each successful frame (temporal.py:200-209), all frames in one GPU pass."""
+    if not times:
+        return []
+    _, rs, rr, ids, _ = ring_layout(base_map)
+    xy = np.stack([c.vertex_array() for c in cartos])
+    stats = dataset.statistics[times]
+    weights = [dataset.statistics[t] / float(dataset.statistics[t].sum() + masses[t]) for t in times]
+    return frame_reports(base_map, (None, rs, rr, len(ids)), xy, stats, weights, raster_k,
+                         [wall_ms] * len(times), device=device)
+
+
+def _frame(seq, t, dataset, res, report, mb, frac, wall_ms, ceiling):
+    """A successful deformation plus its report; a report error fails the frame (temporal.py:231-244)."""
+    if isinstance(report, Exception):
+        log.error("%s frame %d failed: %s", seq.strategy, t, report)
+        return Frame(t, dataset.times[t], None, None, None, mb, frac, wall_ms, error=str(report))
+    fr = Frame(t, dataset.times[t], res.state.mapmodel, res, report, mb, frac, wall_ms,
+               watchdog=report.hamming_avg > ceiling)
+    if fr.watchdog:
+        log.warning("%s frame %d: average shape distortion %.3f exceeds ceiling %.3f", seq.strategy, t,
+                    report.hamming_avg, ceiling)
+    return fr
 
 
 def run_cumulative(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None = None,
@@ -198,49 +231,76 @@ def run_cumulative(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None
     xy, rs, rr, ids, _ = ring_layout(base_map)
     ctx = get_context(k, device, field_dtype == "float64")
     ctx.load_map(xy, rs, rr, region_ranks(ids))
-    ctx.set_batch(dataset.statistics[:1])
     totals = np.array([float(s.sum()) for s in dataset.statistics])  # engine.py:123 (numpy sum)
-    began = time.perf_counter()
-    out_xy, res, cnt, trace = ctx.run_chain(dataset.statistics, totals, np.asarray(masses, dtype=float),
-                                            criteria.error_threshold, criteria.stagnation_window,
-                                            criteria.max_iterations)
-    wall_ms = (time.perf_counter() - began) * 1e3 / max(dataset.step_count, 1)
+    masses = np.asarray(masses, dtype=float)
     n = 1 << k
     sizes = np.diff(rs).astype(np.int64)
-    for t in range(dataset.step_count):
-        r = res[t]
-        frac = None if fractions[t] is None else float(fractions[t])
-        mb = float(masses[t])
-        err = None
-        if r.status == DET_E_RASTER:
-            empty = [rid for rid, c in zip(ids, cnt[t, :-1]) if c == 0]
-            err = RasterizationError(f"zero-pixel region(s) at resolution {n}x{n}: {empty} (resolution too low)")
-        elif r.stop_reason == STOP_COLLAPSED:
-            err = RegionCollapsedError(ids[r.collapsed_region], r.iteration)
-        elif r.stop_reason in (STOP_BDV, STOP_NEGINDEX):
-            raise ValueError("bdv must be positive" if r.stop_reason == STOP_BDV
-                             else "'list' argument must have no negative elements")
-        if err is not None:
-            log.error("cumulative frame %d failed: %s", t, err)
-            seq.frames.append(Frame(t, dataset.times[t], None, None, None, mb, frac, wall_ms, error=str(err)))
-            continue
-        stats_t = dataset.statistics[t]
-        carto = rebuild_fast(base_map, out_xy[t], stats_t, sizes)
-        total_mass = float(totals[t]) + mb
-        weights = stats_t / total_mass * (n * n)
-        counts = cnt[t]
-        records = tuple(IterationRecord(int(q[0]), float(q[1]), float(q[2]), float(q[3]))
-                        for q in trace[t, : r.trace_len])
-        labels = LabelTexture(size=n, labels=_LazyLabels(ctx, 0, -1, (lambda c=carto: c), k, device),
-                              region_ids=tuple(ids), _counts=counts)
-        per_region = np.abs(counts[:-1] - weights) / np.maximum(counts[:-1].astype(float), weights)
-        state = CartogramState(mapmodel=carto, iteration=int(r.iteration), labels=labels,
-                               pixel_counts=counts[:-1].copy(), per_region_error=per_region,
-                               epsilon=float(r.epsilon), xi=float(r.xi), clamp_events=int(r.clamp_events))
-        result = RunResult(state=state, trace=records, stop_reason=STOP_NAMES[r.stop_reason], weights_px=weights,
-                           background_mass=mb)
-        seq.frames.append(Frame(t, dataset.times[t], carto, result, None, mb, frac, wall_ms))
+    frames = [None] * dataset.step_count
+    start, start_xy = 0, None
+    while start < dataset.step_count:
+        # the chain runs on the device from `start`; a frame whose report fails keeps the previous
+        # geometry (temporal.py:229-230 is skipped), so the chain restarts after it
+        ctx.set_batch(dataset.statistics[start : start + 1], xy=start_xy)
+        began = time.perf_counter()
+        out_xy, res, cnt, trace = ctx.run_chain(dataset.statistics[start:], totals[start:], masses[start:],
+                                                criteria.error_threshold, criteria.stagnation_window,
+                                                criteria.max_iterations)
+        wall_ms = (time.perf_counter() - began) * 1e3 / max(dataset.step_count - start, 1)
+        results = {}
+        for i, r in enumerate(res):
+            t = start + i
+            err = None
+            if r.status == DET_E_RASTER:
+                empty = [rid for rid, c in zip(ids, cnt[i, :-1]) if c == 0]
+                err = RasterizationError(f"zero-pixel region(s) at resolution {n}x{n}: {empty} (resolution too low)")
+            elif r.stop_reason == STOP_COLLAPSED:
+                err = RegionCollapsedError(ids[r.collapsed_region], r.iteration)
+            elif r.stop_reason in (STOP_BDV, STOP_NEGINDEX):
+                raise ValueError("bdv must be positive" if r.stop_reason == STOP_BDV
+                                 else "'list' argument must have no negative elements")
+            if err is not None:
+                results[t] = err
+                continue
+            results[t] = _chain_result(ctx, base_map, ids, sizes, dataset.statistics[t], totals[t], masses[t],
+                                       out_xy[i], r, cnt[i], trace[i], n, k, device)
+        ok = [t for t in sorted(results) if not isinstance(results[t], Exception)]
+        reports = _reports(base_map, dataset, masses, [results[t].state.mapmodel for t in ok], ok, report_raster_k,
+                           wall_ms, device)
+        rep_of = dict(zip(ok, reports))
+        restart = None
+        for t in range(start, dataset.step_count):
+            frac = None if fractions[t] is None else float(fractions[t])
+            mb = float(masses[t])
+            res_t = results[t]
+            if isinstance(res_t, Exception):
+                log.error("cumulative frame %d failed: %s", t, res_t)
+                frames[t] = Frame(t, dataset.times[t], None, None, None, mb, frac, wall_ms, error=str(res_t))
+                continue
+            frames[t] = _frame(seq, t, dataset, res_t, rep_of[t], mb, frac, wall_ms, watchdog_ceiling)
+            if frames[t].error is not None:
+                restart = t
+                break
+            start_xy = out_xy[t - start]
+        if restart is None:
+            break
+        start = restart + 1
+    seq.frames.extend(frames)
     return seq
+
+
+def _chain_result(ctx, base_map, ids, sizes, stats_t, total_t, mb, xy_t, r, counts, trace_t, n, k, device):
+    carto = rebuild_fast(base_map, xy_t, stats_t, sizes)
+    total_mass = float(total_t) + float(mb)
+    weights = stats_t / total_mass * (n * n)
+    records = tuple(IterationRecord(int(q[0]), float(q[1]), float(q[2]), float(q[3])) for q in trace_t[: r.trace_len])
+    labels = LabelTexture(size=n, labels=_LazyLabels(ctx, 0, -1, (lambda c=carto: c), k, device),
+                          region_ids=tuple(ids), _counts=counts)
+    per_region = np.abs(counts[:-1] - weights) / np.maximum(counts[:-1].astype(float), weights)
+    state = CartogramState(mapmodel=carto, iteration=int(r.iteration), labels=labels,
+                           pixel_counts=counts[:-1].copy(), per_region_error=per_region,
+                           epsilon=float(r.epsilon), xi=float(r.xi), clamp_events=int(r.clamp_events))
+    return RunResult(state=state, trace=records, stop_reason=STOP_NAMES[r.stop_reason], weights_px=weights,
+                     background_mass=float(mb))
 
 
 def _blend(a, b, fracs, device=0):

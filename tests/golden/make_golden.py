@@ -12,6 +12,7 @@ No reference source is copied.  The fixtures pin the oracle
 
 from __future__ import annotations
 
+import json
 import os
 import sys
 
@@ -140,6 +141,72 @@ def main():
             gj[f"{name}_{key}"] = val
     gj["c1_final_xy"] = runs["c1_final_xy"]
     np.savez_compressed(os.path.join(OUT, "geojson.npz"), **gj)
+    # 7. frame quality metrics (metrics.py:29-260, geomodel.py:380-415): full reports of map/cartogram pairs
+    from cartomorph import metrics as cmet
+    from cartomorph.geomodel import detect_adjacencies
+
+    met = {}
+    eps_adj = cmet.DEFAULT_ADJACENCY_EPSILON
+
+    def idx_pairs(edges, ids):
+        pos = {rid: i for i, rid in enumerate(ids)}
+        out = sorted(tuple(sorted((pos[a], pos[b]))) for a, b in edges)
+        return np.array(out, dtype=np.int32).reshape(-1, 2)
+
+    def save_pair(name, mm, cxy, k, rescale=True):
+        rm = to_reference_map(cm, mm)
+        rc = rm.with_vertex_array(cxy)
+        for key, val in fm.pack_map(mm).items():
+            met[f"{name}_m_{key}"] = val
+        met[f"{name}_c_xy"] = np.asarray(cxy, dtype=float)
+        met[f"{name}_k"] = np.array(k)
+        met[f"{name}_rescale"] = np.array(rescale)
+        vals, avg, mx = cmet.shape_distortion(rm, rc, raster_k=k, rescale=rescale)
+        met[f"{name}_hamming"] = vals
+        rep = cmet.full_report(rm, rc, raster_k=k, rescale_shapes=rescale)
+        met[f"{name}_json"] = np.array(rep.to_json())
+        met[f"{name}_csv"] = np.array(rep.to_csv())
+        met[f"{name}_areas"] = np.array([r.area() for r in rc.regions])
+        met[f"{name}_cent_m"] = np.array([r.centroid() for r in rm.regions])
+        met[f"{name}_cent_c"] = np.array([r.centroid() for r in rc.regions])
+        ids = rm.region_ids()
+        met[f"{name}_adj_m"] = idx_pairs(detect_adjacencies(rm, eps_adj), ids)
+        met[f"{name}_adj_c"] = idx_pairs(detect_adjacencies(rc, eps_adj), ids)
+        met[f"{name}_poserr"] = np.array(cmet.relative_position_error(rm, rc))
+
+    save_pair("c1", c1, runs["c1_final_xy"], 7)
+    save_pair("c1_k6_raw", c1, runs["c1_final_xy"], 6, rescale=False)
+    mo = fm.overlap_holes_multi()
+    save_pair("overlap", mo, np.clip(mo.vertex_array() + rng.normal(0, 0.003, mo.vertex_array().shape), 0, 1), 7)
+    mv = fm.small_voronoi(seed=11, r=40, target=900)
+    save_pair("vor_k8", mv, np.clip(mv.vertex_array() + rng.normal(0, 0.002, mv.vertex_array().shape), 0, 1), 8)
+    mt2 = fm.two_region()
+    save_pair("two", mt2, mt2.vertex_array() * np.array([1.0, 0.9]) + np.array([0.02, 0.03]), 5)
+    # square vs disk (test_metrics.py:103-117) at k=6
+    theta = np.linspace(0.0, 2 * np.pi, 96, endpoint=False)
+    radius = 0.4 / np.sqrt(np.pi)
+    sq = [np.array([[0.3, 0.3], [0.7, 0.3], [0.7, 0.7], [0.3, 0.7]])]
+    disk = [np.stack([0.5 + radius * np.cos(theta), 0.5 + radius * np.sin(theta)], axis=1)]
+    met["sqdisk_a"], met["sqdisk_b"] = sq[0], disk[0]
+    met["sqdisk_hamming"] = np.array(cmet.hamming_distance(sq, disk, raster_k=6))
+    met["sqdisk_hamming_raw"] = np.array(cmet.hamming_distance(sq, disk, raster_k=6, rescale=False))
+    # a clockwise (negative-area) region: NumericError from the rescale
+    try:
+        cmet.hamming_distance([sq[0][::-1]], disk, raster_k=6)
+        raise SystemExit("expected NumericError")
+    except cm.NumericError as exc:
+        met["neg_area_message"] = np.array(str(exc))
+    np.savez_compressed(os.path.join(OUT, "metrics.npz"), **met)
+
+    # 8. temporal frames with their reports and watchdog flags (temporal.py:200-228)
+    tr = dict(fm.pack_map(mt), walk=walk)
+    for strat, fn in [("direct", cm.run_direct), ("cumulative", cm.run_cumulative)]:
+        seq = fn(ds, _criteria(cm, 8), k=6, bdv_multiplier=1.0, watchdog_ceiling=0.02, report_raster_k=6)
+        for t, fr in enumerate(seq.frames):
+            tr[f"{strat}_{t}_report"] = np.array(fr.report.to_json())
+            tr[f"{strat}_{t}_watchdog"] = np.array(fr.watchdog)
+        tr[f"{strat}_series"] = np.array(json.dumps(seq.series(), sort_keys=True))
+    np.savez_compressed(os.path.join(OUT, "temporal_reports.npz"), **tr)
     print("golden fixtures written to", OUT)
 
 
