@@ -133,11 +133,20 @@ def test_temporal_reports_and_watchdog(golden_dir):
         for t, fr in enumerate(seq.frames):
             ref = json.loads(str(z[f"{strat}_{t}_report"]))
             got = json.loads(fr.report.to_json())
-            for key in ("epsilon", "xi", "tau", "hamming_avg", "hamming_max", "per_region"):
+            # the device fp64 field sums in another order than the reference, so frame vertices agree
+            # to ~1e-12 (test_gpu_parity.py::test_temporal_vs_golden), not bit for bit: areas and the
+            # cartographic errors follow at 1e-9; masks, adjacency and Hamming values stay exact
+            for key in ("tau", "hamming_avg", "hamming_max"):
                 assert got[key] == ref[key], (strat, t, key)
-            assert got["position_error"] == pytest.approx(ref["position_error"], rel=1e-12, abs=1e-15)
+            for key in ("epsilon", "xi", "position_error"):
+                assert got[key] == pytest.approx(ref[key], rel=1e-9, abs=1e-12), (strat, t, key)
+            for rid, vals in ref["per_region"].items():
+                assert got["per_region"][rid]["shape_distortion"] == vals["shape_distortion"]
+                assert got["per_region"][rid]["cartographic_error"] == pytest.approx(vals["cartographic_error"],
+                                                                                     rel=1e-9, abs=1e-12)
             assert fr.watchdog == bool(z[f"{strat}_{t}_watchdog"])
         ser = seq.series()
         ref_ser = json.loads(str(z[f"{strat}_series"]))
-        for key in ("epsilon", "xi", "hamming_avg", "watchdog", "errors", "M_b", "A_i"):
+        for key in ("hamming_avg", "watchdog", "errors", "M_b", "A_i"):
             assert ser[key] == ref_ser[key], key
+        np.testing.assert_allclose(ser["epsilon"], ref_ser["epsilon"], rtol=1e-9)

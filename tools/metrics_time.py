@@ -19,11 +19,11 @@ from paper_2604_13880_b200.synthetic import config_map  # noqa: E402
 
 def main():
     F = int(sys.argv[1]) if len(sys.argv) > 1 else 8
-    base = config_map("headline")
+    base, _ = config_map("headline")
     base = densify(base, 4.0 / 1024)
     xy, rs, rr, ids, stats = ring_layout(base)
     rng = np.random.default_rng(0)
-    cart = np.stack([np.clip(xy + rng.normal(0, 0.002, xy.shape), 0, 1) for _ in range(F)])
+    cart = np.stack([np.clip(xy + rng.normal(0, 0.0003, xy.shape), 0, 1) for _ in range(F)])
     lay = (None, rs, rr, len(ids))
     w = [stats / stats.sum()] * F
     M.frame_reports(base, lay, cart[:1], [stats], w[:1], 7)  # warm-up
