@@ -170,10 +170,11 @@ int det_shape_metrics(det_ctx *ctx, int n_regions, const double *xy_a, int rows_
                       const int32_t *ring_start_b, int rings_b, const int32_t *ring_region_b, int frames,
                       int raster_k, int rescale, double *hamming, double *area_b, double *cent_a, double *cent_b,
                       int32_t *status);
-/* detect_adjacencies (geomodel.py:380-415) of one vertex set: row_region is the owning region of
- * every row.  Region index pairs (a < b) sharing >= 2 epsilon-cells; min(count, cap) pairs are
- * written (2 int32 each) and *n_pairs = count. */
-int det_adjacency(det_ctx *ctx, const double *xy, int n_rows, const int32_t *row_region, int n_regions,
+/* detect_adjacencies (geomodel.py:380-415) of `frames` vertex sets (frames*n_rows*2 doubles) sharing
+ * one layout; row_region is the owning region of every row.  Region index pairs (a < b) sharing >= 2
+ * epsilon-cells, as (frame, a, b) int32 triples sorted by frame, a, b; min(count, cap) triples are
+ * written and *n_pairs = count. */
+int det_adjacency(det_ctx *ctx, const double *xy, int frames, int n_rows, const int32_t *row_region, int n_regions,
                   double epsilon, int32_t *pairs, long long cap, long long *n_pairs);
 /* relative_position_error numerator (metrics.py:138-162): per frame, the sum over ordered pairs
  * u != v of |atan2(cross, dot)| between barycenter vectors of cent_m (R*2) and cent_c[f] (R*2),

@@ -83,8 +83,8 @@ EXPORTS = {
                                           ctypes.c_int, _c_int32_p, _c_double_p, ctypes.c_int, _c_int32_p,
                                           ctypes.c_int, _c_int32_p, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                           _c_double_p, _c_double_p, _c_double_p, _c_double_p, _c_int32_p]),
-    "det_adjacency": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, ctypes.c_int, _c_int32_p, ctypes.c_int,
-                                      ctypes.c_double, _c_int32_p, ctypes.c_longlong,
+    "det_adjacency": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, ctypes.c_int, ctypes.c_int, _c_int32_p,
+                                      ctypes.c_int, ctypes.c_double, _c_int32_p, ctypes.c_longlong,
                                       ctypes.POINTER(ctypes.c_longlong)]),
     "det_position_error": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_int, ctypes.c_int,
                                            _c_double_p, ctypes.POINTER(ctypes.c_longlong)]),
@@ -338,16 +338,19 @@ class Context:
         return ham, area, ca, cb, st
 
     def adjacency(self, xy, row_region, n_regions, epsilon):
-        """Region index pairs (a < b) sharing >= 2 epsilon-cells (k_adj_*)."""
-        x = np.ascontiguousarray(xy, dtype=np.float64).reshape(-1, 2)
+        """(frame, a, b) region index triples, a < b sharing >= 2 epsilon-cells (k_adj_*).
+
+        ``xy`` is (rows, 2) or (frames, rows, 2) in one layout.
+        """
         rr = np.ascontiguousarray(row_region, dtype=np.int32)
-        cap = 4 * int(n_regions) + 64
+        x = np.ascontiguousarray(xy, dtype=np.float64).reshape(-1, rr.shape[0], 2)
+        cap = 4 * int(n_regions) * x.shape[0] + 64
         for _ in range(2):
-            out = np.empty((cap, 2), dtype=np.int32)
+            out = np.empty((cap, 3), dtype=np.int32)
             cnt = ctypes.c_longlong(0)
-            self.check(self.lib.det_adjacency(self.h, _p(x, ctypes.c_double), x.shape[0], _p(rr, ctypes.c_int32),
-                                              int(n_regions), float(epsilon), _p(out, ctypes.c_int32), cap,
-                                              ctypes.byref(cnt)))
+            self.check(self.lib.det_adjacency(self.h, _p(x, ctypes.c_double), x.shape[0], rr.shape[0],
+                                              _p(rr, ctypes.c_int32), int(n_regions), float(epsilon),
+                                              _p(out, ctypes.c_int32), cap, ctypes.byref(cnt)))
             if cnt.value <= cap:
                 return out[: cnt.value]
             cap = int(cnt.value)

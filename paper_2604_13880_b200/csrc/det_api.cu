@@ -1156,31 +1156,33 @@ int det_shape_metrics(det_ctx* ctx, int n_regions, const double* xy_a, int rows_
     return DET_OK;
 }
 
-int det_adjacency(det_ctx* ctx, const double* xy, int n_rows, const int32_t* row_region, int n_regions,
+int det_adjacency(det_ctx* ctx, const double* xy, int frames, int n_rows, const int32_t* row_region, int n_regions,
                   double epsilon, int32_t* pairs, long long cap, long long* n_pairs) {
-    if (!ctx || !xy || !row_region || n_rows <= 0 || n_regions <= 0 || !n_pairs || cap < 0 || (cap > 0 && !pairs))
+    if (!ctx || !xy || !row_region || frames <= 0 || n_rows <= 0 || n_regions <= 0 || !n_pairs || cap < 0 ||
+        (cap > 0 && !pairs))
         return fail(ctx, DET_E_ARG, "bad arguments");
     if (!(epsilon > 0.0)) return fail(ctx, DET_E_ARG, "epsilon must be positive");
     for (int v = 0; v < n_rows; ++v)
         if (row_region[v] < 0 || row_region[v] >= n_regions) return fail(ctx, DET_E_ARG, "row_region out of range");
     cudaSetDevice(ctx->device);
-    const int nr = n_rows;
+    const long long n = (long long)n_rows * frames;
+    if (n >= (1LL << 31)) return fail(ctx, DET_E_ARG, "too many vertex rows in one adjacency batch");
     const int R_ = n_regions;
     cudaStream_t s = ctx->stream;
     DVec<double2> dxy;
     DVec<long long> cx, cy, mm;
-    DVec<unsigned long long> keys, skeys, uk, pk, spk, rk;
+    DVec<unsigned long long> keys, skeys, uk, pk, spk, rk, npair;
     DVec<int> nuk, rc, nrun, dreg;
-    DVec<unsigned long long> npair;
     DVec<char> tmp;
-    CK(dxy.alloc(nr));
-    CK(dreg.alloc(nr));
-    CK(cudaMemcpyAsync(dreg.p, row_region, (size_t)nr * sizeof(int), cudaMemcpyHostToDevice, s));
-    CK(cx.alloc(nr));
-    CK(cy.alloc(nr));
+    CK(dxy.alloc(n));
+    CK(dreg.alloc(n_rows));
+    CK(cx.alloc(n));
+    CK(cy.alloc(n));
     CK(mm.alloc(4));
-    CK(cudaMemcpyAsync(dxy.p, xy, (size_t)nr * sizeof(double2), cudaMemcpyHostToDevice, s));
-    k_adj_cells<<<(nr + 255) / 256, 256, 0, s>>>(dxy.p, nr, epsilon, cx.p, cy.p);
+    CK(cudaMemcpyAsync(dxy.p, xy, (size_t)n * sizeof(double2), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(dreg.p, row_region, (size_t)n_rows * sizeof(int), cudaMemcpyHostToDevice, s));
+    const unsigned nb = (unsigned)((n + 255) / 256);
+    k_adj_cells<<<nb, 256, 0, s>>>(dxy.p, n, epsilon, cx.p, cy.p);
     CK(cudaGetLastError());
     auto run_cub = [&](auto&& fn) -> cudaError_t {  // size query, then the call
         size_t bytes = 0;
@@ -1190,37 +1192,40 @@ int det_adjacency(det_ctx* ctx, const double* xy, int n_rows, const int32_t* row
         if (e != cudaSuccess) return e;
         return fn((void*)tmp.p, bytes);
     };
-    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceReduce::Min(t, b, cx.p, mm.p + 0, nr, s); }));
-    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceReduce::Max(t, b, cx.p, mm.p + 1, nr, s); }));
-    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceReduce::Min(t, b, cy.p, mm.p + 2, nr, s); }));
-    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceReduce::Max(t, b, cy.p, mm.p + 3, nr, s); }));
+    const int ni = (int)n;
+    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceReduce::Min(t, b, cx.p, mm.p + 0, ni, s); }));
+    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceReduce::Max(t, b, cx.p, mm.p + 1, ni, s); }));
+    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceReduce::Min(t, b, cy.p, mm.p + 2, ni, s); }));
+    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceReduce::Max(t, b, cy.p, mm.p + 3, ni, s); }));
     long long h_mm[4];
     CK(cudaMemcpyAsync(h_mm, mm.p, sizeof(h_mm), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     AdjGrid g;
     g.mx = h_mm[0] - 1;
     g.my = h_mm[2] - 1;
+    g.sx = h_mm[1] - h_mm[0] + 3;
     g.sy = h_mm[3] - h_mm[2] + 3;
     g.R = R_;
-    const long double span = (long double)(h_mm[1] - h_mm[0] + 3) * (long double)g.sy * (long double)R_;
+    g.n_rows = n_rows;
+    const long double span = (long double)frames * (long double)g.sx * (long double)g.sy * (long double)R_;
     if (span >= 9.0e18L) return fail(ctx, DET_E_ARG, "vertex extent too large for the adjacency cell grid");
     const unsigned long long maxkey = (unsigned long long)span;
     int end_bit = 1;
     while (end_bit < 64 && (maxkey >> end_bit)) ++end_bit;
-    CK(keys.alloc(nr));
-    CK(skeys.alloc(nr));
-    CK(uk.alloc(nr));
+    CK(keys.alloc(n));
+    CK(skeys.alloc(n));
+    CK(uk.alloc(n));
     CK(nuk.alloc(1));
-    k_adj_keys<<<(nr + 255) / 256, 256, 0, s>>>(cx.p, cy.p, dreg.p, nr, g, keys.p);
+    k_adj_keys<<<nb, 256, 0, s>>>(cx.p, cy.p, dreg.p, n, g, keys.p);
     CK(cudaGetLastError());
-    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceRadixSort::SortKeys(t, b, keys.p, skeys.p, nr, 0, end_bit, s); }));
-    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceSelect::Unique(t, b, skeys.p, uk.p, nuk.p, nr, s); }));
-    unsigned long long pcap = (unsigned long long)nr * 4 + 1024, h_np = 0;
+    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceRadixSort::SortKeys(t, b, keys.p, skeys.p, ni, 0, end_bit, s); }));
+    CK(run_cub([&](void* t, size_t& b) { return cub::DeviceSelect::Unique(t, b, skeys.p, uk.p, nuk.p, ni, s); }));
+    unsigned long long pcap = (unsigned long long)n * 2 + 1024, h_np = 0;
     CK(npair.alloc(1));
     for (int attempt = 0; attempt < 2; ++attempt) {
         CK(pk.alloc(pcap));
         CK(cudaMemsetAsync(npair.p, 0, sizeof(unsigned long long), s));
-        k_adj_pairs<<<(nr + 255) / 256, 256, 0, s>>>(uk.p, nuk.p, g, pk.p, pcap, npair.p);
+        k_adj_pairs<<<nb, 256, 0, s>>>(uk.p, nuk.p, g, pk.p, pcap, npair.p);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(&h_np, npair.p, sizeof(h_np), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -1237,7 +1242,7 @@ int det_adjacency(det_ctx* ctx, const double* xy, int n_rows, const int32_t* row
         CK(rc.alloc(np_));
         CK(nrun.alloc(1));
         int pbits = 1;
-        const unsigned long long pmax = (unsigned long long)R_ * (unsigned long long)R_;
+        const unsigned long long pmax = (unsigned long long)frames * R_ * (unsigned long long)R_;
         while (pbits < 64 && (pmax >> pbits)) ++pbits;
         CK(run_cub([&](void* t, size_t& b) { return cub::DeviceRadixSort::SortKeys(t, b, pk.p, spk.p, np_, 0, pbits, s); }));
         CK(run_cub([&](void* t, size_t& b) {
@@ -1252,11 +1257,14 @@ int det_adjacency(det_ctx* ctx, const double* xy, int n_rows, const int32_t* row
         CK(cudaStreamSynchronize(s));
     }
     long long cnt = 0;
+    const unsigned long long RR = (unsigned long long)R_;
     for (int i = 0; i < h_runs; ++i) {
         if (h_cnt[i] < 2) continue;  // one shared corner is not an adjacency (geomodel.py:411-414)
         if (cnt < cap) {
-            pairs[2 * cnt] = (int32_t)(h_keys[i] / (unsigned long long)R_);
-            pairs[2 * cnt + 1] = (int32_t)(h_keys[i] % (unsigned long long)R_);
+            const unsigned long long k = h_keys[i];
+            pairs[3 * cnt] = (int32_t)(k / (RR * RR));
+            pairs[3 * cnt + 1] = (int32_t)((k / RR) % RR);
+            pairs[3 * cnt + 2] = (int32_t)(k % RR);
         }
         ++cnt;
     }

@@ -452,26 +452,29 @@ __global__ void __launch_bounds__(MK_THREADS) k_shape(ShapeLayout La, ShapeLayou
 }
 
 // ---------------- adjacency (geomodel.py:380-415) ----------------
-__global__ void k_adj_cells(const double2* __restrict__ xy, int n_rows, double eps, long long* __restrict__ cx,
+__global__ void k_adj_cells(const double2* __restrict__ xy, long long n, double eps, long long* __restrict__ cx,
                             long long* __restrict__ cy) {
-    const int v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n_rows) return;
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
     const double2 p = xy[v];
     cx[v] = (long long)rint(__ddiv_rn(p.x, eps));  // np.round: half to even
     cy[v] = (long long)rint(__ddiv_rn(p.y, eps));
 }
 
 struct AdjGrid {
-    long long mx, my, sy;  // key = ((cx - mx) * sy + (cy - my)) * R + region
-    int R;
+    // key = ((frame * sx + (cx - mx)) * sy + (cy - my)) * R + region; frames never share a cell
+    long long mx, my, sx, sy;
+    int R, n_rows;
 };
 
 __global__ void k_adj_keys(const long long* __restrict__ cx, const long long* __restrict__ cy,
-                           const int* __restrict__ row_region, int n_rows, AdjGrid g,
+                           const int* __restrict__ row_region, long long n, AdjGrid g,
                            unsigned long long* __restrict__ keys) {
-    const int v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= n_rows) return;
-    keys[v] = (unsigned long long)(((cx[v] - g.mx) * g.sy + (cy[v] - g.my)) * g.R + row_region[v]);
+    const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= n) return;
+    const long long f = v / g.n_rows;
+    const int row = (int)(v - f * g.n_rows);
+    keys[v] = (unsigned long long)(((f * g.sx + (cx[v] - g.mx)) * g.sy + (cy[v] - g.my)) * g.R + row_region[row]);
 }
 
 __device__ __forceinline__ int lower_bound_u64(const unsigned long long* __restrict__ a, int n, unsigned long long x) {
@@ -484,8 +487,8 @@ __device__ __forceinline__ int lower_bound_u64(const unsigned long long* __restr
     return lo;
 }
 
-// one thread per unique (cell, region a): partners b > a owning any of the 3x3 neighbour cells,
-// each counted once per cell of a (geomodel.py:398-408)
+// one thread per unique (frame, cell, region a): partners b > a owning any of the 3x3 neighbour
+// cells, each counted once per cell of a (geomodel.py:398-408); emits (frame*R + a)*R + b
 __global__ void k_adj_pairs(const unsigned long long* __restrict__ uk, const int* __restrict__ n_uk_p, AdjGrid g,
                             unsigned long long* __restrict__ out, unsigned long long cap,
                             unsigned long long* __restrict__ n_out) {
@@ -496,15 +499,16 @@ __global__ void k_adj_pairs(const unsigned long long* __restrict__ uk, const int
     const unsigned long long R = (unsigned long long)g.R;
     const unsigned long long cell = key / R;
     const int a = (int)(key - cell * R);
-    const long long ccx = (long long)cell / g.sy, ccy = (long long)cell - ccx * g.sy;
+    const long long fx = (long long)cell / g.sy, ccy = (long long)cell - fx * g.sy;
+    const long long f = fx / g.sx, ccx = fx - f * g.sx;
     constexpr int CAP = 48;
     int part[CAP];
     int np = 0;
     for (int dx = -1; dx <= 1; ++dx)
         for (int dy = -1; dy <= 1; ++dy) {
             const long long nx = ccx + dx, ny = ccy + dy;
-            if (nx < 0 || ny < 0 || ny >= g.sy) continue;
-            const unsigned long long c2 = (unsigned long long)(nx * g.sy + ny);
+            if (nx < 0 || nx >= g.sx || ny < 0 || ny >= g.sy) continue;
+            const unsigned long long c2 = (unsigned long long)((f * g.sx + nx) * g.sy + ny);
             int i = lower_bound_u64(uk, n_uk, c2 * R + (unsigned long long)(a + 1));
             for (; i < n_uk && uk[i] < (c2 + 1) * R; ++i) {
                 const int b = (int)(uk[i] - c2 * R);
@@ -514,7 +518,7 @@ __global__ void k_adj_pairs(const unsigned long long* __restrict__ uk, const int
                 if (np < CAP) part[np] = b;
                 ++np;
                 const unsigned long long slot = atomicAdd(n_out, 1ull);
-                if (slot < cap) out[slot] = (unsigned long long)a * R + (unsigned long long)b;
+                if (slot < cap) out[slot] = ((unsigned long long)f * R + (unsigned long long)a) * R + (unsigned long long)b;
             }
         }
 }

@@ -129,6 +129,7 @@ def relative_position_error(mapmodel, carto, *, device: int = 0) -> float:
 
 
 def _adjacent_pairs(xy, ring_start, ring_region, n_regions, epsilon, device):
+    """(frame, a, b) triples for one or more vertex sets of one layout."""
     if epsilon <= 0:
         raise ValueError("epsilon must be positive")
     row_region = np.repeat(np.asarray(ring_region, dtype=np.int32), np.diff(ring_start))
@@ -139,7 +140,27 @@ def detect_adjacencies(mapmodel, epsilon: float, *, device: int = 0) -> frozense
     """Region pairs sharing >= 2 epsilon-cells of vertices (geomodel.py:380-415), on the GPU."""
     (xy, rs, rr, r), ids = _layout(mapmodel)
     pairs = _adjacent_pairs(xy, rs, rr, r, epsilon, device)
-    return frozenset(tuple(sorted((ids[a], ids[b]))) for a, b in pairs.tolist())
+    return frozenset(tuple(sorted((ids[a], ids[b]))) for _, a, b in pairs.tolist())
+
+
+def _edge_keys(edges, ids):
+    """Id-pair set -> sorted unique int64 keys min*R + max over region indices (None if an id is unknown)."""
+    pos = {rid: i for i, rid in enumerate(ids)}
+    try:
+        idx = np.array([(pos[a], pos[b]) for a, b in edges], dtype=np.int64).reshape(-1, 2)
+    except KeyError:
+        return None
+    r = len(ids)
+    return np.unique(idx.min(axis=1) * r + idx.max(axis=1))
+
+
+def _tau(keys_m, keys_c) -> float:
+    """topology_distortion on key arrays: 1 - |em & ec| / |em | ec| (metrics.py:40-47)."""
+    inter = np.intersect1d(keys_m, keys_c, assume_unique=True).size
+    union = keys_m.size + keys_c.size - inter
+    if not union:
+        return 0.0
+    return 1.0 - inter / union
 
 
 @dataclass
@@ -188,7 +209,7 @@ class QualityReport:
 class _FrameMetrics:
     """Device results for F cartogram frames that share one vertex layout."""
 
-    def __init__(self, mapmodel, carto_layout, carto_xy, raster_k, rescale, device):
+    def __init__(self, mapmodel, carto_layout, carto_xy, raster_k, rescale, epsilon, device):
         la, self.ids = _layout(mapmodel)
         xy_b, rs_b, rr_b, r = carto_layout
         self.carto_layout = carto_layout
@@ -196,34 +217,57 @@ class _FrameMetrics:
         self.ham, self.area, self.ca, self.cb, self.status = _shapes(
             la, (self.carto_xy, rs_b, rr_b, r), raster_k, rescale, device)
         self.pos = _position_errors(self.ca, self.cb, device) if r >= 2 else None
+        self.mapmodel, self.map_layout, self.epsilon, self.device = mapmodel, la, epsilon, device
+        self._adj = self._map_keys = None
+
+    def carto_keys(self, f: int) -> np.ndarray:
+        """Adjacency keys of frame f; all frames are detected in one device pass on first use."""
+        if self._adj is None:
+            _, rs_b, rr_b, r = self.carto_layout
+            t = _adjacent_pairs(self.carto_xy, rs_b, rr_b, r, self.epsilon, self.device).astype(np.int64)
+            keys = t[:, 1] * r + t[:, 2]
+            cuts = np.searchsorted(t[:, 0], np.arange(self.carto_xy.shape[0] + 1))
+            self._adj = [keys[cuts[i]:cuts[i + 1]] for i in range(self.carto_xy.shape[0])]
+        return self._adj[f]
+
+    def map_keys(self):
+        """mapmodel.adjacency or detect_adjacencies(mapmodel) (metrics.py:231), as keys."""
+        if self._map_keys is None:
+            adj = self.mapmodel.adjacency
+            keys = _edge_keys(adj, self.ids) if adj else None
+            if keys is None and not adj:
+                xy, rs, rr, r = self.map_layout
+                t = _adjacent_pairs(xy, rs, rr, r, self.epsilon, self.device).astype(np.int64)
+                keys = t[:, 1] * r + t[:, 2]
+            self._map_keys = keys if keys is not None else adj
+        return self._map_keys
 
 
-def _assemble(mapmodel, fm: _FrameMetrics, f: int, weights, edges_map, adjacency_epsilon, device, wall_ms):
+def _assemble(mapmodel, fm: _FrameMetrics, f: int, weights, wall_ms):
     """Reference order (metrics.py:225-247): errors, topology, shapes, position; first raise wins."""
     o = fm.area[f]
     if weights is None:
         s = np.array([r.statistic for r in mapmodel.regions], dtype=float)
         weights = s / s.sum() * o.sum()
     eps, xi, per_cart = cartographic_errors(o, weights)
-    _, rs_b, rr_b, r = fm.carto_layout
-    pairs = _adjacent_pairs(fm.carto_xy[f], rs_b, rr_b, r, adjacency_epsilon, device)
-    edges_carto = frozenset(tuple(sorted((fm.ids[a], fm.ids[b]))) for a, b in pairs.tolist())
-    tau = topology_distortion(edges_map, edges_carto)
+    km = fm.map_keys()
+    kc = fm.carto_keys(f)
+    if isinstance(km, np.ndarray):
+        tau = _tau(km, kc)
+    else:  # an adjacency set naming ids outside the map: set arithmetic on id pairs
+        r = len(fm.ids)
+        tau = topology_distortion(km, {(fm.ids[k // r], fm.ids[k % r]) for k in kc.tolist()})
     bad = np.flatnonzero(fm.status[f])
     if bad.size:
         _raise_status(int(fm.status[f, bad[0]]))
     per_shape = fm.ham[f]
     if fm.pos is None:
         raise NumericError("relative position error needs at least two regions")
-    per_region = {rid: {"cartographic_error": float(ce), "shape_distortion": float(sd)}
-                  for rid, ce, sd in zip(fm.ids, per_cart, per_shape)}
+    per_region = {rid: {"cartographic_error": ce, "shape_distortion": sd}
+                  for rid, ce, sd in zip(fm.ids, per_cart.tolist(), per_shape.tolist())}
     return QualityReport(epsilon=eps, xi=xi, tau=tau, hamming_avg=float(per_shape.mean()),
                          hamming_max=float(per_shape.max()), position_error=float(fm.pos[f]),
                          per_region=per_region, wall_ms=wall_ms)
-
-
-def _map_edges(mapmodel, adjacency_epsilon, device):
-    return mapmodel.adjacency or detect_adjacencies(mapmodel, adjacency_epsilon, device=device)
 
 
 def full_report(mapmodel, carto, weights: np.ndarray | None = None, raster_k: int = DEFAULT_HAMMING_K,
@@ -232,42 +276,33 @@ def full_report(mapmodel, carto, weights: np.ndarray | None = None, raster_k: in
     """All six measures for a map/cartogram pair (metrics.py:213-260)."""
     _check_same_regions(mapmodel, carto)
     lb, _ = _layout(carto)
-    fm = _FrameMetrics(mapmodel, lb, lb[0], raster_k, rescale_shapes, device)
-    o = fm.area[0]
-    if weights is None:
-        s = np.array([r.statistic for r in mapmodel.regions], dtype=float)
-        weights = s / s.sum() * o.sum()
-    cartographic_errors(o, weights)  # raises before the adjacency work, as the reference does
-    edges_map = _map_edges(mapmodel, adjacency_epsilon, device)
-    return _assemble(mapmodel, fm, 0, weights, edges_map, adjacency_epsilon, device, wall_ms)
+    fm = _FrameMetrics(mapmodel, lb, lb[0], raster_k, rescale_shapes, adjacency_epsilon, device)
+    return _assemble(mapmodel, fm, 0, weights, wall_ms)
 
 
 def frame_reports(base_map, carto_layout, carto_xy, statistics, weights, raster_k: int = DEFAULT_HAMMING_K,
                   wall_ms=None, adjacency_epsilon: float = DEFAULT_ADJACENCY_EPSILON, *, device: int = 0):
     """``full_report(base_map.with_statistics(s_t), carto_t, weights_t)`` for F frames in one pass.
 
-    ``carto_xy`` is (F, rows, 2) in ``carto_layout``; one shape launch and one position-error
-    launch cover all frames.  Returns per frame a QualityReport, or the CartomorphError the
-    reference would have raised for it.
+    ``carto_xy`` is (F, rows, 2) in ``carto_layout``; one launch each for the shapes, the
+    adjacencies and the position errors covers all frames.  Returns per frame a QualityReport, or
+    the CartomorphError the reference would have raised for it.
     """
     carto_xy = np.asarray(carto_xy, dtype=float)
     n_frames = carto_xy.shape[0]
     if n_frames == 0:
         return []
-    fm = _FrameMetrics(base_map, carto_layout, carto_xy, raster_k, True, device)
-    edges_map = None
+    fm = _FrameMetrics(base_map, carto_layout, carto_xy, raster_k, True, adjacency_epsilon, device)
     out = []
     for f in range(n_frames):
+        w = None
+        if weights is not None:
+            w = np.asarray(weights[f], dtype=float)
+        else:
+            s = np.asarray(statistics[f], dtype=float)
+            w = s / s.sum() * fm.area[f].sum()
         try:
-            w = None if weights is None else np.asarray(weights[f], dtype=float)
-            if w is None:
-                s = np.asarray(statistics[f], dtype=float)
-                w = s / s.sum() * fm.area[f].sum()
-            cartographic_errors(fm.area[f], w)
-            if edges_map is None:
-                edges_map = _map_edges(base_map, adjacency_epsilon, device)
-            out.append(_assemble(base_map, fm, f, w, edges_map, adjacency_epsilon, device,
-                                 None if wall_ms is None else wall_ms[f]))
+            out.append(_assemble(base_map, fm, f, w, None if wall_ms is None else wall_ms[f]))
         except CartomorphError as exc:
             out.append(exc)
     return out
