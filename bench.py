@@ -172,6 +172,20 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ GPU arm
+TRAFFIC_SRC = "profiles/ncu_traffic.json (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch / frames per launch)"
+
+
+def traffic_for(phase, batch):
+    """DRAM bytes of the dominant phase per launch-iteration over `batch` frames, from a committed ncu capture."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            per = json.load(f)["per_frame_bytes_by_phase"]
+        return per[phase] * batch if phase in per else None
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -248,7 +262,12 @@ def main():
     value = iters_total / (ms_max * 1e-3)
 
     # per-phase device times (eager launches, events on the same stream) -> dominant kernel
+    prof_range = os.environ.get("DET_PROFILE_RANGE") == "1"  # ncu --profile-from-start off: these launches
+    if prof_range:
+        torch.cuda.profiler.start()
     ph = ctx.kernel_times(8)
+    if prof_range:
+        torch.cuda.profiler.stop()
     names = ["integral_images", "region", "row", "ctrl"]
     per_iter_ms = {k: v / 8 for k, v in zip(names, ph)}
     dom = max(per_iter_ms, key=per_iter_ms.get)
@@ -301,7 +320,8 @@ def main():
                              % int(args.batch * 35), "iterations_per_time_step": prm["iterations"],
                        "time_steps_per_s": value / prm["iterations"]},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_achieved, "peak": peak, "unit": "GB/s",
-                         "frac": dom_achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": dom_achieved / peak, "traffic": traffic_for(dom, args.batch),
+                         "traffic_source": TRAFFIC_SRC, "peak_kind": peak_kind,
                          "phase_ms_per_iteration": per_iter_ms,
                          "step": {"algorithmic_bytes": step_bytes, "achieved": step_achieved,
                                   "frac": step_achieved / peak}},
