@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_det.so")
+LIB_PATH = os.environ.get("DET_LIB") or os.path.join(_HERE, "_det.so")  # DET_LIB: A/B builds (diagnostics)
 
 DET_OK, DET_E_ARG, DET_E_CUDA, DET_E_RASTER, DET_E_COLLAPSE, DET_E_NUMERIC, DET_E_VALUE, DET_E_STATE = range(8)
 STOP_NAMES = {1: "converged", 2: "stagnation", 3: "max-iterations"}

@@ -797,6 +797,9 @@ int det_bench_kernel_times(det_ctx* ctx, int iters, float* ms_out) {
     cudaEvent_t ev[5];
     for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&ev[i]));
     for (int i = 0; i < 4; ++i) ms_out[i] = 0.f;
+    // diagnostics: DET_KT_REGION_MODE=1 times k_region's advect phase alone (raster skipped)
+    const char* km = getenv("DET_KT_REGION_MODE");
+    const int region_mode = (km && km[0] == '1') ? M_ADVECT : (M_ADVECT | M_RASTER);
     const Topo T = make_topo(ctx);
     const Bufs D = make_bufs(ctx);
     SatSrc S;
@@ -805,7 +808,7 @@ int det_bench_kernel_times(det_ctx* ctx, int iters, float* ms_out) {
         CK(cudaEventRecord(ev[0], ctx->stream));
         launch_sat(ctx, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, ctx->f64 != 0, ctx->B);
         CK(cudaEventRecord(ev[1], ctx->stream));
-        launch_region(ctx, T, D, M_ADVECT | M_RASTER, G_ACTIVE, 0);
+        launch_region(ctx, T, D, region_mode, G_ACTIVE, 0);
         CK(cudaEventRecord(ev[2], ctx->stream));
         launch_row(ctx, T, D, G_ACTIVE, 0);  // includes the control step (last CTA)
         CK(cudaEventRecord(ev[3], ctx->stream));

@@ -32,7 +32,10 @@ constexpr int RW_WARPS = 4;      // warps (regions) per k_region block
 constexpr int RW_ROWCAP = 384;   // vertex rows kept in smem per warp
 constexpr int RW_TCAP = 256;     // toggles per warp window
 constexpr int RW_WROWS = 128;    // texture rows per warp window
-constexpr int RW_UNROLL = 4;     // vertex rows in flight per lane (latency hiding)
+#ifndef DET_RW_UNROLL
+#define DET_RW_UNROLL 2
+#endif
+constexpr int RW_UNROLL = DET_RW_UNROLL;  // vertex rows in flight per lane (2 measured best of 1-8)
 
 // Bilinear sample of the field (displacement.py:209-226): g = p*n - 0.5,
 // i0 = clip(floor(g), 0, n-2), f = clip(g - i0, 0, 1), 4-tap blend.  Index math in
@@ -67,13 +70,26 @@ struct Texels {
 };
 
 template <typename UT>
+struct Vec2;
+template <>
+struct Vec2<float> {
+    using type = float2;
+};
+template <>
+struct Vec2<double> {
+    using type = double2;
+};
+
+// the four texels as (u, v) pairs: one 8-byte (float) / 16-byte (double) load each
+template <typename UT>
 __device__ __forceinline__ Texels<UT> field_load(const UT* __restrict__ uf, const Tap& t) {
+    using V = typename Vec2<UT>::type;
+    const V* __restrict__ u2 = reinterpret_cast<const V*>(uf);
+    const V a = __ldg(u2 + (t.o0 >> 1)), b = __ldg(u2 + (t.o0 >> 1) + 1);
+    const V c = __ldg(u2 + (t.o1 >> 1)), d = __ldg(u2 + (t.o1 >> 1) + 1);
     Texels<UT> x;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        x.v[q] = __ldg(uf + t.o0 + q);
-        x.v[4 + q] = __ldg(uf + t.o1 + q);
-    }
+    x.v[0] = a.x; x.v[1] = a.y; x.v[2] = b.x; x.v[3] = b.y;
+    x.v[4] = c.x; x.v[5] = c.y; x.v[6] = d.x; x.v[7] = d.y;
     return x;
 }
 
@@ -117,13 +133,17 @@ __device__ __forceinline__ int warp_excl_scan_int(int v, int lane, int* total) {
 }
 
 template <typename UT>
-__global__ void __launch_bounds__(RW_WARPS * 32, 8) k_region(Topo T, Bufs D, int mode, int gate, int src) {
+#ifndef DET_RW_MINB
+#define DET_RW_MINB 8
+#endif
+__global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, Bufs D, int mode, int gate, int src) {
     __shared__ int s_jr[RW_WARPS][RW_ROWCAP];       // ceil(y*n - 0.5) clipped to [0, n]
     __shared__ uint16_t s_nx[RW_WARPS][RW_ROWCAP];  // next row of the same ring (region-local index)
     __shared__ int s_tot[RW_WARPS];
     __shared__ uint32_t s_key[RW_WARPS][RW_TCAP];
     __shared__ uint16_t s_col[RW_WARPS][RW_TCAP];
     __shared__ int s_rc[RW_WARPS][RW_WROWS + 1];
+    __shared__ uint32_t s_q[RW_WARPS][64];  // compacted crossing edges (ring buffer)
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int r = blockIdx.x * RW_WARPS + wid, b = blockIdx.y + D.b0;
@@ -241,27 +261,8 @@ __global__ void __launch_bounds__(RW_WARPS * 32, 8) k_region(Topo T, Bufs D, int
         // ---- crossings of every ring edge (raster.py:30-61, flattening :86-89) ----
         if (lane == 0) s_tot[wid] = 0;
         __syncwarp();
-        for (int e = row0 + lane; e < row1; e += 32) {
-            int ja, jb2, en;
-            double2 a, c;
-            if (in_smem) {
-                en = snx[e - row0];
-                ja = sjr[e - row0];
-                jb2 = sjr[en];
-            } else {
-                en = T.row_next[e] - row0;
-                a = gpos[e];
-                c = gpos[row0 + en];
-                ja = min(max(ceil_to_int(__dsub_rn(__dmul_rn(a.y, nd), 0.5)), 0), n);
-                jb2 = min(max(ceil_to_int(__dsub_rn(__dmul_rn(c.y, nd), 0.5)), 0), n);
-            }
-            const int js = max(min(ja, jb2), w0);  // scanlines j in [jlo, jhi) are crossed
-            const int je = min(max(ja, jb2), w1 + back);
-            if (je <= js) continue;  // most short edges cross no scanline centre
-            if (in_smem) {  // endpoints only for the edges that cross a scanline (L1/L2-resident)
-                a = gpos[e];
-                c = gpos[row0 + en];
-            }
+        // toggles of one edge a -> c crossing scanlines [js, je) (raster.py:45-61)
+        auto emit = [&](double2 a, double2 c, int js, int je) {
             a = make_double2(__dmul_rn(a.x, nd), __dmul_rn(a.y, nd));
             c = make_double2(__dmul_rn(c.x, nd), __dmul_rn(c.y, nd));
             const double x0 = a.x, y0 = a.y;
@@ -287,6 +288,47 @@ __global__ void __launch_bounds__(RW_WARPS * 32, 8) k_region(Topo T, Bufs D, int
                     keys[slot] = ((uint32_t)(dest - w0) << 16) | (uint32_t)(i_off + cc);
                     atomicAdd(&rc[dest - w0], 1);
                 }
+            }
+        };
+        if (in_smem) {
+            // edges that cross a scanline centre (~30%) are compacted into a ring queue and
+            // processed 32 at a time, so the float64 crossing work runs on full warps
+            uint32_t* q = s_q[wid];
+            int qh = 0, qt = 0;
+            auto run = [&](uint32_t ent) {
+                const int el = (int)(ent & 0xFFFFu), en = (int)(ent >> 16);
+                const int ja = sjr[el], jb2 = sjr[en];
+                emit(gpos[row0 + el], gpos[row0 + en], max(min(ja, jb2), w0), min(max(ja, jb2), w1 + back));
+            };
+            for (int e0 = 0; e0 < nrows; e0 += 32) {
+                const int el = e0 + lane;
+                bool cr = false;
+                int en = 0;
+                if (el < nrows) {
+                    en = snx[el];
+                    const int ja = sjr[el], jb2 = sjr[en];
+                    cr = min(max(ja, jb2), w1 + back) > max(min(ja, jb2), w0);
+                }
+                const unsigned m = __ballot_sync(FULL, cr);
+                if (cr) q[(qt + __popc(m & ((1u << lane) - 1u))) & 63] = (uint32_t)el | ((uint32_t)en << 16);
+                qt += __popc(m);
+                __syncwarp();
+                if (qt - qh >= 32) {
+                    run(q[(qh + lane) & 63]);
+                    qh += 32;
+                    __syncwarp();
+                }
+            }
+            if (lane < qt - qh) run(q[(qh + lane) & 63]);
+        } else {
+            for (int e = row0 + lane; e < row1; e += 32) {
+                const int en = T.row_next[e] - row0;
+                const double2 a = gpos[e], c = gpos[row0 + en];
+                const int ja = min(max(ceil_to_int(__dsub_rn(__dmul_rn(a.y, nd), 0.5)), 0), n);
+                const int jb2 = min(max(ceil_to_int(__dsub_rn(__dmul_rn(c.y, nd), 0.5)), 0), n);
+                const int js = max(min(ja, jb2), w0);  // scanlines j in [jlo, jhi) are crossed
+                const int je = min(max(ja, jb2), w1 + back);
+                if (je > js) emit(a, c, js, je);
             }
         }
         __syncwarp();
