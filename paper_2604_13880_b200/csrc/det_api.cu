@@ -89,7 +89,6 @@ struct det_ctx {
     Topo g_topo;  // launch signature the graph was captured with
     Bufs g_bufs;
     int g_groups = 0;
-    bool stage_band = false;  // smem-staged float band kernels (DET_STAGE_BAND=1)
     std::vector<cudaStream_t> gstreams;
 };
 
@@ -144,47 +143,54 @@ static Bufs make_bufs(det_ctx* c) {
 template <int CPT, int NT>
 static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S, int gate, int src, int out,
                            bool u64, int B) {
-    const int n = c->n;
+    const int n = c->n, H = c->H, R = c->R;
     const dim3 gb(c->nb, B);
     // float32 in-band arithmetic only for the float32 field from labels; float64 otherwise
     const bool f32 = (src == SRC_LABELS && out == OUT_U && !u64);
-    const bool staged = f32 && c->stage_band;
-    const size_t smem1 = (size_t)2 * (n + c->H - 1) * (f32 ? sizeof(float) : sizeof(double));
+    const size_t sa = f32 ? sizeof(float) : sizeof(double);
+    // the residual-density LUT goes to shared memory when it fits in 48 KB
+    const bool luts = src == SRC_LABELS && (size_t)lut_smem_len(R) * sa <= 48 * 1024;
+    const size_t lut_b = luts ? (size_t)lut_smem_len(R) * sa : 0;
+    const size_t smem1 = ((size_t)2 * (n + H - 1) + (size_t)H * (NT / 32)) * sa;
+#define DET_SAT1(SRC_, A_, L_)                                                                               \
+    do {                                                                                                     \
+        auto fn = k_sat1<CPT, NT, SRC_, A_, L_>;                                                             \
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);                   \
+        fn<<<gb, NT, smem1, c->stream>>>(T, D, S, gate);                                                     \
+    } while (0)
     if (src == SRC_LABELS) {
-        if (staged) {  // smem-staged band
-            const size_t sm1s = ((size_t)c->H * n + 2 * (n + c->H - 1) + std::min(c->R + 1, LUT_SMEM_MAX)) * sizeof(float);
-            cudaFuncSetAttribute(k_sat1s<CPT, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1s);
-            k_sat1s<CPT, NT><<<gb, NT, sm1s, c->stream>>>(T, D, gate);
-        } else if (f32) {
-            cudaFuncSetAttribute(k_sat1<CPT, NT, SRC_LABELS, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-            k_sat1<CPT, NT, SRC_LABELS, float><<<gb, NT, smem1, c->stream>>>(T, D, S, gate);
-        } else {
-            cudaFuncSetAttribute(k_sat1<CPT, NT, SRC_LABELS, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-            k_sat1<CPT, NT, SRC_LABELS, double><<<gb, NT, smem1, c->stream>>>(T, D, S, gate);
-        }
+        // k_sat1 gathers the LUT through L1 (__ldg): staging it per CTA measured slower there
+        if (f32) DET_SAT1(SRC_LABELS, float, false);
+        else DET_SAT1(SRC_LABELS, double, false);
     } else {
-        cudaFuncSetAttribute(k_sat1<CPT, NT, SRC_DENSE, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
-        k_sat1<CPT, NT, SRC_DENSE, double><<<gb, NT, smem1, c->stream>>>(T, D, S, gate);
+        DET_SAT1(SRC_DENSE, double, false);
     }
+#undef DET_SAT1
     const int lanes = n + 2 * (2 * n - 1);
     const int G = std::min(8, c->nb);
     k_sat2<<<dim3((lanes + 31) / 32 + 1, B), 32 * G, 0, c->stream>>>(D, gate);
-    const size_t smem = (size_t)3 * (n + c->H) * (f32 ? sizeof(float) : sizeof(double)) +
-                        (staged ? ((size_t)c->H * n + (size_t)c->H * NT + std::min(c->R + 1, LUT_SMEM_MAX)) * sizeof(float)
-                                : 0);  // + staged band, row prefixes, LUT
-#define DET_SAT3(SRC_, UT_, OUT_, STG_)                                                                            \
+    const size_t smem = ((size_t)3 * (n + H) + 3 * H + (H & 1)) * sa + lut_b;
+#define DET_SAT3(SRC_, UT_, OUT_, L_)                                                                        \
     do {                                                                                                     \
-        auto fn = k_sat3<CPT, NT, SRC_, UT_, OUT_, UT_, STG_>;                                               \
+        auto fn = k_sat3<CPT, NT, SRC_, UT_, OUT_, UT_, L_>;                                                 \
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                    \
         fn<<<gb, NT, smem, c->stream>>>(T, D, S, gate);                                                      \
     } while (0)
     if (out == OUT_CH8) {
-        if (src == SRC_LABELS) DET_SAT3(SRC_LABELS, double, OUT_CH8, false);
-        else DET_SAT3(SRC_DENSE, double, OUT_CH8, false);
+        if (src == SRC_LABELS) {
+            if (luts) DET_SAT3(SRC_LABELS, double, OUT_CH8, true);
+            else DET_SAT3(SRC_LABELS, double, OUT_CH8, false);
+        } else {
+            DET_SAT3(SRC_DENSE, double, OUT_CH8, false);
+        }
     } else if (src == SRC_LABELS) {
-        if (u64) DET_SAT3(SRC_LABELS, double, OUT_U, false);
-        else if (staged) DET_SAT3(SRC_LABELS, float, OUT_U, true);
-        else DET_SAT3(SRC_LABELS, float, OUT_U, false);
+        if (u64) {
+            if (luts) DET_SAT3(SRC_LABELS, double, OUT_U, true);
+            else DET_SAT3(SRC_LABELS, double, OUT_U, false);
+        } else {
+            if (luts) DET_SAT3(SRC_LABELS, float, OUT_U, true);
+            else DET_SAT3(SRC_LABELS, float, OUT_U, false);
+        }
     } else {
         if (u64) DET_SAT3(SRC_DENSE, double, OUT_U, false);
         else DET_SAT3(SRC_DENSE, float, OUT_U, false);
@@ -319,11 +325,10 @@ static int alloc_sat(det_ctx* ctx, int B) {
 }
 
 static int auto_band_height(int n, int B) {
-    // enough band CTAs to fill the 148 SMs twice over, but tall bands amortise the carries;
-    // the float path stages H x n floats in shared memory (<= 64 KB)
+    // enough band CTAs to fill the 148 SMs twice over, but tall bands amortise the carries
+    // and the per-CTA LUT copy (H = 32 at 1024^2 x 16 frames; 16 and 64 measured slower)
     int h = 8;
     while (h < 64 && (long long)(n / (2 * h)) * B >= 2 * 148) h *= 2;
-    while (h > 1 && (size_t)h * n * sizeof(float) > 64 * 1024) h >>= 1;
     return std::min(h, n);
 }
 
@@ -439,7 +444,6 @@ int det_ctx_create(int device, int k, int field_f64, det_ctx** out) {
     ctx->n = 1 << k;
     ctx->f64 = field_f64 ? 1 : 0;
     ctx->H = std::min(8, ctx->n);
-    if (const char* e = getenv("DET_STAGE_BAND")) ctx->stage_band = atoi(e) != 0;
     ctx->nb = ctx->n / ctx->H;
     cudaError_t e = cudaSetDevice(device);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);

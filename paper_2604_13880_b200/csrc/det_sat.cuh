@@ -36,9 +36,12 @@
 namespace det {
 
 // Residual density of CPT consecutive pixels of row j in the accumulator type A
-// (float32 in the float32-field mode, float64 otherwise).
-template <int CPT, int SRC, typename A>
-__device__ __forceinline__ void load_rho(const Bufs& D, const SatSrc& S, int R, int b, int j, int x0, A (&rho)[CPT]) {
+// (float32 in the float32-field mode, float64 otherwise).  `lut` is the cartogram's
+// residual-density table (indexed by region rank, background at R): a shared-memory
+// copy when it fits (LUTS), else global memory.
+template <int CPT, int SRC, typename A, bool LUTS>
+__device__ __forceinline__ void load_rho(const Bufs& D, const SatSrc& S, const A* lut, int R, int b, int j, int x0,
+                                         A (&rho)[CPT]) {
     const int n = D.n;
     if (x0 >= n) {
 #pragma unroll
@@ -58,14 +61,10 @@ __device__ __forceinline__ void load_rho(const Bufs& D, const SatSrc& S, int R, 
                 L[q] = v.x; L[q + 1] = v.y; L[q + 2] = v.z; L[q + 3] = v.w;
             }
         }
-        if (sizeof(A) == 4) {
-            const float* lut = D.lutf + (size_t)b * (R + 1);
 #pragma unroll
-            for (int k = 0; k < CPT; ++k) rho[k] = (A)__ldg(lut + (L[k] < 0 ? R : L[k]));
-        } else {
-            const double* lut = D.lut + (size_t)b * (R + 1);
-#pragma unroll
-            for (int k = 0; k < CPT; ++k) rho[k] = (A)__ldg(lut + (L[k] < 0 ? R : L[k]));
+        for (int k = 0; k < CPT; ++k) {
+            const int ix = L[k] < 0 ? R : L[k];
+            rho[k] = LUTS ? lut[ix] : __ldg(lut + ix);
         }
     } else {
         const double* d = S.d + (size_t)b * D.nn + (size_t)j * n + x0;
@@ -73,6 +72,22 @@ __device__ __forceinline__ void load_rho(const Bufs& D, const SatSrc& S, int R, 
         for (int k = 0; k < CPT; ++k) rho[k] = (A)__dadd_rn(__dmul_rn(d[k], S.scale), S.offset);
     }
 }
+
+// The cartogram's LUT in the accumulator type: global pointer, copied to `s_lut` when LUTS.
+template <typename A, bool LUTS>
+__device__ __forceinline__ const A* band_lut(const Bufs& D, int R, int b, A* s_lut) {
+    const A* g = sizeof(A) == 4 ? reinterpret_cast<const A*>(D.lutf + (size_t)b * (R + 1))
+                                : reinterpret_cast<const A*>(D.lut + (size_t)b * (R + 1));
+    if constexpr (!LUTS) {
+        return g;
+    } else {
+        for (int i = threadIdx.x; i <= R; i += blockDim.x) s_lut[i] = __ldg(g + i);
+        return s_lut;  // published by the caller's first barrier
+    }
+}
+
+// shared-memory LUT length (entries), rounded so what follows stays 8-byte aligned
+__host__ __device__ __forceinline__ int lut_smem_len(int R) { return (R + 2) & ~1; }
 
 template <typename A>
 __device__ __forceinline__ A warp_incl_scan_t(A v) {
@@ -107,54 +122,53 @@ __device__ void block_prefix_smem(A* a, double* out, int len, double* sm) {
 // AD_b(w) = sum_{j in band, i+j<=w} rho (compact index q = w - jt).  Outside the
 // compact range the prefixes are 0 (below) or the band total (above).  In-band sums
 // in A; the x-prefixes and everything downstream in float64.
-template <int CPT, int NT, int SRC, typename A>
+template <int CPT, int NT, int SRC, typename A, bool LUTS>
 __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate) {
-    extern __shared__ unsigned char s_raw1[];  // dg[L] | ad[L] in A
-    __shared__ A s_w[3][32];
+    extern __shared__ unsigned char s_raw1[];  // dg[L] | ad[L] | lut (LUTS) | row partials [H][NW], all in A
+    constexpr int NW = NT / 32;
     __shared__ A s_bd[3][32];
     __shared__ A s_ba[3][32];
     __shared__ double s_red[33];
     const int band = blockIdx.x, b = blockIdx.y + D.b0, t = threadIdx.x;
-    const int lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+    const int lane = t & 31, w = t >> 5;
     if (!gate_open(D.st + b, gate)) return;
-    const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, L = n + H - 1;
+    const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, L = n + H - 1, R = T.R;
     const int x0 = t * CPT;
     const size_t bb = (size_t)b * D.nb + band;
     A* dg = reinterpret_cast<A*>(s_raw1);
     A* ad = dg + L;
+    A* s_lut = ad + L;
+    A* s_rows = s_lut + (LUTS ? lut_smem_len(R) : 0);
+    const A* lut = band_lut<A, LUTS>(D, R, b, s_lut);
+    if (LUTS) __syncthreads();
     A cs[CPT], pd[CPT], pa[CPT];
 #pragma unroll
     for (int k = 0; k < CPT; ++k) cs[k] = pd[k] = pa[k] = (A)0;
 
     A rho_n[CPT];
-    load_rho<CPT, SRC, A>(D, S, T.R, b, jt, x0, rho_n);
+    load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, jt, x0, rho_n);
+    int slot = 0, ps = 2;  // rotating boundary slots: (j - jt) % 3, (j - jt + 2) % 3
     for (int j = jt; j <= jb; ++j) {
-        const int slot = (j - jt) % 3, ps = (j - jt + 2) % 3;
         A rho[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
-        if (j < jb) load_rho<CPT, SRC, A>(D, S, T.R, b, j + 1, x0, rho_n);  // prefetch the next row
+        if (j < jb) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, j + 1, x0, rho_n);  // prefetch the next row
         A ts = (A)0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) ts += rho[k];
         ts = warp_sum(ts);
-        if (lane == 0) s_w[slot][w] = ts;
+        if (lane == 0) s_rows[(j - jt) * NW + w] = ts;  // row totals are summed after the sweep
         __syncthreads();
         A left = __shfl_up_sync(FULL, pd[CPT - 1], 1);
         A right = __shfl_down_sync(FULL, pa[0], 1);
         if (lane == 0) left = (w == 0 || j == jt) ? (A)0 : s_bd[ps][w - 1];
-        if (lane == 31) right = (w == nw - 1 || j == jt) ? (A)0 : s_ba[ps][w + 1];
+        if (lane == 31) right = (w == NW - 1 || j == jt) ? (A)0 : s_ba[ps][w + 1];
         A nd_[CPT], na_[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
             nd_[k] = rho[k] + (k == 0 ? left : pd[k - 1]);
             na_[k] = rho[k] + (k == CPT - 1 ? right : pa[k + 1]);
             cs[k] += rho[k];
-        }
-        if (t == 0) {
-            double s = 0.0;
-            for (int q = 0; q < nw; ++q) s += (double)s_w[slot][q];
-            D.rt[(size_t)b * n + j] = s;
         }
         if (j < jb) {
             if (x0 <= n - 1 && n - 1 < x0 + CPT) dg[n - 1 - j + jb] = nd_[n - 1 - x0];  // diagonal leaves right edge
@@ -164,6 +178,8 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
         if (lane == 0) s_ba[slot][w] = na_[0];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) { pd[k] = nd_[k]; pa[k] = na_[k]; }
+        ps = slot;
+        slot = slot == 2 ? 0 : slot + 1;
     }
     // band bottom: remaining diagonals / anti-diagonals end here; column sums -> x-prefix
     double csum = 0.0;
@@ -177,7 +193,13 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
         csum += x < n ? (double)cs[k] : 0.0;
     }
     double tot;
-    double run = block_excl_scan(csum, s_red, &tot);  // (its barriers also publish dg/ad)
+    double run = block_excl_scan(csum, s_red, &tot);  // (its barriers also publish dg/ad and s_rows)
+    if (t < H) {  // row totals in float64, warp order (as the sweep produced them)
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) s += (double)s_rows[t * NW + q];
+        D.rt[(size_t)b * n + jt + t] = s;
+    }
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
         const int x = x0 + k;
@@ -186,104 +208,6 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
     }
     block_prefix_smem<A>(dg, D.dgc + bb * L, L, s_red);
     block_prefix_smem<A>(ad, D.adc + bb * L, L, s_red);
-}
-
-// ---------------------------------------------------------------------------------
-// float32 path, smem-staged: the band's H x n residual densities are loaded once (all
-// label/LUT loads independent -> high memory-level parallelism) into shared memory.
-constexpr int LUT_SMEM_MAX = 16384;  // float LUT entries copied to shared memory per CTA
-
-// Copy the cartogram's float LUT (R+1 entries) into shared memory when it fits; returns the
-// table to gather from (smem copy or the global array).
-__device__ __forceinline__ const float* stage_lut(const Bufs& D, int R, int b, float* s_lut) {
-    const float* g = D.lutf + (size_t)b * (R + 1);
-    if (R + 1 > LUT_SMEM_MAX) return g;
-    for (int i = threadIdx.x; i <= R; i += blockDim.x) s_lut[i] = __ldg(g + i);
-    __syncthreads();
-    return s_lut;
-}
-
-template <int CPT>
-__device__ __forceinline__ void stage_rho_band(const Bufs& D, const float* lut, int R, int b, int jt, int H, int x0,
-                                               float* rho) {
-    const int n = D.n;
-    if (x0 >= n) return;
-    const int* lab = D.labels + (size_t)b * D.nn + (size_t)jt * n + x0;
-    for (int j0 = 0; j0 < H; j0 += 4) {
-        int L[4][CPT];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (j0 + q >= H) continue;
-#pragma unroll
-            for (int k = 0; k < CPT; k += 2) {
-                const int2 v = *reinterpret_cast<const int2*>(lab + (size_t)(j0 + q) * n + k);
-                L[q][k] = v.x;
-                L[q][k + 1] = v.y;
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (j0 + q >= H) continue;
-#pragma unroll
-            for (int k = 0; k < CPT; ++k) rho[(j0 + q) * n + x0 + k] = lut[L[q][k] < 0 ? R : L[q][k]];
-        }
-    }
-}
-
-// k_sat1 for the float32 path: band sums straight from the staged band, no per-row barriers.
-template <int CPT, int NT>
-__global__ void __launch_bounds__(NT) k_sat1s(Topo T, Bufs D, int gate) {
-    extern __shared__ float s_f1[];  // rho[H][n] | dg[L] | ad[L] | lut[R+1]
-    __shared__ double s_red[33];
-    const int band = blockIdx.x, b = blockIdx.y + D.b0, t = threadIdx.x;
-    const int lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
-    if (!gate_open(D.st + b, gate)) return;
-    const int n = D.n, H = D.H, jt = band * H, L = n + H - 1;
-    const int x0 = t * CPT;
-    const size_t bb = (size_t)b * D.nb + band;
-    float* rho = s_f1;
-    float* dg = rho + H * n;
-    float* ad = dg + L;
-    const float* lut = stage_lut(D, T.R, b, ad + L);
-    stage_rho_band<CPT>(D, lut, T.R, b, jt, H, x0, rho);
-    __syncthreads();
-    for (int jj = w; jj < H; jj += nw) {  // row totals
-        float s = 0.f;
-        for (int x = lane; x < n; x += 32) s += rho[jj * n + x];
-        s = warp_sum(s);
-        if (lane == 0) D.rt[(size_t)b * n + jt + jj] = (double)s;
-    }
-    for (int q = t; q < L; q += blockDim.x) {
-        float sd = 0.f, sa = 0.f;
-        for (int jj = 0; jj < H; ++jj) {
-            const int xd = q - (H - 1) + jj;  // diagonal q = x - j + jb
-            const int xa = q - jj;            // anti-diagonal q = x + j - jt
-            if (xd >= 0 && xd < n) sd += rho[jj * n + xd];
-            if (xa >= 0 && xa < n) sa += rho[jj * n + xa];
-        }
-        dg[q] = sd;
-        ad[q] = sa;
-    }
-    double cs[CPT], csum = 0.0;
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-        float c = 0.f;
-        const int x = x0 + k;
-        if (x < n)
-            for (int jj = 0; jj < H; ++jj) c += rho[jj * n + x];
-        cs[k] = (double)c;
-        csum += cs[k];
-    }
-    double tot;
-    double run = block_excl_scan(csum, s_red, &tot);  // (its barriers also publish dg/ad)
-#pragma unroll
-    for (int k = 0; k < CPT; ++k) {
-        const int x = x0 + k;
-        run += cs[k];
-        if (x < n) D.cs[bb * n + x] = run;
-    }
-    block_prefix_smem<float>(dg, D.dgc + bb * L, L, s_red);
-    block_prefix_smem<float>(ad, D.adc + bb * L, L, s_red);
 }
 
 // ---------------------------------------------------------------------------------
@@ -379,27 +303,31 @@ __global__ void k_sat2(Bufs D, int gate) {
 // ---------------------------------------------------------------------------------
 // Per band: load the float64 carries, then one top-down sweep.  In-band arithmetic
 // in A (float32 when the field is stored as float32), carries rounded to A once.
-template <int CPT, int NT, int SRC, typename UT, int OUT, typename A, bool STAGE>
+template <int CPT, int NT, int SRC, typename UT, int OUT, typename A, bool LUTS>
 __global__ void __launch_bounds__(NT) k_sat3(Topo T, Bufs D, SatSrc S, int gate) {
     extern __shared__ unsigned char s_raw3[];
+    constexpr int NW = NT / 32;
     __shared__ A s_w[3][32];
     __shared__ A s_xa[3][32], s_xu1[3][32], s_xu2[3][32], s_xr[3][32];
     const int band = blockIdx.x, b = blockIdx.y + D.b0, t = threadIdx.x;
-    const int lane = t & 31, w = t >> 5, nw = blockDim.x >> 5;
+    const int lane = t & 31, w = t >> 5;
     if (!gate_open(D.st + b, gate)) return;
-    const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, M = 2 * n - 1;
+    const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, M = 2 * n - 1, R = T.R;
     const int x0 = t * CPT;
+    const bool active = x0 < n;  // n is a multiple of CPT: a thread's columns are all in or all out
     const size_t bb = (size_t)b * D.nb + band;
     const int WN = n + H;
     A* win_dl = reinterpret_cast<A*>(s_raw3);  // DLtot(w), w in [jt-1, jb+n-1]  -> [w-(jt-1)]
     A* win_tu = win_dl + WN;                   // Tu(w),    w in [jt-1, jb+n-2]  -> [w-(jt-1)]
     A* win_tv = win_dl + 2 * WN;               // Tv(v),    v in [-jb, n-1-jt]   -> [v+jb]
+    A* s_rc = win_dl + 3 * WN;                 // per band row: ravg, rowfull(j+1), right boundary
+    A* s_lut = s_rc + 3 * H + (H & 1);
     const double* rowfull = D.rowfull + (size_t)b * (n + 1);
     const double* adT = D.adT + (size_t)b * M;
     const double* dgT = D.dgT + (size_t)b * M;
     const double* csT = D.csT + (size_t)b * n;
 
-    // ---- carries (k_sat2) ----
+    // ---- carries (k_sat2), row constants, LUT ----
     for (int q = t; q < WN; q += blockDim.x) {
         win_dl[q] = (jt == 0 && q == 0) ? (A)0 : (A)D.adSc[bb * WN + q];  // DLtot(-1) = 0
         const int wq = jt - 1 + q;
@@ -407,6 +335,14 @@ __global__ void __launch_bounds__(NT) k_sat3(Topo T, Bufs D, SatSrc S, int gate)
         const int iv = q - jb + n - 1;  // Tv index of v = q - jb
         win_tv[q] = (iv >= 0 && iv < M) ? (A)dgT[iv] : (A)0;
     }
+    const double rf_top = rowfull[jt];
+    for (int q = t; q < H; q += blockDim.x) {
+        const double r0 = rowfull[jt + q], r1 = rowfull[jt + q + 1];
+        s_rc[q] = (A)(0.5 * (r0 + r1));
+        s_rc[H + q] = (A)r1;
+        s_rc[2 * H + q] = (A)(r0 - rf_top);
+    }
+    const A* lut = band_lut<A, LUTS>(D, R, b, s_lut);
     // cc[k]: column-total average cavg(x) = (colfull(x) + colfull(x+1))/2 for the field,
     // colfull(x+1) for the channel dump
     A ul[CPT], al[CPT], cc[CPT], ur[CPT];
@@ -426,92 +362,35 @@ __global__ void __launch_bounds__(NT) k_sat3(Topo T, Bufs D, SatSrc S, int gate)
         s_xu2[2][w] = ul[CPT - 2];
     }
     if (lane == 0) s_xr[2][w] = (A)0;
-    const double rf_top = rowfull[jt];
     const A Cr = (A)rowfull[n];
     const double inv_nd = 1.0 / (double)n;  // exact: n is a power of two
-    const A inv_n = (A)inv_nd;
+    const A inv_n = (A)inv_nd, half_n = (A)(0.5 * inv_nd);
     const A inv2m = (A)(S.outscale != 0.0 ? S.outscale : 0.5 * inv_nd * inv_nd);
     const A xc0 = (A)(((double)x0 + 0.5) * inv_nd);  // pixel-centre x of column x0 (displacement.py:59)
     UT* uf = reinterpret_cast<UT*>(D.uf) + (size_t)b * D.nn * 2;
-    constexpr bool STAGED = STAGE && (sizeof(A) == 4 && SRC == SRC_LABELS);
-    float* srho = reinterpret_cast<float*>(win_dl + 3 * WN);  // staged band (float path)
-    A* s_ex = reinterpret_cast<A*>(srho + (size_t)H * n);      // A(j, x0-1) per (row, thread)
-    __shared__ A s_wt[64][33];                                      // warp totals per row (H <= 64)
+    __syncthreads();  // windows, row constants and LUT published
     A rho_n[CPT];
-    if (STAGED) {
-        const float* lut = stage_lut(D, T.R, b, reinterpret_cast<float*>(s_ex + (size_t)H * NT));
-        stage_rho_band<CPT>(D, lut, T.R, b, jt, H, x0, srho);
-        __syncthreads();
-        // all H row prefixes up front: the scans are independent across rows (ILP), so the
-        // sequential row loop below only carries the vertical/diagonal recurrences
-        for (int j0 = 0; j0 < H; j0 += 4) {
-            A ts[4], wi[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                ts[q] = (A)0;
-                if (j0 + q < H && x0 < n) {
-#pragma unroll
-                    for (int k = 0; k < CPT; ++k) ts[q] += (A)srho[(j0 + q) * n + x0 + k];
-                }
-                wi[q] = ts[q];
-            }
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const A y = __shfl_up_sync(FULL, wi[q], o);
-                    if (lane >= o) wi[q] += y;
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (j0 + q >= H) continue;
-                if (lane == 31) s_wt[j0 + q][w] = wi[q];
-                s_ex[(j0 + q) * NT + t] = wi[q] - ts[q];
-            }
-        }
-        __syncthreads();
-        if (t < H) {  // exclusive prefix of the warp totals of row t, stored in place
-            A run = (A)0;
-            for (int q = 0; q < nw; ++q) {
-                const A v = s_wt[t][q];
-                s_wt[t][q] = run;
-                run += v;
-            }
-        }
-    } else {
-        load_rho<CPT, SRC, A>(D, S, T.R, b, jt, x0, rho_n);
-    }
-    __syncthreads();
+    load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, jt, x0, rho_n);
 
+    int slot = 0, ps = 2;  // rotating boundary slots: (j - jt) % 3, (j - jt + 2) % 3
     for (int j = jt; j <= jb; ++j) {
-        const int slot = (j - jt) % 3, ps = (j - jt + 2) % 3;
         A rho[CPT];
-        if (STAGED) {
 #pragma unroll
-            for (int k = 0; k < CPT; ++k) rho[k] = x0 < n ? (A)srho[(j - jt) * n + x0 + k] : (A)0;
-        } else {
-#pragma unroll
-            for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
-            if (j < jb) load_rho<CPT, SRC, A>(D, S, T.R, b, j + 1, x0, rho_n);  // prefetch the next row
-        }
+        for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
+        if (j < jb) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, j + 1, x0, rho_n);  // prefetch the next row
         A loc[CPT];
         A run = (A)0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) { run += rho[k]; loc[k] = run; }
-        A excl;  // A(j, x0-1)
-        if (STAGED) {
-            excl = s_ex[(j - jt) * NT + t] + s_wt[j - jt][w];
-            __syncthreads();  // boundary values of the previous row (s_x*) are published
-        } else {
-            const A tsum = run;
-            const A winc = warp_incl_scan_t<A>(tsum);
-            if (lane == 31) s_w[slot][w] = winc;
-            __syncthreads();
-            A off = (A)0;
-            for (int q = 0; q < w; ++q) off += s_w[slot][q];
-            excl = off + winc - tsum;
-        }
+        // A(j, x0-1): in-warp scan of the thread sums, then a scan of the warp totals
+        const A tsum = run;
+        const A winc = warp_incl_scan_t<A>(tsum);
+        if (lane == 31) s_w[slot][w] = winc;
+        __syncthreads();
+        A wt = lane < NW ? s_w[slot][lane] : (A)0;
+        wt = warp_incl_scan_t<A>(wt);
+        const A woff = __shfl_sync(FULL, wt, (w + 31) & 31);
+        const A excl = (w == 0 ? (A)0 : woff) + winc - tsum;
         A ap_m1 = __shfl_up_sync(FULL, al[CPT - 1], 1);
         A ul_m1 = __shfl_up_sync(FULL, ul[CPT - 1], 1);
         A ul_m2 = __shfl_up_sync(FULL, ul[CPT - 2], 1);
@@ -520,7 +399,7 @@ __global__ void __launch_bounds__(NT) k_sat3(Topo T, Bufs D, SatSrc S, int gate)
             if (w == 0) { ap_m1 = (A)0; ul_m1 = (A)0; ul_m2 = (A)0; }
             else { ap_m1 = s_xa[ps][w - 1]; ul_m1 = s_xu1[ps][w - 1]; ul_m2 = s_xu2[ps][w - 1]; }
         }
-        if (lane == 31) ur_p = (w == nw - 1) ? (A)(rowfull[j] - rf_top) : s_xr[ps][w + 1];
+        if (lane == 31) ur_p = (w == NW - 1) ? s_rc[2 * H + (j - jt)] : s_xr[ps][w + 1];
         A Av[CPT], an[CPT], uln[CPT], urn[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) Av[k] = excl + loc[k];
@@ -530,69 +409,83 @@ __global__ void __launch_bounds__(NT) k_sat3(Topo T, Bufs D, SatSrc S, int gate)
             uln[k] = Av[k] + (k == 0 ? ul_m1 : ul[k - 1]);
             urn[k] = Av[k] + (k == CPT - 1 ? ur_p : ur[k + 1]);
         }
-        const double rf0d = rowfull[j], rf1d = rowfull[j + 1];
-        const A rf1 = (A)rf1d;
-        const A yc = (A)(((double)j + 0.5) * inv_nd);
-        const A ravg = (A)(0.5 * (rf0d + rf1d));
-        const int wi0 = j + x0 - (jt - 1);
-        A dlw[CPT + 1];  // DLtot(j + x - 1 + q), sliding window over this thread's columns
+        if (active) {
+            const A ravg = s_rc[j - jt], rf1 = s_rc[H + (j - jt)];
+            const A yc = (A)j * inv_n + half_n;  // (j + 0.5) / n, exact in A
+            const int wi0 = j + x0 - (jt - 1);
+            A dlw[CPT + 1];  // DLtot(j + x - 1 + q), sliding window over this thread's columns
 #pragma unroll
-        for (int q = 0; q <= CPT; ++q) dlw[q] = win_dl[wi0 - 1 + q];
+            for (int q = 0; q <= CPT; ++q) dlw[q] = win_dl[wi0 - 1 + q];
+            A ux[CPT], uy[CPT];
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) {
-            const int x = x0 + k;
-            if (x >= n) continue;
-            const A apm1 = k == 0 ? ap_m1 : al[k - 1];
-            const A anm1 = k == 0 ? (ap_m1 + excl) : an[k - 1];
-            const A ulnm1 = k == 0 ? (excl + ul_m2) : uln[k - 1];
-            const A ulpm1 = k == 0 ? ul_m1 : ul[k - 1];
-            const A ulpm2 = k == 0 ? ul_m2 : (k == 1 ? ul_m1 : ul[k - 2]);
-            const A urp1 = k == CPT - 1 ? ur_p : ur[k + 1];
-            const A Dw = dlw[k + 1], Dwm1 = dlw[k];
-            const A Tu = win_tu[wi0 + k - 1];
-            const A Tv = win_tv[x - j + jb];
-            A R_UV = ulpm1 + (Dw - urp1);
-            A R_UVm1 = ulnm1 + (Dw - urn[k]);
-            A R_Um1Vm1 = ulpm2 + (Dwm1 - ur[k]);
-            if (x == 0) { R_UVm1 = (A)0; R_Um1Vm1 = (A)0; }
-            const A bt = R_UVm1;
-            const A at = Tu - R_Um1Vm1 + rho[k];
-            const A gt = Tv - R_UV;
-            if (OUT == OUT_CH8) {
-                const A dt = Cr - at - bt - gt;
-                double* ch = S.ch8 + (size_t)b * 8 * D.nn + (size_t)j * n + x;
-                const size_t nn = D.nn;
-                ch[0] = an[k];
-                ch[nn] = cc[k] - an[k];
-                ch[2 * nn] = Cr - cc[k] - rf1 + an[k];
-                ch[3 * nn] = rf1 - an[k];
-                ch[4 * nn] = at;
-                ch[5 * nn] = bt;
-                ch[6 * nn] = gt;
-                ch[7 * nn] = dt;
-            } else {
-                // anchor combination (displacement.py:128-130) with b = cavg-a, d = ravg-a,
-                // g = C-cavg-ravg+a, delta_t = C-at-bt-gt; since q1+q3 = (1+x-y, 1-x+y) and
-                // q2+q4 = (x+y, x+y) in every case, a's coefficient is (1-2y, 1-2x).
-                const A a = (A)0.25 * (apm1 + al[k] + anm1 + an[k]);
-                const A cavg = cc[k];
-                const A K = cavg + ravg - Cr;
-                const A xc = xc0 + (A)k * inv_n, s2 = xc + yc;
-                const bool below = yc < xc, near = s2 < (A)1;  // displacement.py:62,67
-                const A q3x = below ? xc - yc : (A)0, q3y = below ? (A)0 : yc - xc;
-                const A q2x = near ? s2 : (A)1, q2y = near ? (A)0 : s2 - (A)1;
-                const A q4x = near ? (A)0 : s2 - (A)1, q4y = near ? s2 : (A)1;
-                const A ux = (a * ((A)1 - (A)2 * yc) + cavg * q2x + ravg * q4x - K * q3x + xc * (at + gt) + bt) * inv2m;
-                const A uy = (a * ((A)1 - (A)2 * xc) + cavg * q2y + ravg * q4y - K * q3y + at + yc * (Cr - at - gt)) * inv2m;
-                UT* o = uf + ((size_t)j * n + x) * 2;
-                o[0] = (UT)ux;
-                o[1] = (UT)uy;
+            for (int k = 0; k < CPT; ++k) {
+                const int x = x0 + k;
+                const A apm1 = k == 0 ? ap_m1 : al[k - 1];
+                const A anm1 = k == 0 ? (ap_m1 + excl) : an[k - 1];
+                const A ulnm1 = k == 0 ? (excl + ul_m2) : uln[k - 1];
+                const A ulpm1 = k == 0 ? ul_m1 : ul[k - 1];
+                const A ulpm2 = k == 0 ? ul_m2 : (k == 1 ? ul_m1 : ul[k - 2]);
+                const A urp1 = k == CPT - 1 ? ur_p : ur[k + 1];
+                const A Dw = dlw[k + 1], Dwm1 = dlw[k];
+                const A Tu = win_tu[wi0 + k - 1];
+                const A Tv = win_tv[x - j + jb];
+                const A R_UV = ulpm1 + (Dw - urp1);
+                A R_UVm1 = ulnm1 + (Dw - urn[k]);
+                A R_Um1Vm1 = ulpm2 + (Dwm1 - ur[k]);
+                if (k == 0 && x0 == 0) { R_UVm1 = (A)0; R_Um1Vm1 = (A)0; }
+                const A bt = R_UVm1;
+                const A at = Tu - R_Um1Vm1 + rho[k];
+                const A gt = Tv - R_UV;
+                if (OUT == OUT_CH8) {
+                    const A dt = Cr - at - bt - gt;
+                    double* ch = S.ch8 + (size_t)b * 8 * D.nn + (size_t)j * n + x;
+                    const size_t nn = D.nn;
+                    ch[0] = an[k];
+                    ch[nn] = cc[k] - an[k];
+                    ch[2 * nn] = Cr - cc[k] - rf1 + an[k];
+                    ch[3 * nn] = rf1 - an[k];
+                    ch[4 * nn] = at;
+                    ch[5 * nn] = bt;
+                    ch[6 * nn] = gt;
+                    ch[7 * nn] = dt;
+                } else {
+                    // anchor combination (displacement.py:128-130) with b = cavg-a, d = ravg-a,
+                    // g = C-cavg-ravg+a, delta_t = C-at-bt-gt; since q1+q3 = (1+x-y, 1-x+y) and
+                    // q2+q4 = (x+y, x+y) in every case, a's coefficient is (1-2y, 1-2x).
+                    const A a = (A)0.25 * (apm1 + al[k] + anm1 + an[k]);
+                    const A cavg = cc[k];
+                    const A K = cavg + ravg - Cr;
+                    const A xc = xc0 + (A)k * inv_n, s2 = xc + yc;
+                    const bool below = yc < xc, near = s2 < (A)1;  // displacement.py:62,67
+                    const A q3x = below ? xc - yc : (A)0, q3y = below ? (A)0 : yc - xc;
+                    const A q2x = near ? s2 : (A)1, q2y = near ? (A)0 : s2 - (A)1;
+                    const A q4x = near ? (A)0 : s2 - (A)1, q4y = near ? s2 : (A)1;
+                    ux[k] = (a * ((A)1 - (A)2 * yc) + cavg * q2x + ravg * q4x - K * q3x + xc * (at + gt) + bt) * inv2m;
+                    uy[k] = (a * ((A)1 - (A)2 * xc) + cavg * q2y + ravg * q4y - K * q3y + at + yc * (Cr - at - gt)) * inv2m;
+                }
+            }
+            if (OUT != OUT_CH8) {
+                UT* o = uf + ((size_t)j * n + x0) * 2;
+                if (sizeof(UT) == 4 && CPT % 2 == 0) {  // two pixels per 16-byte store
+#pragma unroll
+                    for (int k = 0; k < CPT; k += 2)
+                        *reinterpret_cast<float4*>(o + 2 * k) =
+                            make_float4((float)ux[k], (float)uy[k], (float)ux[k + 1], (float)uy[k + 1]);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < CPT; ++k) {
+                        o[2 * k] = (UT)ux[k];
+                        o[2 * k + 1] = (UT)uy[k];
+                    }
+                }
             }
         }
         if (lane == 31) { s_xa[slot][w] = an[CPT - 1]; s_xu1[slot][w] = uln[CPT - 1]; s_xu2[slot][w] = uln[CPT - 2]; }
         if (lane == 0) s_xr[slot][w] = urn[0];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) { al[k] = an[k]; ul[k] = uln[k]; ur[k] = urn[k]; }
+        ps = slot;
+        slot = slot == 2 ? 0 : slot + 1;
     }
 }
 
