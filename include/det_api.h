@@ -76,6 +76,10 @@ typedef struct {
 } det_result;
 
 int det_abi_version(void);
+/* Page-locked host buffers for result copies (DMA instead of a staged pageable copy); the
+ * drop-in's Python layer keeps a pool of them.  No reference counterpart (host plumbing). */
+int det_host_alloc(size_t bytes, void **out);
+int det_host_free(void *p);
 const char *det_last_error(const det_ctx *ctx);
 /* device info string (name, SMs, L2) for reports */
 int det_device_info(int device, char *buf, int buflen);

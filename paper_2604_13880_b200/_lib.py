@@ -10,6 +10,7 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
+import weakref
 
 import numpy as np
 
@@ -45,6 +46,8 @@ class DetResult(ctypes.Structure):
 
 EXPORTS = {
     "det_abi_version": (ctypes.c_int, []),
+    "det_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
+    "det_host_free": (ctypes.c_int, [ctypes.c_void_p]),
     "det_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),
     "det_device_info": (ctypes.c_int, [ctypes.c_int, ctypes.c_char_p, ctypes.c_int]),
     "det_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]),
@@ -113,6 +116,60 @@ def load_library(path: str = LIB_PATH):
 
 def _p(a, ctype):
     return a.ctypes.data_as(ctypes.POINTER(ctype)) if a is not None else None
+
+
+class _PinnedBlock:
+    """One page-locked host allocation (det_host_alloc); freed when the last user is gone."""
+
+    def __init__(self, lib, nbytes):
+        ptr = ctypes.c_void_p()
+        if lib.det_host_alloc(nbytes, ctypes.byref(ptr)) != DET_OK or not ptr.value:
+            raise MemoryError(f"det_host_alloc({nbytes}) failed")
+        self.lib, self.ptr, self.nbytes = lib, ptr.value, nbytes
+
+    def __del__(self):
+        try:
+            self.lib.det_host_free(self.ptr)
+        except Exception:  # noqa: BLE001 -- interpreter shutdown
+            pass
+
+
+class PinnedPool:
+    """Numpy arrays backed by page-locked host memory, recycled when their last view dies.
+
+    Device->host result copies into these run as DMA at full link speed, without the
+    staging copy and page faults of a fresh pageable array.
+    """
+
+    def __init__(self, lib):
+        self.lib = lib
+        self.free = {}
+        self.lock = threading.Lock()
+        self.misses = 0  # allocations the pool could not serve (diagnostics)
+
+    def reserve(self, nbytes):
+        with self.lock:
+            if not self.free.get(nbytes):
+                self.free.setdefault(nbytes, []).append(_PinnedBlock(self.lib, nbytes))
+
+    def _release(self, blk):
+        with self.lock:
+            self.free.setdefault(blk.nbytes, []).append(blk)
+
+    def empty(self, shape, dtype=np.float64) -> np.ndarray:
+        dt = np.dtype(dtype)
+        count = int(np.prod(shape))
+        nbytes = max(count * dt.itemsize, 1)
+        with self.lock:
+            lst = self.free.get(nbytes)
+            blk = lst.pop() if lst else None
+        if blk is None:
+            self.misses += 1
+            blk = _PinnedBlock(self.lib, nbytes)
+        buf = (ctypes.c_char * nbytes).from_address(blk.ptr)
+        buf._blk = blk  # the block lives as long as any view of this buffer
+        weakref.finalize(buf, self._release, blk)
+        return np.frombuffer(buf, dtype=dt, count=count).reshape(shape)
 
 
 class DetError(RuntimeError):
@@ -242,10 +299,18 @@ class Context:
         self.check(self.lib.det_get_result(self.h, b, ctypes.byref(r)))
         return r
 
-    def vertices(self, b=0):
-        out = np.empty((self.n_rows, 2), dtype=np.float64)
+    def vertices(self, b=0, out=None):
+        if out is None:
+            out = np.empty((self.n_rows, 2), dtype=np.float64)
         self.check(self.lib.det_get_vertices(self.h, b, _p(out, ctypes.c_double)))
         return out
+
+    @property
+    def pinned(self) -> PinnedPool:
+        pool = getattr(self, "_pinned", None)
+        if pool is None:
+            pool = self._pinned = PinnedPool(self.lib)
+        return pool
 
     def labels(self, b=0):
         out = np.empty((self.n, self.n), dtype=np.int32)

@@ -420,6 +420,18 @@ static const double2* state_rows(det_ctx* ctx, int b);
 
 int det_abi_version(void) { return 1; }
 
+int det_host_alloc(size_t bytes, void** out) {
+    if (!out) return DET_E_ARG;
+    *out = nullptr;
+    if (bytes == 0) return DET_OK;
+    return cudaHostAlloc(out, bytes, cudaHostAllocDefault) == cudaSuccess ? DET_OK : DET_E_CUDA;
+}
+
+int det_host_free(void* p) {
+    if (!p) return DET_OK;
+    return cudaFreeHost(p) == cudaSuccess ? DET_OK : DET_E_CUDA;
+}
+
 const char* det_last_error(const det_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int det_device_info(int device, char* buf, int buflen) {

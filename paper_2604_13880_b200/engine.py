@@ -22,12 +22,14 @@ from __future__ import annotations
 import itertools
 from dataclasses import dataclass, field, replace
 
+import time
+
 import numpy as np
 
 from ._context import get_context, region_ranks
 from ._lib import STOP_BDV, STOP_COLLAPSED, STOP_NAMES, STOP_NEGINDEX
 from .errors import NumericError, RasterizationError, RegionCollapsedError
-from .geomodel import densify, rebuild, rebuild_fast, ring_layout, ring_sizes
+from .geomodel import deferred_rebuild, densify, rebuild, rebuild_fast, ring_layout, ring_sizes
 from .raster import LabelTexture, _LazyLabels, rasterize_labels
 
 DENSIFY_EDGE_PIXELS = 4.0
@@ -50,6 +52,18 @@ class IterationRecord:
     epsilon: float
     xi: float
     millis: float
+
+
+def trace_records(tr: np.ndarray, it_off: int = 0) -> tuple:
+    """(T, 4) device trace rows -> IterationRecord tuple (built without the frozen-dataclass
+    __setattr__ path: one trace per cartogram per run is thousands of records)."""
+    new = object.__new__
+    out = []
+    for it, eps, xi, ms in tr.tolist():
+        rec = new(IterationRecord)
+        rec.__dict__.update(iteration=int(it) + it_off, epsilon=eps, xi=xi, millis=ms)
+        out.append(rec)
+    return tuple(out)
 
 
 @dataclass(frozen=True)
@@ -173,6 +187,8 @@ class BatchEngine:
             for b in range(B)])
         total_mass = self.total_statistic + self.background_mass
         self.weights_px = stats / total_mass[:, None] * self.m
+        # page-locked host block for the result vertices of one run_all (setup, like device buffers)
+        ctx.pinned.reserve(B * self._xy.shape[0] * 16)
 
     # -- device context ----------------------------------------------------------
     def _ctx(self):
@@ -200,10 +216,21 @@ class BatchEngine:
 
     def run_all(self, criteria=None, iteration_offset: int = 0, clamp_offset: int = 0):
         """List of RunResult (or the CartomorphError/ValueError instance a cartogram raised)."""
+        t0 = time.perf_counter()
         ctx = self.launch(criteria)
-        return [self._collect(ctx, b, iteration_offset, clamp_offset) for b in range(self.B)]
+        t1 = time.perf_counter()
+        verts = ctx.pinned.empty((self.B, self._xy.shape[0], 2))
+        t2 = time.perf_counter()
+        out, per = [], []
+        for b in range(self.B):
+            tb = time.perf_counter()
+            out.append(self._collect(ctx, b, iteration_offset, clamp_offset, verts[b]))
+            per.append(round((time.perf_counter() - tb) * 1e3, 2))
+        self.last_timing = {"launch_s": t1 - t0, "pinned_s": t2 - t1, "collect_s": time.perf_counter() - t2,
+                            "pinned_misses": ctx.pinned.misses, "per_frame_ms": per}
+        return out
 
-    def _collect(self, ctx, b, it_off=0, cl_off=0):
+    def _collect(self, ctx, b, it_off=0, cl_off=0, verts_out=None):
         r = ctx.result(b)
         if r.stop_reason == STOP_COLLAPSED:
             return RegionCollapsedError(self.region_ids[r.collapsed_region], r.iteration + it_off)
@@ -212,11 +239,11 @@ class BatchEngine:
         if r.stop_reason == STOP_NEGINDEX:
             return ValueError("'list' argument must have no negative elements")
         tr = ctx.trace(b, r.trace_len)
-        records = tuple(IterationRecord(int(t[0]) + it_off, float(t[1]), float(t[2]), float(t[3])) for t in tr)
-        verts = ctx.vertices(b)
+        records = trace_records(tr, it_off)
+        verts = ctx.vertices(b, verts_out)
         counts = ctx.counts(b)
         clamps = int(r.clamp_events) + (cl_off if r.stop_reason != 2 else 0)
-        result_map = rebuild_fast(self.initial_map, verts, self.statistics[b], self._sizes)
+        result_map = deferred_rebuild(self.initial_map, verts, self.statistics[b], self._sizes)
         lazy = _LazyLabels(ctx, b, getattr(ctx, "generation", None), lambda: result_map, self.k, self.device)
         labels = LabelTexture(size=self.n, labels=lazy, region_ids=tuple(self.region_ids), _counts=counts)
         state = CartogramState(mapmodel=result_map, iteration=int(r.iteration) + it_off,

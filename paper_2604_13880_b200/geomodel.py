@@ -135,6 +135,53 @@ def ring_sizes(mapmodel) -> np.ndarray:
     return np.array([np.asarray(r).shape[0] for reg in mapmodel.regions for r in reg.rings], dtype=np.int64)
 
 
+class _DeferredMapModel(MapModel):
+    """A MapModel whose Region objects are built from a host vertex array on first access.
+
+    Result maps of batched runs are views of the vertices already copied back from the
+    device; building 10^3-10^4 Region dataclasses per frame would cost more than the GPU
+    run itself, so it happens on first access to ``regions`` (``vertex_array`` needs no
+    Regions at all).  Everything else -- equality, ``dataclasses.replace``, ``with_*`` --
+    behaves as for a MapModel (the first field access materialises the regions).
+    """
+
+    def __getattr__(self, name):
+        if name == "regions":
+            base, verts, stats, sizes = self.__dict__["_deferred"]
+            regs = rebuild_fast(base, verts, stats, sizes).regions
+            object.__setattr__(self, "regions", regs)
+            return regs
+        raise AttributeError(name)
+
+    def vertex_array(self) -> np.ndarray:
+        if "regions" not in self.__dict__:
+            return np.array(self.__dict__["_deferred"][1], dtype=float)
+        return super().vertex_array()
+
+    def __eq__(self, other):  # compares as a MapModel (dataclass __eq__ requires the same class)
+        if isinstance(other, MapModel):
+            return (self.regions, self.adjacency, self.normalization) == (
+                other.regions, other.adjacency, other.normalization)
+        return NotImplemented
+
+    __hash__ = MapModel.__hash__
+
+
+def deferred_rebuild(mapmodel, verts: np.ndarray, statistics=None, sizes=None):
+    """``rebuild_fast`` whose Region objects are built on first access (own MapModel only)."""
+    if type(mapmodel) is not MapModel and not isinstance(mapmodel, _DeferredMapModel):
+        return rebuild_fast(mapmodel, verts, statistics, sizes)
+    verts = np.asarray(verts, dtype=float)
+    if sizes is None:
+        sizes = ring_sizes(mapmodel)
+    if int(sizes.sum()) != verts.shape[0]:
+        raise ValueError("vertex array length mismatch")
+    obj = object.__new__(_DeferredMapModel)
+    obj.__dict__.update(adjacency=mapmodel.adjacency, normalization=mapmodel.normalization,
+                        _deferred=(mapmodel, verts, statistics, sizes))
+    return obj
+
+
 def rebuild_fast(mapmodel, verts: np.ndarray, statistics=None, sizes=None):
     """``rebuild`` (+ optional new statistics) in one pass; rings are views of ``verts``.
 

@@ -28,9 +28,9 @@ import numpy as np
 from ._context import get_context, region_ranks
 from ._lib import DET_E_RASTER, STOP_BDV, STOP_COLLAPSED, STOP_NAMES, STOP_NEGINDEX
 from .engine import (DENSIFY_EDGE_PIXELS, BatchEngine, CartogramEngine, CartogramState, IterationRecord, RunResult,
-                     StoppingCriteria)
+                     StoppingCriteria, trace_records)
 from .errors import CartomorphError, IngestionError, RasterizationError, RegionCollapsedError
-from .geomodel import densify, rebuild, rebuild_fast, ring_layout
+from .geomodel import deferred_rebuild, densify, rebuild, rebuild_fast, ring_layout
 from .metrics import frame_reports
 from .raster import LabelTexture, _LazyLabels, rasterize_labels
 
@@ -289,10 +289,10 @@ def run_cumulative(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None
 
 
 def _chain_result(ctx, base_map, ids, sizes, stats_t, total_t, mb, xy_t, r, counts, trace_t, n, k, device):
-    carto = rebuild_fast(base_map, xy_t, stats_t, sizes)
+    carto = deferred_rebuild(base_map, xy_t, stats_t, sizes)
     total_mass = float(total_t) + float(mb)
     weights = stats_t / total_mass * (n * n)
-    records = tuple(IterationRecord(int(q[0]), float(q[1]), float(q[2]), float(q[3])) for q in trace_t[: r.trace_len])
+    records = trace_records(trace_t[: r.trace_len])
     labels = LabelTexture(size=n, labels=_LazyLabels(ctx, 0, -1, (lambda c=carto: c), k, device),
                           region_ids=tuple(ids), _counts=counts)
     per_region = np.abs(counts[:-1] - weights) / np.maximum(counts[:-1].astype(float), weights)
@@ -314,7 +314,7 @@ def _blend(a, b, fracs, device=0):
     out = ctx.interpolate(np.concatenate([va.ravel(), sa]), np.concatenate([vb.ravel(), sb]), fracs)
     nv = va.size
     sizes = np.array([np.asarray(r).shape[0] for reg in a.regions for r in reg.rings], dtype=np.int64)
-    return [rebuild_fast(a, o[:nv].reshape(-1, 2), o[nv:], sizes) for o in out]
+    return [deferred_rebuild(a, o[:nv].reshape(-1, 2), o[nv:], sizes) for o in out]
 
 
 def interpolate_vertices(a, b, fraction: float, device: int = 0):
