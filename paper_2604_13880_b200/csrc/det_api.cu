@@ -86,6 +86,7 @@ struct det_ctx {
     cudaGraphExec_t gexec = nullptr;
     bool g_valid = false;
     int groups = 2;
+    bool sep_ctrl = true;  // control step as its own kernel (DET_SEP_CTRL=0: k_row's last CTA)
     Topo g_topo;  // launch signature the graph was captured with
     Bufs g_bufs;
     int g_groups = 0;
@@ -230,6 +231,17 @@ static void launch_row(det_ctx* c, const Topo& T, const Bufs& D, int gate, int c
     k_row<<<dim3((c->n + rpc - 1) / rpc, c->B), rpc * 32, smem, c->stream>>>(T, D, gate, ctrl_mode);
 }
 
+// k_row + the loop control step: fused into k_row's last CTA per cartogram, or (sep_ctrl) a
+// separate 1024-thread k_ctrl per cartogram after it
+static void launch_row_ctrl(det_ctx* c, const Topo& T, const Bufs& D, int gate, int ctrl_mode) {
+    if (c->sep_ctrl && ctrl_mode >= 0) {
+        launch_row(c, T, D, gate, CTRL_SEPARATE);
+        k_ctrl<<<c->B, CTRL_THREADS, 0, c->stream>>>(T, D, ctrl_mode, gate);
+    } else {
+        launch_row(c, T, D, gate, ctrl_mode);
+    }
+}
+
 static void enqueue_iteration(det_ctx* c, int b0 = 0, int Bg = -1, cudaStream_t s = nullptr) {
     if (Bg < 0) Bg = c->B;
     cudaStream_t keep = c->stream;
@@ -243,7 +255,7 @@ static void enqueue_iteration(det_ctx* c, int b0 = 0, int Bg = -1, cudaStream_t 
     memset(&S, 0, sizeof(S));
     launch_sat(c, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, c->f64 != 0, Bg);
     launch_region(c, T, D, M_ADVECT | M_RASTER, G_ACTIVE, 0);
-    launch_row(c, T, D, G_ACTIVE, 0);
+    launch_row_ctrl(c, T, D, G_ACTIVE, 0);
     c->B = Bsave;
     c->stream = keep;
 }
@@ -451,6 +463,7 @@ int det_ctx_create(int device, int k, int field_f64, det_ctx** out) {
     *out = nullptr;
     if (k < 4 || k > 13) return DET_E_ARG;
     det_ctx* ctx = new det_ctx();
+    if (const char* e = getenv("DET_SEP_CTRL")) ctx->sep_ctrl = atoi(e) != 0;  // A/B switch (diagnostics)
     ctx->device = device;
     ctx->k = k;
     ctx->n = 1 << k;
@@ -816,6 +829,9 @@ int det_bench_kernel_times(det_ctx* ctx, int iters, float* ms_out) {
     // diagnostics: DET_KT_REGION_MODE=1 times k_region's advect phase alone (raster skipped)
     const char* km = getenv("DET_KT_REGION_MODE");
     const int region_mode = (km && km[0] == '1') ? M_ADVECT : (M_ADVECT | M_RASTER);
+    // DET_KT_ROW_MODE=-1 times k_row without the evaluation / LUT part of the control step
+    const char* rm = getenv("DET_KT_ROW_MODE");
+    const int row_mode = (rm && rm[0] == '-') ? -1 : 0;
     const Topo T = make_topo(ctx);
     const Bufs D = make_bufs(ctx);
     SatSrc S;
@@ -826,7 +842,7 @@ int det_bench_kernel_times(det_ctx* ctx, int iters, float* ms_out) {
         CK(cudaEventRecord(ev[1], ctx->stream));
         launch_region(ctx, T, D, region_mode, G_ACTIVE, 0);
         CK(cudaEventRecord(ev[2], ctx->stream));
-        launch_row(ctx, T, D, G_ACTIVE, 0);  // includes the control step (last CTA)
+        launch_row_ctrl(ctx, T, D, G_ACTIVE, row_mode);  // includes the control step
         CK(cudaEventRecord(ev[3], ctx->stream));
         CK(cudaEventRecord(ev[4], ctx->stream));
         CK(cudaEventSynchronize(ev[4]));

@@ -10,7 +10,8 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr uint32_t SENT = 0xffffffffu;
 constexpr int REG_THREADS = 128;   // k_region block
 constexpr int ROW_THREADS = 256;   // k_row block
-constexpr int CTRL_THREADS = 256;  // k_ctrl block
+constexpr int CTRL_THREADS = 1024;  // k_ctrl block (one per cartogram)
+constexpr int CTRL_SEPARATE = -2;  // k_row ctrl_mode: leave the control step to k_ctrl
 constexpr int TOG_CAP = 4096;      // toggles per k_region window (smem keys, power of two)
 
 enum Mode { M_ADVECT = 1, M_RASTER = 2 };

@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
     const size_t rb = (size_t)b * n + j;
     int* cnt = D.cnt_acc + (size_t)b * (T.R + 1);
     if (j < n) {
-        for (int i = lane; i < n; i += 32) lab_s[i] = SENT;
+        for (int i = lane; i < n; i += 32) lab_s[i] = SENT;  // (16-byte stores measured slower here)
         const int c0 = D.rowcnt[rb];
         __syncwarp();
         if (lane == 0) {
@@ -460,6 +460,7 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
             __threadfence();
         }
     }
+    if (ctrl_mode == CTRL_SEPARATE) return;  // the control step runs as k_ctrl after this kernel
     // ---- completion: the CTA that finishes the last row of this cartogram runs the control step ----
     __syncthreads();
     if (threadIdx.x == 0) s_last = atomicAdd(&D.rowdone[b], 1) == (int)gridDim.x - 1;

@@ -34,8 +34,9 @@ if __name__ == "__main__":
         print(json.dumps(measure()))
     else:
         out = {}
-        for mode in ("full", "advect_only"):
-            env = dict(os.environ, DET_KT_REGION_MODE="1" if mode == "advect_only" else "0")
+        for mode in ("full", "advect_only", "row_no_eval"):
+            env = dict(os.environ, DET_KT_REGION_MODE="1" if mode == "advect_only" else "0",
+                       DET_KT_ROW_MODE="-1" if mode == "row_no_eval" else "0")
             r = subprocess.run([sys.executable, __file__, "child"], env=env, capture_output=True, text=True)
             out[mode] = json.loads(r.stdout.strip().splitlines()[-1]) if r.returncode == 0 else r.stderr[-500:]
         print(json.dumps(out))
