@@ -303,8 +303,11 @@ __global__ void k_sat2(Bufs D, int gate) {
 // ---------------------------------------------------------------------------------
 // Per band: load the float64 carries, then one top-down sweep.  In-band arithmetic
 // in A (float32 when the field is stored as float32), carries rounded to A once.
+#ifndef DET_SAT3_MINB
+#define DET_SAT3_MINB 4  // 64 registers, no spills: 512 band CTAs fit one wave (3 and 5 measured slower)
+#endif
 template <int CPT, int NT, int SRC, typename UT, int OUT, typename A, bool LUTS>
-__global__ void __launch_bounds__(NT) k_sat3(Topo T, Bufs D, SatSrc S, int gate) {
+__global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(Topo T, Bufs D, SatSrc S, int gate) {
     extern __shared__ unsigned char s_raw3[];
     constexpr int NW = NT / 32;
     __shared__ A s_w[3][32];
