@@ -168,8 +168,7 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     }
 #undef DET_SAT1
     const int lanes = n + 2 * (2 * n - 1);
-    const int G = std::min(8, c->nb);
-    k_sat2<<<dim3((lanes + 31) / 32 + 1, B), 32 * G, 0, c->stream>>>(D, gate);
+    k_sat2<<<dim3((lanes + SAT2_THREADS - 1) / SAT2_THREADS + 1, B), SAT2_THREADS, 0, c->stream>>>(D, gate);
     const size_t smem = ((size_t)3 * (n + H) + 3 * H + (H & 1)) * sa + lut_b;
 #define DET_SAT3(SRC_, UT_, OUT_, L_)                                                                        \
     do {                                                                                                     \

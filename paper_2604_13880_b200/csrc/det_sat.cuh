@@ -218,10 +218,12 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
 //   dgXc[b][x]  = sum_{b'<b} DG_b'(x - jt + 1)        (UL carry, x in [0,n))
 //   adSc[b][q]  = sum_{b'>=b} AD_b'(jt - 1 + q)        (DLtot window, q in [0,n+H))
 // and totals csT[x] = colfull(x+1), dgT[idx] = Tv(v), adT[w] = Tu(w).
-__global__ void k_sat2(Bufs D, int gate) {
-    __shared__ double s_g[32][33];
+constexpr int SAT2_THREADS = 128;
+constexpr int SAT2_CHUNK = 16;  // bands loaded per round (independent loads in flight)
+
+__global__ void __launch_bounds__(SAT2_THREADS) k_sat2(Bufs D, int gate) {
     __shared__ double s_red[33];
-    const int b = blockIdx.y + D.b0, t = threadIdx.x, lx = t & 31, g = t >> 5, G = blockDim.x >> 5;
+    const int b = blockIdx.y + D.b0, t = threadIdx.x;
     if (!gate_open(D.st + b, gate)) return;
     const int n = D.n, H = D.H, nb = D.nb, L = n + H - 1, M = 2 * n - 1;
     if (blockIdx.x == gridDim.x - 1) {
@@ -238,65 +240,57 @@ __global__ void k_sat2(Bufs D, int gate) {
         if (t == 0) rf[n] = tot;
         return;
     }
+    // one thread per lane: every band of one column / diagonal / anti-diagonal, streamed in
+    // chunks of independent loads (forward for the prefixes, backward for the suffix)
     const int lanes = n + 2 * M;
-    const int l = blockIdx.x * 32 + lx;
-    const bool valid = l < lanes;
+    const int l = blockIdx.x * blockDim.x + t;
+    if (l >= lanes) return;
     const int type = l < n ? 0 : (l < n + M ? 1 : 2);
     const int idx = type == 0 ? l : (type == 1 ? l - n : l - n - M);
-    const int per = (nb + G - 1) / G;
-    const int bA = min(nb, g * per), bE = min(nb, bA + per);
     const size_t base = (size_t)b * nb;
-
     auto val = [&](int band) -> double {
-        if (!valid) return 0.0;
         if (type == 0) return D.cs[(base + band) * n + idx];
-        int q;
-        const double* arr;
-        if (type == 1) {
-            q = idx - (n - 1) + (band * H + H - 1);  // v + jb
-            arr = D.dgc;
-        } else {
-            q = idx - band * H;                      // w - jt
-            arr = D.adc;
-        }
+        const int q = type == 1 ? idx - (n - 1) + (band * H + H - 1)  // v + jb
+                                : idx - band * H;                     // w - jt
         if (q < 0) return 0.0;
-        return arr[(base + band) * L + min(q, L - 1)];
+        return (type == 1 ? D.dgc : D.adc)[(base + band) * L + min(q, L - 1)];
     };
-    double sum = 0.0;
-    for (int band = bA; band < bE; ++band) sum += val(band);
-    s_g[g][lx] = sum;
-    __syncthreads();
-    double before = 0.0, after = 0.0, total = 0.0;
-    for (int q = 0; q < G; ++q) {
-        const double v = s_g[q][lx];
-        total += v;
-        if (q < g) before += v;
-        if (q > g) after += v;
-    }
-    if (!valid) return;
+    double run = 0.0;
     if (type != 2) {
-        double run = before;
-        for (int band = bA; band < bE; ++band) {
-            if (type == 0) {
-                D.csX[(base + band) * n + idx] = run;
-            } else {
-                const int x = idx - n + band * H;  // v + jt - 1, v = idx - (n-1)
-                if (x >= 0 && x < n) D.dgXc[(base + band) * n + x] = run;
+        for (int b0 = 0; b0 < nb; b0 += SAT2_CHUNK) {
+            double v[SAT2_CHUNK];
+#pragma unroll
+            for (int k = 0; k < SAT2_CHUNK; ++k) v[k] = b0 + k < nb ? val(b0 + k) : 0.0;
+#pragma unroll
+            for (int k = 0; k < SAT2_CHUNK; ++k) {
+                const int band = b0 + k;
+                if (band >= nb) break;
+                if (type == 0) {
+                    D.csX[(base + band) * n + idx] = run;
+                } else {
+                    const int x = idx - n + band * H;  // v + jt - 1, v = idx - (n-1)
+                    if (x >= 0 && x < n) D.dgXc[(base + band) * n + x] = run;
+                }
+                run += v[k];
             }
-            run += val(band);
         }
+        if (type == 0) D.csT[(size_t)b * n + idx] = run;
+        else D.dgT[(size_t)b * M + idx] = run;
     } else {
-        double run = after;
-        for (int band = bE - 1; band >= bA; --band) {
-            run += val(band);
-            const int q = idx - band * H + 1;  // w - (jt - 1)
-            if (q >= 0 && q < L + 1) D.adSc[(base + band) * (L + 1) + q] = run;
+        for (int e0 = nb; e0 > 0; e0 -= SAT2_CHUNK) {
+            double v[SAT2_CHUNK];
+#pragma unroll
+            for (int k = 0; k < SAT2_CHUNK; ++k) v[k] = e0 - 1 - k >= 0 ? val(e0 - 1 - k) : 0.0;
+#pragma unroll
+            for (int k = 0; k < SAT2_CHUNK; ++k) {
+                const int band = e0 - 1 - k;
+                if (band < 0) break;
+                run += v[k];
+                const int q = idx - band * H + 1;  // w - (jt - 1)
+                if (q >= 0 && q < L + 1) D.adSc[(base + band) * (L + 1) + q] = run;
+            }
         }
-    }
-    if (g == 0) {
-        if (type == 0) D.csT[(size_t)b * n + idx] = total;
-        else if (type == 1) D.dgT[(size_t)b * M + idx] = total;
-        else D.adT[(size_t)b * M + idx] = total;
+        D.adT[(size_t)b * M + idx] = run;
     }
 }
 
