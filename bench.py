@@ -114,9 +114,11 @@ def build_workload(batch: int, rank: int, world: int):
     from paper_2604_13880_b200.synthetic import config_map, random_walk
 
     m, prm = config_map("headline")
-    frames = batch * world
-    walk = random_walk(m.statistics(), frames, 0.15, seed=7)
-    return m, prm, walk[rank * batch:(rank + 1) * batch]
+    # weak scaling: every rank runs its own `batch`-frame walk from the base statistics (rank 0's
+    # is the N=1 workload), so per-GPU work has the same distribution at every N -- one long walk
+    # sliced across ranks would drift far enough on high ranks for frames to collapse
+    walk = random_walk(m.statistics(), batch, 0.15, seed=7 + 1009 * rank)
+    return m, prm, walk
 
 
 # ------------------------------------------------------------------ CPU reference arm / baseline
