@@ -141,6 +141,23 @@ static Bufs make_bufs(det_ctx* c) {
 }
 
 // ----------------------------- launch helpers ---------------------------------
+// Dynamic shared-memory opt-in.  The attribute is process-wide per kernel, so contexts on other
+// threads (one per steering session) must never lower it under a launch being captured: every
+// caller sets the same value, the device's opt-in maximum minus the kernel's static shared memory
+// (idempotent, race-free).
+template <typename F>
+static void smem_optin(F fn) {
+    static int max_optin = [] {
+        int dev = 0, v = 48 * 1024;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        return v;
+    }();
+    cudaFuncAttributes a;
+    if (cudaFuncGetAttributes(&a, fn) != cudaSuccess) return;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin - (int)a.sharedSizeBytes);
+}
+
 template <int CPT, int NT>
 static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S, int gate, int src, int out,
                            bool u64, int B) {
@@ -156,7 +173,7 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
 #define DET_SAT1(SRC_, A_, L_)                                                                               \
     do {                                                                                                     \
         auto fn = k_sat1<CPT, NT, SRC_, A_, L_>;                                                             \
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);                   \
+        smem_optin(fn);                                                                                      \
         fn<<<gb, NT, smem1, c->stream>>>(T, D, S, gate);                                                     \
     } while (0)
     if (src == SRC_LABELS) {
@@ -173,7 +190,7 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
 #define DET_SAT3(SRC_, UT_, OUT_, L_)                                                                        \
     do {                                                                                                     \
         auto fn = k_sat3<CPT, NT, SRC_, UT_, OUT_, UT_, L_>;                                                 \
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                    \
+        smem_optin(fn);                                                                                      \
         fn<<<gb, NT, smem, c->stream>>>(T, D, S, gate);                                                      \
     } while (0)
     if (out == OUT_CH8) {
@@ -226,7 +243,7 @@ static void launch_row(det_ctx* c, const Topo& T, const Bufs& D, int gate, int c
     while (rpc > 1 && (size_t)rpc * c->n * sizeof(uint32_t) > 64 * 1024) rpc >>= 1;
     rpc = std::min(rpc, c->n);
     const size_t smem = (size_t)rpc * c->n * sizeof(uint32_t);
-    cudaFuncSetAttribute(k_row, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    smem_optin(k_row);
     k_row<<<dim3((c->n + rpc - 1) / rpc, c->B), rpc * 32, smem, c->stream>>>(T, D, gate, ctrl_mode);
 }
 

@@ -207,6 +207,30 @@ def main():
             tr[f"{strat}_{t}_watchdog"] = np.array(fr.watchdog)
         tr[f"{strat}_series"] = np.array(json.dumps(seq.series(), sort_keys=True))
     np.savez_compressed(os.path.join(OUT, "temporal_reports.npz"), **tr)
+    # 9. one steering-service frame (service.py:202-236 composition): engine + report + GeoJSON
+    from cartomorph.geomodel import to_geojson as ref_geojson
+
+    ms = fm.small_voronoi(seed=13, r=14, target=400, shuffle_ids=False)
+    rbase = to_reference_map(cm, ms)
+    sv = {}
+    for key, val in fm.pack_map(ms).items():
+        sv[f"m_{key}"] = val
+    for t, (mass, k, hk, strat) in enumerate([(0.3, 6, 6, "direct"), (0.6, 7, 5, "direct")]):
+        stats_t = ms.statistics() * np.exp(np.random.default_rng(90 + t).normal(0, 0.3, len(ms.regions)))
+        eng = cm.CartogramEngine(rbase.with_statistics(stats_t),
+                                 criteria=cm.StoppingCriteria(1e-300, 10**9, 12), k=k,
+                                 background_mass=mass, apply_densify=False)
+        res = eng.run()
+        carto = res.state.mapmodel
+        weights = stats_t / (float(stats_t.sum()) + mass)
+        rep = cmet.full_report(rbase.with_statistics(stats_t), carto, weights=weights, raster_k=hk, wall_ms=1.0)
+        sv[f"f{t}_stats"] = stats_t
+        sv[f"f{t}_cfg"] = np.array([mass, k, hk])
+        sv[f"f{t}_report"] = np.array(json.dumps(rep.to_dict(), sort_keys=True))
+        sv[f"f{t}_geojson"] = np.array(ref_geojson(carto, rep.per_region).decode())
+        sv[f"f{t}_xy"] = carto.vertex_array()
+        sv[f"f{t}_stop"] = np.array(res.stop_reason)
+    np.savez_compressed(os.path.join(OUT, "service_frames.npz"), **sv)
     print("golden fixtures written to", OUT)
 
 
