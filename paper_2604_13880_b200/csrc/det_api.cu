@@ -62,10 +62,9 @@ struct det_ctx {
     std::string err;
     // topology
     int R = 0, n_rows = 0, n_uniq = 0, n_rings = 0;
-    std::vector<int> h_row_uniq, h_ring_start, h_region_ring0;
+    std::vector<int> h_ring_start, h_region_ring0;
     std::vector<double> h_xy_uniq, h_xy_rows;
-    DVec<int> region_row0, row_uniq, row_next, region_rank, rank_region, ring_start, region_ring0;
-    DVec<uint8_t> row_owner;
+    DVec<int> region_row0, region_rank, rank_region, ring_start, region_ring0;
     // batch
     int B = 0, cap = 64, nb = 0, trace_cap = 0;
     DVec<double2> pos_init, pos0, pos1, best;
@@ -115,9 +114,8 @@ static Topo make_topo(det_ctx* c) {
     t.n_uniq = c->n_uniq;
     t.R = c->R;
     t.region_row0 = c->region_row0.p;
-    t.row_uniq = c->row_uniq.p;
-    t.row_next = c->row_next.p;
-    t.row_owner = c->row_owner.p;
+    t.ring_start = c->ring_start.p;
+    t.region_ring0 = c->region_ring0.p;
     t.region_rank = c->region_rank.p;
     t.rank_region = c->rank_region.p;
     return t;
@@ -531,8 +529,7 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
         return fail(ctx, DET_E_ARG, "invalid map arguments");
     cudaSetDevice(ctx->device);
     if (ring_start[0] != 0 || ring_start[n_rings] != n_rows) return fail(ctx, DET_E_ARG, "ring_start must span all rows");
-    std::vector<int> reg_row0(n_regions + 1, -1), reg_ring0(n_regions + 1, 0), next(n_rows), uniq(n_rows), rank_reg(n_regions, -1);
-    std::vector<uint8_t> owner(n_rows, 0);
+    std::vector<int> reg_row0(n_regions + 1, -1), reg_ring0(n_regions + 1, 0), rank_reg(n_regions, -1);
     int prev_region = -1;
     for (int q = 0; q < n_rings; ++q) {
         const int r = ring_region[q];
@@ -543,7 +540,6 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
             reg_row0[prev_region] = ring_start[q];
             reg_ring0[prev_region] = q;
         }
-        for (int v = ring_start[q]; v < ring_start[q + 1]; ++v) next[v] = (v + 1 < ring_start[q + 1]) ? v + 1 : ring_start[q];
     }
     if (prev_region != n_regions - 1) return fail(ctx, DET_E_ARG, "every region needs at least one ring");
     reg_row0[n_regions] = n_rows;
@@ -555,10 +551,6 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
     }
     // vertex rows are stored per ring row (coalesced); rows duplicating a shared vertex
     // evolve bit-identically, so no de-duplication is needed
-    for (int v = 0; v < n_rows; ++v) {
-        uniq[v] = v;
-        owner[v] = 1;
-    }
     ctx->R = n_regions;
     ctx->n_rows = n_rows;
     ctx->n_rings = n_rings;
@@ -569,17 +561,11 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
     CK(ctx->region_row0.alloc(n_regions + 1));
     CK(ctx->region_ring0.alloc(n_regions + 1));
     CK(ctx->ring_start.alloc(n_rings + 1));
-    CK(ctx->row_uniq.alloc(n_rows));
-    CK(ctx->row_next.alloc(n_rows));
-    CK(ctx->row_owner.alloc(n_rows));
     CK(ctx->region_rank.alloc(n_regions));
     CK(ctx->rank_region.alloc(n_regions));
     CK(cudaMemcpy(ctx->region_row0.p, reg_row0.data(), (n_regions + 1) * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->region_ring0.p, reg_ring0.data(), (n_regions + 1) * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->ring_start.p, ring_start, (n_rings + 1) * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->row_uniq.p, uniq.data(), n_rows * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->row_next.p, next.data(), n_rows * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->row_owner.p, owner.data(), n_rows, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->region_rank.p, region_rank, n_regions * sizeof(int), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(ctx->rank_region.p, rank_reg.data(), n_regions * sizeof(int), cudaMemcpyHostToDevice));
     ctx->B = 0;

@@ -51,9 +51,8 @@ struct Params {
 struct Topo {
     int n_rows, n_uniq, R;
     const int* region_row0;   // R+1: first vertex row of each region (regions' rows are contiguous)
-    const int* row_uniq;      // n_rows: unique-vertex index of each row
-    const int* row_next;      // n_rows: next row of the same ring (wraps)
-    const uint8_t* row_owner; // n_rows: 1 for the first row referencing its unique vertex
+    const int* ring_start;    // n_rings+1: first vertex row of each ring
+    const int* region_ring0;  // R+1: first ring of each region (a region's rings are contiguous)
     const int* region_rank;   // R: rank of region in ascending region_id order
     const int* rank_region;   // R: inverse
 };

@@ -162,6 +162,16 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
     uint16_t* colb = s_col[wid];
     int* rc = s_rc[wid];
 
+    // next row of the same ring (wraps): from the region's ring boundaries, no per-row table
+    const int rq0 = T.region_ring0[r], rq1 = T.region_ring0[r + 1];
+    auto next_row = [&](int v) -> int {
+        if (rq1 - rq0 == 1) return v + 1 < row1 ? v + 1 : row0;
+        int q = rq0;
+        while (T.ring_start[q + 1] <= v) ++q;
+        const int e = T.ring_start[q + 1];
+        return v + 1 < e ? v + 1 : T.ring_start[q];
+    };
+
     const double2* __restrict__ pin;
     double2* __restrict__ pout = nullptr;
     bool bestcopy = false;
@@ -226,7 +236,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
             const int ir = min(max(ceil_to_int(__dsub_rn(xs, 0.5)), 0), n);
             if (in_smem) {
                 sjr[v - row0] = jr;
-                snx[v - row0] = (uint16_t)(T.row_next[v] - row0);
+                snx[v - row0] = (uint16_t)(next_row(v) - row0);
             }
             jmn = min(jmn, jr); jmx = max(jmx, jr);
             imn = min(imn, ir); imx = max(imx, ir);
@@ -322,7 +332,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
             if (lane < qt - qh) run(q[(qh + lane) & 63]);
         } else {
             for (int e = row0 + lane; e < row1; e += 32) {
-                const int en = T.row_next[e] - row0;
+                const int en = next_row(e) - row0;
                 const double2 a = gpos[e], c = gpos[row0 + en];
                 const int ja = min(max(ceil_to_int(__dsub_rn(__dmul_rn(a.y, nd), 0.5)), 0), n);
                 const int jb2 = min(max(ceil_to_int(__dsub_rn(__dmul_rn(c.y, nd), 0.5)), 0), n);
@@ -357,6 +367,19 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
             }
         }
         __syncwarp();
+        // reserve every row's span slots now -- each row of crossings pairs into (c+1)/2 spans --
+        // so the global atomics' latency overlaps the scatter and the sort below
+        constexpr int RW_QPL = RW_WROWS / 32;  // rows per lane
+        int sbase[RW_QPL];
+#pragma unroll
+        for (int u = 0; u < RW_QPL; ++u) {
+            const int q = lane + 32 * u;
+            sbase[u] = 0;
+            if (q < W) {
+                const int c = (q + 1 < W ? rc[q + 1] : tot) - rc[q];
+                if (c > 0) sbase[u] = atomicAdd(&D.rowcnt[(size_t)b * n + w0 + q], (c + 1) >> 1);
+            }
+        }
         // scatter columns into row buckets; a bucket's cursor runs from its start to the next start
         for (int p = lane; p < tot; p += 32) {
             const uint32_t key = keys[p];
@@ -365,7 +388,10 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
         }
         __syncwarp();
         // after the scatter rc[q] = end of bucket q = start of bucket q+1
-        for (int q = lane; q < W; q += 32) {
+#pragma unroll
+        for (int u = 0; u < RW_QPL; ++u) {
+            const int q = lane + 32 * u;
+            if (q >= W) break;
             const int s = q == 0 ? 0 : rc[q - 1], e = rc[q];
             // insertion sort of the (few) crossings of this row, then even-odd pairing
             for (int i = s + 1; i < e; ++i) {
@@ -374,14 +400,13 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
                 while (k >= s && colb[k] > x) { colb[k + 1] = colb[k]; --k; }
                 colb[k + 1] = x;
             }
-            const int row = w0 + q;
-            for (int i = s; i < e; i += 2) {
+            const size_t rb = (size_t)b * n + w0 + q;
+            int slot = sbase[u];
+            for (int i = s; i < e; i += 2, ++slot) {
                 const int col = colb[i];
-                const int end = i + 1 < e ? (int)colb[i + 1] : i_end;
-                if (end <= col) continue;
-                area += end - col;
-                const size_t rb = (size_t)b * n + row;
-                const int slot = atomicAdd(&D.rowcnt[rb], 1);
+                int end = i + 1 < e ? (int)colb[i + 1] : i_end;
+                if (end > col) area += end - col;
+                else end = col;  // empty pair: a zero-length span keeps the reserved slot valid
                 if (slot < D.cap)
                     D.spans[rb * D.cap + slot] = (rank << 32) | ((unsigned long long)end << 16) | (unsigned long long)col;
                 else
