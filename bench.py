@@ -249,7 +249,11 @@ def main():
             ctx.sync()
         it0, _ = ctx.progress()
         barrier()
+        if os.environ.get("DET_PROFILE_RANGE") == "2":  # ncu --profile-from-start off: the timed graph launches
+            torch.cuda.profiler.start()
         ms = ctx.time_iterations(args.steps)
+        if os.environ.get("DET_PROFILE_RANGE") == "2":
+            torch.cuda.profiler.stop()
         barrier()
         it1, act = ctx.progress()
     executed = int((it1 - it0).sum())  # iterations actually executed (a collapsed frame stops counting)
@@ -264,7 +268,7 @@ def main():
     value = iters_total / (ms_max * 1e-3)
 
     # per-phase device times (eager launches, events on the same stream) -> dominant kernel
-    prof_range = os.environ.get("DET_PROFILE_RANGE") == "1"  # ncu --profile-from-start off: these launches
+    prof_range = os.environ.get("DET_PROFILE_RANGE") == "1"  # ncu --profile-from-start off: the eager launches
     if prof_range:
         torch.cuda.profiler.start()
     ph = ctx.kernel_times(8)
@@ -351,7 +355,9 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
                     "d2h_bytes_per_step": d2h / e2e_steps, "steps": e2e_steps,
                     "host_split": getattr(be, "last_timing", {})},
-            "gpu_launches": 6 * args.steps,
+            # 6 kernels (k_sat1/2/3, k_region, k_row, k_ctrl) per frame group per iteration: full 16-iteration
+            # chunks run as a CUDA graph with min(groups, batch) branches, the remainder eagerly
+            "gpu_launches": 6 * (min(args.groups, args.batch) * 16 * (args.steps // 16) + args.steps % 16),
             "iterations_executed": iters_total, "frames_active_after": int(act.sum()),
             "clocks": clk.summary(),
             "device": device_info(local),
