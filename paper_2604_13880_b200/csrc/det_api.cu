@@ -167,7 +167,9 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     // the residual-density LUT goes to shared memory when it fits in 48 KB
     const bool luts = src == SRC_LABELS && (size_t)lut_smem_len(R) * sa <= 48 * 1024;
     const size_t lut_b = luts ? (size_t)lut_smem_len(R) * sa : 0;
-    const size_t smem1 = ((size_t)2 * (n + H - 1) + (size_t)H * (NT / 32)) * sa;
+    // + the label ring (lab_kp rows of NT*CPT ints) when reading labels
+    const size_t ring_b = (src == SRC_LABELS && f32) ? (size_t)lab_kp(CPT * NT) * NT * CPT * sizeof(int) : 0;
+    const size_t smem1 = ((size_t)2 * (n + H - 1) + (size_t)H * (NT / 32)) * sa + ring_b + 16;
 #define DET_SAT1(SRC_, A_, L_)                                                                               \
     do {                                                                                                     \
         auto fn = k_sat1<CPT, NT, SRC_, A_, L_>;                                                             \
@@ -184,7 +186,7 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
 #undef DET_SAT1
     const int lanes = n + 2 * (2 * n - 1);
     k_sat2<<<dim3((lanes + SAT2_THREADS - 1) / SAT2_THREADS + 1, B), SAT2_THREADS, 0, c->stream>>>(D, gate);
-    const size_t smem = ((size_t)3 * (n + H) + 3 * H + (H & 1)) * sa + lut_b;
+    const size_t smem = ((size_t)3 * (n + H) + 3 * H + (H & 1)) * sa + lut_b + ring_b + 16;
 #define DET_SAT3(SRC_, UT_, OUT_, L_)                                                                        \
     do {                                                                                                     \
         auto fn = k_sat3<CPT, NT, SRC_, UT_, OUT_, UT_, L_>;                                                 \

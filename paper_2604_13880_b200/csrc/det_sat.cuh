@@ -89,6 +89,80 @@ __device__ __forceinline__ const A* band_lut(const Bufs& D, int R, int b, A* s_l
 // shared-memory LUT length (entries), rounded so what follows stays 8-byte aligned
 __host__ __device__ __forceinline__ int lut_smem_len(int R) { return (R + 2) & ~1; }
 
+// Label rows staged through a KP-slot shared-memory ring with cp.async (no registers held
+// for the prefetch): each thread copies and later reads only its own CPT labels, so a
+// wait_group is all the synchronisation needed.  Row j sits in slot j % KP; the refill
+// for row j + KP - 1 reuses the slot of row j - 1, whose labels were consumed a full row
+// earlier (a cp.async write is not ordered against this thread's earlier shared loads).
+// ring slots (prefetch distance KP - 1 rows): 4, or 2 for 8192-column rows, whose ring would
+// not fit next to the carry windows in one CTA's shared memory
+__host__ __device__ constexpr int lab_kp(int cols) { return cols >= 8192 ? 2 : 4; }
+
+// first 16-byte aligned int slot at or after p (cp.async 16-byte copies and int4 reads)
+template <typename T>
+__device__ __forceinline__ int* align16(T* p) {
+    return reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+}
+
+template <int CPT, int KP>
+struct LabelRing {
+    int* q;          // KP slots of `stride` ints
+    const int* lab;  // cartogram's label texture, row 0
+    int stride, n, x0, j_last;
+    bool active;
+    __device__ __forceinline__ void issue(int row, int slot) {
+        if (active && row <= j_last) {
+            int* dst = q + slot * stride + x0;
+            const int* src = lab + (size_t)row * n + x0;
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+            if (CPT % 4 == 0) {
+#pragma unroll
+                for (int c = 0; c < CPT; c += 4)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + 4 * c), "l"(src + c) : "memory");
+            } else {
+#pragma unroll
+                for (int c = 0; c < CPT; c += 2)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa + 4 * c), "l"(src + c) : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+    __device__ __forceinline__ void wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(KP - 2) : "memory"); }
+    __device__ __forceinline__ void prologue(int jt) {
+#pragma unroll
+        for (int p = 0; p < KP - 1; ++p) issue(jt + p, p);
+    }
+    // labels of row j (slot (j - jt) % KP) -> residual densities; then the refill
+    template <typename A>
+    __device__ __forceinline__ void take(int j, int jt, const A* lut, int R, A (&rho)[CPT]) {
+        const int r = j - jt;
+        wait();
+        if (active) {
+            const int* src = q + (r & (KP - 1)) * stride + x0;
+            int L[CPT];
+            if (CPT % 4 == 0) {
+#pragma unroll
+                for (int c = 0; c < CPT; c += 4) {
+                    const int4 v = *reinterpret_cast<const int4*>(src + c);
+                    L[c] = v.x; L[c + 1] = v.y; L[c + 2] = v.z; L[c + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < CPT; c += 2) {
+                    const int2 v = *reinterpret_cast<const int2*>(src + c);
+                    L[c] = v.x; L[c + 1] = v.y;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) rho[k] = lut[L[k] < 0 ? R : L[k]];
+        } else {
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) rho[k] = (A)0;
+        }
+        issue(j + KP - 1, (r + KP - 1) & (KP - 1));
+    }
+};
+
 template <typename A>
 __device__ __forceinline__ A warp_incl_scan_t(A v) {
     const int lane = threadIdx.x & 31;
@@ -141,18 +215,36 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
     A* s_rows = s_lut + (LUTS ? lut_smem_len(R) : 0);
     const A* lut = band_lut<A, LUTS>(D, R, b, s_lut);
     if (LUTS) __syncthreads();
+    // labels through the shared-memory ring on the float path (the float64 path's carry windows
+    // leave no room for it at 8192 columns); register prefetch otherwise
+    constexpr bool RING = SRC == SRC_LABELS && sizeof(A) == 4;
+    LabelRing<CPT, lab_kp(CPT * NT)> ring;
+    if (RING) {
+        ring.q = align16(s_rows + H * NW);
+        ring.lab = D.labels + (size_t)b * D.nn;
+        ring.stride = NT * CPT;
+        ring.n = n;
+        ring.x0 = x0;
+        ring.j_last = jb;
+        ring.active = x0 < n;
+        ring.prologue(jt);
+    }
     A cs[CPT], pd[CPT], pa[CPT];
 #pragma unroll
     for (int k = 0; k < CPT; ++k) cs[k] = pd[k] = pa[k] = (A)0;
 
     A rho_n[CPT];
-    load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, jt, x0, rho_n);
+    if (!RING) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, jt, x0, rho_n);
     int slot = 0, ps = 2;  // rotating boundary slots: (j - jt) % 3, (j - jt + 2) % 3
     for (int j = jt; j <= jb; ++j) {
         A rho[CPT];
+        if (RING) {
+            ring.take(j, jt, lut, R, rho);
+        } else {
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
-        if (j < jb) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, j + 1, x0, rho_n);  // prefetch the next row
+            for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
+            if (j < jb) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, j + 1, x0, rho_n);  // prefetch the next row
+        }
         A ts = (A)0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) ts += rho[k];
@@ -365,16 +457,34 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
     const A inv2m = (A)(S.outscale != 0.0 ? S.outscale : 0.5 * inv_nd * inv_nd);
     const A xc0 = (A)(((double)x0 + 0.5) * inv_nd);  // pixel-centre x of column x0 (displacement.py:59)
     UT* uf = reinterpret_cast<UT*>(D.uf) + (size_t)b * D.nn * 2;
+    // labels through the shared-memory ring on the float path (the float64 path's carry windows
+    // leave no room for it at 8192 columns); register prefetch otherwise
+    constexpr bool RING = SRC == SRC_LABELS && sizeof(A) == 4;
+    LabelRing<CPT, lab_kp(CPT * NT)> ring;
+    if (RING) {
+        ring.q = align16(s_lut + (LUTS ? lut_smem_len(R) : 0));
+        ring.lab = D.labels + (size_t)b * D.nn;
+        ring.stride = NT * CPT;
+        ring.n = n;
+        ring.x0 = x0;
+        ring.j_last = jb;
+        ring.active = active;
+        ring.prologue(jt);
+    }
     __syncthreads();  // windows, row constants and LUT published
     A rho_n[CPT];
-    load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, jt, x0, rho_n);
+    if (!RING) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, jt, x0, rho_n);
 
     int slot = 0, ps = 2;  // rotating boundary slots: (j - jt) % 3, (j - jt + 2) % 3
     for (int j = jt; j <= jb; ++j) {
         A rho[CPT];
+        if (RING) {
+            ring.take(j, jt, lut, R, rho);
+        } else {
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
-        if (j < jb) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, j + 1, x0, rho_n);  // prefetch the next row
+            for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
+            if (j < jb) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, j + 1, x0, rho_n);  // prefetch the next row
+        }
         A loc[CPT];
         A run = (A)0;
 #pragma unroll
