@@ -2,16 +2,16 @@
 //
 // A context owns one CUDA stream, the map topology, a batch of cartograms and
 // all device buffers.  det_run() keeps the whole iteration loop on the device:
-// one iteration = k_sat1 -> k_sat2 -> k_sat3 -> k_region -> k_row -> k_ctrl,
-// captured G times into a CUDA graph; kernels of finished cartograms exit on
-// their device-side `active` flag, and the host only polls the flags once per
-// graph launch.
+// one iteration = k_sat1 -> k_sat2 -> k_sat3 -> k_region -> k_row -> k_ctrl per
+// frame group; 16 iterations of every group are captured into one CUDA graph,
+// the groups as parallel branches (fork/join).  Kernels of finished cartograms
+// exit on their device-side `active` flag, and the host only polls the flags
+// once per graph launch.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
-#include <unordered_map>
 #include <vector>
 
 #include "../../include/det_api.h"

@@ -211,7 +211,8 @@ __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
     }
 }
 
-// Host-driven control step (evaluation of the start state): one CTA per cartogram.
+// The control step as its own kernel, one 1024-thread CTA per cartogram: the evaluation of
+// the start state, and each loop iteration's step after k_row (launch_row_ctrl).
 __global__ void __launch_bounds__(CTRL_THREADS) k_ctrl(Topo T, Bufs D, int cmode, int gate) {
     if (!gate_open(D.st + blockIdx.x + D.b0, gate)) return;
     ctrl_body(T, D, blockIdx.x + D.b0, cmode);
