@@ -1,0 +1,61 @@
+"""Result plumbing on the GPU: page-locked result blocks are never recycled under live results,
+and deferred result maps materialise exactly the reference's Region structure."""
+
+import gc
+
+import numpy as np
+import pytest
+
+import fixture_maps as fm
+
+pytestmark = pytest.mark.gpu
+
+
+def _engine(stats_scale=1.0):
+    import paper_2604_13880_b200 as P
+
+    m = fm.small_voronoi(seed=4, r=30, target=700)
+    s = m.statistics()
+    walk = np.stack([s * stats_scale * np.exp(np.random.default_rng(t).normal(0, 0.3, s.shape)) for t in range(4)])
+    return m, P.BatchEngine(m, walk, criteria=P.StoppingCriteria(1e-300, 10**9, 6), k=7)
+
+
+def test_pinned_results_survive_later_runs():
+    import paper_2604_13880_b200 as P
+
+    m, be = _engine()
+    res1 = be.run_all()
+    keep = [r.state.mapmodel.vertex_array() for r in res1]
+    # a second run on another engine and a rerun of this one must not touch res1's buffers
+    _, be2 = _engine(2.0)
+    res2 = be2.run_all()
+    res3 = be.run_all(P.StoppingCriteria(1e-300, 10**9, 3))
+    for r, k in zip(res1, keep):
+        np.testing.assert_array_equal(r.state.mapmodel.vertex_array(), k)
+    assert not np.array_equal(res3[0].state.mapmodel.vertex_array(), keep[0])  # 3 vs 6 iterations
+    # once the results are gone their block returns to the pool and is reused
+    ctx = be._ctx()
+    misses = ctx.pinned.misses
+    del res1, res2, res3, r
+    gc.collect()
+    be.run_all()
+    assert ctx.pinned.misses == misses
+
+
+def test_deferred_result_map_matches_rebuild():
+    from paper_2604_13880_b200.geomodel import MapModel, rebuild
+
+    m, be = _engine()
+    res = be.run_all()
+    cm = res[1].state.mapmodel
+    assert "regions" not in cm.__dict__  # nothing built yet
+    xy = cm.vertex_array()
+    ref = rebuild(m.with_statistics(be.statistics[1]), xy)
+    assert isinstance(cm, MapModel)
+    assert cm.region_ids() == ref.region_ids()
+    np.testing.assert_array_equal(cm.statistics(), ref.statistics())
+    for a, b in zip(cm.regions, ref.regions):
+        assert len(a.rings) == len(b.rings)
+        for ra, rb in zip(a.rings, b.rings):
+            np.testing.assert_array_equal(ra, rb)
+    np.testing.assert_allclose([r.area() for r in cm.regions], be.areas(1), rtol=1e-12)
