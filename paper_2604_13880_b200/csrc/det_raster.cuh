@@ -23,6 +23,7 @@
 //            of a cartogram derives the background count and runs the control step
 //            (det_ctrl.cuh) -- no separate launch.
 #pragma once
+#include <type_traits>
 #include "det_common.cuh"
 #include "det_ctrl.cuh"
 
@@ -67,6 +68,29 @@ __device__ __forceinline__ Tap field_tap(int n, double px, double py) {
     return t;
 }
 
+// Float-field tap: the fraction only feeds a float blend, so floor / clamp / fraction run in
+// float32 after one float64 FMA.  The texel choice can differ from the float64 rule only where
+// the fraction is within float rounding of 0 or 1, where both neighbours blend to the same value.
+struct TapF {
+    int o0, o1;
+    float fx, fy;
+};
+
+__device__ __forceinline__ TapF field_tap_f(int n, double px, double py) {
+    constexpr float M = 12582912.0f;  // 1.5 * 2^23: x + M rounded down holds floor(x) in its low bits
+    const float gx = (float)fma(px, (double)n, -0.5), gy = (float)fma(py, (double)n, -0.5);
+    const float tx = __fadd_rd(gx, M), ty = __fadd_rd(gy, M);
+    const int ix = min(max(__float_as_int(tx) - 0x4B400000, 0), n - 2);
+    const int iy = min(max(__float_as_int(ty) - 0x4B400000, 0), n - 2);
+    const float hi = (float)(n - 2);
+    TapF t;
+    t.fx = __saturatef(gx - fminf(fmaxf(tx - M, 0.0f), hi));
+    t.fy = __saturatef(gy - fminf(fmaxf(ty - M, 0.0f), hi));
+    t.o0 = (iy * n + ix) * 2;
+    t.o1 = t.o0 + n * 2;
+    return t;
+}
+
 template <typename UT>
 struct Texels {
     UT v[8];
@@ -84,8 +108,8 @@ struct Vec2<double> {
 };
 
 // the four texels as (u, v) pairs: one 8-byte (float) / 16-byte (double) load each
-template <typename UT>
-__device__ __forceinline__ Texels<UT> field_load(const UT* __restrict__ uf, const Tap& t) {
+template <typename UT, typename TP>
+__device__ __forceinline__ Texels<UT> field_load(const UT* __restrict__ uf, const TP& t) {
     using V = typename Vec2<UT>::type;
     const V* __restrict__ u2 = reinterpret_cast<const V*>(uf);
     const V a = __ldg(u2 + (t.o0 >> 1)), b = __ldg(u2 + (t.o0 >> 1) + 1);
@@ -96,8 +120,8 @@ __device__ __forceinline__ Texels<UT> field_load(const UT* __restrict__ uf, cons
     return x;
 }
 
-template <typename UT>
-__device__ __forceinline__ double2 field_blend(const Texels<UT>& x, const Tap& t) {
+template <typename UT, typename TP>
+__device__ __forceinline__ double2 field_blend(const Texels<UT>& x, const TP& t) {
     const UT fx = (UT)t.fx, fy = (UT)t.fy;
     const UT gxm = (UT)1 - fx, gym = (UT)1 - fy;
     const UT sx = x.v[0] * gxm * gym + x.v[2] * fx * gym + x.v[4] * gxm * fy + x.v[6] * fx * fy;
@@ -202,16 +226,18 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
         }
         double2 nq[RW_UNROLL];
         if (mode & M_ADVECT) {
-            Tap tp[RW_UNROLL];
+            using TP = typename std::conditional<sizeof(UT) == 4, TapF, Tap>::type;
+            TP tp[RW_UNROLL];
             Texels<UT> tx[RW_UNROLL];
 #pragma unroll
             for (int q = 0; q < RW_UNROLL; ++q) {
-                tp[q] = field_tap(n, p[q].x, p[q].y);
-                tx[q] = field_load<UT>(uf, tp[q]);
+                if constexpr (sizeof(UT) == 4) tp[q] = field_tap_f(n, p[q].x, p[q].y);
+                else tp[q] = field_tap(n, p[q].x, p[q].y);
+                tx[q] = field_load<UT, TP>(uf, tp[q]);
             }
 #pragma unroll
             for (int q = 0; q < RW_UNROLL; ++q) {
-                const double2 s = field_blend<UT>(tx[q], tp[q]);
+                const double2 s = field_blend<UT, TP>(tx[q], tp[q]);
                 const double mx = p[q].x + s.x, my = p[q].y + s.y;
                 const double cx = mx < 0.0 ? 0.0 : (mx > 1.0 ? 1.0 : mx);  // np.clip (no NaNs here)
                 const double cy = my < 0.0 ? 0.0 : (my > 1.0 ? 1.0 : my);
