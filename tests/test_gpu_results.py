@@ -59,3 +59,27 @@ def test_deferred_result_map_matches_rebuild():
         for ra, rb in zip(a.rings, b.rings):
             np.testing.assert_array_equal(ra, rb)
     np.testing.assert_allclose([r.area() for r in cm.regions], be.areas(1), rtol=1e-12)
+
+
+@pytest.mark.parametrize("groups", [1, 2, 3, 8])
+def test_frame_group_partitions_are_bit_identical(groups):
+    """Graph branches over uneven frame partitions (5 frames in 1/2/3/8 groups) change nothing."""
+    import paper_2604_13880_b200 as P
+    from paper_2604_13880_b200._context import get_context
+
+    m = fm.small_voronoi(seed=9, r=40, target=900)
+    s = m.statistics()
+    walk = np.stack([s * np.exp(np.random.default_rng(40 + t).normal(0, 0.3, s.shape)) for t in range(5)])
+    crit = P.StoppingCriteria(1e-300, 10**9, 40)  # 40 iterations: two full 16-iteration graph launches + tail
+    ctx = get_context(7)
+    ctx.set_groups(1)
+    ref = P.BatchEngine(m, walk, criteria=crit, k=7).run_all()
+    ctx.set_groups(groups)
+    try:
+        got = P.BatchEngine(m, walk, criteria=crit, k=7).run_all()
+    finally:
+        ctx.set_groups(8)
+    for a, b in zip(ref, got):
+        np.testing.assert_array_equal(a.state.mapmodel.vertex_array(), b.state.mapmodel.vertex_array())
+        np.testing.assert_array_equal(a.state.pixel_counts, b.state.pixel_counts)
+        assert [t.epsilon for t in a.trace] == [t.epsilon for t in b.trace]
