@@ -143,6 +143,11 @@ int det_get_counts(det_ctx *ctx, int b, int64_t *counts_out);    /* R+1      */
 int det_get_region_error(det_ctx *ctx, int b, double *out);      /* R        */
 int det_get_trace(det_ctx *ctx, int b, double *out);             /* trace_len*4: iter, eps, xi, millis */
 int det_get_areas(det_ctx *ctx, int b, double *out);             /* R: Region.area() (geomodel.py:63-65) */
+/* Every cartogram's results in one call (the batched RunResult.state of engine.py:46-72): any output
+ * may be NULL; xy_out B*n_rows*2, counts_out B*(R+1), err_out B*R, trace_out B*trace_rows*4 (rows
+ * past a cartogram's trace_len are unspecified). */
+int det_get_results(det_ctx *ctx, double *xy_out, int64_t *counts_out, double *err_out, double *trace_out,
+                    int trace_rows);
 
 /* Stage-level entry points (parity tests; integral.py:155, displacement.py:198-238). */
 /* u = t(d) - t(const) at pixel centres for a dense density d (n*n float64);

@@ -75,6 +75,8 @@ EXPORTS = {
     "det_get_region_error": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p]),
     "det_get_trace": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p]),
     "det_get_areas": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int, _c_double_p]),
+    "det_get_results": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_int64_p, _c_double_p, _c_double_p,
+                                        ctypes.c_int]),
     "det_field": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p, _c_double_p, _c_double_p]),
     "det_mapping": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p]),
     "det_density": (ctypes.c_int, [ctypes.c_void_p, _c_int32_p, _c_double_p, ctypes.c_int, ctypes.c_double,
@@ -298,6 +300,16 @@ class Context:
         r = DetResult()
         self.check(self.lib.det_get_result(self.h, b, ctypes.byref(r)))
         return r
+
+    def results_all(self, xy_out, trace_rows):
+        """Vertices (into xy_out, B x rows x 2), counts, per-region errors and traces of every cartogram."""
+        counts = np.empty((self.B, self.R + 1), dtype=np.int64)
+        errs = np.empty((self.B, self.R), dtype=np.float64)
+        trace = np.empty((self.B, max(int(trace_rows), 0), 4), dtype=np.float64)
+        self.check(self.lib.det_get_results(self.h, _p(xy_out, ctypes.c_double), _p(counts, ctypes.c_int64),
+                                            _p(errs, ctypes.c_double), _p(trace, ctypes.c_double),
+                                            int(trace_rows)))
+        return counts, errs, trace
 
     def vertices(self, b=0, out=None):
         if out is None:

@@ -981,6 +981,33 @@ int det_get_trace(det_ctx* ctx, int b, double* out) {
     return DET_OK;
 }
 
+int det_get_results(det_ctx* ctx, double* xy_out, int64_t* counts_out, double* err_out, double* trace_out,
+                    int trace_rows) {
+    if (!ctx || !ctx->ran) return fail(ctx, DET_E_STATE, "no result");
+    if (trace_out && trace_rows < 0) return fail(ctx, DET_E_ARG, "bad trace_rows");
+    cudaSetDevice(ctx->device);
+    const int B = ctx->B, R = ctx->R;
+    cudaStream_t s = ctx->stream;
+    if (xy_out)
+        for (int b = 0; b < B; ++b)
+            CK(cudaMemcpyAsync(xy_out + (size_t)b * ctx->n_rows * 2, state_rows(ctx, b), ctx->n_rows * sizeof(double2),
+                               cudaMemcpyDeviceToHost, s));
+    std::vector<int> c;
+    if (counts_out) {
+        c.resize((size_t)B * (R + 1));
+        CK(cudaMemcpyAsync(c.data(), ctx->cnt_state.p, c.size() * sizeof(int), cudaMemcpyDeviceToHost, s));
+    }
+    if (err_out) CK(cudaMemcpyAsync(err_out, ctx->rerr.p, (size_t)B * R * sizeof(double), cudaMemcpyDeviceToHost, s));
+    const int rows = std::min(trace_rows, ctx->trace_cap);
+    if (trace_out && rows > 0)
+        CK(cudaMemcpy2DAsync(trace_out, (size_t)trace_rows * 4 * sizeof(double), ctx->trace.p,
+                             (size_t)ctx->trace_cap * 4 * sizeof(double), (size_t)rows * 4 * sizeof(double), B,
+                             cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (size_t i = 0; i < c.size(); ++i) counts_out[i] = c[i];
+    return DET_OK;
+}
+
 int det_get_areas(det_ctx* ctx, int b, double* out) {
     if (!ctx || !out || b < 0 || b >= ctx->B) return fail(ctx, DET_E_ARG, "bad arguments");
     cudaSetDevice(ctx->device);

@@ -220,35 +220,40 @@ class BatchEngine:
         ctx = self.launch(criteria)
         t1 = time.perf_counter()
         verts = ctx.pinned.empty((self.B, self._xy.shape[0], 2))
-        t2 = time.perf_counter()
-        out, per = [], []
-        for b in range(self.B):
-            tb = time.perf_counter()
-            out.append(self._collect(ctx, b, iteration_offset, clamp_offset, verts[b]))
-            per.append(round((time.perf_counter() - tb) * 1e3, 2))
-        self.last_timing = {"launch_s": t1 - t0, "pinned_s": t2 - t1, "collect_s": time.perf_counter() - t2,
-                            "pinned_misses": ctx.pinned.misses, "per_frame_ms": per}
+        res = [ctx.result(b) for b in range(self.B)]
+        counts, errs, traces = ctx.results_all(verts, max([r.trace_len for r in res] + [0]))
+        out = [self._collect(ctx, b, iteration_offset, clamp_offset, verts[b], (res[b], counts[b], errs[b], traces[b]))
+               for b in range(self.B)]
+        self.last_timing = {"launch_s": t1 - t0, "collect_s": time.perf_counter() - t1,
+                            "pinned_misses": ctx.pinned.misses}
         return out
 
-    def _collect(self, ctx, b, it_off=0, cl_off=0, verts_out=None):
-        r = ctx.result(b)
+    def _collect(self, ctx, b, it_off=0, cl_off=0, verts_out=None, fetched=None):
+        """RunResult of cartogram b; ``fetched`` = (result, counts, errors, trace) already read back
+        for every cartogram at once (run_all), else read here."""
+        r = ctx.result(b) if fetched is None else fetched[0]
         if r.stop_reason == STOP_COLLAPSED:
             return RegionCollapsedError(self.region_ids[r.collapsed_region], r.iteration + it_off)
         if r.stop_reason == STOP_BDV:
             return ValueError("bdv must be positive")
         if r.stop_reason == STOP_NEGINDEX:
             return ValueError("'list' argument must have no negative elements")
-        tr = ctx.trace(b, r.trace_len)
+        if fetched is None:
+            tr = ctx.trace(b, r.trace_len)
+            verts = ctx.vertices(b, verts_out)
+            counts = ctx.counts(b)
+            rerr = ctx.region_error(b)
+        else:
+            tr = fetched[3][: r.trace_len]
+            verts, counts, rerr = verts_out, fetched[1], fetched[2]
         records = trace_records(tr, it_off)
-        verts = ctx.vertices(b, verts_out)
-        counts = ctx.counts(b)
         clamps = int(r.clamp_events) + (cl_off if r.stop_reason != 2 else 0)
         result_map = deferred_rebuild(self.initial_map, verts, self.statistics[b], self._sizes)
         lazy = _LazyLabels(ctx, b, getattr(ctx, "generation", None), lambda: result_map, self.k, self.device)
         labels = LabelTexture(size=self.n, labels=lazy, region_ids=tuple(self.region_ids), _counts=counts)
         state = CartogramState(mapmodel=result_map, iteration=int(r.iteration) + it_off,
                                labels=labels, pixel_counts=counts[:-1].copy(),
-                               per_region_error=ctx.region_error(b), epsilon=float(r.epsilon), xi=float(r.xi),
+                               per_region_error=rerr, epsilon=float(r.epsilon), xi=float(r.xi),
                                clamp_events=clamps)
         return RunResult(state=state, trace=records, stop_reason=STOP_NAMES[r.stop_reason],
                          weights_px=self.weights_px[b].copy(), background_mass=float(self.background_mass[b]))
