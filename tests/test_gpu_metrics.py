@@ -150,3 +150,25 @@ def test_temporal_reports_and_watchdog(golden_dir):
         for key in ("hamming_avg", "watchdog", "errors", "M_b", "A_i"):
             assert ser[key] == ref_ser[key], key
         np.testing.assert_allclose(ser["epsilon"], ref_ser["epsilon"], rtol=1e-9)
+
+
+def test_headline_scale_shapes_and_adjacency_match_oracle():
+    """3000-region map, ~400k rows: every 97th region's Hamming value (k=7) and the full adjacency
+    set of a deformed copy equal the oracle's."""
+    from oracle import metrics_oracle as MO
+    from paper_2604_13880_b200 import detect_adjacencies, shape_distortion
+    from paper_2604_13880_b200.geomodel import densify
+    from paper_2604_13880_b200.synthetic import config_map
+
+    m, _ = config_map("headline")
+    m = densify(m, 4.0 / 1024)
+    rng = np.random.default_rng(77)
+    c = m.with_vertex_array(np.clip(m.vertex_array() + rng.normal(0, 3e-4, m.vertex_array().shape), 0, 1))
+    vals, _, _ = shape_distortion(m, c, raster_k=7)
+    for r in range(0, len(m.regions), 97):
+        ra = [np.asarray(x) for x in m.regions[r].rings]
+        rc = [np.asarray(x) for x in c.regions[r].rings]
+        assert vals[r] == MO.hamming(ra, rc, 7), r
+    pos = {rid: i for i, rid in enumerate(c.region_ids())}
+    got = {tuple(sorted((pos[a], pos[b]))) for a, b in detect_adjacencies(c, 0.5 / 1024)}
+    assert got == MO.adjacency([[np.asarray(x) for x in reg.rings] for reg in c.regions], 0.5 / 1024)
