@@ -44,32 +44,68 @@ __device__ __forceinline__ Mom3 ring_term(const double2* __restrict__ p, int a, 
 }
 
 // numpy pairwise_sum (loops_utils.h): n < 8 sequential from 0; n <= 128 eight accumulators;
-// larger n split at n/2 rounded down to a multiple of 8.
-__device__ Mom3 pw_moments(const double2* __restrict__ p, int a, int V, int lo, int cnt) {
+// larger n split at n/2 rounded down to a multiple of 8.  The split tree is walked with an
+// explicit stack (a recursive version overflows the per-thread stack on long rings).
+__device__ __noinline__ Mom3 pw_leaf(const double2* __restrict__ p, int a, int V, int lo, int cnt) {
     if (cnt < 8) {
         Mom3 r{0.0, 0.0, 0.0};
         for (int i = 0; i < cnt; ++i) r = mom_add(r, ring_term(p, a, V, lo + i));
         return r;
     }
-    if (cnt <= 128) {
-        Mom3 acc[8];
+    Mom3 acc[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = ring_term(p, a, V, lo + j);
-        int i = 8;
-        for (; i < cnt - (cnt % 8); i += 8) {
+    for (int j = 0; j < 8; ++j) acc[j] = ring_term(p, a, V, lo + j);
+    int i = 8;
+    for (; i < cnt - (cnt % 8); i += 8) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) acc[j] = mom_add(acc[j], ring_term(p, a, V, lo + i + j));
-        }
-        Mom3 r = mom_add(mom_add(mom_add(acc[0], acc[1]), mom_add(acc[2], acc[3])),
-                         mom_add(mom_add(acc[4], acc[5]), mom_add(acc[6], acc[7])));
-        for (; i < cnt; ++i) r = mom_add(r, ring_term(p, a, V, lo + i));
-        return r;
+        for (int j = 0; j < 8; ++j) acc[j] = mom_add(acc[j], ring_term(p, a, V, lo + i + j));
     }
-    int n2 = cnt / 2;
-    n2 -= n2 % 8;
-    const Mom3 l = pw_moments(p, a, V, lo, n2);
-    const Mom3 h = pw_moments(p, a, V, lo + n2, cnt - n2);
-    return mom_add(l, h);
+    Mom3 r = mom_add(mom_add(mom_add(acc[0], acc[1]), mom_add(acc[2], acc[3])),
+                     mom_add(mom_add(acc[4], acc[5]), mom_add(acc[6], acc[7])));
+    for (; i < cnt; ++i) r = mom_add(r, ring_term(p, a, V, lo + i));
+    return r;
+}
+
+__device__ __forceinline__ int pw_split(int cnt) {
+    const int n2 = cnt / 2;
+    return n2 - n2 % 8;
+}
+
+__device__ Mom3 pw_moments(const double2* __restrict__ p, int a, int V, int lo0, int cnt0) {
+    constexpr int DEPTH = 26;  // split depth for rings of up to 128 * 2^25 vertices
+    int s_lo[DEPTH], s_cnt[DEPTH];
+    bool s_right[DEPTH];  // the node's left subtree is done, s_left holds its sum
+    Mom3 s_left[DEPTH];
+    int sp = 0;
+    s_lo[0] = lo0;
+    s_cnt[0] = cnt0;
+    s_right[0] = false;
+    for (;;) {
+        if (s_cnt[sp] > 128) {  // descend into the left half
+            const int n2 = pw_split(s_cnt[sp]);
+            ++sp;
+            s_lo[sp] = s_lo[sp - 1];
+            s_cnt[sp] = n2;
+            s_right[sp] = false;
+            continue;
+        }
+        Mom3 ret = pw_leaf(p, a, V, s_lo[sp], s_cnt[sp]);
+        for (;;) {  // return upwards: a finished left half starts its sibling, a right half combines
+            if (sp == 0) return ret;
+            --sp;
+            if (!s_right[sp]) {
+                const int n2 = pw_split(s_cnt[sp]);
+                s_left[sp] = ret;
+                s_right[sp] = true;
+                ++sp;
+                s_lo[sp] = s_lo[sp - 1] + n2;
+                s_cnt[sp] = s_cnt[sp - 1] - n2;
+                s_right[sp] = false;
+                break;
+            }
+            ret = mom_add(s_left[sp], ret);
+        }
+    }
 }
 
 struct ShapeMap {

@@ -172,3 +172,20 @@ def test_headline_scale_shapes_and_adjacency_match_oracle():
     pos = {rid: i for i, rid in enumerate(c.region_ids())}
     got = {tuple(sorted((pos[a], pos[b]))) for a, b in detect_adjacencies(c, 0.5 / 1024)}
     assert got == MO.adjacency([[np.asarray(x) for x in reg.rings] for reg in c.regions], 0.5 / 1024)
+
+
+def test_long_rings_shape_distortion_matches_oracle():
+    """Rings of ~5000 vertices: the pairwise moment sums walk a deep split tree (regression: a
+    recursive version overflowed the per-thread stack)."""
+    from oracle import metrics_oracle as MO
+    from paper_2604_13880_b200 import shape_distortion
+    from paper_2604_13880_b200.geomodel import densify
+
+    m = densify(fm.two_region(), 0.0005)
+    assert max(np.asarray(r).shape[0] for reg in m.regions for r in reg.rings) > 4000
+    rng = np.random.default_rng(3)
+    c = m.with_vertex_array(np.clip(m.vertex_array() + rng.normal(0, 0.002, m.vertex_array().shape), 0, 1))
+    got, _, _ = shape_distortion(m, c, raster_k=6)
+    want = [MO.hamming([np.asarray(x) for x in a.rings], [np.asarray(x) for x in b.rings], 6)
+            for a, b in zip(m.regions, c.regions)]
+    np.testing.assert_array_equal(got, want)

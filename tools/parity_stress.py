@@ -23,8 +23,51 @@ import paper_2604_13880_b200 as P  # noqa: E402
 from oracle import det_oracle as O  # noqa: E402
 
 
+def metrics_stress(budget, seed0):
+    """Random map pairs: GPU Hamming values (k 3..8, rescale on/off) and adjacency sets vs the oracle."""
+    from oracle import metrics_oracle as MO
+    from paper_2604_13880_b200 import detect_adjacencies, shape_distortion
+
+    t0 = time.perf_counter()
+    out = {"metric_cases": 0, "metric_regions": 0, "metric_mismatch": None}
+    i = 0
+    while time.perf_counter() - t0 < budget and out["metric_mismatch"] is None:
+        r = np.random.default_rng(seed0 + 7919 * i)
+        i += 1
+        m = fm.small_voronoi(seed=int(r.integers(1 << 20)), r=int(r.integers(2, 40)), target=int(r.integers(100, 1200)))
+        c = m.with_vertex_array(np.clip(m.vertex_array() + r.normal(0, float(r.choice([0.001, 0.005, 0.02])),
+                                                                     m.vertex_array().shape), 0, 1))
+        k, resc = int(r.integers(3, 9)), bool(r.integers(2))
+        rm = [[np.asarray(x) for x in reg.rings] for reg in m.regions]
+        rc = [[np.asarray(x) for x in reg.rings] for reg in c.regions]
+        try:
+            want = np.array([MO.hamming(a, b, k, resc) for a, b in zip(rm, rc)])
+        except Exception:  # noqa: BLE001 -- degenerate shape: the GPU must raise as well
+            try:
+                shape_distortion(m, c, raster_k=k, rescale=resc)
+                out["metric_mismatch"] = {"case": i, "kind": "oracle raised, gpu did not"}
+            except Exception:  # noqa: BLE001
+                pass
+            continue
+        got, _, _ = shape_distortion(m, c, raster_k=k, rescale=resc)
+        out["metric_cases"] += 1
+        out["metric_regions"] += len(rm)
+        if not np.array_equal(got, want):
+            out["metric_mismatch"] = {"case": i, "kind": "hamming", "k": k, "rescale": resc,
+                                      "regions": int((got != want).sum())}
+            break
+        pos = {rid: q for q, rid in enumerate(c.region_ids())}
+        adj = {tuple(sorted((pos[a], pos[b]))) for a, b in detect_adjacencies(c, 0.5 / 1024)}
+        if adj != MO.adjacency(rc, 0.5 / 1024):
+            out["metric_mismatch"] = {"case": i, "kind": "adjacency"}
+    return out
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
+    if len(sys.argv) > 2 and sys.argv[2] == "metrics":
+        print(json.dumps(metrics_stress(budget, int(time.time()) % 100000)))
+        return
     rng = np.random.default_rng(int(time.time()) % 100000)
     seed0 = int(rng.integers(1 << 30))
     t0 = time.perf_counter()
