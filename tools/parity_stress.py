@@ -63,8 +63,57 @@ def metrics_stress(budget, seed0):
     return out
 
 
+def engine_stress(budget, seed0):
+    """Random stopping criteria, bdv modes and multipliers (float64 field): stop reason, stop
+    iteration, counts and collapse region equal the oracle engine's; vertices within 1e-9."""
+    t0 = time.perf_counter()
+    out = {"engine_runs": 0, "stops": {}, "engine_mismatch": None}
+    i = 0
+    while time.perf_counter() - t0 < budget and out["engine_mismatch"] is None:
+        r = np.random.default_rng(seed0 + 104729 * i)
+        i += 1
+        m = fm.small_voronoi(seed=int(r.integers(1 << 20)), r=int(r.integers(2, 30)), target=int(r.integers(100, 900)))
+        m = m.with_statistics(np.exp(r.normal(0, float(r.choice([0.5, 1.5, 3.0])), len(m.regions))))
+        k = int(r.integers(5, 8))
+        mode = str(r.choice(["fixed-mass", "rederive"]))
+        mult = float(r.choice([0.3, 1.0, 2.0]))
+        thr = float(r.choice([1e-300, 0.05, 0.2]))
+        win = int(r.choice([3, 8, 10**9]))
+        its = int(r.integers(5, 40))
+        crit = P.StoppingCriteria(thr, win, its)
+        try:
+            res = P.CartogramEngine(m, criteria=crit, k=k, bdv_multiplier=mult, bdv_mode=mode,
+                                    field_dtype="float64").run()
+            got = ("ok", res.stop_reason, res.state.iteration, res.state.pixel_counts, res.state.mapmodel.vertex_array())
+        except P.RegionCollapsedError as exc:
+            got = ("collapse", exc.region_id, exc.iteration, None, None)
+        except Exception as exc:  # noqa: BLE001
+            got = ("error", type(exc).__name__, str(exc), None, None)
+        f = O.FlatMap.from_mapmodel(m)
+        try:
+            ores = O.OracleEngine(f, k=k, bdv_multiplier=mult, bdv_mode=mode).run(thr, win, its)
+            want = ("ok", ores.stop_reason, ores.iteration, ores.counts, ores.rows)
+        except O.OracleCollapseError as exc:
+            want = ("collapse", exc.region_id, exc.iteration, None, None)
+        except Exception as exc:  # noqa: BLE001
+            want = ("error", type(exc).__name__, str(exc), None, None)
+        out["engine_runs"] += 1
+        key = got[0] + ":" + str(got[1])
+        out["stops"][key] = out["stops"].get(key, 0) + 1
+        same = got[:3] == want[:3] if got[0] != "ok" else (
+            got[:3] == want[:3] and np.array_equal(got[3], want[3]) and np.abs(got[4] - want[4]).max() <= 1e-9)
+        if not same:
+            out["engine_mismatch"] = {"case": i, "got": [str(x)[:80] for x in got[:3]],
+                                      "want": [str(x)[:80] for x in want[:3]], "k": k, "mode": mode,
+                                      "mult": mult, "thr": thr, "win": win, "its": its}
+    return out
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
+    if len(sys.argv) > 2 and sys.argv[2] == "engine":
+        print(json.dumps(engine_stress(budget, int(time.time()) % 100000)))
+        return
     if len(sys.argv) > 2 and sys.argv[2] == "metrics":
         print(json.dumps(metrics_stress(budget, int(time.time()) % 100000)))
         return
