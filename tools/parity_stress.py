@@ -95,8 +95,8 @@ def engine_stress(budget, seed0):
             want = ("ok", ores.stop_reason, ores.iteration, ores.counts, ores.rows)
         except O.OracleCollapseError as exc:
             want = ("collapse", exc.region_id, exc.iteration, None, None)
-        except Exception as exc:  # noqa: BLE001
-            want = ("error", type(exc).__name__, str(exc), None, None)
+        except Exception as exc:  # noqa: BLE001 -- the oracle's error types carry an "Oracle" prefix
+            want = ("error", type(exc).__name__.replace("Oracle", "", 1), str(exc), None, None)
         out["engine_runs"] += 1
         key = got[0] + ":" + str(got[1])
         out["stops"][key] = out["stops"].get(key, 0) + 1
