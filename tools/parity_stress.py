@@ -109,8 +109,56 @@ def engine_stress(budget, seed0):
     return out
 
 
+def temporal_stress(budget, seed0):
+    """Direct / cumulative frame sequences (float64 field) vs the oracle's run_frames: per frame the
+    same success/failure, counts equal, vertices within 1e-9 (a frame failing only in its quality
+    report -- outside the oracle's engine-only restatement -- ends the comparison of that sequence)."""
+    t0 = time.perf_counter()
+    out = {"sequences": 0, "frames": 0, "failed_frames": 0, "report_failures": 0, "temporal_mismatch": None}
+    i = 0
+    while time.perf_counter() - t0 < budget and out["temporal_mismatch"] is None:
+        r = np.random.default_rng(seed0 + 15485863 * i)
+        i += 1
+        m = fm.small_voronoi(seed=int(r.integers(1 << 20)), r=int(r.integers(3, 25)), target=int(r.integers(150, 700)))
+        T, k = 4, int(r.integers(5, 7))
+        sig = float(r.choice([0.1, 0.5, 1.5]))
+        s0 = m.statistics()
+        walk = np.stack([s0 * np.exp(r.normal(0, sig, s0.shape)) for _ in range(T)])
+        cumulative = bool(r.integers(2))
+        crit = P.StoppingCriteria(1e-300, 10**9, 6)
+        ds = P.TimeSeriesDataset(m, tuple(f"t{q}" for q in range(T)), walk)
+        fn = P.run_cumulative if cumulative else P.run_direct
+        seq = fn(ds, crit, k=k, field_dtype="float64")
+        ref = O.run_frames(O.FlatMap.from_mapmodel(m), walk, k, cumulative, error_threshold=1e-300,
+                           stagnation_window=10**9, max_iterations=6)
+        out["sequences"] += 1
+        for t, (fr, rf) in enumerate(zip(seq.frames, ref)):
+            out["frames"] += 1
+            if isinstance(rf, Exception):
+                out["failed_frames"] += 1
+                if fr.error != str(rf):
+                    out["temporal_mismatch"] = {"case": i, "t": t, "ours": str(fr.error)[:120], "oracle": str(rf)[:120]}
+                    break
+                continue
+            if fr.error is not None:
+                if any(w in fr.error for w in ("Hamming", "non-positive area", "cartographic error", "position error")):
+                    out["report_failures"] += 1
+                    break
+                out["temporal_mismatch"] = {"case": i, "t": t, "ours": fr.error[:120], "oracle": "ok"}
+                break
+            ok = (np.array_equal(fr.result.state.pixel_counts, rf.counts) and
+                  np.abs(fr.mapmodel.vertex_array() - rf.rows).max() <= 1e-9)
+            if not ok:
+                out["temporal_mismatch"] = {"case": i, "t": t, "kind": "state", "cumulative": cumulative, "k": k}
+                break
+    return out
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
+    if len(sys.argv) > 2 and sys.argv[2] == "temporal":
+        print(json.dumps(temporal_stress(budget, int(time.time()) % 100000)))
+        return
     if len(sys.argv) > 2 and sys.argv[2] == "engine":
         print(json.dumps(engine_stress(budget, int(time.time()) % 100000)))
         return
