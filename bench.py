@@ -30,7 +30,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "DET iterations/s at 1024^2 texture, 200k vertices; time steps/s over 8 GPUs"
+METRIC = "DET iterations/s at 1024\u00b2 texture, 200k vertices; time steps/s over 8 GPUs"  # BASELINE.json verbatim
 UNIT = "DET iterations/s"
 K_TEX = 10
 

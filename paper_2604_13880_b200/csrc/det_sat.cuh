@@ -89,11 +89,13 @@ __device__ __forceinline__ const A* band_lut(const Bufs& D, int R, int b, A* s_l
 // shared-memory LUT length (entries), rounded so what follows stays 8-byte aligned
 __host__ __device__ __forceinline__ int lut_smem_len(int R) { return (R + 2) & ~1; }
 
-// Label rows staged through a KP-slot shared-memory ring with cp.async (no registers held
-// for the prefetch): each thread copies and later reads only its own CPT labels, so a
-// wait_group is all the synchronisation needed.  Row j sits in slot j % KP; the refill
-// for row j + KP - 1 reuses the slot of row j - 1, whose labels were consumed a full row
-// earlier (a cp.async write is not ordered against this thread's earlier shared loads).
+// Label rows staged through a KP-slot shared-memory ring with 1-D TMA bulk copies
+// (cp.async.bulk, completion on one mbarrier per slot): one elected thread moves a whole row
+// (n int32, 16-byte aligned) per copy, so no thread spends instructions or registers on the
+// prefetch.  Row j sits in slot (j - jt) % KP.  At the start of iteration r the elected thread
+// refills the slot every thread consumed in iteration r - 1 -- that iteration's __syncthreads
+// has passed, and a proxy fence orders those generic reads before the async-proxy write --
+// with row r + KP - 1, so the prefetch distance is KP - 1 rows.
 // ring slots (prefetch distance KP - 1 rows): 4, or 2 for 8192-column rows, whose ring would
 // not fit next to the carry windows in one CTA's shared memory
 __host__ __device__ constexpr int lab_kp(int cols) { return cols >= 8192 ? 2 : 4; }
@@ -107,38 +109,54 @@ __device__ __forceinline__ int* align16(T* p) {
 template <int CPT, int KP>
 struct LabelRing {
     int* q;          // KP slots of `stride` ints
+    uint64_t* bar;   // KP mbarriers
     const int* lab;  // cartogram's label texture, row 0
-    int stride, n, x0, j_last;
+    int stride, n, x0, jt, j_last;
     bool active;
-    __device__ __forceinline__ void issue(int row, int slot) {
-        if (active && row <= j_last) {
-            int* dst = q + slot * stride + x0;
-            const int* src = lab + (size_t)row * n + x0;
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
-            if (CPT % 4 == 0) {
+    __device__ __forceinline__ static unsigned sm(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+    // one thread, before the CTA's first barrier
+    __device__ __forceinline__ void init() {
+        if (threadIdx.x == 0) {
 #pragma unroll
-                for (int c = 0; c < CPT; c += 4)
-                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa + 4 * c), "l"(src + c) : "memory");
-            } else {
-#pragma unroll
-                for (int c = 0; c < CPT; c += 2)
-                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa + 4 * c), "l"(src + c) : "memory");
-            }
+            for (int s = 0; s < KP; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm(bar + s)));
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
     }
-    __device__ __forceinline__ void wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(KP - 2) : "memory"); }
-    __device__ __forceinline__ void prologue(int jt) {
+    __device__ __forceinline__ void issue(int row, int slot) {  // elected thread only
+        if (row > j_last) return;
+        const unsigned bytes = (unsigned)n * 4u;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm(bar + slot)), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                         sm(q + slot * stride)),
+                     "l"(lab + (size_t)row * n), "r"(bytes), "r"(sm(bar + slot))
+                     : "memory");
+    }
+    __device__ __forceinline__ void prologue() {  // after init() and a barrier
+        if (threadIdx.x == 0) {
 #pragma unroll
-        for (int p = 0; p < KP - 1; ++p) issue(jt + p, p);
+            for (int p = 0; p < KP - 1; ++p) issue(jt + p, p);
+        }
     }
-    // labels of row j (slot (j - jt) % KP) -> residual densities; then the refill
+    __device__ __forceinline__ void wait(int slot, unsigned parity) {
+        unsigned done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(sm(bar + slot)), "r"(parity)
+                : "memory");
+        }
+    }
+    // labels of row j -> residual densities (refilling the previous row's slot first)
     template <typename A>
-    __device__ __forceinline__ void take(int j, int jt, const A* lut, int R, A (&rho)[CPT]) {
+    __device__ __forceinline__ void take(int j, const A* lut, int R, A (&rho)[CPT]) {
         const int r = j - jt;
-        wait();
+        if (threadIdx.x == 0) issue(j + KP - 1, (r + KP - 1) % KP);
+        wait(r % KP, (unsigned)((r / KP) & 1));
         if (active) {
-            const int* src = q + (r & (KP - 1)) * stride + x0;
+            const int* src = q + (r % KP) * stride + x0;
             int L[CPT];
             if (CPT % 4 == 0) {
 #pragma unroll
@@ -159,7 +177,6 @@ struct LabelRing {
 #pragma unroll
             for (int k = 0; k < CPT; ++k) rho[k] = (A)0;
         }
-        issue(j + KP - 1, (r + KP - 1) & (KP - 1));
     }
 };
 
@@ -218,16 +235,21 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
     // labels through the shared-memory ring on the float path (the float64 path's carry windows
     // leave no room for it at 8192 columns); register prefetch otherwise
     constexpr bool RING = SRC == SRC_LABELS && sizeof(A) == 4;
+    __shared__ uint64_t s_bar[4];
     LabelRing<CPT, lab_kp(CPT * NT)> ring;
     if (RING) {
         ring.q = align16(s_rows + H * NW);
+        ring.bar = s_bar;
         ring.lab = D.labels + (size_t)b * D.nn;
         ring.stride = NT * CPT;
         ring.n = n;
         ring.x0 = x0;
+        ring.jt = jt;
         ring.j_last = jb;
         ring.active = x0 < n;
-        ring.prologue(jt);
+        ring.init();
+        __syncthreads();
+        ring.prologue();
     }
     A cs[CPT], pd[CPT], pa[CPT];
 #pragma unroll
@@ -239,7 +261,7 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
     for (int j = jt; j <= jb; ++j) {
         A rho[CPT];
         if (RING) {
-            ring.take(j, jt, lut, R, rho);
+            ring.take(j, lut, R, rho);
         } else {
 #pragma unroll
             for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
@@ -460,18 +482,22 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
     // labels through the shared-memory ring on the float path (the float64 path's carry windows
     // leave no room for it at 8192 columns); register prefetch otherwise
     constexpr bool RING = SRC == SRC_LABELS && sizeof(A) == 4;
+    __shared__ uint64_t s_bar[4];
     LabelRing<CPT, lab_kp(CPT * NT)> ring;
     if (RING) {
         ring.q = align16(s_lut + (LUTS ? lut_smem_len(R) : 0));
+        ring.bar = s_bar;
         ring.lab = D.labels + (size_t)b * D.nn;
         ring.stride = NT * CPT;
         ring.n = n;
         ring.x0 = x0;
+        ring.jt = jt;
         ring.j_last = jb;
         ring.active = active;
-        ring.prologue(jt);
+        ring.init();
     }
-    __syncthreads();  // windows, row constants and LUT published
+    __syncthreads();  // windows, row constants, LUT and the ring's mbarriers published
+    if (RING) ring.prologue();
     A rho_n[CPT];
     if (!RING) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, jt, x0, rho_n);
 
@@ -479,7 +505,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
     for (int j = jt; j <= jb; ++j) {
         A rho[CPT];
         if (RING) {
-            ring.take(j, jt, lut, R, rho);
+            ring.take(j, lut, R, rho);
         } else {
 #pragma unroll
             for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
