@@ -61,9 +61,9 @@ struct det_ctx {
     cudaStream_t stream = nullptr;
     std::string err;
     // topology
-    int R = 0, n_rows = 0, n_uniq = 0, n_rings = 0;
+    int R = 0, n_rows = 0, n_rings = 0;
     std::vector<int> h_ring_start, h_region_ring0;
-    std::vector<double> h_xy_uniq, h_xy_rows;
+    std::vector<double> h_xy_rows;
     DVec<int> region_row0, region_rank, rank_region, ring_start, region_ring0;
     // batch
     int B = 0, cap = 64, nb = 0, trace_cap = 0;
@@ -111,7 +111,6 @@ static Topo make_topo(det_ctx* c) {
     Topo t;
     memset(&t, 0, sizeof(t));
     t.n_rows = c->n_rows;
-    t.n_uniq = c->n_uniq;
     t.R = c->R;
     t.region_row0 = c->region_row0.p;
     t.ring_start = c->ring_start.p;
@@ -556,7 +555,6 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
     ctx->R = n_regions;
     ctx->n_rows = n_rows;
     ctx->n_rings = n_rings;
-    ctx->n_uniq = n_rows;
     ctx->h_xy_rows.assign(xy, xy + (size_t)n_rows * 2);
     ctx->h_ring_start.assign(ring_start, ring_start + n_rings + 1);
     ctx->h_region_ring0 = reg_ring0;

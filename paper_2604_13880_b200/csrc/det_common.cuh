@@ -49,7 +49,7 @@ struct Params {
 };
 
 struct Topo {
-    int n_rows, n_uniq, R;
+    int n_rows, R;
     const int* region_row0;   // R+1: first vertex row of each region (regions' rows are contiguous)
     const int* ring_start;    // n_rings+1: first vertex row of each ring
     const int* region_ring0;  // R+1: first ring of each region (a region's rings are contiguous)

@@ -20,16 +20,15 @@ float64 expressions so the target weights are bit-identical.
 from __future__ import annotations
 
 import itertools
-from dataclasses import dataclass, field, replace
-
 import time
+from dataclasses import dataclass, field, replace
 
 import numpy as np
 
 from ._context import get_context, region_ranks
 from ._lib import STOP_BDV, STOP_COLLAPSED, STOP_NAMES, STOP_NEGINDEX
 from .errors import NumericError, RasterizationError, RegionCollapsedError
-from .geomodel import deferred_rebuild, densify, rebuild, rebuild_fast, ring_layout, ring_sizes
+from .geomodel import deferred_rebuild, densify, rebuild, ring_layout
 from .raster import LabelTexture, _LazyLabels, rasterize_labels
 
 DENSIFY_EDGE_PIXELS = 4.0

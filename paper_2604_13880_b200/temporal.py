@@ -27,10 +27,9 @@ import numpy as np
 
 from ._context import get_context, region_ranks
 from ._lib import DET_E_RASTER, STOP_BDV, STOP_COLLAPSED, STOP_NAMES, STOP_NEGINDEX
-from .engine import (DENSIFY_EDGE_PIXELS, BatchEngine, CartogramEngine, CartogramState, IterationRecord, RunResult,
-                     StoppingCriteria, trace_records)
+from .engine import DENSIFY_EDGE_PIXELS, BatchEngine, CartogramState, RunResult, StoppingCriteria, trace_records
 from .errors import CartomorphError, IngestionError, RasterizationError, RegionCollapsedError
-from .geomodel import deferred_rebuild, densify, rebuild, rebuild_fast, ring_layout
+from .geomodel import deferred_rebuild, densify, ring_layout
 from .metrics import frame_reports
 from .raster import LabelTexture, _LazyLabels, rasterize_labels
 

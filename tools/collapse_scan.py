@@ -1,7 +1,6 @@
 """Diagnostic: first-collapse iteration of headline-size maps under several statistic spreads (GPU)."""
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
 import paper_2604_13880_b200 as P
 from paper_2604_13880_b200.synthetic import voronoi_map, random_walk
 

@@ -1,9 +1,7 @@
 """Phase timing of the end-to-end public-API call (BatchEngine.run_all) on the headline workload."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
 import paper_2604_13880_b200 as P
-from paper_2604_13880_b200 import engine as E
 from paper_2604_13880_b200.synthetic import config_map, random_walk
 
 m, prm = config_map("headline")

@@ -1,7 +1,6 @@
 """Wall time of the transition modes on BASELINE config 2 (cumulative, 12 x 100) and a direct run."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
 import paper_2604_13880_b200 as P
 from paper_2604_13880_b200.synthetic import config_map, random_walk
 
