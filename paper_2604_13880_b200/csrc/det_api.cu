@@ -63,7 +63,7 @@ struct det_ctx {
     // topology
     int R = 0, n_rows = 0, n_rings = 0;
     std::vector<int> h_ring_start, h_region_ring0;
-    std::vector<double> h_xy_rows;
+    DVec<double2> xy_rows;  // the loaded vertex rows, device resident (start geometry of every batch)
     DVec<int> region_row0, region_rank, rank_region, ring_start, region_ring0;
     // batch
     int B = 0, cap = 64, nb = 0, trace_cap = 0;
@@ -555,7 +555,8 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
     ctx->R = n_regions;
     ctx->n_rows = n_rows;
     ctx->n_rings = n_rings;
-    ctx->h_xy_rows.assign(xy, xy + (size_t)n_rows * 2);
+    CK(ctx->xy_rows.alloc(n_rows));
+    CK(cudaMemcpyAsync(ctx->xy_rows.p, xy, (size_t)n_rows * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
     ctx->h_ring_start.assign(ring_start, ring_start + n_rings + 1);
     ctx->h_region_ring0 = reg_ring0;
     CK(ctx->region_row0.alloc(n_regions + 1));
@@ -585,7 +586,7 @@ int det_set_batch(det_ctx* ctx, int batch, const double* xy, const double* stats
     if (xy) {
         CK(cudaMemcpyAsync(ctx->pos_init.p, xy, (size_t)batch * rowb, cudaMemcpyHostToDevice, ctx->stream));
     } else {  // one upload of the loaded rows, replicated on the device
-        CK(cudaMemcpyAsync(ctx->pos_init.p, ctx->h_xy_rows.data(), rowb, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(ctx->pos_init.p, ctx->xy_rows.p, rowb, cudaMemcpyDeviceToDevice, ctx->stream));
         for (int b = 1; b < batch; ++b)
             CK(cudaMemcpyAsync(ctx->pos_init.p + (size_t)b * ctx->n_rows, ctx->pos_init.p, rowb, cudaMemcpyDeviceToDevice,
                                ctx->stream));
