@@ -53,6 +53,13 @@ def phase_bytes(n: int, n_unique: int, n_rows: int, n_regions: int) -> dict:
     }
 
 
+def timed_launches(steps: int, groups: int, batch: int) -> int:
+    """Our kernel launches in the timed region: 6 kernels (k_sat1/2/3, k_region, k_row, k_ctrl) per
+    frame group per iteration; full 16-iteration chunks run as a CUDA graph with min(groups, batch)
+    branches, the remainder eagerly over the whole batch."""
+    return 6 * (min(groups, batch) * 16 * (steps // 16) + steps % 16)
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -355,9 +362,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / e2e_steps,
                     "d2h_bytes_per_step": d2h / e2e_steps, "steps": e2e_steps,
                     "host_split": getattr(be, "last_timing", {})},
-            # 6 kernels (k_sat1/2/3, k_region, k_row, k_ctrl) per frame group per iteration: full 16-iteration
-            # chunks run as a CUDA graph with min(groups, batch) branches, the remainder eagerly
-            "gpu_launches": 6 * (min(args.groups, args.batch) * 16 * (args.steps // 16) + args.steps % 16),
+            "gpu_launches": timed_launches(args.steps, args.groups, args.batch),
             "iterations_executed": iters_total, "frames_active_after": int(act.sum()),
             "clocks": clk.summary(),
             "device": device_info(local),
