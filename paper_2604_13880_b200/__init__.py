@@ -19,6 +19,7 @@ from .displacement import (AnchorSet, DisplacementField, advect, anchors, base_m
 from .raster import BACKGROUND, DensityTexture, LabelTexture, build_density, default_bdv, rasterize_labels
 from .metrics import (QualityReport, cartographic_errors, full_report, hamming_distance, relative_position_error,
                       shape_distortion, topology_distortion)
+from .sweep import sweep_bdv
 from .temporal import (AreaFractionPolicy, Frame, FrameSequence, TimeSeriesDataset, background_mass_schedule,
                        interpolate_frames, interpolate_vertices, run_cumulative, run_direct)
 

@@ -231,6 +231,21 @@ def main():
         sv[f"f{t}_xy"] = carto.vertex_array()
         sv[f"f{t}_stop"] = np.array(res.stop_reason)
     np.savez_compressed(os.path.join(OUT, "service_frames.npz"), **sv)
+
+    # 10. the bdv multiplier sweep of cli.py:265-300 (engine + report per multiplier, CSV rows)
+    msw = fm.small_voronoi(seed=21, r=12, target=500, shuffle_ids=False)
+    rsw = to_reference_map(cm, msw)
+    sw = dict(fm.pack_map(msw))
+    rows = []
+    for mult in [0.5, 1.0, 1.7]:
+        eng = cm.CartogramEngine(rsw, criteria=cm.StoppingCriteria(0.01, 32, 15), k=6, bdv_multiplier=mult)
+        res = eng.run()
+        weights = rsw.statistics() / (eng.total_statistic + eng.background_mass)
+        rep = cmet.full_report(eng.initial_map, res.state.mapmodel, weights=weights, raster_k=6, wall_ms=0.0)
+        rows.append(f"{mult:.6g},{res.stop_reason},{res.state.iteration},{res.state.xi:.9g},{res.state.epsilon:.9g},"
+                    f"{rep.tau:.9g},{rep.hamming_avg:.9g},{rep.hamming_max:.9g},{rep.position_error:.9g}")
+    sw["rows"] = np.array(rows)
+    np.savez_compressed(os.path.join(OUT, "sweep.npz"), **sw)
     print("golden fixtures written to", OUT)
 
 
