@@ -9,6 +9,9 @@ import paper_2604_13880_b200 as P  # noqa: E402
 from paper_2604_13880_b200.synthetic import config_map  # noqa: E402
 
 m, prm = config_map(sys.argv[1] if len(sys.argv) > 1 else "headline")
+if len(sys.argv) > 2:  # band height override for the experiment
+    from paper_2604_13880_b200._context import get_context
+    get_context(prm["k"]).set_band_height(int(sys.argv[2]))
 crit = P.StoppingCriteria(1e-300, 10**9, 200)
 P.CartogramEngine(m, criteria=crit, k=prm["k"]).run()  # warm (allocation, graph capture)
 out = {}
