@@ -154,8 +154,41 @@ def temporal_stress(budget, seed0):
     return out
 
 
+def polygon_stress(budget, seed0):
+    """Random star / self-intersecting rings, holes, overlapping regions, shuffled ids, k 4..9:
+    GPU labels vs oracle labels (bit-exact), or the same ValueError."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_live_reference import _random_map
+
+    t0 = time.perf_counter()
+    out = {"polygon_cases": 0, "raised_both": 0, "polygon_mismatch": None}
+    i = 0
+    while time.perf_counter() - t0 < budget and out["polygon_mismatch"] is None:
+        r = np.random.default_rng(seed0 + 31337 * i)
+        i += 1
+        m = _random_map(r, int(r.integers(1, 12)))
+        k = int(r.integers(4, 10))
+        try:
+            want = O.FlatMap.from_mapmodel(m).labels(k)
+        except ValueError:
+            try:
+                P.rasterize_labels(m, k, check_collapse=False)
+                out["polygon_mismatch"] = {"case": i, "kind": "oracle raised, gpu did not"}
+            except ValueError:
+                out["raised_both"] += 1
+            continue
+        got = np.asarray(P.rasterize_labels(m, k, check_collapse=False).labels)
+        out["polygon_cases"] += 1
+        if not np.array_equal(got, want):
+            out["polygon_mismatch"] = {"case": i, "k": k, "pixels": int((got != want).sum())}
+    return out
+
+
 def main():
     budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
+    if len(sys.argv) > 2 and sys.argv[2] == "polygons":
+        print(json.dumps(polygon_stress(budget, int(time.time()) % 100000)))
+        return
     if len(sys.argv) > 2 and sys.argv[2] == "temporal":
         print(json.dumps(temporal_stress(budget, int(time.time()) % 100000)))
         return
