@@ -67,7 +67,9 @@ struct det_ctx {
     DVec<int> region_row0, region_rank, rank_region, ring_start, region_ring0;
     // batch
     int B = 0, cap = 64, nb = 0, trace_cap = 0;
-    DVec<double2> pos_init, pos0, pos1, best;
+    // pos0/pos1/best hold float2 rows on the float32-field path (sized as double2 either way);
+    // rows64 is the widened copy of a float state handed to the read-back / area paths
+    DVec<double2> pos_init, pos0, pos1, best, rows64;
     DVec<int> labels, cnt_acc, cnt_state, rowcnt, maxspan, rowdone;
     DVec<unsigned long long> spans;
     DVec<float> lutf;
@@ -168,7 +170,8 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     const size_t lut_b = luts ? (size_t)lut_smem_len(R) * sa : 0;
     // + the label ring (lab_kp rows of NT*CPT ints) when reading labels
     const size_t ring_b = (src == SRC_LABELS && f32) ? (size_t)lab_kp(CPT * NT) * NT * CPT * sizeof(int) : 0;
-    const size_t smem1 = ((size_t)2 * (n + H - 1) + (size_t)H * (NT / 32)) * sa + ring_b + 16;
+    const size_t ring1_b = (src == SRC_LABELS && f32) ? (size_t)lab_kp1(CPT * NT) * NT * CPT * sizeof(int) : 0;
+    const size_t smem1 = ((size_t)2 * (n + H - 1) + (size_t)H * (NT / 32)) * sa + ring1_b + 16;
 #define DET_SAT1(SRC_, A_, L_)                                                                               \
     do {                                                                                                     \
         auto fn = k_sat1<CPT, NT, SRC_, A_, L_>;                                                             \
@@ -229,9 +232,11 @@ static void launch_sat(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S
     }
 }
 
-static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, int gate, int src) {
+// f64_rows: rasterise double2 rows (the start geometry) whatever the context's field type
+static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, int gate, int src,
+                          bool f64_rows = false) {
     const dim3 g((c->R + RW_WARPS - 1) / RW_WARPS, c->B);
-    if (c->f64) k_region<double><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
+    if (c->f64 || f64_rows) k_region<double><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
     else k_region<float><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
 }
 
@@ -370,6 +375,7 @@ static int alloc_batch(det_ctx* ctx, int B) {
     CK(ctx->pos0.alloc((size_t)B * ctx->n_rows));
     CK(ctx->pos1.alloc((size_t)B * ctx->n_rows));
     CK(ctx->best.alloc((size_t)B * ctx->n_rows));
+    if (!ctx->f64) CK(ctx->rows64.alloc((size_t)B * ctx->n_rows));
     CK(ctx->labels.alloc((size_t)B * nn));
     CK(ctx->cnt_acc.alloc((size_t)B * (ctx->R + 1)));
     CK(ctx->cnt_state.alloc((size_t)B * (ctx->R + 1)));
@@ -401,13 +407,21 @@ static int alloc_batch(det_ctx* ctx, int B) {
 // capacity until no row overflows.  Leaves the counts in cnt_acc.
 static int raster_start(det_ctx* ctx) {
     for (int attempt = 0; attempt < 8; ++attempt) {
-        CK(cudaMemcpyAsync(ctx->pos0.p, ctx->pos_init.p, (size_t)ctx->B * ctx->n_rows * sizeof(double2),
-                           cudaMemcpyDeviceToDevice, ctx->stream));
+        const long long nrow = (long long)ctx->B * ctx->n_rows;
+        if (ctx->f64) {
+            CK(cudaMemcpyAsync(ctx->pos0.p, ctx->pos_init.p, (size_t)nrow * sizeof(double2), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+        } else {  // float32 state: the start rows rounded once; the start raster stays on the exact rows
+            k_rows_to_f32<<<(unsigned)std::min<long long>((nrow + 255) / 256, 4096), 256, 0, ctx->stream>>>(
+                ctx->pos_init.p, nrow, reinterpret_cast<float2*>(ctx->pos0.p));
+        }
         const Topo T = make_topo(ctx);
         const Bufs D = make_bufs(ctx);
+        Bufs D0 = D;
+        D0.pos0 = ctx->pos_init.p;
         k_init_state<<<(ctx->B + 127) / 128, 128, 0, ctx->stream>>>(D);
         CK(cudaMemsetAsync(ctx->cnt_acc.p, 0, (size_t)ctx->B * (ctx->R + 1) * sizeof(int), ctx->stream));
-        launch_region(ctx, T, D, M_RASTER, G_ALWAYS, 0);
+        launch_region(ctx, T, D0, M_RASTER, G_ALWAYS, 0, true);
         launch_row(ctx, T, D, G_ALWAYS, -1);
         CK(cudaGetLastError());
         std::vector<Carto> hs(ctx->B);
@@ -926,7 +940,13 @@ static const double2* state_rows(det_ctx* ctx, int b) {
     const size_t off = (size_t)b * ctx->n_rows;
     if (!ctx->ran) return ctx->pos_init.p + off;
     const int src = result_src(ctx, b);
-    return (src == 2 ? ctx->best.p : (src == 1 ? ctx->pos1.p : ctx->pos0.p)) + off;
+    const double2* p = (src == 2 ? ctx->best.p : (src == 1 ? ctx->pos1.p : ctx->pos0.p));
+    if (ctx->f64) return p + off;
+    // float32 state: widen cartogram b's rows into its slot of rows64 (stream-ordered)
+    if (ctx->rows64.alloc((size_t)ctx->B * ctx->n_rows) != cudaSuccess) return nullptr;
+    k_rows_to_f64<<<(unsigned)std::min<int>((ctx->n_rows + 255) / 256, 2048), 256, 0, ctx->stream>>>(
+        reinterpret_cast<const float2*>(p) + off, ctx->n_rows, ctx->rows64.p + off);
+    return ctx->rows64.p + off;
 }
 
 int det_get_vertices(det_ctx* ctx, int b, double* xy_out) {

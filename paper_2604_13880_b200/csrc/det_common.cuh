@@ -61,9 +61,11 @@ struct Bufs {
     int B, n, k, cap, H, nb;
     int b0;           // first cartogram of this launch (frame groups run as parallel graph branches)
     size_t nn;
-    double2* pos0;
-    double2* pos1;
-    double2* best;
+    // vertex rows (ping-pong state + best state): double2 on the float64-field path, float2 on
+    // the float32-field path (k_region<UT> reads them as Vec2<UT>)
+    void* pos0;
+    void* pos1;
+    void* best;
     int* labels;
     int* cnt_acc;
     int* cnt_state;
@@ -115,6 +117,11 @@ __device__ __forceinline__ int ceil_to_int(double v) {
 }
 __device__ __forceinline__ int floor_to_int(double v) {
     return (int)(unsigned)__double_as_longlong(__dadd_rd(v, ROUND_MAGIC));
+}
+// ceil(v) for a float with -1 < v < 2^22 (the scaled texture range): adding 1.5*2^23 in
+// round-up mode leaves ceil(v) in the low mantissa bits -- FP32 pipe only
+__device__ __forceinline__ int ceil_to_int_f(float v) {
+    return __float_as_int(__fadd_ru(v, 12582912.0f)) - 0x4B400000;
 }
 __device__ __forceinline__ double floor_exact(double v) {  // floor(v) as a double, FP64 pipe only
     return __dsub_rn(__dadd_rd(v, ROUND_MAGIC), ROUND_MAGIC);

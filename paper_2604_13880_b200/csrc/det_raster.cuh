@@ -129,6 +129,36 @@ __device__ __forceinline__ double2 field_blend(const Texels<UT>& x, const TP& t)
     return make_double2((double)sx, (double)sy);
 }
 
+// float state path: the same blend, result kept in float (the position update is a float add)
+__device__ __forceinline__ float2 field_blend_f(const Texels<float>& x, const TapF& t) {
+    const float gxm = 1.0f - t.fx, gym = 1.0f - t.fy;
+    const float sx = x.v[0] * gxm * gym + x.v[2] * t.fx * gym + x.v[4] * gxm * t.fy + x.v[6] * t.fx * t.fy;
+    const float sy = x.v[1] * gxm * gym + x.v[3] * t.fx * gym + x.v[5] * gxm * t.fy + x.v[7] * t.fx * t.fy;
+    return make_float2(sx, sy);
+}
+
+// Tap of a float position: p*n is exact (n a power of two) and p*n - 0.5 is exact whenever it is
+// >= -0.25, so one FMA gives the reference's g; below that the tap clamps to column/row 0 with
+// fraction 0 either way.
+__device__ __forceinline__ TapF field_tap_pf(int n, float px, float py) {
+    constexpr float M = 12582912.0f;
+    const float nf = (float)n;
+    const float gx = fmaf(px, nf, -0.5f), gy = fmaf(py, nf, -0.5f);
+    const float tx = __fadd_rd(gx, M), ty = __fadd_rd(gy, M);
+    const int ix = min(max(__float_as_int(tx) - 0x4B400000, 0), n - 2);
+    const int iy = min(max(__float_as_int(ty) - 0x4B400000, 0), n - 2);
+    const float hi = (float)(n - 2);
+    TapF t;
+    t.fx = __saturatef(gx - fminf(fmaxf(tx - M, 0.0f), hi));
+    t.fy = __saturatef(gy - fminf(fmaxf(ty - M, 0.0f), hi));
+    t.o0 = (iy * n + ix) * 2;
+    t.o1 = t.o0 + n * 2;
+    return t;
+}
+
+__device__ __forceinline__ double2 to_d2(const double2& p) { return p; }
+__device__ __forceinline__ double2 to_d2(const float2& p) { return make_double2((double)p.x, (double)p.y); }
+
 template <typename UT>
 __device__ __forceinline__ double2 sample_field(const UT* __restrict__ uf, int n, double px, double py) {
     const Tap t = field_tap(n, px, py);
@@ -199,70 +229,101 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
         return v + 1 < e ? v + 1 : T.ring_start[q];
     };
 
-    const double2* __restrict__ pin;
-    double2* __restrict__ pout = nullptr;
+    // vertex rows: float64 on the float64-field path, float32 on the float32-field path
+    using PT = typename Vec2<UT>::type;
+    constexpr bool FS = sizeof(UT) == 4;
+    const PT* __restrict__ pin;
+    PT* __restrict__ pout = nullptr;
+    PT* __restrict__ pbest = reinterpret_cast<PT*>(D.best) + ub;
     bool bestcopy = false;
     if (mode & M_ADVECT) {
         const int cur = st->next_iter - 1;
-        pin = ((cur & 1) ? D.pos1 : D.pos0) + ub;
-        pout = ((cur & 1) ? D.pos0 : D.pos1) + ub;
+        pin = reinterpret_cast<const PT*>((cur & 1) ? D.pos1 : D.pos0) + ub;
+        pout = reinterpret_cast<PT*>((cur & 1) ? D.pos0 : D.pos1) + ub;
         bestcopy = st->best_pending != 0;
     } else {
-        pin = (src == 0 ? D.pos0 : (src == 1 ? D.pos1 : D.best)) + ub;
+        pin = reinterpret_cast<const PT*>(src == 0 ? D.pos0 : (src == 1 ? D.pos1 : D.best)) + ub;
     }
-    const double2* gpos = (mode & M_ADVECT) ? pout : pin;  // row positions for huge regions
+    const PT* gpos = (mode & M_ADVECT) ? pout : pin;  // row positions for huge regions
     const UT* uf = reinterpret_cast<const UT*>(D.uf) + (size_t)b * D.nn * 2;
 
-    // ---- phase A: advect every vertex row (RW_UNROLL rows in flight per lane); per-row
-    //      scaled coordinates and scanline / column indices for the raster ----
+    // ---- phase A: advect every vertex row (Q rows in flight per lane); per-row scaled
+    //      coordinates and scanline / column indices for the raster ----
     int jmn = n, jmx = 0, imn = n, imx = 0;
     int ncl = 0;
-    for (int base = row0; base < row1; base += 32 * RW_UNROLL) {
-        double2 p[RW_UNROLL];
+    auto chunk = [&](auto QC, int base) {
+        constexpr int Q = decltype(QC)::value;
+        PT p[Q];
 #pragma unroll
-        for (int q = 0; q < RW_UNROLL; ++q) {
+        for (int q = 0; q < Q; ++q) {
             const int v = base + q * 32 + lane;
-            p[q] = v < row1 ? pin[v] : make_double2(0.5, 0.5);
+            p[q] = v < row1 ? pin[v] : PT{0.5, 0.5};
         }
-        double2 nq[RW_UNROLL];
+        PT nq[Q];
         if (mode & M_ADVECT) {
-            using TP = typename std::conditional<sizeof(UT) == 4, TapF, Tap>::type;
-            TP tp[RW_UNROLL];
-            Texels<UT> tx[RW_UNROLL];
+            if constexpr (FS) {
+                // float state: tap, blend, update and clamp in float32
+                TapF tp[Q];
+                Texels<float> tx[Q];
 #pragma unroll
-            for (int q = 0; q < RW_UNROLL; ++q) {
-                if constexpr (sizeof(UT) == 4) tp[q] = field_tap_f(n, p[q].x, p[q].y);
-                else tp[q] = field_tap(n, p[q].x, p[q].y);
-                tx[q] = field_load<UT, TP>(uf, tp[q]);
-            }
+                for (int q = 0; q < Q; ++q) {
+                    tp[q] = field_tap_pf(n, p[q].x, p[q].y);
+                    tx[q] = field_load<float, TapF>(reinterpret_cast<const float*>(uf), tp[q]);
+                }
 #pragma unroll
-            for (int q = 0; q < RW_UNROLL; ++q) {
-                const double2 s = field_blend<UT, TP>(tx[q], tp[q]);
-                const double mx = p[q].x + s.x, my = p[q].y + s.y;
-                const double cx = mx < 0.0 ? 0.0 : (mx > 1.0 ? 1.0 : mx);  // np.clip (no NaNs here)
-                const double cy = my < 0.0 ? 0.0 : (my > 1.0 ? 1.0 : my);
-                const int v = base + q * 32 + lane;
-                if (v < row1) ncl += (cx != mx) + (cy != my);
-                nq[q] = make_double2(cx, cy);
+                for (int q = 0; q < Q; ++q) {
+                    const float2 s = field_blend_f(tx[q], tp[q]);
+                    const float mx = p[q].x + s.x, my = p[q].y + s.y;
+                    const float cx = mx < 0.0f ? 0.0f : (mx > 1.0f ? 1.0f : mx);  // np.clip (no NaNs here)
+                    const float cy = my < 0.0f ? 0.0f : (my > 1.0f ? 1.0f : my);
+                    const int v = base + q * 32 + lane;
+                    if (v < row1) ncl += (cx != mx) + (cy != my);
+                    nq[q] = PT{cx, cy};
+                }
+            } else {
+                Tap tp[Q];
+                Texels<UT> tx[Q];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    tp[q] = field_tap(n, (double)p[q].x, (double)p[q].y);
+                    tx[q] = field_load<UT, Tap>(uf, tp[q]);
+                }
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    const double2 s = field_blend<UT, Tap>(tx[q], tp[q]);
+                    const double mx = p[q].x + s.x, my = p[q].y + s.y;
+                    const double cx = mx < 0.0 ? 0.0 : (mx > 1.0 ? 1.0 : mx);  // np.clip (no NaNs here)
+                    const double cy = my < 0.0 ? 0.0 : (my > 1.0 ? 1.0 : my);
+                    const int v = base + q * 32 + lane;
+                    if (v < row1) ncl += (cx != mx) + (cy != my);
+                    nq[q] = PT{cx, cy};
+                }
             }
         } else {
 #pragma unroll
-            for (int q = 0; q < RW_UNROLL; ++q) nq[q] = p[q];
+            for (int q = 0; q < Q; ++q) nq[q] = p[q];
         }
 #pragma unroll
-        for (int q = 0; q < RW_UNROLL; ++q) {
+        for (int q = 0; q < Q; ++q) {
             const int v = base + q * 32 + lane;
             if (v >= row1) continue;
             if (mode & M_ADVECT) {
                 pout[v] = nq[q];
-                if (bestcopy) D.best[ub + v] = p[q];
+                if (bestcopy) pbest[v] = p[q];
             }
             // x*n, y*n are exact (n is a power of two); ceil is monotone, so the crop
             // (raster.py:71-74) and each edge's scanline range (raster.py:45-46) are
             // min/max of these per-row integers
-            const double xs = __dmul_rn(nq[q].x, nd), ys = __dmul_rn(nq[q].y, nd);
-            const int jr = min(max(ceil_to_int(__dsub_rn(ys, 0.5)), 0), n);
-            const int ir = min(max(ceil_to_int(__dsub_rn(xs, 0.5)), 0), n);
+            int jr, ir;
+            if constexpr (FS) {  // y*n - 0.5 is exact in float wherever its ceil is not 0
+                const float nf = (float)n;
+                jr = min(max(ceil_to_int_f(nq[q].y * nf - 0.5f), 0), n);
+                ir = min(max(ceil_to_int_f(nq[q].x * nf - 0.5f), 0), n);
+            } else {
+                const double xs = __dmul_rn(nq[q].x, nd), ys = __dmul_rn(nq[q].y, nd);
+                jr = min(max(ceil_to_int(__dsub_rn(ys, 0.5)), 0), n);
+                ir = min(max(ceil_to_int(__dsub_rn(xs, 0.5)), 0), n);
+            }
             if (in_smem) {
                 sjr[v - row0] = jr;
                 snx[v - row0] = (uint16_t)(next_row(v) - row0);
@@ -270,7 +331,12 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
             jmn = min(jmn, jr); jmx = max(jmx, jr);
             imn = min(imn, ir); imx = max(imx, ir);
         }
-    }
+    };
+    // full rounds of RW_UNROLL rows per lane while more than one warp of rows remains, then a
+    // one-row tail (no lane slots idle for a whole extra round)
+    int base = row0;
+    for (; base + 32 < row1; base += 32 * RW_UNROLL) chunk(std::integral_constant<int, RW_UNROLL>{}, base);
+    if (base < row1) chunk(std::integral_constant<int, 1>{}, base);
     if (mode & M_ADVECT) {
         ncl = warp_sum(ncl);
         if (lane == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
@@ -337,7 +403,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
             auto run = [&](uint32_t ent) {
                 const int el = (int)(ent & 0xFFFFu), en = (int)(ent >> 16);
                 const int ja = sjr[el], jb2 = sjr[en];
-                emit(gpos[row0 + el], gpos[row0 + en], max(min(ja, jb2), w0), min(max(ja, jb2), w1 + back));
+                emit(to_d2(gpos[row0 + el]), to_d2(gpos[row0 + en]), max(min(ja, jb2), w0), min(max(ja, jb2), w1 + back));
             };
             for (int e0 = 0; e0 < nrows; e0 += 32) {
                 const int el = e0 + lane;
@@ -362,7 +428,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
         } else {
             for (int e = row0 + lane; e < row1; e += 32) {
                 const int en = next_row(e) - row0;
-                const double2 a = gpos[e], c = gpos[row0 + en];
+                const double2 a = to_d2(gpos[e]), c = to_d2(gpos[row0 + en]);
                 const int ja = min(max(ceil_to_int(__dsub_rn(__dmul_rn(a.y, nd), 0.5)), 0), n);
                 const int jb2 = min(max(ceil_to_int(__dsub_rn(__dmul_rn(c.y, nd), 0.5)), 0), n);
                 const int js = max(min(ja, jb2), w0);  // scanlines j in [jlo, jhi) are crossed
@@ -535,6 +601,19 @@ __global__ void k_interpolate(const double* __restrict__ a, const double* __rest
         const long long e = i - (long long)f * len;
         out[i] = __dadd_rn(a[e], __dmul_rn(fr[f], __dsub_rn(b[e], a[e])));
     }
+}
+
+// Vertex-row format conversions of the float32-field path's float2 state (load: round to nearest;
+// read-back: exact widening).
+__global__ void k_rows_to_f32(const double2* __restrict__ in, long long len, float2* __restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x) {
+        const double2 p = in[i];
+        out[i] = make_float2(__double2float_rn(p.x), __double2float_rn(p.y));
+    }
+}
+__global__ void k_rows_to_f64(const float2* __restrict__ in, long long len, double2* __restrict__ out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x)
+        out[i] = to_d2(in[i]);
 }
 
 // Rank texture -> region-index texture (output format of rasterize_labels).

@@ -99,11 +99,18 @@ __host__ __device__ __forceinline__ int lut_smem_len(int R) { return (R + 2) & ~
 // ring slots (prefetch distance KP - 1 rows): 4, or 2 for 8192-column rows, whose ring would
 // not fit next to the carry windows in one CTA's shared memory
 __host__ __device__ constexpr int lab_kp(int cols) { return cols >= 8192 ? 2 : 4; }
+// k_sat1 takes each row one iteration early (its LUT gathers overlap the previous row), so it keeps
+// a deeper ring where shared memory allows
+__host__ __device__ constexpr int lab_kp1(int cols) { return cols >= 8192 ? 2 : (cols >= 4096 ? 4 : 6); }
 
 // first 16-byte aligned int slot at or after p (cp.async 16-byte copies and int4 reads)
+// (offset arithmetic on the pointer itself, so the compiler keeps it in the shared window: LDS,
+// not generic LD, for the ring reads)
 template <typename T>
 __device__ __forceinline__ int* align16(T* p) {
-    return reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+    char* c = reinterpret_cast<char*>(p);
+    const unsigned mis = (unsigned)(reinterpret_cast<uintptr_t>(c) & 15u);
+    return reinterpret_cast<int*>(c + ((16u - mis) & 15u));
 }
 
 template <int CPT, int KP>
@@ -235,8 +242,8 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
     // labels through the shared-memory ring on the float path (the float64 path's carry windows
     // leave no room for it at 8192 columns); register prefetch otherwise
     constexpr bool RING = SRC == SRC_LABELS && sizeof(A) == 4;
-    __shared__ uint64_t s_bar[4];
-    LabelRing<CPT, lab_kp(CPT * NT)> ring;
+    __shared__ uint64_t s_bar[6];
+    LabelRing<CPT, lab_kp1(CPT * NT)> ring;
     if (RING) {
         ring.q = align16(s_rows + H * NW);
         ring.bar = s_bar;
@@ -255,17 +262,18 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
 #pragma unroll
     for (int k = 0; k < CPT; ++k) cs[k] = pd[k] = pa[k] = (A)0;
 
+    // densities one row ahead: row j+1's label wait and LUT gathers are issued before row j's work
     A rho_n[CPT];
-    if (!RING) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, jt, x0, rho_n);
+    if (RING) ring.take(jt, lut, R, rho_n);
+    else load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, jt, x0, rho_n);
     int slot = 0, ps = 2;  // rotating boundary slots: (j - jt) % 3, (j - jt + 2) % 3
     for (int j = jt; j <= jb; ++j) {
         A rho[CPT];
-        if (RING) {
-            ring.take(j, lut, R, rho);
-        } else {
 #pragma unroll
-            for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
-            if (j < jb) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, j + 1, x0, rho_n);  // prefetch the next row
+        for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
+        if (j < jb) {
+            if (RING) ring.take(j + 1, lut, R, rho_n);  // refills row j's slot: every take(j) preceded barrier j-1
+            else load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, j + 1, x0, rho_n);
         }
         A ts = (A)0;
 #pragma unroll
@@ -285,7 +293,9 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
             cs[k] += rho[k];
         }
         if (j < jb) {
-            if (x0 <= n - 1 && n - 1 < x0 + CPT) dg[n - 1 - j + jb] = nd_[n - 1 - x0];  // diagonal leaves right edge
+            // diagonal leaves the right edge: n is a multiple of CPT, so column n-1 is the last
+            // column of thread n/CPT - 1 (a static register index -- no local-memory array)
+            if (x0 == n - CPT) dg[n - 1 - j + jb] = nd_[CPT - 1];
             if (x0 == 0) ad[j - jt] = na_[0];                                           // anti-diagonal leaves left edge
         }
         if (lane == 31) s_bd[slot][w] = nd_[CPT - 1];
@@ -456,19 +466,29 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
     const A* lut = band_lut<A, LUTS>(D, R, b, s_lut);
     // cc[k]: column-total average cavg(x) = (colfull(x) + colfull(x+1))/2 for the field,
     // colfull(x+1) for the channel dump
+    // PF (float32 field): al[k] carries the column-pair sum alpha(j-1, x-1) + alpha(j-1, x) instead
+    // of alpha itself -- each thread advances it from its own row prefixes, so the straight
+    // channel needs no neighbour exchange and a = (pair(j-1) + pair(j)) / 4
+    constexpr bool PF = OUT == OUT_U && sizeof(A) == 4;
     A ul[CPT], al[CPT], cc[CPT], ur[CPT];
+    A al_left = (PF && x0 > 0 && active) ? (A)D.csX[bb * n + x0 - 1] : (A)0;
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
         const int x = x0 + k;
         const bool in = x < n;
         al[k] = in ? (A)D.csX[bb * n + x] : (A)0;
+        if (PF) {
+            const A t = al[k];
+            al[k] = al_left + t;
+            al_left = t;
+        }
         ul[k] = in ? (A)D.dgXc[bb * n + x] : (A)0;
         const double cfi = in ? csT[x] : 0.0, cfe = (in && x > 0) ? csT[x - 1] : 0.0;
         cc[k] = (A)(OUT == OUT_CH8 ? cfi : 0.5 * (cfe + cfi));
         ur[k] = (A)0;
     }
     if (lane == 31) {  // boundary values of "row jt-1" = carries
-        s_xa[2][w] = al[CPT - 1];
+        if (!PF) s_xa[2][w] = al[CPT - 1];
         s_xu1[2][w] = ul[CPT - 1];
         s_xu2[2][w] = ul[CPT - 2];
     }
@@ -524,13 +544,13 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
         wt = warp_incl_scan_t<A>(wt);
         const A woff = __shfl_sync(FULL, wt, (w + 31) & 31);
         const A excl = (w == 0 ? (A)0 : woff) + winc - tsum;
-        A ap_m1 = __shfl_up_sync(FULL, al[CPT - 1], 1);
+        A ap_m1 = PF ? (A)0 : __shfl_up_sync(FULL, al[CPT - 1], 1);
         A ul_m1 = __shfl_up_sync(FULL, ul[CPT - 1], 1);
         A ul_m2 = __shfl_up_sync(FULL, ul[CPT - 2], 1);
         A ur_p = __shfl_down_sync(FULL, ur[0], 1);
         if (lane == 0) {
             if (w == 0) { ap_m1 = (A)0; ul_m1 = (A)0; ul_m2 = (A)0; }
-            else { ap_m1 = s_xa[ps][w - 1]; ul_m1 = s_xu1[ps][w - 1]; ul_m2 = s_xu2[ps][w - 1]; }
+            else { if (!PF) ap_m1 = s_xa[ps][w - 1]; ul_m1 = s_xu1[ps][w - 1]; ul_m2 = s_xu2[ps][w - 1]; }
         }
         if (lane == 31) ur_p = (w == NW - 1) ? s_rc[2 * H + (j - jt)] : s_xr[ps][w + 1];
         A Av[CPT], an[CPT], uln[CPT], urn[CPT];
@@ -538,13 +558,16 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
         for (int k = 0; k < CPT; ++k) Av[k] = excl + loc[k];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) {
-            an[k] = al[k] + Av[k];
+            // PF: the new column-pair sum (A(j, x-1) + A(j, x) added; A(j, x0-1) = excl)
+            an[k] = PF ? al[k] + ((k == 0 ? excl : Av[k - 1]) + Av[k]) : al[k] + Av[k];
             uln[k] = Av[k] + (k == 0 ? ul_m1 : ul[k - 1]);
             urn[k] = Av[k] + (k == CPT - 1 ? ur_p : ur[k + 1]);
         }
         if (active) {
             const A ravg = s_rc[j - jt], rf1 = s_rc[H + (j - jt)];
             const A yc = (A)j * inv_n + half_n;  // (j + 0.5) / n, exact in A
+            // PF row constants: y - 1, (1 - 2y) / 4, ravg - C
+            const A ycm1 = yc - (A)1, c1y = (A)0.25 - (A)0.5 * yc, rmc = ravg - Cr;
             const int wi0 = j + x0 - (jt - 1);
             A dlw[CPT + 1];  // DLtot(j + x - 1 + q), sliding window over this thread's columns
 #pragma unroll
@@ -581,6 +604,30 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
                     ch[5 * nn] = bt;
                     ch[6 * nn] = gt;
                     ch[7 * nn] = dt;
+                } else if constexpr (PF) {
+                    // the same anchor combination with the case splits of displacement.py:62,67 as
+                    // min/max: with e = x + y - 1 and d = x - y,
+                    //   q2x = q4y = 1 + min(e, 0),  q2y = q4x = max(e, 0),  q3 = (max(d, 0), max(-d, 0))
+                    const A a4 = al[k] + an[k];  // 4a
+                    const A cavg = cc[k];
+                    const A xc = xc0 + (A)k * inv_n;
+                    const A e = xc + ycm1, d = xc - yc;
+                    const A mn = fminf(e, (A)0), mx = fmaxf(e, (A)0);
+                    const A dp = fmaxf(d, (A)0), dn = fmaxf(-d, (A)0);
+                    const A nK = -(cavg + rmc);
+                    const A t = at + gt;
+                    A vx = fmaf(a4, c1y, cavg);
+                    vx = fmaf(cavg, mn, vx);
+                    vx = fmaf(ravg, mx, vx);
+                    vx = fmaf(nK, dp, vx);
+                    vx = fmaf(xc, t, vx);
+                    ux[k] = (vx + bt) * inv2m;
+                    A vy = fmaf(a4, fmaf(xc, (A)-0.5, (A)0.25), ravg);
+                    vy = fmaf(cavg, mx, vy);
+                    vy = fmaf(ravg, mn, vy);
+                    vy = fmaf(nK, dn, vy);
+                    vy = fmaf(yc, Cr - t, vy);
+                    uy[k] = (vy + at) * inv2m;
                 } else {
                     // anchor combination (displacement.py:128-130) with b = cavg-a, d = ravg-a,
                     // g = C-cavg-ravg+a, delta_t = C-at-bt-gt; since q1+q3 = (1+x-y, 1-x+y) and
@@ -613,7 +660,11 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
                 }
             }
         }
-        if (lane == 31) { s_xa[slot][w] = an[CPT - 1]; s_xu1[slot][w] = uln[CPT - 1]; s_xu2[slot][w] = uln[CPT - 2]; }
+        if (lane == 31) {
+            if (!PF) s_xa[slot][w] = an[CPT - 1];
+            s_xu1[slot][w] = uln[CPT - 1];
+            s_xu2[slot][w] = uln[CPT - 2];
+        }
         if (lane == 0) s_xr[slot][w] = urn[0];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) { al[k] = an[k]; ul[k] = uln[k]; ur[k] = urn[k]; }
