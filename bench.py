@@ -53,11 +53,18 @@ def phase_bytes(n: int, n_unique: int, n_rows: int, n_regions: int) -> dict:
     }
 
 
-def timed_launches(steps: int, groups: int, batch: int) -> int:
-    """Our kernel launches in the timed region: 6 kernels (k_sat1/2/3, k_region, k_row, k_ctrl) per
-    frame group per iteration; full 16-iteration chunks run as a CUDA graph with min(groups, batch)
-    branches, the remainder eagerly over the whole batch."""
-    return 6 * (min(groups, batch) * 16 * (steps // 16) + steps % 16)
+def kernels_per_iteration(field: str) -> int:
+    """k_sat1/2/3, k_region, k_row, k_ctrl, plus k_advect_rows on the float32 path (advect as its
+    own kernel when DET_SPLIT_ADVECT=1; fused into k_region by default)."""
+    split = field == "float32" and os.environ.get("DET_SPLIT_ADVECT", "0") == "1"
+    return 7 if split else 6
+
+
+def timed_launches(steps: int, groups: int, batch: int, per_iter: int = 7) -> int:
+    """Our kernel launches in the timed region: per_iter kernels per frame group per iteration;
+    full 16-iteration chunks run as a CUDA graph with min(groups, batch) branches, the remainder
+    eagerly over the whole batch."""
+    return per_iter * (min(groups, batch) * 16 * (steps // 16) + steps % 16)
 
 
 def load_peaks():
@@ -369,7 +376,7 @@ def main():
                     "d2h_bytes_per_step": d2h / e2e_steps, "steps": e2e_steps,
                     "runs_it_per_s": [e2e_steps * args.batch * world / t for t in e2e_runs],
                     "host_split": getattr(be, "last_timing", {})},
-            "gpu_launches": timed_launches(args.steps, args.groups, args.batch),
+            "gpu_launches": timed_launches(args.steps, args.groups, args.batch, kernels_per_iteration(args.field)),
             "iterations_executed": iters_total, "frames_active_after": int(act.sum()),
             "clocks": clk.summary(),
             "device": device_info(local),

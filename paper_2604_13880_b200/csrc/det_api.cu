@@ -88,6 +88,7 @@ struct det_ctx {
     bool g_valid = false;
     int groups = 8;  // graph branches (clamped to the batch); 1/2/4/8 measured 41.5/42.4/43.9/44.2k it/s
     bool sep_ctrl = true;  // control step as its own kernel (DET_SEP_CTRL=0: k_row's last CTA)
+    bool split_adv = false;  // float32 state: advect as the flat k_advect_rows (DET_SPLIT_ADVECT=1); 48.6k vs 51.4k fused
     Topo g_topo;  // launch signature the graph was captured with
     Bufs g_bufs;
     int g_groups = 0;
@@ -187,7 +188,10 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     }
 #undef DET_SAT1
     const int lanes = n + 2 * (2 * n - 1);
-    k_sat2<<<dim3((lanes + SAT2_THREADS - 1) / SAT2_THREADS + 1, B), SAT2_THREADS, 0, c->stream>>>(D, gate);
+    if (f32)  // float32 field: band carries split over the warps of a CTA (one memory round trip)
+        k_sat2p<<<dim3((lanes + 31) / 32 + 1, B), 32 * SAT2_PARTS, 0, c->stream>>>(D, gate);
+    else
+        k_sat2<<<dim3((lanes + SAT2_THREADS - 1) / SAT2_THREADS + 1, B), SAT2_THREADS, 0, c->stream>>>(D, gate);
     const size_t smem = ((size_t)3 * (n + H) + 3 * H + (H & 1)) * sa + lut_b + ring_b + 16;
 #define DET_SAT3(SRC_, UT_, OUT_, L_)                                                                        \
     do {                                                                                                     \
@@ -240,6 +244,19 @@ static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, in
     else k_region<float><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
 }
 
+// One iteration's advect + raster: the flat advect kernel then a raster-only k_region (float32
+// state), or k_region's fused advect phase.  Returns the number of kernels launched.
+static int launch_advect_raster(det_ctx* c, const Topo& T, const Bufs& D, int gate, int region_mode) {
+    if (!c->f64 && c->split_adv && (region_mode & M_ADVECT)) {
+        const int per = ADV_THREADS * ADV_RPT;
+        k_advect_rows<<<dim3((T.n_rows + per - 1) / per, c->B), ADV_THREADS, 0, c->stream>>>(T, D, gate);
+        if (region_mode & M_RASTER) launch_region(c, T, D, M_RASTER | M_POSTADV, gate, 0);
+        return (region_mode & M_RASTER) ? 2 : 1;
+    }
+    launch_region(c, T, D, region_mode, gate, 0);
+    return 1;
+}
+
 // ctrl_mode: -1 raster only, 0 loop evaluation, 1 final (best-state) evaluation
 static void launch_row(det_ctx* c, const Topo& T, const Bufs& D, int gate, int ctrl_mode) {
     // one warp per texture row; up to 8 rows per CTA within a 64 KB label-row budget
@@ -274,7 +291,7 @@ static void enqueue_iteration(det_ctx* c, int b0 = 0, int Bg = -1, cudaStream_t 
     SatSrc S;
     memset(&S, 0, sizeof(S));
     launch_sat(c, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, c->f64 != 0, Bg);
-    launch_region(c, T, D, M_ADVECT | M_RASTER, G_ACTIVE, 0);
+    launch_advect_raster(c, T, D, G_ACTIVE, M_ADVECT | M_RASTER);
     launch_row_ctrl(c, T, D, G_ACTIVE, 0);
     c->B = Bsave;
     c->stream = keep;
@@ -493,6 +510,7 @@ int det_ctx_create(int device, int k, int field_f64, det_ctx** out) {
     if (k < 4 || k > 13) return DET_E_ARG;
     det_ctx* ctx = new det_ctx();
     if (const char* e = getenv("DET_SEP_CTRL")) ctx->sep_ctrl = atoi(e) != 0;  // A/B switch (diagnostics)
+    if (const char* e = getenv("DET_SPLIT_ADVECT")) ctx->split_adv = atoi(e) != 0;  // A/B switch (diagnostics)
     ctx->device = device;
     ctx->k = k;
     ctx->n = 1 << k;
@@ -857,7 +875,7 @@ int det_bench_kernel_times(det_ctx* ctx, int iters, float* ms_out) {
         CK(cudaEventRecord(ev[0], ctx->stream));
         launch_sat(ctx, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, ctx->f64 != 0, ctx->B);
         CK(cudaEventRecord(ev[1], ctx->stream));
-        launch_region(ctx, T, D, region_mode, G_ACTIVE, 0);
+        launch_advect_raster(ctx, T, D, G_ACTIVE, region_mode);
         CK(cudaEventRecord(ev[2], ctx->stream));
         launch_row_ctrl(ctx, T, D, G_ACTIVE, row_mode);  // includes the control step
         CK(cudaEventRecord(ev[3], ctx->stream));

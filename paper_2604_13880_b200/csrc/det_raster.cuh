@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
         pin = reinterpret_cast<const PT*>((cur & 1) ? D.pos1 : D.pos0) + ub;
         pout = reinterpret_cast<PT*>((cur & 1) ? D.pos0 : D.pos1) + ub;
         bestcopy = st->best_pending != 0;
+    } else if (mode & M_POSTADV) {  // this iteration's advected rows (k_advect_rows output)
+        const int cur = st->next_iter - 1;
+        pin = reinterpret_cast<const PT*>((cur & 1) ? D.pos0 : D.pos1) + ub;
     } else {
         pin = reinterpret_cast<const PT*>(src == 0 ? D.pos0 : (src == 1 ? D.pos1 : D.best)) + ub;
     }
@@ -516,6 +519,54 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
     if (lane == 0) cnt[r] = area;  // provisional; k_row subtracts pixels lost to lower ranks
 }
 
+// Advect as its own flat kernel (float32 state): ADV_RPT rows per thread over the whole row range
+// of each cartogram (grid.y), every lane busy and ~64 warps per SM to cover the position -> texel
+// load chain; the same float arithmetic as k_region's phase A (displacement.py:209-238).
+constexpr int ADV_THREADS = 256;
+constexpr int ADV_RPT = 2;
+__global__ void __launch_bounds__(ADV_THREADS) k_advect_rows(Topo T, Bufs D, int gate) {
+    const int b = blockIdx.y + D.b0;
+    Carto* st = D.st + b;
+    if (!gate_open(st, gate)) return;
+    const int n = D.n;
+    const size_t ub = (size_t)b * T.n_rows;
+    const int cur = st->next_iter - 1;
+    const float2* __restrict__ pin = reinterpret_cast<const float2*>((cur & 1) ? D.pos1 : D.pos0) + ub;
+    float2* __restrict__ pout = reinterpret_cast<float2*>((cur & 1) ? D.pos0 : D.pos1) + ub;
+    float2* __restrict__ pbest = reinterpret_cast<float2*>(D.best) + ub;
+    const bool bestcopy = st->best_pending != 0;
+    const float* uf = reinterpret_cast<const float*>(D.uf) + (size_t)b * D.nn * 2;
+    const int v0 = blockIdx.x * (ADV_THREADS * ADV_RPT) + threadIdx.x;
+    float2 p[ADV_RPT];
+    TapF tp[ADV_RPT];
+    Texels<float> tx[ADV_RPT];
+#pragma unroll
+    for (int q = 0; q < ADV_RPT; ++q) {
+        const int v = v0 + q * ADV_THREADS;
+        p[q] = v < T.n_rows ? pin[v] : make_float2(0.5f, 0.5f);
+    }
+#pragma unroll
+    for (int q = 0; q < ADV_RPT; ++q) {
+        tp[q] = field_tap_pf(n, p[q].x, p[q].y);
+        tx[q] = field_load<float, TapF>(uf, tp[q]);
+    }
+    int ncl = 0;
+#pragma unroll
+    for (int q = 0; q < ADV_RPT; ++q) {
+        const int v = v0 + q * ADV_THREADS;
+        if (v >= T.n_rows) continue;
+        const float2 s = field_blend_f(tx[q], tp[q]);
+        const float mx = p[q].x + s.x, my = p[q].y + s.y;
+        const float cx = mx < 0.0f ? 0.0f : (mx > 1.0f ? 1.0f : mx);  // np.clip (no NaNs here)
+        const float cy = my < 0.0f ? 0.0f : (my > 1.0f ? 1.0f : my);
+        ncl += (cx != mx) + (cy != my);
+        pout[v] = make_float2(cx, cy);
+        if (bestcopy) pbest[v] = p[q];
+    }
+    ncl = warp_sum(ncl);
+    if ((threadIdx.x & 31) == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
+}
+
 // One warp per texture row; rpc rows per CTA.  ctrl_mode: -1 raster only (background
 // count), 0 loop evaluation, 1 final re-evaluation.
 __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_mode) {
@@ -530,8 +581,12 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
     const size_t rb = (size_t)b * n + j;
     int* cnt = D.cnt_acc + (size_t)b * (T.R + 1);
     if (j < n) {
-        for (int i = lane; i < n; i += 32) lab_s[i] = SENT;  // (16-byte stores measured slower here)
+        // the row's span count and its first 32 span slots are loaded together (cap >= 64), so the
+        // common row pays one memory round trip, overlapped with the SENT fill
+        const unsigned long long* sp = D.spans + rb * D.cap;
         const int c0 = D.rowcnt[rb];
+        const unsigned long long v_first = sp[lane];
+        for (int i = lane; i < n; i += 32) lab_s[i] = SENT;  // (16-byte stores measured slower here)
         __syncwarp();
         if (lane == 0) {
             D.rowcnt[rb] = 0;
@@ -539,10 +594,9 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
             if (c0 > 0) atomicMax(&D.maxspan[b], c0);
         }
         const int c = min(c0, D.cap);
-        const unsigned long long* sp = D.spans + rb * D.cap;
         bool lost = false;
         for (int s0 = 0; s0 < c; s0 += 32) {
-            const unsigned long long v = s0 + lane < c ? sp[s0 + lane] : 0ull;
+            const unsigned long long v = s0 + lane < c ? (s0 == 0 ? v_first : sp[s0 + lane]) : 0ull;
             const int lo = (int)(v & 0xFFFFull), hi = (int)((v >> 16) & 0xFFFFull);
             const uint32_t rk = (uint32_t)(v >> 32);
             const bool longspan = hi - lo > 16;

@@ -418,6 +418,108 @@ __global__ void __launch_bounds__(SAT2_THREADS) k_sat2(Bufs D, int gate) {
     }
 }
 
+// Float32-field variant of k_sat2: each lane's bands are split over SAT2_PARTS warps of the CTA
+// (one warp per part, 32 lanes per CTA), so every thread keeps at most SAT2P_CH band values in
+// flight and the lane's bands are fetched in one memory round trip; the parts' sums are combined
+// through shared memory.  Same outputs as k_sat2 (summation grouped by part).
+constexpr int SAT2_PARTS = 4;
+constexpr int SAT2P_CH = 8;
+
+__global__ void __launch_bounds__(32 * SAT2_PARTS) k_sat2p(Bufs D, int gate) {
+    __shared__ double s_part[SAT2_PARTS][32];
+    __shared__ double s_red[33];
+    const int b = blockIdx.y + D.b0, t = threadIdx.x, lane = t & 31, part = t >> 5;
+    if (!gate_open(D.st + b, gate)) return;
+    const int n = D.n, H = D.H, nb = D.nb, L = n + H - 1, M = 2 * n - 1;
+    if (blockIdx.x == gridDim.x - 1) {
+        // rowfull[J] = sum_{j<J} rt[j]
+        const double* rt = D.rt + (size_t)b * n;
+        double* rf = D.rowfull + (size_t)b * (n + 1);
+        const int per = (n + blockDim.x - 1) / blockDim.x;
+        const int a = min(n, t * per), e = min(n, a + per);
+        double s = 0.0;
+        for (int i = a; i < e; ++i) s += rt[i];
+        double tot;
+        double run = block_excl_scan(s, s_red, &tot);
+        for (int i = a; i < e; ++i) { rf[i] = run; run += rt[i]; }
+        if (t == 0) rf[n] = tot;
+        return;
+    }
+    const int lanes = n + 2 * M;
+    const int l = blockIdx.x * 32 + lane;
+    const bool ok = l < lanes;
+    const int type = l < n ? 0 : (l < n + M ? 1 : 2);
+    const int idx = type == 0 ? l : (type == 1 ? l - n : l - n - M);
+    const size_t base = (size_t)b * nb;
+    auto val = [&](int band) -> double {
+        if (type == 0) return D.cs[(base + band) * n + idx];
+        const int q = type == 1 ? idx - (n - 1) + (band * H + H - 1)  // v + jb
+                                : idx - band * H;                     // w - jt
+        if (q < 0) return 0.0;
+        return (type == 1 ? D.dgc : D.adc)[(base + band) * L + min(q, L - 1)];
+    };
+    const int per = (nb + SAT2_PARTS - 1) / SAT2_PARTS;
+    const int p0 = min(nb, part * per), p1 = min(nb, p0 + per);
+    // pass 1: this part's sum (the first chunk stays in registers for pass 2)
+    double v0[SAT2P_CH];
+    double loc = 0.0;
+#pragma unroll
+    for (int k = 0; k < SAT2P_CH; ++k) {
+        v0[k] = (ok && p0 + k < p1) ? val(p0 + k) : 0.0;
+        loc += v0[k];
+    }
+    for (int c0 = p0 + SAT2P_CH; c0 < p1; ++c0) loc += ok ? val(c0) : 0.0;
+    s_part[part][lane] = loc;
+    __syncthreads();
+    if (!ok) return;
+    double run = 0.0;  // forward: parts before this one; backward (type 2): parts after it
+    if (type != 2) {
+        for (int q = 0; q < part; ++q) run += s_part[q][lane];
+        auto put = [&](int band) {
+            if (type == 0) {
+                D.csX[(base + band) * n + idx] = run;
+            } else {
+                const int x = idx - n + band * H;  // v + jt - 1, v = idx - (n-1)
+                if (x >= 0 && x < n) D.dgXc[(base + band) * n + x] = run;
+            }
+        };
+#pragma unroll
+        for (int k = 0; k < SAT2P_CH; ++k) {
+            if (p0 + k < p1) {
+                put(p0 + k);
+                run += v0[k];
+            }
+        }
+        for (int band = p0 + SAT2P_CH; band < p1; ++band) {
+            const double v = val(band);
+            put(band);
+            run += v;
+        }
+        if (part == SAT2_PARTS - 1) {
+            if (type == 0) D.csT[(size_t)b * n + idx] = run;
+            else D.dgT[(size_t)b * M + idx] = run;
+        }
+    } else {
+        for (int q = SAT2_PARTS - 1; q > part; --q) run += s_part[q][lane];
+        auto put = [&](int band) {
+            const int q = idx - band * H + 1;  // w - (jt - 1)
+            if (q >= 0 && q < L + 1) D.adSc[(base + band) * (L + 1) + q] = run;
+        };
+        for (int band = p1 - 1; band >= p0 + SAT2P_CH; --band) {
+            run += val(band);
+            put(band);
+        }
+#pragma unroll
+        for (int k = SAT2P_CH - 1; k >= 0; --k) {
+            if (p0 + k < p1) {
+                run += v0[k];
+                put(p0 + k);
+            }
+        }
+        if (part == 0) D.adT[(size_t)b * M + idx] = run;
+    }
+}
+
 // ---------------------------------------------------------------------------------
 // Per band: load the float64 carries, then one top-down sweep.  In-band arithmetic
 // in A (float32 when the field is stored as float32), carries rounded to A once.
