@@ -67,9 +67,10 @@ struct det_ctx {
     DVec<int> region_row0, region_rank, rank_region, ring_start, region_ring0;
     // batch
     int B = 0, cap = 64, nb = 0, trace_cap = 0;
-    // pos0/pos1/best hold float2 rows on the float32-field path (sized as double2 either way);
+    // pos0 (the state rows, advected in place) and best hold float2 rows on the float32-field
+    // path (sized as double2 either way);
     // rows64 is the widened copy of a float state handed to the read-back / area paths
-    DVec<double2> pos_init, pos0, pos1, best, rows64;
+    DVec<double2> pos_init, pos0, best, rows64;
     DVec<int> labels, cnt_acc, cnt_state, rowcnt, maxspan, rowdone;
     DVec<unsigned long long> spans;
     DVec<float> lutf;
@@ -128,7 +129,7 @@ static Bufs make_bufs(det_ctx* c) {
     memset(&d, 0, sizeof(d));
     d.B = c->B; d.n = c->n; d.k = c->k; d.cap = c->cap; d.H = c->H; d.nb = c->nb;
     d.nn = (size_t)c->n * c->n;
-    d.pos0 = c->pos0.p; d.pos1 = c->pos1.p; d.best = c->best.p;
+    d.pos0 = c->pos0.p; d.best = c->best.p;
     d.labels = c->labels.p; d.cnt_acc = c->cnt_acc.p; d.cnt_state = c->cnt_state.p;
     d.spans = c->spans.p; d.rowcnt = c->rowcnt.p; d.maxspan = c->maxspan.p; d.rowdone = c->rowdone.p;
     d.lut = c->lut.p; d.lutf = c->lutf.p; d.stats = c->stats.p; d.weights = c->weights.p; d.rerr = c->rerr.p;
@@ -390,7 +391,6 @@ static int alloc_batch(det_ctx* ctx, int B) {
     }
     CK(ctx->pos_init.alloc((size_t)B * ctx->n_rows));
     CK(ctx->pos0.alloc((size_t)B * ctx->n_rows));
-    CK(ctx->pos1.alloc((size_t)B * ctx->n_rows));
     CK(ctx->best.alloc((size_t)B * ctx->n_rows));
     if (!ctx->f64) CK(ctx->rows64.alloc((size_t)B * ctx->n_rows));
     CK(ctx->labels.alloc((size_t)B * nn));
@@ -950,7 +950,7 @@ int det_get_result(det_ctx* ctx, int b, det_result* out) {
 static int result_src(det_ctx* ctx, int b) {
     const Carto& c = ctx->h_st[b];
     if (c.stop == S_STAGNATION) return 2;
-    return c.res_iter & 1;
+    return 0;  // the state rows are advected in place in pos0
 }
 
 // Device pointer to cartogram b's rows of the returned state (or the start rows before a run).
@@ -958,7 +958,7 @@ static const double2* state_rows(det_ctx* ctx, int b) {
     const size_t off = (size_t)b * ctx->n_rows;
     if (!ctx->ran) return ctx->pos_init.p + off;
     const int src = result_src(ctx, b);
-    const double2* p = (src == 2 ? ctx->best.p : (src == 1 ? ctx->pos1.p : ctx->pos0.p));
+    const double2* p = src == 2 ? ctx->best.p : ctx->pos0.p;
     if (ctx->f64) return p + off;
     // float32 state: widen cartogram b's rows into its slot of rows64 (stream-ordered)
     if (ctx->rows64.alloc((size_t)ctx->B * ctx->n_rows) != cudaSuccess) return nullptr;

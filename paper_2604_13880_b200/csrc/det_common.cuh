@@ -41,6 +41,8 @@ struct Carto {
     unsigned long long t_prev;
 };
 
+static_assert(sizeof(Carto) % 16 == 0, "k_region reads the first four state words as one int4");
+
 // Per-cartogram constants (CartogramEngine.__init__, engine.py:98-141; StoppingCriteria).
 struct Params {
     double background_mass, mult, mean_density0, S;
@@ -62,10 +64,9 @@ struct Bufs {
     int B, n, k, cap, H, nb;
     int b0;           // first cartogram of this launch (frame groups run as parallel graph branches)
     size_t nn;
-    // vertex rows (ping-pong state + best state): double2 on the float64-field path, float2 on
-    // the float32-field path (k_region<UT> reads them as Vec2<UT>)
+    // vertex rows (state, advected in place, + best state): double2 on the float64-field path,
+    // float2 on the float32-field path (k_region<UT> reads them as Vec2<UT>)
     void* pos0;
-    void* pos1;
     void* best;
     int* labels;
     int* cnt_acc;

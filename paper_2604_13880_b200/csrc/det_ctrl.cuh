@@ -43,7 +43,8 @@ __global__ void k_reactivate(Bufs D) {
 
 // cmode -1: background count only; 0: loop evaluation of state next_iter; 1: final re-evaluation
 // of the best state.  Executed by one whole CTA (blockDim multiple of 32).
-__device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
+// gate: checked after the first round of count loads is issued (one memory round trip for both).
+__device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode, int gate = G_ALWAYS) {
     __shared__ double s_es[32], s_em[32];
     __shared__ long long s_os[32];
     __shared__ int s_fz[32];
@@ -57,6 +58,9 @@ __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
     const double* s = D.stats + (size_t)b * R;
     double* er = D.rerr + (size_t)b * R;
     const bool eval = cmode >= 0;
+    // the state and constants the serial section reads, loaded up front with the counts
+    const Carto c0 = *st;
+    const Params P = D.prm[b];
     int fz = INT_MAX;
     long long osum = 0;
     double es = 0.0, em = -INFINITY;
@@ -69,6 +73,7 @@ __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
             o[q] = r < R ? __ldcg(acc + r) : 0;
             wr[q] = (eval && r < R) ? wt[r] : 1.0;
         }
+        if (r0 == 0 && !(gate == G_ACTIVE ? c0.active != 0 : (gate == G_FINAL ? c0.final_pending != 0 : true))) return;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int r = r0 + q * blockDim.x + t;
@@ -108,12 +113,11 @@ __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
     fz = s_fz[0];
     es = s_es[0];
     em = s_em[0];
-    const Params P = D.prm[b];
-    const int it = cmode == 0 ? st->next_iter : st->best_iter;
+    const int it = cmode == 0 ? c0.next_iter : c0.best_iter;
     if (t == 0) {
         s_cont = 0;
         int stop = S_RUNNING;
-        if (st->err & E_NEGIDX) {
+        if (c0.err & E_NEGIDX) {
             stop = S_NEGINDEX;
             st->res_iter = it;
         } else if (fz < R) {
@@ -130,14 +134,14 @@ __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
                 st->clamps = 0;  // evaluate() returns a fresh state (engine.py:204-208)
             } else {
                 const unsigned long long now = globaltimer();
-                const double ms = (double)(now - st->t_prev) * 1e-6;
+                const double ms = (double)(now - c0.t_prev) * 1e-6;
                 st->t_prev = now;
                 if (it < D.trace_cap) {
                     double* tr = D.trace + ((size_t)b * D.trace_cap + it) * 4;
                     tr[0] = (double)it; tr[1] = eps; tr[2] = xi; tr[3] = ms;
                     st->trace_len = it + 1;
                 }
-                if (xi < st->best_xi) {
+                if (xi < c0.best_xi) {
                     st->best_xi = xi;
                     st->best_iter = it;
                     st->best_pending = 1;
@@ -146,7 +150,7 @@ __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
                 }
                 if (xi < P.thr) {
                     stop = S_CONVERGED;
-                } else if (it - st->best_iter >= P.window) {
+                } else if (it - (xi < c0.best_xi ? it : c0.best_iter) >= P.window) {
                     stop = S_STAGNATION;
                     st->final_pending = 1;
                 } else if (it >= P.max_iter) {
@@ -214,8 +218,7 @@ __device__ void ctrl_body(const Topo& T, const Bufs& D, int b, int cmode) {
 // The control step as its own kernel, one 1024-thread CTA per cartogram: the evaluation of
 // the start state, and each loop iteration's step after k_row (launch_row_ctrl).
 __global__ void __launch_bounds__(CTRL_THREADS) k_ctrl(Topo T, Bufs D, int cmode, int gate) {
-    if (!gate_open(D.st + blockIdx.x + D.b0, gate)) return;
-    ctrl_body(T, D, blockIdx.x + D.b0, cmode);
+    ctrl_body(T, D, blockIdx.x + D.b0, cmode, gate);
 }
 
 }  // namespace det

@@ -33,7 +33,10 @@ namespace det {
 #define DET_RW_WARPS 2  // 1, 2, 4 measured: 2 frees slots of finished regions sooner without over-splitting
 #endif
 constexpr int RW_WARPS = DET_RW_WARPS;  // warps (regions) per CTA
-constexpr int RW_ROWCAP = 384;   // vertex rows kept in smem per warp
+#ifndef DET_RW_ROWCAP
+#define DET_RW_ROWCAP 384
+#endif
+constexpr int RW_ROWCAP = DET_RW_ROWCAP;  // vertex rows kept in smem per warp (288 with 16-bit jr: 1% slower)
 constexpr int RW_TCAP = 256;     // toggles per warp window
 constexpr int RW_WROWS = 128;    // texture rows per warp window
 #ifndef DET_RW_UNROLL
@@ -206,10 +209,13 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
     const int r = blockIdx.x * RW_WARPS + wid, b = blockIdx.y + D.b0;
     if (r >= T.R) return;
     Carto* st = D.st + b;
-    if (!gate_open(st, gate)) return;
+    // the region's bounds and the cartogram's state words in one memory round trip, then the gate
+    const int row0 = T.region_row0[r], row1 = T.region_row0[r + 1];
+    const int rq0 = T.region_ring0[r], rq1 = T.region_ring0[r + 1];
+    const int4 sth = *reinterpret_cast<const int4*>(st);  // active, next_iter, best_iter, best_pending
+    if (gate == G_ACTIVE ? sth.x == 0 : (gate == G_FINAL && st->final_pending == 0)) return;
     const int n = D.n;
     const double nd = (double)n;
-    const int row0 = T.region_row0[r], row1 = T.region_row0[r + 1];
     const int nrows = row1 - row0;
     const size_t ub = (size_t)b * T.n_rows;
     const bool in_smem = nrows <= RW_ROWCAP;
@@ -220,7 +226,6 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
     int* rc = s_rc[wid];
 
     // next row of the same ring (wraps): from the region's ring boundaries, no per-row table
-    const int rq0 = T.region_ring0[r], rq1 = T.region_ring0[r + 1];
     auto next_row = [&](int v) -> int {
         if (rq1 - rq0 == 1) return v + 1 < row1 ? v + 1 : row0;
         int q = rq0;
@@ -232,22 +237,14 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
     // vertex rows: float64 on the float64-field path, float32 on the float32-field path
     using PT = typename Vec2<UT>::type;
     constexpr bool FS = sizeof(UT) == 4;
-    const PT* __restrict__ pin;
-    PT* __restrict__ pout = nullptr;
+    // the state rows live in pos0 and are advected IN PLACE: each row is read and rewritten by the
+    // same lane, and other lanes read it only after a __syncwarp (no ping-pong, so the buffer
+    // does not depend on the iteration counter and the row loads need no state round trip)
     PT* __restrict__ pbest = reinterpret_cast<PT*>(D.best) + ub;
-    bool bestcopy = false;
-    if (mode & M_ADVECT) {
-        const int cur = st->next_iter - 1;
-        pin = reinterpret_cast<const PT*>((cur & 1) ? D.pos1 : D.pos0) + ub;
-        pout = reinterpret_cast<PT*>((cur & 1) ? D.pos0 : D.pos1) + ub;
-        bestcopy = st->best_pending != 0;
-    } else if (mode & M_POSTADV) {  // this iteration's advected rows (k_advect_rows output)
-        const int cur = st->next_iter - 1;
-        pin = reinterpret_cast<const PT*>((cur & 1) ? D.pos0 : D.pos1) + ub;
-    } else {
-        pin = reinterpret_cast<const PT*>(src == 0 ? D.pos0 : (src == 1 ? D.pos1 : D.best)) + ub;
-    }
-    const PT* gpos = (mode & M_ADVECT) ? pout : pin;  // row positions for huge regions
+    const bool bestcopy = (mode & M_ADVECT) && sth.w != 0;
+    PT* const pin = reinterpret_cast<PT*>((mode & (M_ADVECT | M_POSTADV)) || src == 0 ? D.pos0 : D.best) + ub;
+    PT* const pout = pin;
+    const PT* gpos = pin;  // row positions for huge regions
     const UT* uf = reinterpret_cast<const UT*>(D.uf) + (size_t)b * D.nn * 2;
 
     // ---- phase A: advect every vertex row (Q rows in flight per lane); per-row scaled
@@ -530,9 +527,8 @@ __global__ void __launch_bounds__(ADV_THREADS) k_advect_rows(Topo T, Bufs D, int
     if (!gate_open(st, gate)) return;
     const int n = D.n;
     const size_t ub = (size_t)b * T.n_rows;
-    const int cur = st->next_iter - 1;
-    const float2* __restrict__ pin = reinterpret_cast<const float2*>((cur & 1) ? D.pos1 : D.pos0) + ub;
-    float2* __restrict__ pout = reinterpret_cast<float2*>((cur & 1) ? D.pos0 : D.pos1) + ub;
+    float2* const pin = reinterpret_cast<float2*>(D.pos0) + ub;  // advected in place (see k_region)
+    float2* const pout = pin;
     float2* __restrict__ pbest = reinterpret_cast<float2*>(D.best) + ub;
     const bool bestcopy = st->best_pending != 0;
     const float* uf = reinterpret_cast<const float*>(D.uf) + (size_t)b * D.nn * 2;
@@ -567,6 +563,11 @@ __global__ void __launch_bounds__(ADV_THREADS) k_advect_rows(Topo T, Bufs D, int
     if ((threadIdx.x & 31) == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
 }
 
+#ifndef DET_ROW_PRE
+#define DET_ROW_PRE 4
+#endif
+constexpr int ROW_PRE = DET_ROW_PRE;  // span rounds k_row loads before it knows the row's count
+
 // One warp per texture row; rpc rows per CTA.  ctrl_mode: -1 raster only (background
 // count), 0 loop evaluation, 1 final re-evaluation.
 __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_mode) {
@@ -576,16 +577,18 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
     const int b = blockIdx.y + D.b0, n = D.n;
     const int j = blockIdx.x * rpc + wid;
     Carto* st = D.st + b;
-    if (!gate_open(st, gate)) return;
     uint32_t* lab_s = s_lab + (size_t)wid * n;
     const size_t rb = (size_t)b * n + j;
     int* cnt = D.cnt_acc + (size_t)b * (T.R + 1);
+    // the row's span count and its first ROW_PRE rounds of span slots are loaded together with
+    // the gate word (cap >= 64), so the common row pays one memory round trip
+    const unsigned long long* sp = D.spans + rb * D.cap;
+    const int c0 = j < n ? D.rowcnt[rb] : 0;
+    unsigned long long v_pre[ROW_PRE];
+#pragma unroll
+    for (int q = 0; q < ROW_PRE; ++q) v_pre[q] = (j < n && q * 32 + lane < D.cap) ? sp[q * 32 + lane] : 0ull;
+    if (!gate_open(st, gate)) return;
     if (j < n) {
-        // the row's span count and its first 32 span slots are loaded together (cap >= 64), so the
-        // common row pays one memory round trip, overlapped with the SENT fill
-        const unsigned long long* sp = D.spans + rb * D.cap;
-        const int c0 = D.rowcnt[rb];
-        const unsigned long long v_first = sp[lane];
         for (int i = lane; i < n; i += 32) lab_s[i] = SENT;  // (16-byte stores measured slower here)
         __syncwarp();
         if (lane == 0) {
@@ -596,7 +599,17 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
         const int c = min(c0, D.cap);
         bool lost = false;
         for (int s0 = 0; s0 < c; s0 += 32) {
-            const unsigned long long v = s0 + lane < c ? (s0 == 0 ? v_first : sp[s0 + lane]) : 0ull;
+            unsigned long long v = 0ull;
+            if (s0 + lane < c) {
+                if (s0 < ROW_PRE * 32) {  // a prefetched round (static register pick)
+                    v = v_pre[0];
+#pragma unroll
+                    for (int q = 1; q < ROW_PRE; ++q)
+                        if (s0 == q * 32) v = v_pre[q];
+                } else {
+                    v = sp[s0 + lane];
+                }
+            }
             const int lo = (int)(v & 0xFFFFull), hi = (int)((v >> 16) & 0xFFFFull);
             const uint32_t rk = (uint32_t)(v >> 32);
             const bool longspan = hi - lo > 16;

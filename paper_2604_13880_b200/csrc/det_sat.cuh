@@ -101,7 +101,10 @@ __host__ __device__ __forceinline__ int lut_smem_len(int R) { return (R + 2) & ~
 __host__ __device__ constexpr int lab_kp(int cols) { return cols >= 8192 ? 2 : 4; }
 // k_sat1 takes each row one iteration early (its LUT gathers overlap the previous row), so it keeps
 // a deeper ring where shared memory allows
-__host__ __device__ constexpr int lab_kp1(int cols) { return cols >= 8192 ? 2 : (cols >= 4096 ? 4 : 6); }
+#ifndef DET_KP1
+#define DET_KP1 6
+#endif
+__host__ __device__ constexpr int lab_kp1(int cols) { return cols >= 8192 ? 2 : (cols >= 4096 ? 4 : DET_KP1); }
 
 // first 16-byte aligned int slot at or after p (cp.async 16-byte copies and int4 reads)
 // (offset arithmetic on the pointer itself, so the compiler keeps it in the shared window: LDS,
