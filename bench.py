@@ -45,8 +45,9 @@ def phase_bytes(n: int, n_unique: int, n_rows: int, n_regions: int) -> dict:
     return {
         # integral images -> field: read labels (4 n^2), write the float32 field (8 n^2)
         "integral_images": 12.0 * n * n,
-        # advect + crossings: per unique vertex read 16 B + write 16 B + 4 field texels (32 B)
-        "region": 64.0 * n_unique,
+        # advect + crossings: per unique vertex read 8 B + write 8 B (float32 state) + 4 float2
+        # field texels (32 B)
+        "region": 48.0 * n_unique,
         # paint: write labels (4 n^2)
         "row": 4.0 * n * n,
         "ctrl": 0.0,
@@ -354,11 +355,15 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32+f64" if args.field == "float32" else "f64",
+            "data": "synthetic",
             "config": {"workload": "headline: 3000-region Voronoi map (seed 3), %d unique vertices / %d rows, "
                                    "1024^2 texture, direct-mode time steps, %d frames per GPU, 1 step = 1 DET "
                                    "iteration of every frame" % (n_unique, n_rows, args.batch),
                        "frames_per_gpu": args.batch, "k": K_TEX, "field_storage": args.field,
+                       "arithmetic": ("float32 field, vertex state and in-band sums; float64 raster crossings, "
+                                      "band carries and control step" if args.field == "float32" else
+                                      "float64 throughout (trajectory-identical to the reference)"),
                        "e2e_note": "median of 3 timed public-API calls (map upload, run, results back), "
                                    "gc.collect() before each; pinned result buffer reserved at BatchEngine "
                                    "construction",

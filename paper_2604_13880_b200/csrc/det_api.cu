@@ -89,6 +89,7 @@ struct det_ctx {
     bool g_valid = false;
     int groups = 8;  // graph branches (clamped to the batch); 1/2/4/8 measured 41.5/42.4/43.9/44.2k it/s
     bool sep_ctrl = true;  // control step as its own kernel (DET_SEP_CTRL=0: k_row's last CTA)
+    bool sat1w = true;  // float32 field: barrier-free k_sat1w (DET_SAT1W=0: k_sat1)
     bool split_adv = false;  // float32 state: advect as the flat k_advect_rows (DET_SPLIT_ADVECT=1); 48.6k vs 51.4k fused
     Topo g_topo;  // launch signature the graph was captured with
     Bufs g_bufs;
@@ -180,7 +181,18 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
         smem_optin(fn);                                                                                      \
         fn<<<gb, NT, smem1, c->stream>>>(T, D, S, gate);                                                     \
     } while (0)
-    if (src == SRC_LABELS) {
+    // barrier-free sweep, one TMA ring per warp slice (k_sat1w; DET_SAT1W_CPT columns per thread
+    // where the band kernels use 4)
+    constexpr int CPT1 = (CPT == 4 && NT * 4 / DET_SAT1W_CPT <= 1024 && NT * 4 / DET_SAT1W_CPT >= 32) ? DET_SAT1W_CPT : CPT;
+    constexpr int NT1 = NT * CPT / CPT1;
+    if (src == SRC_LABELS && f32 && c->sat1w && n % (32 * CPT1) == 0) {
+        constexpr int NW = NT1 / 32, KP = lab_kp1(CPT1 * NT1);
+        const size_t smem1w = ((size_t)2 * (n + H - 1) + (size_t)3 * H * NW) * sizeof(float) + 16 +
+                              (size_t)NW * KP * 32 * CPT1 * sizeof(int);
+        auto fn = k_sat1w<CPT1, NT1>;
+        smem_optin(fn);
+        fn<<<gb, NT1, smem1w, c->stream>>>(T, D, gate);
+    } else if (src == SRC_LABELS) {
         // k_sat1 gathers the LUT through L1 (__ldg): staging it per CTA measured slower there
         if (f32) DET_SAT1(SRC_LABELS, float, false);
         else DET_SAT1(SRC_LABELS, double, false);
@@ -511,6 +523,7 @@ int det_ctx_create(int device, int k, int field_f64, det_ctx** out) {
     det_ctx* ctx = new det_ctx();
     if (const char* e = getenv("DET_SEP_CTRL")) ctx->sep_ctrl = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SPLIT_ADVECT")) ctx->split_adv = atoi(e) != 0;  // A/B switch (diagnostics)
+    if (const char* e = getenv("DET_SAT1W")) ctx->sat1w = atoi(e) != 0;  // A/B switch (diagnostics)
     ctx->device = device;
     ctx->k = k;
     ctx->n = 1 << k;

@@ -338,6 +338,191 @@ __global__ void __launch_bounds__(NT) k_sat1(Topo T, Bufs D, SatSrc S, int gate)
 }
 
 // ---------------------------------------------------------------------------------
+// k_sat1w: k_sat1 for the float32 field with no CTA barrier in the row sweep.  Each warp owns a
+// 32*CPT-column slice: it streams its slice of every label row through its own 1-D TMA ring and
+// carries diagonal / anti-diagonal partial sums only inside the slice (zero at the slice edge).
+// The partial leaving the slice after each row is recorded (exitD / exitA); a band is at most
+// 64 rows <= the slice width, so a diagonal crosses at most one slice edge and its band sum is
+// the recorded partial plus the neighbour slice's continuation, added once at the band end.
+// Outputs equal k_sat1's (the in-band sums are grouped per slice).
+template <int CPT, int KP>
+struct WarpRing {
+    int* q;          // KP slots of 32*CPT ints (this warp's)
+    uint64_t* bar;   // KP mbarriers (this warp's)
+    const int* lab;  // label row 0, this warp's first column
+    int n, jt, j_last;
+    unsigned bytes;  // valid bytes of the slice (0: slice beyond the texture)
+    __device__ __forceinline__ static unsigned sm(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+    __device__ __forceinline__ void init(int lane) {
+        if (lane == 0) {
+#pragma unroll
+            for (int s = 0; s < KP; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(sm(bar + s)));
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncwarp();
+    }
+    __device__ __forceinline__ void issue(int row, int slot) {  // lane 0 only
+        if (row > j_last || bytes == 0) return;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(sm(bar + slot)), "r"(bytes)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                         sm(q + slot * 32 * CPT)),
+                     "l"(lab + (size_t)row * n), "r"(bytes), "r"(sm(bar + slot))
+                     : "memory");
+    }
+    __device__ __forceinline__ void prologue(int lane) {
+        if (lane == 0) {
+#pragma unroll
+            for (int p = 0; p < KP - 1; ++p) issue(jt + p, p);
+        }
+    }
+    // row j -> residual densities; refills row j-1's slot (every lane finished reading it: the
+    // __syncwarp below orders those reads before lane 0's async-proxy write)
+    template <typename A>
+    __device__ __forceinline__ void take(int j, int lane, bool active, const A* lut, int R, A (&rho)[CPT]) {
+        const int r = j - jt;
+        __syncwarp();
+        if (lane == 0) issue(j + KP - 1, (r + KP - 1) % KP);
+        if (bytes == 0) {
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) rho[k] = (A)0;
+            return;
+        }
+        const int slot = r % KP;
+        const unsigned parity = (unsigned)((r / KP) & 1);
+        unsigned done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(sm(bar + slot)), "r"(parity)
+                : "memory");
+        }
+        if (active) {
+            const int* src = q + slot * 32 * CPT + lane * CPT;
+            int L[CPT];
+#pragma unroll
+            for (int c = 0; c < CPT; c += 2) {
+                const int2 v = *reinterpret_cast<const int2*>(src + c);
+                L[c] = v.x; L[c + 1] = v.y;
+            }
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) rho[k] = __ldg(lut + (L[k] < 0 ? R : L[k]));
+        } else {
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) rho[k] = (A)0;
+        }
+    }
+};
+
+#ifndef DET_SAT1W_CPT
+#define DET_SAT1W_CPT 4  // columns per thread of k_sat1w at CPT=4 configs (2: 49.7k, 4: 52.6k it/s)
+#endif
+template <int CPT, int NT>
+__global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
+    using A = float;
+    constexpr int NW = NT / 32, W = 32 * CPT, KP = lab_kp1(CPT * NT);
+    // dg[L] | ad[L] | row partials [H][NW] | exitD [NW][H] | exitA [NW][H] | rings (16-B aligned)
+    extern __shared__ unsigned char s_raw1[];
+    __shared__ uint64_t s_bar[NW * KP];
+    __shared__ double s_red[33];
+    const int band = blockIdx.x, b = blockIdx.y + D.b0, t = threadIdx.x;
+    const int lane = t & 31, w = t >> 5;
+    if (!gate_open(D.st + b, gate)) return;
+    const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, L = n + H - 1, R = T.R;
+    const int x0 = t * CPT, c0 = w * W;
+    const bool active = x0 < n;
+    const size_t bb = (size_t)b * D.nb + band;
+    A* dg = reinterpret_cast<A*>(s_raw1);
+    A* ad = dg + L;
+    A* s_rows = ad + L;
+    A* exD = s_rows + H * NW;
+    A* exA = exD + NW * H;
+    const A* lut = reinterpret_cast<const A*>(D.lutf + (size_t)b * (R + 1));
+    WarpRing<CPT, KP> ring;
+    ring.q = align16(exA + NW * H) + w * KP * W;
+    ring.bar = s_bar + w * KP;
+    ring.lab = D.labels + (size_t)b * D.nn + c0;
+    ring.n = n;
+    ring.jt = jt;
+    ring.j_last = jb;
+    ring.bytes = (unsigned)(max(0, min(W, n - c0)) * 4);
+    ring.init(lane);
+    ring.prologue(lane);
+
+    A cs[CPT], pd[CPT], pa[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) cs[k] = pd[k] = pa[k] = (A)0;
+    A rho_n[CPT];
+    ring.take(jt, lane, active, lut, R, rho_n);
+    for (int j = jt; j <= jb; ++j) {
+        A rho[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
+        if (j < jb) ring.take(j + 1, lane, active, lut, R, rho_n);  // next row's gathers in flight
+        A ts = (A)0;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) ts += rho[k];
+        ts = warp_sum(ts);
+        if (lane == 0) s_rows[(j - jt) * NW + w] = ts;  // row totals are summed after the sweep
+        A left = __shfl_up_sync(FULL, pd[CPT - 1], 1);
+        A right = __shfl_down_sync(FULL, pa[0], 1);
+        if (lane == 0) left = (A)0;    // partials restart at the slice edge
+        if (lane == 31) right = (A)0;
+        // in place, so the diagonal recurrence runs right to left and the anti-diagonal one left to
+        // right (each reads its neighbour's previous-row partial before it is overwritten)
+#pragma unroll
+        for (int k = CPT - 1; k >= 0; --k) pd[k] = rho[k] + (k == 0 ? left : pd[k - 1]);
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) pa[k] = rho[k] + (k == CPT - 1 ? right : pa[k + 1]);
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) cs[k] += rho[k];
+        if (lane == 31) exD[w * H + (j - jt)] = pd[CPT - 1];  // diagonal leaving the slice's right edge
+        if (lane == 0) exA[w * H + (j - jt)] = pa[0];  // anti-diagonal leaving the slice's left edge
+    }
+    __syncthreads();  // exits, row partials published
+    // band-bottom entries + the neighbour slice's part of each crossing diagonal
+    double csum = 0.0;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int x = x0 + k;
+        if (x < n) {
+            const int xi = x - c0;                       // column inside the slice
+            A vd = pd[k], va = pa[k];
+            if (w > 0 && xi <= H - 2) vd += exD[(w - 1) * H + (H - 2 - xi)];
+            const int xr = W - 1 - xi;                   // columns to the slice's right edge
+            if (w < NW - 1 && c0 + W < n && xr <= H - 2) va += exA[(w + 1) * H + (H - 2 - xr)];
+            dg[x] = vd;
+            ad[H - 1 + x] = va;
+        }
+        csum += x < n ? (double)cs[k] : 0.0;
+    }
+    // diagonals leaving the texture's right edge / anti-diagonals leaving its left edge (j < jb)
+    if (t < H - 1) {
+        const int wl = (n - 1) / W;  // slice holding column n-1
+        dg[n - 1 - (jt + t) + jb] = exD[wl * H + t];
+        ad[t] = exA[t];
+    }
+    double tot;
+    double run = block_excl_scan(csum, s_red, &tot);  // (its barriers also publish dg/ad)
+    if (t < H) {  // row totals in float64, warp order
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) s += (double)s_rows[t * NW + q];
+        D.rt[(size_t)b * n + jt + t] = s;
+    }
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int x = x0 + k;
+        run += (double)cs[k];
+        if (x < n) D.cs[bb * n + x] = run;
+    }
+    block_prefix_smem<A>(dg, D.dgc + bb * L, L, s_red);
+    block_prefix_smem<A>(ad, D.adc + bb * L, L, s_red);
+}
+
+// ---------------------------------------------------------------------------------
 // Band-direction carries.  Lanes: [0,n) columns x, [n,3n-1) diagonals (idx=v+n-1),
 // [3n-1,5n-2) anti-diagonals w.  blockDim = 32*G (G band groups).  The last block
 // column computes rowfull (row-total prefix) instead.  Outputs per band b:
@@ -526,6 +711,9 @@ __global__ void __launch_bounds__(32 * SAT2_PARTS) k_sat2p(Bufs D, int gate) {
 // ---------------------------------------------------------------------------------
 // Per band: load the float64 carries, then one top-down sweep.  In-band arithmetic
 // in A (float32 when the field is stored as float32), carries rounded to A once.
+#ifndef DET_SAT3_F2
+#define DET_SAT3_F2 1
+#endif
 #ifndef DET_SAT3_MINB
 #define DET_SAT3_MINB 4  // 64 registers, no spills: 512 band CTAs fit one wave (3 and 5 measured slower)
 #endif
@@ -721,6 +909,18 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
                     const A dp = fmaxf(d, (A)0), dn = fmaxf(-d, (A)0);
                     const A nK = -(cavg + rmc);
                     const A t = at + gt;
+#if DET_SAT3_F2
+                    // (ux, uy) as one packed pair: FFMA2 / FADD2 / FMUL2 (sm_100 f32x2)
+                    float2 v = __ffma2_rn(make_float2(a4, a4), make_float2(c1y, fmaf(xc, -0.5f, 0.25f)),
+                                          make_float2(cavg, ravg));
+                    v = __ffma2_rn(make_float2(cavg, cavg), make_float2(mn, mx), v);
+                    v = __ffma2_rn(make_float2(ravg, ravg), make_float2(mx, mn), v);
+                    v = __ffma2_rn(make_float2(nK, nK), make_float2(dp, dn), v);
+                    v = __ffma2_rn(make_float2(xc, yc), make_float2(t, Cr - t), v);
+                    v = __fmul2_rn(__fadd2_rn(v, make_float2(bt, at)), make_float2(inv2m, inv2m));
+                    ux[k] = v.x;
+                    uy[k] = v.y;
+#else
                     A vx = fmaf(a4, c1y, cavg);
                     vx = fmaf(cavg, mn, vx);
                     vx = fmaf(ravg, mx, vx);
@@ -733,6 +933,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
                     vy = fmaf(nK, dn, vy);
                     vy = fmaf(yc, Cr - t, vy);
                     uy[k] = (vy + at) * inv2m;
+#endif
                 } else {
                     // anchor combination (displacement.py:128-130) with b = cavg-a, d = ravg-a,
                     // g = C-cavg-ravg+a, delta_t = C-at-bt-gt; since q1+q3 = (1+x-y, 1-x+y) and

@@ -28,7 +28,7 @@ def test_algorithmic_bytes_match_survey_table(bench):
     assert bench.algorithmic_bytes_per_iteration(1024, 200_000) == pytest.approx(55.8e6, rel=2e-3)
     assert bench.algorithmic_bytes_per_iteration(4096, 1_000_000) == pytest.approx(601.8e6, rel=2e-3)
     ph = bench.phase_bytes(1024, 200_000, 400_000, 3000)
-    assert ph["integral_images"] == 12 * 1024 * 1024 and ph["region"] == 64 * 200_000
+    assert ph["integral_images"] == 12 * 1024 * 1024 and ph["region"] == 48 * 200_000
 
 
 def test_traffic_lookup_reads_committed_capture(bench):
