@@ -382,3 +382,57 @@ def test_config5_stress_scale(P):
     dv = np.abs(r32.state.mapmodel.vertex_array() - r64.state.mapmodel.vertex_array()).max()
     assert dv <= 1e-5, dv
     assert np.array_equal(r64.state.labels.labels, O.FlatMap.from_mapmodel(r64.state.mapmodel).labels(12))
+
+
+# ---------------------------------------------------------------- float32-path variants
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2604_13880_b200 as P
+from paper_2604_13880_b200.synthetic import voronoi_map
+m = voronoi_map(200, seed=7, target_unique=20000, sigma=0.8)
+res = P.run(m, P.StoppingCriteria(1e-300, 10**9, 30), k=10, field_dtype="float32")
+np.save({out!r}, np.concatenate([res.state.mapmodel.vertex_array().ravel(),
+                                 res.state.pixel_counts.astype(np.float64)]))
+"""
+
+
+@pytest.mark.parametrize("env", [{"DET_SAT1W": "0"}, {"DET_SPLIT_ADVECT": "1"}])
+def test_float_path_kernel_variants_agree(P, tmp_path, env):
+    """The float32 path's A/B kernel variants (k_sat1 with CTA barriers instead of the barrier-free
+    k_sat1w; the advect as its own flat kernel instead of inside k_region) give the same cartogram:
+    vertices within float rounding (1e-5), pixel counts within a few pixels."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for i, e in enumerate([{}, env]):
+        out = str(tmp_path / f"v{i}.npy")
+        code = _VARIANT_SCRIPT.format(root=root, out=out)
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **e), capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    nv = outs[0].size - 200
+    dv = np.abs(outs[0][:nv] - outs[1][:nv]).max()
+    assert dv <= 1e-5, dv
+    assert np.abs(outs[0][nv:] - outs[1][nv:]).max() <= 4
+
+
+def test_float_state_start_raster_is_exact(P):
+    """Float32 vertex state: the start raster (iteration 0's counts and error) is computed on the
+    exact float64 rows, identical to the float64 path; later states stay within the tolerances."""
+    m = fm.config1()
+    crit = P.StoppingCriteria(1e-300, 10**9, 40)
+    r32 = P.run(m, crit, k=8, bdv_multiplier=0.5, field_dtype="float32")
+    r64 = P.run(m, crit, k=8, bdv_multiplier=0.5, field_dtype="float64")
+    assert r32.trace[0].epsilon == r64.trace[0].epsilon and r32.trace[0].xi == r64.trace[0].xi
+    np.testing.assert_array_equal(r32.weights_px, r64.weights_px)
+    dv = np.abs(r32.state.mapmodel.vertex_array() - r64.state.mapmodel.vertex_array()).max()
+    assert dv <= VERT_TOL, dv
+    a32 = np.array([r.area() for r in r32.state.mapmodel.regions])
+    a64 = np.array([r.area() for r in r64.state.mapmodel.regions])
+    assert np.allclose(a32, a64, rtol=AREA_RTOL)
+    # the float32 state's own raster is still bit-exact against the oracle on its (float32) rows
+    ref = O.FlatMap.from_mapmodel(r32.state.mapmodel).labels(8)
+    assert np.array_equal(r32.state.labels.labels, ref)
