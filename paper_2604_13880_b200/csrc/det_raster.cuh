@@ -39,6 +39,9 @@ constexpr int RW_WARPS = DET_RW_WARPS;  // warps (regions) per CTA
 constexpr int RW_ROWCAP = DET_RW_ROWCAP;  // vertex rows kept in smem per warp (288 with 16-bit jr: 1% slower)
 constexpr int RW_TCAP = 256;     // toggles per warp window
 constexpr int RW_WROWS = 128;    // texture rows per warp window
+#ifndef DET_RW_PIPE
+#define DET_RW_PIPE 1
+#endif
 #ifndef DET_RW_UNROLL
 #define DET_RW_UNROLL 2
 #endif
@@ -251,6 +254,32 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
     //      coordinates and scanline / column indices for the raster ----
     int jmn = n, jmx = 0, imn = n, imx = 0;
     int ncl = 0;
+    // per advected row: store (in place), best copy, scanline / column index, crop extent
+    auto finish = [&](int v, const PT& pold, const PT& pnew) {
+        if (mode & M_ADVECT) {
+            pout[v] = pnew;
+            if (bestcopy) pbest[v] = pold;
+        }
+        // x*n, y*n are exact (n is a power of two); ceil is monotone, so the crop
+        // (raster.py:71-74) and each edge's scanline range (raster.py:45-46) are
+        // min/max of these per-row integers
+        int jr, ir;
+        if constexpr (FS) {  // y*n - 0.5 is exact in float wherever its ceil is not 0
+            const float nf = (float)n;
+            jr = min(max(ceil_to_int_f(pnew.y * nf - 0.5f), 0), n);
+            ir = min(max(ceil_to_int_f(pnew.x * nf - 0.5f), 0), n);
+        } else {
+            const double xs = __dmul_rn(pnew.x, nd), ys = __dmul_rn(pnew.y, nd);
+            jr = min(max(ceil_to_int(__dsub_rn(ys, 0.5)), 0), n);
+            ir = min(max(ceil_to_int(__dsub_rn(xs, 0.5)), 0), n);
+        }
+        if (in_smem) {
+            sjr[v - row0] = jr;
+            snx[v - row0] = (uint16_t)(next_row(v) - row0);
+        }
+        jmn = min(jmn, jr); jmx = max(jmx, jr);
+        imn = min(imn, ir); imx = max(imx, ir);
+    };
     auto chunk = [&](auto QC, int base) {
         constexpr int Q = decltype(QC)::value;
         PT p[Q];
@@ -306,37 +335,60 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             const int v = base + q * 32 + lane;
-            if (v >= row1) continue;
-            if (mode & M_ADVECT) {
-                pout[v] = nq[q];
-                if (bestcopy) pbest[v] = p[q];
-            }
-            // x*n, y*n are exact (n is a power of two); ceil is monotone, so the crop
-            // (raster.py:71-74) and each edge's scanline range (raster.py:45-46) are
-            // min/max of these per-row integers
-            int jr, ir;
-            if constexpr (FS) {  // y*n - 0.5 is exact in float wherever its ceil is not 0
-                const float nf = (float)n;
-                jr = min(max(ceil_to_int_f(nq[q].y * nf - 0.5f), 0), n);
-                ir = min(max(ceil_to_int_f(nq[q].x * nf - 0.5f), 0), n);
-            } else {
-                const double xs = __dmul_rn(nq[q].x, nd), ys = __dmul_rn(nq[q].y, nd);
-                jr = min(max(ceil_to_int(__dsub_rn(ys, 0.5)), 0), n);
-                ir = min(max(ceil_to_int(__dsub_rn(xs, 0.5)), 0), n);
-            }
-            if (in_smem) {
-                sjr[v - row0] = jr;
-                snx[v - row0] = (uint16_t)(next_row(v) - row0);
-            }
-            jmn = min(jmn, jr); jmx = max(jmx, jr);
-            imn = min(imn, ir); imx = max(imx, ir);
+            if (v < row1) finish(v, p[q], nq[q]);
         }
     };
     // full rounds of RW_UNROLL rows per lane while more than one warp of rows remains, then a
     // one-row tail (no lane slots idle for a whole extra round)
-    int base = row0;
-    for (; base + 32 < row1; base += 32 * RW_UNROLL) chunk(std::integral_constant<int, RW_UNROLL>{}, base);
-    if (base < row1) chunk(std::integral_constant<int, 1>{}, base);
+    bool done_a = false;
+#if DET_RW_PIPE
+    if constexpr (FS) {
+        if (mode & M_ADVECT) {
+            // software-pipelined float advect: the next chunk's row loads are issued together with
+            // this chunk's texel gather, so a region pays one round trip per chunk, not two
+            constexpr int Q = RW_UNROLL;
+            float2 pc[Q], pn[Q];
+            auto ld = [&](float2 (&dst)[Q], int base) {
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    const int v = base + q * 32 + lane;
+                    dst[q] = v < row1 ? pin[v] : make_float2(0.5f, 0.5f);
+                }
+            };
+            ld(pc, row0);
+            for (int base = row0; base < row1; base += 32 * Q) {
+                TapF tp[Q];
+                Texels<float> tx[Q];
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    tp[q] = field_tap_pf(n, pc[q].x, pc[q].y);
+                    tx[q] = field_load<float, TapF>(reinterpret_cast<const float*>(uf), tp[q]);
+                }
+                if (base + 32 * Q < row1) ld(pn, base + 32 * Q);
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    const float2 sm = field_blend_f(tx[q], tp[q]);
+                    const float mx = pc[q].x + sm.x, my = pc[q].y + sm.y;
+                    const float cx = mx < 0.0f ? 0.0f : (mx > 1.0f ? 1.0f : mx);  // np.clip (no NaNs here)
+                    const float cy = my < 0.0f ? 0.0f : (my > 1.0f ? 1.0f : my);
+                    const int v = base + q * 32 + lane;
+                    if (v < row1) {
+                        ncl += (cx != mx) + (cy != my);
+                        finish(v, pc[q], make_float2(cx, cy));
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < Q; ++q) pc[q] = pn[q];
+            }
+            done_a = true;
+        }
+    }
+#endif
+    if (!done_a) {
+        int base = row0;
+        for (; base + 32 < row1; base += 32 * RW_UNROLL) chunk(std::integral_constant<int, RW_UNROLL>{}, base);
+        if (base < row1) chunk(std::integral_constant<int, 1>{}, base);
+    }
     if (mode & M_ADVECT) {
         ncl = warp_sum(ncl);
         if (lane == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
@@ -563,6 +615,9 @@ __global__ void __launch_bounds__(ADV_THREADS) k_advect_rows(Topo T, Bufs D, int
     if ((threadIdx.x & 31) == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
 }
 
+#ifndef DET_ROW_RED
+#define DET_ROW_RED 0  // 1: non-returning atomics + clash check + exact repaint (53.3k vs 54.7k: clashes are common)
+#endif
 #ifndef DET_ROW_PRE
 #define DET_ROW_PRE 4
 #endif
@@ -597,8 +652,8 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
             if (c0 > 0) atomicMax(&D.maxspan[b], c0);
         }
         const int c = min(c0, D.cap);
-        bool lost = false;
-        for (int s0 = 0; s0 < c; s0 += 32) {
+        // slot s of the row's span list (prefetched rounds from registers)
+        auto span_at = [&](int s0) -> unsigned long long {
             unsigned long long v = 0ull;
             if (s0 + lane < c) {
                 if (s0 < ROW_PRE * 32) {  // a prefetched round (static register pick)
@@ -610,15 +665,80 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
                     v = sp[s0 + lane];
                 }
             }
+            return v;
+        };
+#if DET_ROW_RED
+        // paint with non-returning shared atomicMin (no per-pixel wait on the old value); overlaps
+        // are detected afterwards: the row's painted-pixel count equals the sum of its span lengths
+        // unless two spans claimed a pixel
+        int mylen = 0;
+        for (int s0 = 0; s0 < c; s0 += 32) {
+            const unsigned long long v = span_at(s0);
             const int lo = (int)(v & 0xFFFFull), hi = (int)((v >> 16) & 0xFFFFull);
             const uint32_t rk = (uint32_t)(v >> 32);
             const bool longspan = hi - lo > 16;
-            if (!longspan) {  // lane paints its own short span
+            mylen += hi - lo;
+            if (!longspan)  // lane paints its own short span
+                for (int i = lo; i < hi; ++i) atomicMin(&lab_s[i], rk);
+            unsigned lm = __ballot_sync(FULL, longspan);
+            while (lm) {  // the warp paints long spans together
+                const int q = __ffs(lm) - 1;
+                lm &= lm - 1;
+                const int qlo = __shfl_sync(FULL, lo, q), qhi = __shfl_sync(FULL, hi, q);
+                const uint32_t qrk = __shfl_sync(FULL, rk, q);
+                for (int i = qlo + lane; i < qhi; i += 32) atomicMin(&lab_s[i], qrk);
+            }
+        }
+        __syncwarp();
+        // the label texture holds region RANKS (-1 = background); det_get_labels maps them
+        // back to region indices (raster.py:107 stores indices) -- saves a gather per pixel
+        int4* lab4 = reinterpret_cast<int4*>(D.labels + (size_t)b * D.nn + (size_t)j * n);
+        const int4* src4 = reinterpret_cast<const int4*>(lab_s);
+        int painted = 0;
+        for (int i = lane; i < (n >> 2); i += 32) {
+            const int4 x = src4[i];
+            lab4[i] = x;  // SENT == -1 bitwise
+            painted += (x.x != -1) + (x.y != -1) + (x.z != -1) + (x.w != -1);
+        }
+        // (warp_sum leaves the total in lane 0 only: broadcast, so the branch below is warp-uniform)
+        const bool clash = __shfl_sync(FULL, warp_sum(painted) != warp_sum(mylen), 0);
+        if (clash) {
+            // a pixel was claimed twice on this row (spans of two regions, or of one region --
+            // the original rule counts both): repaint the row with returning atomics, which
+            // decrement the loser of every claim exactly as before (raster.py:142-146)
+            for (int i = lane; i < n; i += 32) lab_s[i] = SENT;
+            __syncwarp();
+            for (int s0 = 0; s0 < c; s0 += 32) {
+                const unsigned long long v = span_at(s0);
+                const int lo = (int)(v & 0xFFFFull), hi = (int)((v >> 16) & 0xFFFFull);
+                const uint32_t rk = (uint32_t)(v >> 32);
                 for (int i = lo; i < hi; ++i) {
                     const uint32_t old = atomicMin(&lab_s[i], rk);
-                    if (old != SENT) {  // the higher rank loses the pixel
-                        atomicAdd(&cnt[T.rank_region[max(old, rk)]], -1);
-                        lost = true;
+                    if (old != SENT) atomicAdd(&cnt[T.rank_region[max(old, rk)]], -1);
+                }
+            }
+            __syncwarp();
+            for (int i = lane; i < (n >> 2); i += 32) lab4[i] = src4[i];
+            __threadfence();  // order the (rare) count corrections before this CTA signs off
+        }
+#else
+        bool lost = false;
+        for (int s0 = 0; s0 < c; s0 += 32) {
+            const unsigned long long v = span_at(s0);
+            const int lo = (int)(v & 0xFFFFull), hi = (int)((v >> 16) & 0xFFFFull);
+            const uint32_t rk = (uint32_t)(v >> 32);
+            const bool longspan = hi - lo > 16;
+            if (!longspan) {  // lane paints its own short span, 4 claims in flight per step
+                for (int i0 = lo; i0 < hi; i0 += 4) {
+                    uint32_t old[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) old[q] = i0 + q < hi ? atomicMin(&lab_s[i0 + q], rk) : SENT;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        if (old[q] != SENT) {  // the higher rank loses the pixel
+                            atomicAdd(&cnt[T.rank_region[max(old[q], rk)]], -1);
+                            lost = true;
+                        }
                     }
                 }
             }
@@ -646,6 +766,7 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
         if (lost) {  // order the (rare) count corrections before this CTA signs off
             __threadfence();
         }
+#endif
     }
     if (ctrl_mode == CTRL_SEPARATE) return;  // the control step runs as k_ctrl after this kernel
     // ---- completion: the CTA that finishes the last row of this cartogram runs the control step ----
