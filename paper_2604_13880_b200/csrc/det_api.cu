@@ -1038,10 +1038,21 @@ int det_get_results(det_ctx* ctx, double* xy_out, int64_t* counts_out, double* e
     cudaSetDevice(ctx->device);
     const int B = ctx->B, R = ctx->R;
     cudaStream_t s = ctx->stream;
-    if (xy_out)
-        for (int b = 0; b < B; ++b)
-            CK(cudaMemcpyAsync(xy_out + (size_t)b * ctx->n_rows * 2, state_rows(ctx, b), ctx->n_rows * sizeof(double2),
-                               cudaMemcpyDeviceToHost, s));
+    if (xy_out) {
+        bool all_state = !ctx->f64;  // float32 state, no frame returning its best rows: one widen, one copy
+        for (int b = 0; b < B && all_state; ++b) all_state = result_src(ctx, b) == 0;
+        if (all_state) {
+            const long long len = (long long)B * ctx->n_rows;
+            CK(ctx->rows64.alloc((size_t)len));
+            k_rows_to_f64<<<(unsigned)std::min<long long>((len + 255) / 256, 8192), 256, 0, s>>>(
+                reinterpret_cast<const float2*>(ctx->pos0.p), len, ctx->rows64.p);
+            CK(cudaMemcpyAsync(xy_out, ctx->rows64.p, (size_t)len * sizeof(double2), cudaMemcpyDeviceToHost, s));
+        } else {
+            for (int b = 0; b < B; ++b)
+                CK(cudaMemcpyAsync(xy_out + (size_t)b * ctx->n_rows * 2, state_rows(ctx, b),
+                                   ctx->n_rows * sizeof(double2), cudaMemcpyDeviceToHost, s));
+        }
+    }
     std::vector<int> c;
     if (counts_out) {
         c.resize((size_t)B * (R + 1));

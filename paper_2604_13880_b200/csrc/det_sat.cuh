@@ -711,6 +711,9 @@ __global__ void __launch_bounds__(32 * SAT2_PARTS) k_sat2p(Bufs D, int gate) {
 // ---------------------------------------------------------------------------------
 // Per band: load the float64 carries, then one top-down sweep.  In-band arithmetic
 // in A (float32 when the field is stored as float32), carries rounded to A once.
+#ifndef DET_SAT3_PIPE
+#define DET_SAT3_PIPE 0  // 1: 53.6k vs 54.7k (spills at the 64-register cap)
+#endif
 #ifndef DET_SAT3_F2
 #define DET_SAT3_F2 1
 #endif
@@ -813,11 +816,17 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
     if (RING) ring.prologue();
     A rho_n[CPT];
     if (!RING) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, jt, x0, rho_n);
+    // DET_SAT3_PIPE: row j+1's label wait and LUT reads are issued at the top of row j (as in k_sat1)
+    if (RING && DET_SAT3_PIPE) ring.take(jt, lut, R, rho_n);
 
     int slot = 0, ps = 2;  // rotating boundary slots: (j - jt) % 3, (j - jt + 2) % 3
     for (int j = jt; j <= jb; ++j) {
         A rho[CPT];
-        if (RING) {
+        if (RING && DET_SAT3_PIPE) {
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
+            if (j < jb) ring.take(j + 1, lut, R, rho_n);  // refills row j's slot: every take(j) preceded barrier j-1
+        } else if (RING) {
             ring.take(j, lut, R, rho);
         } else {
 #pragma unroll
