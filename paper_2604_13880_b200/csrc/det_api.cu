@@ -160,6 +160,9 @@ static void smem_optin(F fn) {
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin - (int)a.sharedSizeBytes);
 }
 
+#ifndef DET_SAT3_CPT
+#define DET_SAT3_CPT 4  // k_sat3 columns per thread on the float32 path
+#endif
 template <int CPT, int NT>
 static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S, int gate, int src, int out,
                            bool u64, int B) {
@@ -224,8 +227,15 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
             if (luts) DET_SAT3(SRC_LABELS, double, OUT_U, true);
             else DET_SAT3(SRC_LABELS, double, OUT_U, false);
         } else {
-            if (luts) DET_SAT3(SRC_LABELS, float, OUT_U, true);
-            else DET_SAT3(SRC_LABELS, float, OUT_U, false);
+            // float32 field: DET_SAT3_CPT columns per thread (the ring row and windows are unchanged)
+            constexpr int CPT3 = (CPT == 4 && NT * 4 / DET_SAT3_CPT >= 32) ? DET_SAT3_CPT : CPT;
+            constexpr int NT3 = NT * CPT / CPT3;
+            const size_t ring3_b = (size_t)lab_kp(CPT3 * NT3) * NT3 * CPT3 * sizeof(int);
+            const size_t smem3 = ((size_t)3 * (n + H) + 3 * H + (H & 1)) * sa + lut_b + ring3_b + 16;
+            auto fn = luts ? k_sat3<CPT3, NT3, SRC_LABELS, float, OUT_U, float, true>
+                           : k_sat3<CPT3, NT3, SRC_LABELS, float, OUT_U, float, false>;
+            smem_optin(fn);
+            fn<<<gb, NT3, smem3, c->stream>>>(T, D, S, gate);
         }
     } else {
         if (u64) DET_SAT3(SRC_DENSE, double, OUT_U, false);
