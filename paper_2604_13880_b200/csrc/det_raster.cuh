@@ -200,8 +200,9 @@ template <typename UT>
 #define DET_RW_MINB (32 / DET_RW_WARPS)  // 32 resident warps per SM (64 registers)
 #endif
 __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, Bufs D, int mode, int gate, int src) {
-    __shared__ int s_jr[RW_WARPS][RW_ROWCAP];       // ceil(y*n - 0.5) clipped to [0, n]
-    __shared__ uint16_t s_nx[RW_WARPS][RW_ROWCAP];  // next row of the same ring (region-local index)
+    // per row: ceil(y*n - 0.5) clipped to [0, n] (low 16 bits) | next row of the same ring,
+    // region-local (high 16 bits) -- one load per edge end
+    __shared__ uint32_t s_jn[RW_WARPS][RW_ROWCAP];
     __shared__ int s_tot[RW_WARPS];
     __shared__ uint32_t s_key[RW_WARPS][RW_TCAP];
     __shared__ uint16_t s_col[RW_WARPS][RW_TCAP];
@@ -222,8 +223,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
     const int nrows = row1 - row0;
     const size_t ub = (size_t)b * T.n_rows;
     const bool in_smem = nrows <= RW_ROWCAP;
-    int* sjr = s_jr[wid];
-    uint16_t* snx = s_nx[wid];
+    uint32_t* sjn = s_jn[wid];
     uint32_t* keys = s_key[wid];
     uint16_t* colb = s_col[wid];
     int* rc = s_rc[wid];
@@ -274,8 +274,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
             ir = min(max(ceil_to_int(__dsub_rn(xs, 0.5)), 0), n);
         }
         if (in_smem) {
-            sjr[v - row0] = jr;
-            snx[v - row0] = (uint16_t)(next_row(v) - row0);
+            sjn[v - row0] = (uint32_t)jr | ((uint32_t)(next_row(v) - row0) << 16);
         }
         jmn = min(jmn, jr); jmx = max(jmx, jr);
         imn = min(imn, ir); imx = max(imx, ir);
@@ -454,7 +453,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
             int qh = 0, qt = 0;
             auto run = [&](uint32_t ent) {
                 const int el = (int)(ent & 0xFFFFu), en = (int)(ent >> 16);
-                const int ja = sjr[el], jb2 = sjr[en];
+                const int ja = (int)(sjn[el] & 0xFFFFu), jb2 = (int)(sjn[en] & 0xFFFFu);
                 emit(to_d2(gpos[row0 + el]), to_d2(gpos[row0 + en]), max(min(ja, jb2), w0), min(max(ja, jb2), w1 + back));
             };
             for (int e0 = 0; e0 < nrows; e0 += 32) {
@@ -462,8 +461,9 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
                 bool cr = false;
                 int en = 0;
                 if (el < nrows) {
-                    en = snx[el];
-                    const int ja = sjr[el], jb2 = sjr[en];
+                    const uint32_t jl = sjn[el];
+                    en = (int)(jl >> 16);
+                    const int ja = (int)(jl & 0xFFFFu), jb2 = (int)(sjn[en] & 0xFFFFu);
                     cr = min(max(ja, jb2), w1 + back) > max(min(ja, jb2), w0);
                 }
                 const unsigned m = __ballot_sync(FULL, cr);
