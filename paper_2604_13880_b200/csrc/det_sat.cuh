@@ -31,6 +31,7 @@
 //           the displacement u at every pixel centre (or the 8 channels).
 // All accumulation is float64; only the stored field may be float32.
 #pragma once
+#include <type_traits>
 #include "det_common.cuh"
 
 namespace det {
@@ -734,10 +735,11 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
     const bool active = x0 < n;  // n is a multiple of CPT: a thread's columns are all in or all out
     const size_t bb = (size_t)b * D.nb + band;
     const int WN = n + H;
-    A* win_dl = reinterpret_cast<A*>(s_raw3);  // DLtot(w), w in [jt-1, jb+n-1]  -> [w-(jt-1)]
-    A* win_tu = win_dl + WN;                   // Tu(w),    w in [jt-1, jb+n-2]  -> [w-(jt-1)]
-    A* win_tv = win_dl + 2 * WN;               // Tv(v),    v in [-jb, n-1-jt]   -> [v+jb]
-    A* s_rc = win_dl + 3 * WN;                 // per band row: ravg, rowfull(j+1), right boundary
+    // DLtot(w) and Tu(w) interleaved, w in [jt-1, jb+n-1] -> [w-(jt-1)]: one 2-wide load per w
+    using A2 = typename std::conditional<sizeof(A) == 4, float2, double2>::type;
+    A2* win_dt = reinterpret_cast<A2*>(s_raw3);
+    A* win_tv = reinterpret_cast<A*>(win_dt + WN);  // Tv(v), v in [-jb, n-1-jt] -> [v+jb]
+    A* s_rc = win_tv + WN;                          // per band row: ravg, rowfull(j+1), right boundary
     A* s_lut = s_rc + 3 * H + (H & 1);
     const double* rowfull = D.rowfull + (size_t)b * (n + 1);
     const double* adT = D.adT + (size_t)b * M;
@@ -746,9 +748,9 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
 
     // ---- carries (k_sat2), row constants, LUT ----
     for (int q = t; q < WN; q += blockDim.x) {
-        win_dl[q] = (jt == 0 && q == 0) ? (A)0 : (A)D.adSc[bb * WN + q];  // DLtot(-1) = 0
+        win_dt[q].x = (jt == 0 && q == 0) ? (A)0 : (A)D.adSc[bb * WN + q];  // DLtot(-1) = 0
         const int wq = jt - 1 + q;
-        win_tu[q] = (wq >= 0 && wq < M) ? (A)adT[wq] : (A)0;
+        win_dt[q].y = (wq >= 0 && wq < M) ? (A)adT[wq] : (A)0;  // Tu(w), defined up to jb+n-2
         const int iv = q - jb + n - 1;  // Tv index of v = q - jb
         win_tv[q] = (iv >= 0 && iv < M) ? (A)dgT[iv] : (A)0;
     }
@@ -843,7 +845,12 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
         if (lane == 31) s_w[slot][w] = winc;
         __syncthreads();
         A wt = lane < NW ? s_w[slot][lane] : (A)0;
-        wt = warp_incl_scan_t<A>(wt);
+        // scan of the NW warp totals: log2(NW) steps, not a full 32-lane scan
+#pragma unroll
+        for (int o = 1; o < NW; o <<= 1) {
+            const A tt = __shfl_up_sync(FULL, wt, o);
+            if (lane >= o) wt += tt;
+        }
         const A woff = __shfl_sync(FULL, wt, (w + 31) & 31);
         const A excl = (w == 0 ? (A)0 : woff) + winc - tsum;
         A ap_m1 = PF ? (A)0 : __shfl_up_sync(FULL, al[CPT - 1], 1);
@@ -873,7 +880,13 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
             const int wi0 = j + x0 - (jt - 1);
             A dlw[CPT + 1];  // DLtot(j + x - 1 + q), sliding window over this thread's columns
 #pragma unroll
-            for (int q = 0; q <= CPT; ++q) dlw[q] = win_dl[wi0 - 1 + q];
+            A tuw[CPT];
+#pragma unroll
+            for (int q = 0; q <= CPT; ++q) {
+                const A2 v = win_dt[wi0 - 1 + q];
+                dlw[q] = v.x;
+                if (q < CPT) tuw[q] = v.y;
+            }
             A ux[CPT], uy[CPT];
 #pragma unroll
             for (int k = 0; k < CPT; ++k) {
@@ -885,7 +898,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
                 const A ulpm2 = k == 0 ? ul_m2 : (k == 1 ? ul_m1 : ul[k - 2]);
                 const A urp1 = k == CPT - 1 ? ur_p : ur[k + 1];
                 const A Dw = dlw[k + 1], Dwm1 = dlw[k];
-                const A Tu = win_tu[wi0 + k - 1];
+                const A Tu = tuw[k];
                 const A Tv = win_tv[x - j + jb];
                 const A R_UV = ulpm1 + (Dw - urp1);
                 A R_UVm1 = ulnm1 + (Dw - urn[k]);
