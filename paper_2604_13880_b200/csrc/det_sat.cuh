@@ -403,10 +403,18 @@ struct WarpRing {
         if (active) {
             const int* src = q + slot * 32 * CPT + lane * CPT;
             int L[CPT];
+            if constexpr (CPT % 4 == 0) {
 #pragma unroll
-            for (int c = 0; c < CPT; c += 2) {
-                const int2 v = *reinterpret_cast<const int2*>(src + c);
-                L[c] = v.x; L[c + 1] = v.y;
+                for (int c = 0; c < CPT; c += 4) {
+                    const int4 v = *reinterpret_cast<const int4*>(src + c);
+                    L[c] = v.x; L[c + 1] = v.y; L[c + 2] = v.z; L[c + 3] = v.w;
+                }
+            } else {
+#pragma unroll
+                for (int c = 0; c < CPT; c += 2) {
+                    const int2 v = *reinterpret_cast<const int2*>(src + c);
+                    L[c] = v.x; L[c + 1] = v.y;
+                }
             }
 #pragma unroll
             for (int k = 0; k < CPT; ++k) rho[k] = __ldg(lut + (L[k] < 0 ? R : L[k]));
