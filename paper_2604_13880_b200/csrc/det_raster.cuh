@@ -618,6 +618,9 @@ __global__ void __launch_bounds__(ADV_THREADS) k_advect_rows(Topo T, Bufs D, int
 #ifndef DET_ROW_RED
 #define DET_ROW_RED 0  // 1: non-returning atomics + clash check + exact repaint (53.3k vs 54.7k: clashes are common)
 #endif
+#ifndef DET_ROW_FILL16
+#define DET_ROW_FILL16 0
+#endif
 #ifndef DET_ROW_PRE
 #define DET_ROW_PRE 4
 #endif
@@ -644,7 +647,11 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
     for (int q = 0; q < ROW_PRE; ++q) v_pre[q] = (j < n && q * 32 + lane < D.cap) ? sp[q * 32 + lane] : 0ull;
     if (!gate_open(st, gate)) return;
     if (j < n) {
+#if DET_ROW_FILL16
+        for (int i = lane; i < (n >> 2); i += 32) reinterpret_cast<uint4*>(lab_s)[i] = make_uint4(SENT, SENT, SENT, SENT);
+#else
         for (int i = lane; i < n; i += 32) lab_s[i] = SENT;  // (16-byte stores measured slower here)
+#endif
         __syncwarp();
         if (lane == 0) {
             D.rowcnt[rb] = 0;

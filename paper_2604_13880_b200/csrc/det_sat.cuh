@@ -887,8 +887,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
             const A ycm1 = yc - (A)1, c1y = (A)0.25 - (A)0.5 * yc, rmc = ravg - Cr;
             const int wi0 = j + x0 - (jt - 1);
             A dlw[CPT + 1];  // DLtot(j + x - 1 + q), sliding window over this thread's columns
-#pragma unroll
-            A tuw[CPT];
+            A tuw[CPT];      // Tu(j + x - 1 + q)
 #pragma unroll
             for (int q = 0; q <= CPT; ++q) {
                 const A2 v = win_dt[wi0 - 1 + q];
