@@ -190,9 +190,11 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     constexpr int NT1 = NT * CPT / CPT1;
     if (src == SRC_LABELS && f32 && c->sat1w && n % (32 * CPT1) == 0) {
         constexpr int NW = NT1 / 32, KP = lab_kp1(CPT1 * NT1);
-        const size_t smem1w = ((size_t)2 * (n + H - 1) + (size_t)3 * H * NW) * sizeof(float) + 16 +
-                              (size_t)NW * KP * 32 * CPT1 * sizeof(int);
-        auto fn = k_sat1w<CPT1, NT1>;
+        size_t smem1w = ((size_t)2 * (n + H - 1) + (size_t)3 * H * NW) * sizeof(float) + 16 +
+                        (size_t)NW * KP * 32 * CPT1 * sizeof(int);
+        const bool l1 = DET_SAT1W_LUTS && (size_t)lut_smem_len(R) * sizeof(float) <= 48 * 1024;
+        if (l1) smem1w += (size_t)lut_smem_len(R) * sizeof(float);
+        auto fn = l1 ? k_sat1w<CPT1, NT1, true> : k_sat1w<CPT1, NT1, false>;
         smem_optin(fn);
         fn<<<gb, NT1, smem1w, c->stream>>>(T, D, gate);
     } else if (src == SRC_LABELS) {

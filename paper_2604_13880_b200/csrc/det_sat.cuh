@@ -417,7 +417,7 @@ struct WarpRing {
                 }
             }
 #pragma unroll
-            for (int k = 0; k < CPT; ++k) rho[k] = __ldg(lut + (L[k] < 0 ? R : L[k]));
+            for (int k = 0; k < CPT; ++k) rho[k] = lut[L[k] < 0 ? R : L[k]];  // (global: read-only path)
         } else {
 #pragma unroll
             for (int k = 0; k < CPT; ++k) rho[k] = (A)0;
@@ -425,10 +425,13 @@ struct WarpRing {
     }
 };
 
+#ifndef DET_SAT1W_LUTS
+#define DET_SAT1W_LUTS 1
+#endif
 #ifndef DET_SAT1W_CPT
 #define DET_SAT1W_CPT 4  // columns per thread of k_sat1w at CPT=4 configs (2: 49.7k, 4: 52.6k it/s)
 #endif
-template <int CPT, int NT>
+template <int CPT, int NT, bool LUTS>
 __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
     using A = float;
     constexpr int NW = NT / 32, W = 32 * CPT, KP = lab_kp1(CPT * NT);
@@ -448,7 +451,12 @@ __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
     A* s_rows = ad + L;
     A* exD = s_rows + H * NW;
     A* exA = exD + NW * H;
-    const A* lut = reinterpret_cast<const A*>(D.lutf + (size_t)b * (R + 1));
+    const A* glut = reinterpret_cast<const A*>(D.lutf + (size_t)b * (R + 1));
+    // LUTS: the LUT staged in shared memory after the rings
+    A* s_lut = reinterpret_cast<A*>(align16(exA + NW * H) + NW * KP * W);
+    if (LUTS)
+        for (int i = t; i <= R; i += NT) s_lut[i] = __ldg(glut + i);
+    const A* lut = LUTS ? s_lut : glut;
     WarpRing<CPT, KP> ring;
     ring.q = align16(exA + NW * H) + w * KP * W;
     ring.bar = s_bar + w * KP;
@@ -459,6 +467,7 @@ __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
     ring.bytes = (unsigned)(max(0, min(W, n - c0)) * 4);
     ring.init(lane);
     ring.prologue(lane);
+    if (LUTS) __syncthreads();  // LUT published
 
     A cs[CPT], pd[CPT], pa[CPT];
 #pragma unroll
