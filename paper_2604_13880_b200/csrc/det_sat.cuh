@@ -628,8 +628,11 @@ __global__ void __launch_bounds__(SAT2_THREADS) k_sat2(Bufs D, int gate) {
 // (one warp per part, 32 lanes per CTA), so every thread keeps at most SAT2P_CH band values in
 // flight and the lane's bands are fetched in one memory round trip; the parts' sums are combined
 // through shared memory.  Same outputs as k_sat2 (summation grouped by part).
-constexpr int SAT2_PARTS = 4;
-constexpr int SAT2P_CH = 8;
+#ifndef DET_SAT2_PARTS
+#define DET_SAT2_PARTS 4
+#endif
+constexpr int SAT2_PARTS = DET_SAT2_PARTS;
+constexpr int SAT2P_CH = 32 / DET_SAT2_PARTS;  // bands per part in registers (32 bands at 1024^2)
 
 __global__ void __launch_bounds__(32 * SAT2_PARTS) k_sat2p(Bufs D, int gate) {
     __shared__ double s_part[SAT2_PARTS][32];
