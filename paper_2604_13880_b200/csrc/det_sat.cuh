@@ -99,7 +99,10 @@ __host__ __device__ __forceinline__ int lut_smem_len(int R) { return (R + 2) & ~
 // with row r + KP - 1, so the prefetch distance is KP - 1 rows.
 // ring slots (prefetch distance KP - 1 rows): 4, or 2 for 8192-column rows, whose ring would
 // not fit next to the carry windows in one CTA's shared memory
-__host__ __device__ constexpr int lab_kp(int cols) { return cols >= 8192 ? 2 : 4; }
+#ifndef DET_KP3
+#define DET_KP3 4
+#endif
+__host__ __device__ constexpr int lab_kp(int cols) { return cols >= 8192 ? 2 : (cols >= 4096 ? 4 : DET_KP3); }
 // k_sat1 takes each row one iteration early (its LUT gathers overlap the previous row), so it keeps
 // a deeper ring where shared memory allows
 #ifndef DET_KP1
