@@ -75,12 +75,17 @@ __device__ __forceinline__ void load_rho(const Bufs& D, const SatSrc& S, const A
 }
 
 // The cartogram's LUT in the accumulator type: global pointer, copied to `s_lut` when LUTS.
-template <typename A, bool LUTS>
+// BIAS: the shared copy is stored background-first (s_lut[0] = background, s_lut[r+1] = rank r) and
+// the returned pointer is s_lut + 1, so a label L >= -1 indexes it directly (no background select).
+template <typename A, bool LUTS, bool BIAS = false>
 __device__ __forceinline__ const A* band_lut(const Bufs& D, int R, int b, A* s_lut) {
     const A* g = sizeof(A) == 4 ? reinterpret_cast<const A*>(D.lutf + (size_t)b * (R + 1))
                                 : reinterpret_cast<const A*>(D.lut + (size_t)b * (R + 1));
     if constexpr (!LUTS) {
         return g;
+    } else if constexpr (BIAS) {
+        for (int i = threadIdx.x; i <= R; i += blockDim.x) s_lut[i] = __ldg(g + (i == 0 ? R : i - 1));
+        return s_lut + 1;  // published by the caller's first barrier
     } else {
         for (int i = threadIdx.x; i <= R; i += blockDim.x) s_lut[i] = __ldg(g + i);
         return s_lut;  // published by the caller's first barrier
@@ -164,7 +169,7 @@ struct LabelRing {
         }
     }
     // labels of row j -> residual densities (refilling the previous row's slot first)
-    template <typename A>
+    template <typename A, bool BIAS = false>
     __device__ __forceinline__ void take(int j, const A* lut, int R, A (&rho)[CPT]) {
         const int r = j - jt;
         if (threadIdx.x == 0) issue(j + KP - 1, (r + KP - 1) % KP);
@@ -186,7 +191,7 @@ struct LabelRing {
                 }
             }
 #pragma unroll
-            for (int k = 0; k < CPT; ++k) rho[k] = lut[L[k] < 0 ? R : L[k]];
+            for (int k = 0; k < CPT; ++k) rho[k] = BIAS ? lut[L[k]] : lut[L[k] < 0 ? R : L[k]];
         } else {
 #pragma unroll
             for (int k = 0; k < CPT; ++k) rho[k] = (A)0;
@@ -383,7 +388,7 @@ struct WarpRing {
     }
     // row j -> residual densities; refills row j-1's slot (every lane finished reading it: the
     // __syncwarp below orders those reads before lane 0's async-proxy write)
-    template <typename A>
+    template <typename A, bool BIAS = false>
     __device__ __forceinline__ void take(int j, int lane, bool active, const A* lut, int R, A (&rho)[CPT]) {
         const int r = j - jt;
         __syncwarp();
@@ -420,7 +425,7 @@ struct WarpRing {
                 }
             }
 #pragma unroll
-            for (int k = 0; k < CPT; ++k) rho[k] = lut[L[k] < 0 ? R : L[k]];  // (global: read-only path)
+            for (int k = 0; k < CPT; ++k) rho[k] = BIAS ? lut[L[k]] : lut[L[k] < 0 ? R : L[k]];
         } else {
 #pragma unroll
             for (int k = 0; k < CPT; ++k) rho[k] = (A)0;
@@ -457,9 +462,9 @@ __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
     const A* glut = reinterpret_cast<const A*>(D.lutf + (size_t)b * (R + 1));
     // LUTS: the LUT staged in shared memory after the rings
     A* s_lut = reinterpret_cast<A*>(align16(exA + NW * H) + NW * KP * W);
-    if (LUTS)
-        for (int i = t; i <= R; i += NT) s_lut[i] = __ldg(glut + i);
-    const A* lut = LUTS ? s_lut : glut;
+    if (LUTS)  // background-first (see band_lut): labels index s_lut + 1 directly
+        for (int i = t; i <= R; i += NT) s_lut[i] = __ldg(glut + (i == 0 ? R : i - 1));
+    const A* lut = LUTS ? s_lut + 1 : glut;
     WarpRing<CPT, KP> ring;
     ring.q = align16(exA + NW * H) + w * KP * W;
     ring.bar = s_bar + w * KP;
@@ -476,12 +481,12 @@ __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
 #pragma unroll
     for (int k = 0; k < CPT; ++k) cs[k] = pd[k] = pa[k] = (A)0;
     A rho_n[CPT];
-    ring.take(jt, lane, active, lut, R, rho_n);
+    ring.template take<A, LUTS>(jt, lane, active, lut, R, rho_n);
     for (int j = jt; j <= jb; ++j) {
         A rho[CPT];
 #pragma unroll
         for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
-        if (j < jb) ring.take(j + 1, lane, active, lut, R, rho_n);  // next row's gathers in flight
+        if (j < jb) ring.template take<A, LUTS>(j + 1, lane, active, lut, R, rho_n);  // next row's gathers in flight
         A ts = (A)0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) ts += rho[k];
@@ -784,7 +789,9 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
         s_rc[H + q] = (A)r1;
         s_rc[2 * H + q] = (A)(r0 - rf_top);
     }
-    const A* lut = band_lut<A, LUTS>(D, R, b, s_lut);
+    // float ring path: background-first shared LUT, labels index it directly (band_lut BIAS)
+    constexpr bool LB = LUTS && SRC == SRC_LABELS && sizeof(A) == 4;
+    const A* lut = band_lut<A, LUTS, LB>(D, R, b, s_lut);
     // cc[k]: column-total average cavg(x) = (colfull(x) + colfull(x+1))/2 for the field,
     // colfull(x+1) for the channel dump
     // PF (float32 field): al[k] carries the column-pair sum alpha(j-1, x-1) + alpha(j-1, x) instead
@@ -842,7 +849,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
     A rho_n[CPT];
     if (!RING) load_rho<CPT, SRC, A, LUTS>(D, S, lut, R, b, jt, x0, rho_n);
     // DET_SAT3_PIPE: row j+1's label wait and LUT reads are issued at the top of row j (as in k_sat1)
-    if (RING && DET_SAT3_PIPE) ring.take(jt, lut, R, rho_n);
+    if (RING && DET_SAT3_PIPE) ring.template take<A, LB>(jt, lut, R, rho_n);
 
     int slot = 0, ps = 2;  // rotating boundary slots: (j - jt) % 3, (j - jt + 2) % 3
     for (int j = jt; j <= jb; ++j) {
@@ -850,9 +857,9 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
         if (RING && DET_SAT3_PIPE) {
 #pragma unroll
             for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
-            if (j < jb) ring.take(j + 1, lut, R, rho_n);  // refills row j's slot: every take(j) preceded barrier j-1
+            if (j < jb) ring.template take<A, LB>(j + 1, lut, R, rho_n);  // refills row j's slot: every take(j) preceded barrier j-1
         } else if (RING) {
-            ring.take(j, lut, R, rho);
+            ring.template take<A, LB>(j, lut, R, rho);
         } else {
 #pragma unroll
             for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
