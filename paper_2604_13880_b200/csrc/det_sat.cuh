@@ -481,6 +481,7 @@ __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
 #pragma unroll
     for (int k = 0; k < CPT; ++k) cs[k] = pd[k] = pa[k] = (A)0;
     A rho_n[CPT];
+    A ts_even = (A)0;  // the even row's partial, reduced together with the odd row (H is even)
     ring.template take<A, LUTS>(jt, lane, active, lut, R, rho_n);
     for (int j = jt; j <= jb; ++j) {
         A rho[CPT];
@@ -490,8 +491,22 @@ __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
         A ts = (A)0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) ts += rho[k];
-        ts = warp_sum(ts);
-        if (lane == 0) s_rows[(j - jt) * NW + w] = ts;  // row totals are summed after the sweep
+        // slice row totals, two rows per butterfly: after one exchange the lower half-warp holds
+        // the even row's partials and the upper half the odd row's, so 5 shuffles serve 2 rows
+        if (((j - jt) & 1) == 0) {
+            ts_even = ts;
+            if (j == jb) {  // odd band height (H = 1): the last row is reduced alone
+                const A t1 = warp_sum(ts);
+                if (lane == 0) s_rows[(j - jt) * NW + w] = t1;
+            }
+        } else {
+            const bool up = (lane & 16) != 0;
+            A keep = (up ? ts : ts_even) + __shfl_xor_sync(FULL, up ? ts_even : ts, 16);
+#pragma unroll
+            for (int o = 8; o; o >>= 1) keep += __shfl_xor_sync(FULL, keep, o);
+            if (lane == 0) s_rows[(j - 1 - jt) * NW + w] = keep;
+            if (lane == 16) s_rows[(j - jt) * NW + w] = keep;
+        }
         A left = __shfl_up_sync(FULL, pd[CPT - 1], 1);
         A right = __shfl_down_sync(FULL, pa[0], 1);
         if (lane == 0) left = (A)0;    // partials restart at the slice edge

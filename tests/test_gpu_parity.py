@@ -436,3 +436,20 @@ def test_float_state_start_raster_is_exact(P):
     # the float32 state's own raster is still bit-exact against the oracle on its (float32) rows
     ref = O.FlatMap.from_mapmodel(r32.state.mapmodel).labels(8)
     assert np.array_equal(r32.state.labels.labels, ref)
+
+
+def test_band_height_independence(P):
+    """The band kernels give the same cartogram for any band height (1, 2, 16 or the automatic
+    one): k_sat1w's paired row-total butterfly, its odd-height tail and the slice-edge joins."""
+    from paper_2604_13880_b200.synthetic import voronoi_map
+
+    m = voronoi_map(60, seed=2, target_unique=6000, sigma=0.6)
+    crit = P.StoppingCriteria(1e-300, 10**9, 5)
+    outs = []
+    for h in (0, 1, 2, 16):
+        be = P.BatchEngine(m, np.atleast_2d(m.statistics()), criteria=crit, k=8, bdv_multiplier=1.0)
+        ctx = be._ctx()
+        if h:
+            ctx.set_band_height(h)
+        outs.append(be.run_all(crit)[0].state.mapmodel.vertex_array())
+    assert max(np.abs(o - outs[0]).max() for o in outs) <= 1e-5
