@@ -88,9 +88,9 @@ int det_device_info(int device, char *buf, int buflen);
  * storage precision (0: float32, 1: float64; accumulation is float64 always). */
 int det_ctx_create(int device, int k, int field_f64, det_ctx **out);
 void det_ctx_destroy(det_ctx *ctx);
-/* number of frame groups run as parallel CUDA-graph branches (default 2) */
+/* number of frame groups run as parallel CUDA-graph branches (default 8, clamped to the batch) */
 int det_set_groups(det_ctx *ctx, int groups);
-/* band height of the integral-image kernels (power of two, default: auto) */
+/* band height of the integral-image kernels (power of two <= n; 0 restores the automatic choice) */
 int det_set_band_height(det_ctx *ctx, int h);
 
 /* Topology + initial vertices of one map: MapModel.vertex_array() rows

@@ -571,11 +571,12 @@ int det_set_groups(det_ctx* ctx, int groups) {
 }
 
 int det_set_band_height(det_ctx* ctx, int h) {
-    if (!ctx || h < 1 || (h & (h - 1)) || h > ctx->n) return fail(ctx, DET_E_ARG, "band height must be a power of two <= n");
+    if (!ctx || h < 0 || (h & (h - 1)) || h > ctx->n)
+        return fail(ctx, DET_E_ARG, "band height must be a power of two <= n (0: automatic)");
     cudaSetDevice(ctx->device);
-    ctx->H = h;
-    ctx->nb = ctx->n / h;
-    ctx->h_fixed = true;
+    ctx->h_fixed = h != 0;
+    ctx->H = h ? h : auto_band_height(ctx->n, std::max(ctx->B, 1));
+    ctx->nb = ctx->n / ctx->H;
     invalidate_graph(ctx);
     if (ctx->B > 0) return alloc_sat(ctx, ctx->B);
     return DET_OK;

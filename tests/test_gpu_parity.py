@@ -452,4 +452,5 @@ def test_band_height_independence(P):
         if h:
             ctx.set_band_height(h)
         outs.append(be.run_all(crit)[0].state.mapmodel.vertex_array())
+        ctx.set_band_height(0)  # back to the automatic height for the shared per-thread context
     assert max(np.abs(o - outs[0]).max() for o in outs) <= 1e-5
