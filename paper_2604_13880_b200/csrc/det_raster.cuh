@@ -618,6 +618,9 @@ __global__ void __launch_bounds__(ADV_THREADS) k_advect_rows(Topo T, Bufs D, int
 #ifndef DET_ROW_RED
 #define DET_ROW_RED 0  // 1: non-returning atomics + clash check + exact repaint (53.3k vs 54.7k: clashes are common)
 #endif
+#ifndef DET_ROW_TMA
+#define DET_ROW_TMA 1
+#endif
 #ifndef DET_ROW_FILL16
 #define DET_ROW_FILL16 0
 #endif
@@ -767,9 +770,25 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
         __syncwarp();
         // the label texture holds region RANKS (-1 = background); det_get_labels maps them
         // back to region indices (raster.py:107 stores indices) -- saves a gather per pixel
-        int4* lab4 = reinterpret_cast<int4*>(D.labels + (size_t)b * D.nn + (size_t)j * n);
+        int* lab_g = D.labels + (size_t)b * D.nn + (size_t)j * n;
+#if DET_ROW_TMA
+        // the row leaves shared memory as one 1-D TMA bulk store issued by lane 0 (SENT == -1
+        // bitwise); the generic-proxy paint is fenced for the async proxy first, and lane 0 waits
+        // for the store to complete before the warp's shared row can go away
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(lab_g),
+                         "r"((unsigned)__cvta_generic_to_shared(lab_s)), "r"((unsigned)n * 4u)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+        }
+        __syncwarp();
+#else
+        int4* lab4 = reinterpret_cast<int4*>(lab_g);
         const int4* src4 = reinterpret_cast<const int4*>(lab_s);
         for (int i = lane; i < (n >> 2); i += 32) lab4[i] = src4[i];  // SENT == -1 bitwise
+#endif
         if (lost) {  // order the (rare) count corrections before this CTA signs off
             __threadfence();
         }
