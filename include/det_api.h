@@ -84,9 +84,16 @@ const char *det_last_error(const det_ctx *ctx);
 /* device info string (name, SMs, L2) for reports */
 int det_device_info(int device, char *buf, int buflen);
 
-/* k in [4, 13] (raster.py:138-139); field_f64 selects the displacement-field
- * storage precision (0: float32, 1: float64; accumulation is float64 always). */
-int det_ctx_create(int device, int k, int field_f64, det_ctx **out);
+/* Arithmetic precision of the iteration (CartogramEngine's field_dtype):
+ *   DET_PREC_FLOAT64  float64 field, vertex state and sums: the reference's arithmetic
+ *                     (engine.py:170-180), trajectory-identical to it;
+ *   DET_PREC_MIXED    float32 displacement field and in-band sums, float64 vertex state,
+ *                     position update and raster crossings;
+ *   DET_PREC_FLOAT32  float32 field and vertex state (float64 crossings and carries). */
+enum { DET_PREC_FLOAT32 = 0, DET_PREC_FLOAT64 = 1, DET_PREC_MIXED = 2 };
+/* k in [4, 13] (raster.py:138-139); precision is one of DET_PREC_*.  Replaces the per-engine
+ * set-up of CartogramEngine.__init__ (engine.py:98-141): one context per thread/stream. */
+int det_ctx_create(int device, int k, int precision, det_ctx **out);
 void det_ctx_destroy(det_ctx *ctx);
 /* number of frame groups run as parallel CUDA-graph branches (default 8, clamped to the batch) */
 int det_set_groups(det_ctx *ctx, int groups);
@@ -155,6 +162,13 @@ int det_get_results(det_ctx *ctx, double *xy_out, int64_t *counts_out, double *e
 int det_field(det_ctx *ctx, const double *d, double *u_out, double *channels_out, double *total_out);
 /* t(d) itself at pixel centres (mapping_grid, displacement.py:102-131), n*n*2 */
 int det_mapping(det_ctx *ctx, const double *d, double *t_out);
+/* mapping_grid (displacement.py:102-131) of a given channel set (8*n*n float64: alpha, beta,
+ * gamma, delta, alpha_t, beta_t, gamma_t, delta_t; total = C), minus `base` (n*n*2) when base is
+ * non-NULL (residual_field, displacement.py:198-206).  Reference float64 op order. */
+int det_mapping_channels(det_ctx *ctx, const double *channels, double total, const double *base, double *t_out);
+/* mapping_point (displacement.py:150-170) at n_pts points (x, y) of the same channel set */
+int det_mapping_points(det_ctx *ctx, const double *channels, double total, const double *xy, int n_pts,
+                       double *out);
 /* build_density (raster.py:166-184) of a label texture: d_out n*n, counts_out n_regions+1 */
 int det_density(det_ctx *ctx, const int32_t *labels, const double *stats, int n_regions, double bdv, double *d_out,
                 int64_t *counts_out);

@@ -16,14 +16,16 @@ from ._lib import Context
 _tls = threading.local()
 
 
-def get_context(k: int, device: int = 0, field_f64: bool = False) -> Context:
+def get_context(k: int, device: int = 0, precision: str = "float32") -> Context:
+    """The calling thread's context for (device, k, precision); precision is a field_dtype
+    ("float32", "float64" or "mixed")."""
     cache = getattr(_tls, "cache", None)
     if cache is None:
         cache = _tls.cache = {}
-    key = (device, k, bool(field_f64))
+    key = (device, k, precision)
     ctx = cache.get(key)
     if ctx is None:
-        ctx = cache[key] = Context(k, device=device, field_f64=field_f64)
+        ctx = cache[key] = Context(k, device=device, precision=precision)
     return ctx
 
 

@@ -20,6 +20,8 @@ LIB_PATH = os.environ.get("DET_LIB") or os.path.join(_HERE, "_det.so")  # DET_LI
 DET_OK, DET_E_ARG, DET_E_CUDA, DET_E_RASTER, DET_E_COLLAPSE, DET_E_NUMERIC, DET_E_VALUE, DET_E_STATE = range(8)
 STOP_NAMES = {1: "converged", 2: "stagnation", 3: "max-iterations"}
 STOP_COLLAPSED, STOP_BDV, STOP_NEGINDEX = 4, 5, 6
+# field_dtype -> DET_PREC_* (include/det_api.h)
+PRECISIONS = {"float32": 0, "float64": 1, "mixed": 2}
 
 _c_double_p = ctypes.POINTER(ctypes.c_double)
 _c_int32_p = ctypes.POINTER(ctypes.c_int32)
@@ -184,11 +186,14 @@ class DetError(RuntimeError):
 class Context:
     """One device context (CUDA stream + buffers) of the DET engine."""
 
-    def __init__(self, k: int, device: int = 0, field_f64: bool = False):
+    def __init__(self, k: int, device: int = 0, precision: str = "float32"):
+        if precision not in PRECISIONS:
+            raise ValueError(f"field_dtype must be one of {sorted(PRECISIONS)}")
         self.lib = load_library()
-        self.k, self.n, self.device, self.field_f64 = k, 1 << k, device, bool(field_f64)
+        self.k, self.n, self.device, self.precision = k, 1 << k, device, precision
+        self.field_f64 = precision == "float64"
         h = ctypes.c_void_p()
-        rc = self.lib.det_ctx_create(device, k, int(field_f64), ctypes.byref(h))
+        rc = self.lib.det_ctx_create(device, k, PRECISIONS[precision], ctypes.byref(h))
         if rc != DET_OK:
             raise DetError(rc, "det_ctx_create failed (no usable CUDA device?)")
         self.h = h

@@ -20,6 +20,7 @@
 #include "det_raster.cuh"
 #include "det_sat.cuh"
 #include "det_metrics.cuh"
+#include "det_mapping.cuh"
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_reduce.cuh>
@@ -57,7 +58,7 @@ constexpr int kGraphIters = 16;
 }  // namespace
 
 struct det_ctx {
-    int device = 0, k = 10, n = 1024, f64 = 0, H = 8;
+    int device = 0, k = 10, n = 1024, f64 = 0, s64 = 0, H = 8;  // f64: float64 field; s64: float64 vertex state
     cudaStream_t stream = nullptr;
     std::string err;
     // topology
@@ -188,15 +189,22 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     // where the band kernels use 4)
     constexpr int CPT1 = (CPT == 4 && NT * 4 / DET_SAT1W_CPT <= 1024 && NT * 4 / DET_SAT1W_CPT >= 32) ? DET_SAT1W_CPT : CPT;
     constexpr int NT1 = NT * CPT / CPT1;
-    if (src == SRC_LABELS && f32 && c->sat1w && n % (32 * CPT1) == 0) {
+    if (src == SRC_LABELS && out == OUT_U && c->sat1w && n % (32 * CPT1) == 0 && (f32 || n <= 4096)) {
+        // barrier-free band sums in the field's arithmetic type (float32 or float64)
         constexpr int NW = NT1 / 32, KP = lab_kp1(CPT1 * NT1);
-        size_t smem1w = ((size_t)2 * (n + H - 1) + (size_t)3 * H * NW) * sizeof(float) + 16 +
+        size_t smem1w = ((size_t)2 * (n + H - 1) + (size_t)3 * H * NW) * sa + 16 +
                         (size_t)NW * KP * 32 * CPT1 * sizeof(int);
-        const bool l1 = DET_SAT1W_LUTS && (size_t)lut_smem_len(R) * sizeof(float) <= 48 * 1024;
-        if (l1) smem1w += (size_t)lut_smem_len(R) * sizeof(float);
-        auto fn = l1 ? k_sat1w<CPT1, NT1, true> : k_sat1w<CPT1, NT1, false>;
-        smem_optin(fn);
-        fn<<<gb, NT1, smem1w, c->stream>>>(T, D, gate);
+        const bool l1 = DET_SAT1W_LUTS && (size_t)lut_smem_len(R) * sa <= 48 * 1024;
+        if (l1) smem1w += (size_t)lut_smem_len(R) * sa;
+        if (f32) {
+            auto fn = l1 ? k_sat1w<CPT1, NT1, true, float> : k_sat1w<CPT1, NT1, false, float>;
+            smem_optin(fn);
+            fn<<<gb, NT1, smem1w, c->stream>>>(T, D, gate);
+        } else {
+            auto fn = l1 ? k_sat1w<CPT1, NT1, true, double> : k_sat1w<CPT1, NT1, false, double>;
+            smem_optin(fn);
+            fn<<<gb, NT1, smem1w, c->stream>>>(T, D, gate);
+        }
     } else if (src == SRC_LABELS) {
         // k_sat1 gathers the LUT through L1 (__ldg): staging it per CTA measured slower there
         if (f32) DET_SAT1(SRC_LABELS, float, false);
@@ -206,7 +214,7 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     }
 #undef DET_SAT1
     const int lanes = n + 2 * (2 * n - 1);
-    if (f32)  // float32 field: band carries split over the warps of a CTA (one memory round trip)
+    if (src == SRC_LABELS && out == OUT_U)  // band carries split over the warps of a CTA (one memory round trip)
         k_sat2p<<<dim3((lanes + 31) / 32 + 1, B), 32 * SAT2_PARTS, 0, c->stream>>>(D, gate);
     else
         k_sat2<<<dim3((lanes + SAT2_THREADS - 1) / SAT2_THREADS + 1, B), SAT2_THREADS, 0, c->stream>>>(D, gate);
@@ -265,14 +273,15 @@ static void launch_sat(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S
 static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, int gate, int src,
                           bool f64_rows = false) {
     const dim3 g((c->R + RW_WARPS - 1) / RW_WARPS, c->B);
-    if (c->f64 || f64_rows) k_region<double><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
-    else k_region<float><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
+    if (c->f64) k_region<double, double><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
+    else if (c->s64 || f64_rows) k_region<float, double><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
+    else k_region<float, float><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
 }
 
 // One iteration's advect + raster: the flat advect kernel then a raster-only k_region (float32
 // state), or k_region's fused advect phase.  Returns the number of kernels launched.
 static int launch_advect_raster(det_ctx* c, const Topo& T, const Bufs& D, int gate, int region_mode) {
-    if (!c->f64 && c->split_adv && (region_mode & M_ADVECT)) {
+    if (!c->s64 && c->split_adv && (region_mode & M_ADVECT)) {
         const int per = ADV_THREADS * ADV_RPT;
         k_advect_rows<<<dim3((T.n_rows + per - 1) / per, c->B), ADV_THREADS, 0, c->stream>>>(T, D, gate);
         if (region_mode & M_RASTER) launch_region(c, T, D, M_RASTER | M_POSTADV, gate, 0);
@@ -416,7 +425,7 @@ static int alloc_batch(det_ctx* ctx, int B) {
     CK(ctx->pos_init.alloc((size_t)B * ctx->n_rows));
     CK(ctx->pos0.alloc((size_t)B * ctx->n_rows));
     CK(ctx->best.alloc((size_t)B * ctx->n_rows));
-    if (!ctx->f64) CK(ctx->rows64.alloc((size_t)B * ctx->n_rows));
+    if (!ctx->s64) CK(ctx->rows64.alloc((size_t)B * ctx->n_rows));
     CK(ctx->labels.alloc((size_t)B * nn));
     CK(ctx->cnt_acc.alloc((size_t)B * (ctx->R + 1)));
     CK(ctx->cnt_state.alloc((size_t)B * (ctx->R + 1)));
@@ -449,7 +458,7 @@ static int alloc_batch(det_ctx* ctx, int B) {
 static int raster_start(det_ctx* ctx) {
     for (int attempt = 0; attempt < 8; ++attempt) {
         const long long nrow = (long long)ctx->B * ctx->n_rows;
-        if (ctx->f64) {
+        if (ctx->s64) {
             CK(cudaMemcpyAsync(ctx->pos0.p, ctx->pos_init.p, (size_t)nrow * sizeof(double2), cudaMemcpyDeviceToDevice,
                                ctx->stream));
         } else {  // float32 state: the start rows rounded once; the start raster stays on the exact rows
@@ -528,10 +537,10 @@ int det_device_info(int device, char* buf, int buflen) {
     return DET_OK;
 }
 
-int det_ctx_create(int device, int k, int field_f64, det_ctx** out) {
+int det_ctx_create(int device, int k, int precision, det_ctx** out) {
     if (!out) return DET_E_ARG;
     *out = nullptr;
-    if (k < 4 || k > 13) return DET_E_ARG;
+    if (k < 4 || k > 13 || precision < DET_PREC_FLOAT32 || precision > DET_PREC_MIXED) return DET_E_ARG;
     det_ctx* ctx = new det_ctx();
     if (const char* e = getenv("DET_SEP_CTRL")) ctx->sep_ctrl = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SPLIT_ADVECT")) ctx->split_adv = atoi(e) != 0;  // A/B switch (diagnostics)
@@ -539,7 +548,8 @@ int det_ctx_create(int device, int k, int field_f64, det_ctx** out) {
     ctx->device = device;
     ctx->k = k;
     ctx->n = 1 << k;
-    ctx->f64 = field_f64 ? 1 : 0;
+    ctx->f64 = precision == DET_PREC_FLOAT64;
+    ctx->s64 = precision != DET_PREC_FLOAT32;
     ctx->H = std::min(8, ctx->n);
     ctx->nb = ctx->n / ctx->H;
     cudaError_t e = cudaSetDevice(device);
@@ -985,7 +995,7 @@ static const double2* state_rows(det_ctx* ctx, int b) {
     if (!ctx->ran) return ctx->pos_init.p + off;
     const int src = result_src(ctx, b);
     const double2* p = src == 2 ? ctx->best.p : ctx->pos0.p;
-    if (ctx->f64) return p + off;
+    if (ctx->s64) return p + off;
     // float32 state: widen cartogram b's rows into its slot of rows64 (stream-ordered)
     if (ctx->rows64.alloc((size_t)ctx->B * ctx->n_rows) != cudaSuccess) return nullptr;
     k_rows_to_f64<<<(unsigned)std::min<int>((ctx->n_rows + 255) / 256, 2048), 256, 0, ctx->stream>>>(
@@ -1052,7 +1062,7 @@ int det_get_results(det_ctx* ctx, double* xy_out, int64_t* counts_out, double* e
     const int B = ctx->B, R = ctx->R;
     cudaStream_t s = ctx->stream;
     if (xy_out) {
-        bool all_state = !ctx->f64;  // float32 state, no frame returning its best rows: one widen, one copy
+        bool all_state = !ctx->s64;  // float32 state, no frame returning its best rows: one widen, one copy
         for (int b = 0; b < B && all_state; ++b) all_state = result_src(ctx, b) == 0;
         if (all_state) {
             const long long len = (long long)B * ctx->n_rows;
@@ -1155,6 +1165,50 @@ int det_mapping(det_ctx* ctx, const double* d, double* t_out) {
     if (!ctx || !d || !t_out) return fail(ctx, DET_E_ARG, "bad arguments");
     cudaSetDevice(ctx->device);
     return field_impl(ctx, d, t_out, nullptr, nullptr, true);
+}
+
+// mapping_grid / residual_field (displacement.py:102-131,198-206) from given channels
+int det_mapping_channels(det_ctx* ctx, const double* channels, double total, const double* base, double* t_out) {
+    if (!ctx || !channels || !t_out) return fail(ctx, DET_E_ARG, "bad arguments");
+    if (!(total > 0)) return fail(ctx, DET_E_NUMERIC, "mapping undefined for zero total density");
+    cudaSetDevice(ctx->device);
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    DVec<double> ch, bs, out;
+    CK(ch.alloc(nn * 8));
+    CK(out.alloc(nn * 2));
+    CK(cudaMemcpyAsync(ch.p, channels, nn * 8 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    if (base) {
+        CK(bs.alloc(nn * 2));
+        CK(cudaMemcpyAsync(bs.p, base, nn * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    k_map_grid<<<(unsigned)std::min<size_t>((nn + 255) / 256, 148 * 16), 256, 0, ctx->stream>>>(
+        ch.p, total, ctx->n, base ? bs.p : nullptr, out.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(t_out, out.p, nn * 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return DET_OK;
+}
+
+// mapping_point (displacement.py:150-170) at n_pts points from given channels
+int det_mapping_points(det_ctx* ctx, const double* channels, double total, const double* xy, int n_pts,
+                       double* out) {
+    if (!ctx || !channels || !xy || !out || n_pts < 0) return fail(ctx, DET_E_ARG, "bad arguments");
+    if (!(total > 0)) return fail(ctx, DET_E_NUMERIC, "mapping undefined for zero total density");
+    cudaSetDevice(ctx->device);
+    if (n_pts == 0) return DET_OK;
+    const size_t nn = (size_t)ctx->n * ctx->n;
+    DVec<double> ch, pin, pout;
+    CK(ch.alloc(nn * 8));
+    CK(pin.alloc((size_t)n_pts * 2));
+    CK(pout.alloc((size_t)n_pts * 2));
+    CK(cudaMemcpyAsync(ch.p, channels, nn * 8 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(pin.p, xy, (size_t)n_pts * 2 * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    k_map_points<<<(n_pts + 127) / 128, 128, 0, ctx->stream>>>(ch.p, total, ctx->n, (const double2*)pin.p, n_pts,
+                                                              (double2*)pout.p);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, pout.p, (size_t)n_pts * 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return DET_OK;
 }
 
 int det_density(det_ctx* ctx, const int32_t* labels, const double* stats, int n_regions, double bdv, double* d_out,

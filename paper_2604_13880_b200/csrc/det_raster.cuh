@@ -195,7 +195,10 @@ __device__ __forceinline__ int warp_excl_scan_int(int v, int lane, int* total) {
     return x - v;
 }
 
-template <typename UT>
+// UT: field element type (float / double); ST: vertex-state element type.  <float, float> is the
+// float32 path, <double, double> the float64 path, <float, double> the mixed path (float32 field,
+// float64 state and position update).
+template <typename UT, typename ST = UT>
 #ifndef DET_RW_MINB
 #define DET_RW_MINB (32 / DET_RW_WARPS)  // 32 resident warps per SM (64 registers)
 #endif
@@ -237,9 +240,9 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
         return v + 1 < e ? v + 1 : T.ring_start[q];
     };
 
-    // vertex rows: float64 on the float64-field path, float32 on the float32-field path
-    using PT = typename Vec2<UT>::type;
-    constexpr bool FS = sizeof(UT) == 4;
+    // vertex rows: float64 on the float64 and mixed paths, float32 on the float32 path
+    using PT = typename Vec2<ST>::type;
+    constexpr bool FS = sizeof(ST) == 4;
     // the state rows live in pos0 and are advected IN PLACE: each row is read and rewritten by the
     // same lane, and other lanes read it only after a __syncwarp (no ping-pong, so the buffer
     // does not depend on the iteration counter and the row loads need no state round trip)

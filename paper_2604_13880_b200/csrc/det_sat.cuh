@@ -199,6 +199,17 @@ struct LabelRing {
     }
 };
 
+// 256-bit global stores (sm_100: STG.256): one whole 32-byte sector per thread and instruction
+__device__ __forceinline__ void st_global_v4f64(void* p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+__device__ __forceinline__ void st_global_v8f32(void* p, float a, float b, float c, float d, float e, float f,
+                                                float g, float h) {
+    asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(a), "f"(b), "f"(c),
+                 "f"(d), "f"(e), "f"(f), "f"(g), "f"(h)
+                 : "memory");
+}
+
 template <typename A>
 __device__ __forceinline__ A warp_incl_scan_t(A v) {
     const int lane = threadIdx.x & 31;
@@ -439,9 +450,8 @@ struct WarpRing {
 #ifndef DET_SAT1W_CPT
 #define DET_SAT1W_CPT 4  // columns per thread of k_sat1w at CPT=4 configs (2: 49.7k, 4: 52.6k it/s)
 #endif
-template <int CPT, int NT, bool LUTS>
+template <int CPT, int NT, bool LUTS, typename A = float>
 __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
-    using A = float;
     constexpr int NW = NT / 32, W = 32 * CPT, KP = lab_kp1(CPT * NT);
     // dg[L] | ad[L] | row partials [H][NW] | exitD [NW][H] | exitA [NW][H] | rings (16-B aligned)
     extern __shared__ unsigned char s_raw1[];
@@ -459,7 +469,8 @@ __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
     A* s_rows = ad + L;
     A* exD = s_rows + H * NW;
     A* exA = exD + NW * H;
-    const A* glut = reinterpret_cast<const A*>(D.lutf + (size_t)b * (R + 1));
+    const A* glut = sizeof(A) == 4 ? reinterpret_cast<const A*>(D.lutf + (size_t)b * (R + 1))
+                                   : reinterpret_cast<const A*>(D.lut + (size_t)b * (R + 1));
     // LUTS: the LUT staged in shared memory after the rings
     A* s_lut = reinterpret_cast<A*>(align16(exA + NW * H) + NW * KP * W);
     if (LUTS)  // background-first (see band_lut): labels index s_lut + 1 directly
@@ -764,8 +775,12 @@ __global__ void __launch_bounds__(32 * SAT2_PARTS) k_sat2p(Bufs D, int gate) {
 #ifndef DET_SAT3_MINB
 #define DET_SAT3_MINB 4  // 64 registers, no spills: 512 band CTAs fit one wave (3 and 5 measured slower)
 #endif
+#ifndef DET_SAT3_MINB64
+#define DET_SAT3_MINB64 2  // float64 in-band arithmetic: up to 128 registers (64 spill ~300 bytes)
+#endif
 template <int CPT, int NT, int SRC, typename UT, int OUT, typename A, bool LUTS>
-__global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(Topo T, Bufs D, SatSrc S, int gate) {
+__global__ void __launch_bounds__(NT, (NT <= 256 ? (sizeof(A) == 8 ? DET_SAT3_MINB64 : DET_SAT3_MINB) : 1))
+    k_sat3(Topo T, Bufs D, SatSrc S, int gate) {
     extern __shared__ unsigned char s_raw3[];
     constexpr int NW = NT / 32;
     __shared__ A s_w[3][32];
@@ -1018,7 +1033,16 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB : 1)) k_sat3(To
             }
             if (OUT != OUT_CH8) {
                 UT* o = uf + ((size_t)j * n + x0) * 2;
-                if (sizeof(UT) == 4 && CPT % 2 == 0) {  // two pixels per 16-byte store
+                if (sizeof(UT) == 8 && CPT % 2 == 0) {  // two float64 pixels per 32-byte store (whole sectors)
+#pragma unroll
+                    for (int k = 0; k < CPT; k += 2)
+                        st_global_v4f64(o + 2 * k, (double)ux[k], (double)uy[k], (double)ux[k + 1], (double)uy[k + 1]);
+                } else if (sizeof(UT) == 4 && CPT % 4 == 0) {  // four float32 pixels per 32-byte store
+#pragma unroll
+                    for (int k = 0; k < CPT; k += 4)
+                        st_global_v8f32(o + 2 * k, (float)ux[k], (float)uy[k], (float)ux[k + 1], (float)uy[k + 1],
+                                        (float)ux[k + 2], (float)uy[k + 2], (float)ux[k + 3], (float)uy[k + 3]);
+                } else if (sizeof(UT) == 4 && CPT % 2 == 0) {  // two pixels per 16-byte store
 #pragma unroll
                     for (int k = 0; k < CPT; k += 2)
                         *reinterpret_cast<float4*>(o + 2 * k) =

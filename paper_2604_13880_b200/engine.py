@@ -26,7 +26,7 @@ from dataclasses import dataclass, field, replace
 import numpy as np
 
 from ._context import get_context, region_ranks
-from ._lib import STOP_BDV, STOP_COLLAPSED, STOP_NAMES, STOP_NEGINDEX
+from ._lib import PRECISIONS, STOP_BDV, STOP_COLLAPSED, STOP_NAMES, STOP_NEGINDEX
 from .errors import NumericError, RasterizationError, RegionCollapsedError
 from .geomodel import deferred_rebuild, densify, rebuild, ring_layout
 from .raster import LabelTexture, _LazyLabels, rasterize_labels
@@ -124,8 +124,8 @@ class BatchEngine:
                  start_vertices=None, *, device: int = 0, field_dtype: str = "float32"):
         if bdv_mode not in ("fixed-mass", "rederive"):
             raise ValueError("bdv_mode must be 'fixed-mass' or 'rederive'")
-        if field_dtype not in ("float32", "float64"):
-            raise ValueError("field_dtype must be 'float32' or 'float64'")
+        if field_dtype not in PRECISIONS:
+            raise ValueError("field_dtype must be 'float64', 'mixed' or 'float32'")
         if not (4 <= k <= 13):
             raise ValueError("texture exponent k must be in [4, 13]")
         stats = np.atleast_2d(np.asarray(statistics, dtype=float))
@@ -137,7 +137,7 @@ class BatchEngine:
         self.k, self.n = k, 1 << k
         self.m = self.n * self.n
         self.bdv_mode = bdv_mode
-        self.device, self.field_f64 = device, field_dtype == "float64"
+        self.device, self.field_dtype = device, field_dtype
         if apply_densify:
             mapmodel = densify(mapmodel, DENSIFY_EDGE_PIXELS / self.n)
         self.initial_map = mapmodel
@@ -191,7 +191,7 @@ class BatchEngine:
 
     # -- device context ----------------------------------------------------------
     def _ctx(self):
-        ctx = get_context(self.k, self.device, self.field_f64)
+        ctx = get_context(self.k, self.device, self.field_dtype)
         if getattr(ctx, "_owner_token", None) is not self._token or self._token is None:
             ctx.load_map(self._xy, self._rs, self._rr, self._rank)
             ctx.set_batch(self.statistics, None if self._start is None else self._start)

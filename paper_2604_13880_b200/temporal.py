@@ -228,7 +228,7 @@ def run_cumulative(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None
     base_map = densify(dataset.mapmodel, DENSIFY_EDGE_PIXELS / (1 << k))
     seq = FrameSequence(strategy="cumulative", dataset=dataset, base_map=base_map)
     xy, rs, rr, ids, _ = ring_layout(base_map)
-    ctx = get_context(k, device, field_dtype == "float64")
+    ctx = get_context(k, device, field_dtype)
     ctx.load_map(xy, rs, rr, region_ranks(ids))
     totals = np.array([float(s.sum()) for s in dataset.statistics])  # engine.py:123 (numpy sum)
     masses = np.asarray(masses, dtype=float)
