@@ -211,7 +211,7 @@ def main():
     ap.add_argument("--batch", type=int, default=16, help="frames per GPU")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--band", type=int, default=0, help="band height of the integral-image kernels (0 = auto)")
-    ap.add_argument("--field", default="float32", choices=["float32", "mixed", "float64"])
+    ap.add_argument("--field", default="float64", choices=["float64", "mixed", "float32"])
     ap.add_argument("--groups", type=int, default=8, help="frame groups run as parallel graph branches")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=0)

@@ -175,8 +175,9 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     // the residual-density LUT goes to shared memory when it fits in 48 KB
     const bool luts = src == SRC_LABELS && (size_t)lut_smem_len(R) * sa <= 48 * 1024;
     const size_t lut_b = luts ? (size_t)lut_smem_len(R) * sa : 0;
-    // + the label ring (lab_kp rows of NT*CPT ints) when reading labels
-    const size_t ring_b = (src == SRC_LABELS && f32) ? (size_t)lab_kp(CPT * NT) * NT * CPT * sizeof(int) : 0;
+    // k_sat3's label ring (lab_kp rows of NT*CPT ints; see RING in k_sat3)
+    const size_t ring_b = (src == SRC_LABELS && out == OUT_U && (f32 || CPT * NT <= 4096))
+                              ? (size_t)lab_kp(CPT * NT) * NT * CPT * sizeof(int) : 0;
     const size_t ring1_b = (src == SRC_LABELS && f32) ? (size_t)lab_kp1(CPT * NT) * NT * CPT * sizeof(int) : 0;
     const size_t smem1 = ((size_t)2 * (n + H - 1) + (size_t)H * (NT / 32)) * sa + ring1_b + 16;
 #define DET_SAT1(SRC_, A_, L_)                                                                               \

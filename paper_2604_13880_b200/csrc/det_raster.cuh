@@ -202,7 +202,10 @@ template <typename UT, typename ST = UT>
 #ifndef DET_RW_MINB
 #define DET_RW_MINB (32 / DET_RW_WARPS)  // 32 resident warps per SM (64 registers)
 #endif
-__global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, Bufs D, int mode, int gate, int src) {
+#ifndef DET_RW_MINB64
+#define DET_RW_MINB64 (24 / DET_RW_WARPS)  // float64 state: 24 warps per SM (80 registers)
+#endif
+__global__ void __launch_bounds__(RW_WARPS * 32, sizeof(ST) == 8 ? DET_RW_MINB64 : DET_RW_MINB) k_region(Topo T, Bufs D, int mode, int gate, int src) {
     // per row: ceil(y*n - 0.5) clipped to [0, n] (low 16 bits) | next row of the same ring,
     // region-local (high 16 bits) -- one load per edge end
     __shared__ uint32_t s_jn[RW_WARPS][RW_ROWCAP];
@@ -344,21 +347,21 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
     // one-row tail (no lane slots idle for a whole extra round)
     bool done_a = false;
 #if DET_RW_PIPE
-    if constexpr (FS) {
-        if (mode & M_ADVECT) {
-            // software-pipelined float advect: the next chunk's row loads are issued together with
-            // this chunk's texel gather, so a region pays one round trip per chunk, not two
-            constexpr int Q = RW_UNROLL;
-            float2 pc[Q], pn[Q];
-            auto ld = [&](float2 (&dst)[Q], int base) {
+    if (mode & M_ADVECT) {
+        // software-pipelined advect: the next chunk's row loads are issued together with this
+        // chunk's texel gather, so a region pays one round trip per chunk, not two
+        constexpr int Q = RW_UNROLL;
+        PT pc[Q], pn[Q];
+        auto ld = [&](PT (&dst)[Q], int base) {
 #pragma unroll
-                for (int q = 0; q < Q; ++q) {
-                    const int v = base + q * 32 + lane;
-                    dst[q] = v < row1 ? pin[v] : make_float2(0.5f, 0.5f);
-                }
-            };
-            ld(pc, row0);
-            for (int base = row0; base < row1; base += 32 * Q) {
+            for (int q = 0; q < Q; ++q) {
+                const int v = base + q * 32 + lane;
+                dst[q] = v < row1 ? pin[v] : PT{0.5, 0.5};
+            }
+        };
+        ld(pc, row0);
+        for (int base = row0; base < row1; base += 32 * Q) {
+            if constexpr (FS) {  // float state: tap, blend, update and clamp in float32
                 TapF tp[Q];
                 Texels<float> tx[Q];
 #pragma unroll
@@ -379,11 +382,32 @@ __global__ void __launch_bounds__(RW_WARPS * 32, DET_RW_MINB) k_region(Topo T, B
                         finish(v, pc[q], make_float2(cx, cy));
                     }
                 }
+            } else {  // float64 state: float64 tap and update (displacement.py:209-238 op order)
+                Tap tp[Q];
+                Texels<UT> tx[Q];
 #pragma unroll
-                for (int q = 0; q < Q; ++q) pc[q] = pn[q];
+                for (int q = 0; q < Q; ++q) {
+                    tp[q] = field_tap(n, (double)pc[q].x, (double)pc[q].y);
+                    tx[q] = field_load<UT, Tap>(uf, tp[q]);
+                }
+                if (base + 32 * Q < row1) ld(pn, base + 32 * Q);
+#pragma unroll
+                for (int q = 0; q < Q; ++q) {
+                    const double2 sm = field_blend<UT, Tap>(tx[q], tp[q]);
+                    const double mx = pc[q].x + sm.x, my = pc[q].y + sm.y;
+                    const double cx = mx < 0.0 ? 0.0 : (mx > 1.0 ? 1.0 : mx);  // np.clip (no NaNs here)
+                    const double cy = my < 0.0 ? 0.0 : (my > 1.0 ? 1.0 : my);
+                    const int v = base + q * 32 + lane;
+                    if (v < row1) {
+                        ncl += (cx != mx) + (cy != my);
+                        finish(v, pc[q], PT{cx, cy});
+                    }
+                }
             }
-            done_a = true;
+#pragma unroll
+            for (int q = 0; q < Q; ++q) pc[q] = pn[q];
         }
+        done_a = true;
     }
 #endif
     if (!done_a) {

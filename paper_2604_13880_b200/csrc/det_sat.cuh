@@ -805,6 +805,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? (sizeof(A) == 8 ? DET_SAT3_MI
     const double* csT = D.csT + (size_t)b * n;
 
     // ---- carries (k_sat2), row constants, LUT ----
+#pragma unroll 4
     for (int q = t; q < WN; q += blockDim.x) {
         win_dt[q].x = (jt == 0 && q == 0) ? (A)0 : (A)D.adSc[bb * WN + q];  // DLtot(-1) = 0
         const int wq = jt - 1 + q;
@@ -820,7 +821,10 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? (sizeof(A) == 8 ? DET_SAT3_MI
         s_rc[2 * H + q] = (A)(r0 - rf_top);
     }
     // float ring path: background-first shared LUT, labels index it directly (band_lut BIAS)
-    constexpr bool LB = LUTS && SRC == SRC_LABELS && sizeof(A) == 4;
+    // labels through the shared-memory TMA ring (float path; float64 path up to 4096 columns --
+    // at 8192 its carry windows leave no room); register prefetch otherwise
+    constexpr bool RING = SRC == SRC_LABELS && OUT == OUT_U && (sizeof(A) == 4 || CPT * NT <= 4096);
+    constexpr bool LB = LUTS && RING;
     const A* lut = band_lut<A, LUTS, LB>(D, R, b, s_lut);
     // cc[k]: column-total average cavg(x) = (colfull(x) + colfull(x+1))/2 for the field,
     // colfull(x+1) for the channel dump
@@ -857,9 +861,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? (sizeof(A) == 8 ? DET_SAT3_MI
     const A inv2m = (A)(S.outscale != 0.0 ? S.outscale : 0.5 * inv_nd * inv_nd);
     const A xc0 = (A)(((double)x0 + 0.5) * inv_nd);  // pixel-centre x of column x0 (displacement.py:59)
     UT* uf = reinterpret_cast<UT*>(D.uf) + (size_t)b * D.nn * 2;
-    // labels through the shared-memory ring on the float path (the float64 path's carry windows
-    // leave no room for it at 8192 columns); register prefetch otherwise
-    constexpr bool RING = SRC == SRC_LABELS && sizeof(A) == 4;
     __shared__ uint64_t s_bar[4];
     LabelRing<CPT, lab_kp(CPT * NT)> ring;
     if (RING) {

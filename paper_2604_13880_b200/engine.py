@@ -121,7 +121,7 @@ class BatchEngine:
 
     def __init__(self, mapmodel, statistics, criteria=None, k: int = 10, bdv_multiplier=1.0,
                  background_mass=None, bdv_mode: str = "fixed-mass", apply_densify: bool = True,
-                 start_vertices=None, *, device: int = 0, field_dtype: str = "float32"):
+                 start_vertices=None, *, device: int = 0, field_dtype: str = "float64"):
         if bdv_mode not in ("fixed-mass", "rederive"):
             raise ValueError("bdv_mode must be 'fixed-mass' or 'rederive'")
         if field_dtype not in PRECISIONS:
@@ -268,7 +268,7 @@ class CartogramEngine:
     def __init__(self, mapmodel, criteria: StoppingCriteria | None = None, k: int = 10,
                  bdv_multiplier: float = 1.0, background_mass: float | None = None,
                  bdv_mode: str = "fixed-mass", apply_densify: bool = True, *, device: int = 0,
-                 field_dtype: str = "float32"):
+                 field_dtype: str = "float64"):
         if bdv_mode not in ("fixed-mass", "rederive"):
             raise ValueError("bdv_mode must be 'fixed-mass' or 'rederive'")
         if bdv_multiplier <= 0:

@@ -38,7 +38,7 @@ class ComputedFrame:
 
 
 def compute_frame(start_geometry, base_map, stats_t, mass: float, fraction: float | None, params, *,
-                  device: int = 0, field_dtype: str = "float32") -> ComputedFrame:
+                  device: int = 0, field_dtype: str = "float64") -> ComputedFrame:
     """One session frame as service.py:202-236 computes it.
 
     ``params`` carries the session parameters the reference reads (``threshold``,

@@ -23,7 +23,7 @@ SWEEP_HEADER = "multiplier,stop_reason,iterations,xi,epsilon,tau,hamming_avg,ham
 
 
 def sweep_bdv(mapmodel, multipliers, criteria: StoppingCriteria | None = None, k: int = 10, hamming_k: int = 7, *,
-              device: int = 0, field_dtype: str = "float32"):
+              device: int = 0, field_dtype: str = "float64"):
     """``(csv_text, results)`` for the sorted multipliers (cli.py:265-300); ``results[i]`` is the
     RunResult (or the CartomorphError) of the i-th sorted multiplier."""
     mults = sorted(float(m) for m in multipliers)

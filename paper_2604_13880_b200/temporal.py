@@ -154,7 +154,7 @@ def _masses(dataset, policy, k, bdv_multiplier):
 def run_direct(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None = None,
                policy: AreaFractionPolicy | None = None, k: int = 10, bdv_multiplier: float = 1.0,
                watchdog_ceiling: float = DEFAULT_WATCHDOG_CEILING, report_raster_k: int = 7, *,
-               device: int = 0, field_dtype: str = "float32") -> FrameSequence:
+               device: int = 0, field_dtype: str = "float64") -> FrameSequence:
     """Every frame deformed independently from the original map -- all frames in one GPU batch."""
     criteria = criteria or StoppingCriteria()
     masses, fractions = _masses(dataset, policy, k, bdv_multiplier)
@@ -217,7 +217,7 @@ def _frame(seq, t, dataset, res, report, mb, frac, wall_ms, ceiling):
 def run_cumulative(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None = None,
                    policy: AreaFractionPolicy | None = None, k: int = 10, bdv_multiplier: float = 1.0,
                    watchdog_ceiling: float = DEFAULT_WATCHDOG_CEILING, report_raster_k: int = 7, *,
-                   device: int = 0, field_dtype: str = "float32") -> FrameSequence:
+                   device: int = 0, field_dtype: str = "float64") -> FrameSequence:
     """Each frame starts from the previous frame's deformed map (temporal.py:271-290).
 
     The whole chain stays on the GPU (``det_run_chain``): frame t+1 starts from frame t's
