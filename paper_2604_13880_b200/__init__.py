@@ -12,10 +12,10 @@ library and a CUDA device.
 from .engine import (BatchEngine, CartogramEngine, CartogramState, IterationRecord, RunResult, StoppingCriteria,
                      cartographic_error_arrays, run, target_weights)
 from .errors import CartomorphError, IngestionError, NumericError, RasterizationError, RegionCollapsedError
-from .geomodel import MapModel, Region, densify, detect_adjacencies, shoelace_area, to_geojson, with_adjacency
+from .geomodel import MapModel, Region, densify, ring_centroid, detect_adjacencies, shoelace_area, to_geojson, with_adjacency
 from .integral import IntegralImageSet, integral_images, straight_inims, tilted_inims
 from .displacement import (AnchorSet, DisplacementField, advect, anchors, base_mapping, mapping_grid,
-                           residual_field)
+                           mapping_point, residual_field)
 from .raster import BACKGROUND, DensityTexture, LabelTexture, build_density, default_bdv, rasterize_labels
 from .metrics import (QualityReport, cartographic_errors, full_report, hamming_distance, relative_position_error,
                       shape_distortion, topology_distortion)

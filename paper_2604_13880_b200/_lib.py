@@ -81,6 +81,10 @@ EXPORTS = {
                                         ctypes.c_int]),
     "det_field": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p, _c_double_p, _c_double_p]),
     "det_mapping": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p]),
+    "det_mapping_channels": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, ctypes.c_double, _c_double_p,
+                                             _c_double_p]),
+    "det_mapping_points": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, ctypes.c_double, _c_double_p,
+                                           ctypes.c_int, _c_double_p]),
     "det_density": (ctypes.c_int, [ctypes.c_void_p, _c_int32_p, _c_double_p, ctypes.c_int, ctypes.c_double,
                                     _c_double_p, _c_int64_p]),
     "det_interpolate": (ctypes.c_int, [ctypes.c_void_p, _c_double_p, _c_double_p, ctypes.c_longlong, _c_double_p,
@@ -380,6 +384,24 @@ class Context:
         t = np.empty((self.n, self.n, 2), dtype=np.float64)
         self.check(self.lib.det_mapping(self.h, _p(d, ctypes.c_double), _p(t, ctypes.c_double)))
         return t
+
+    def mapping_channels(self, channels, total, base=None):
+        """mapping_grid of a channel set (8, n, n), minus `base` (n, n, 2) when given."""
+        ch = np.ascontiguousarray(channels, dtype=np.float64)
+        bs = None if base is None else np.ascontiguousarray(base, dtype=np.float64)
+        t = np.empty((self.n, self.n, 2), dtype=np.float64)
+        self.check(self.lib.det_mapping_channels(self.h, _p(ch, ctypes.c_double), float(total),
+                                                 _p(bs, ctypes.c_double), _p(t, ctypes.c_double)))
+        return t
+
+    def mapping_points(self, channels, total, xy):
+        """mapping_point at (N, 2) points of a channel set (8, n, n)."""
+        ch = np.ascontiguousarray(channels, dtype=np.float64)
+        pts = np.ascontiguousarray(xy, dtype=np.float64).reshape(-1, 2)
+        out = np.empty_like(pts)
+        self.check(self.lib.det_mapping_points(self.h, _p(ch, ctypes.c_double), float(total),
+                                               _p(pts, ctypes.c_double), pts.shape[0], _p(out, ctypes.c_double)))
+        return out
 
     def interpolate(self, a, b, fracs):
         a = np.ascontiguousarray(a, dtype=np.float64).ravel()

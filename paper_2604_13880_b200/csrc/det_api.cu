@@ -484,7 +484,6 @@ static int raster_start(det_ctx* ctx) {
         bool ovf = false;
         for (int b = 0; b < ctx->B; ++b) {
             mx = std::max(mx, ms[b]);
-            if (hs[b].err & E_TOGGLE_OVF) return fail(ctx, DET_E_STATE, "more than 4096 crossings on one scanline of a region");
             ovf |= (hs[b].err & E_SPAN_OVF) != 0;
         }
         const int want = std::max(64, 2 * mx + 32);  // headroom for deformation
@@ -749,7 +748,6 @@ static int run_once(det_ctx* ctx, const det_criteria* crit, bool* overflow) {
         bool any = false;
         for (int b = 0; b < B; ++b) {
             if (ctx->h_st[b].err & E_SPAN_OVF) { *overflow = true; return DET_OK; }
-            if (ctx->h_st[b].err & E_TOGGLE_OVF) return fail(ctx, DET_E_STATE, "more than 4096 crossings on one scanline of a region");
             any |= ctx->h_st[b].active != 0;
         }
         if (!any) break;

@@ -12,13 +12,12 @@ constexpr int REG_THREADS = 128;   // k_region block
 constexpr int ROW_THREADS = 256;   // k_row block
 constexpr int CTRL_THREADS = 1024;  // k_ctrl block (one per cartogram)
 constexpr int CTRL_SEPARATE = -2;  // k_row ctrl_mode: leave the control step to k_ctrl
-constexpr int TOG_CAP = 4096;      // toggles per k_region window (smem keys, power of two)
 
 // M_POSTADV: raster the rows k_advect_rows just wrote (the advect runs as its own kernel)
 enum Mode { M_ADVECT = 1, M_RASTER = 2, M_POSTADV = 4 };
 enum Gate { G_ALWAYS = 0, G_ACTIVE = 1, G_FINAL = 2 };
 enum Stop { S_RUNNING = 0, S_CONVERGED = 1, S_STAGNATION = 2, S_MAXITER = 3, S_COLLAPSED = 4, S_BDV = 5, S_NEGINDEX = 6 };
-enum Err { E_SPAN_OVF = 1, E_NEGIDX = 2, E_TOGGLE_OVF = 4 };
+enum Err { E_SPAN_OVF = 1, E_NEGIDX = 2 };
 enum Src { SRC_LABELS = 0, SRC_DENSE = 1 };
 enum Out { OUT_U = 0, OUT_CH8 = 1 };
 

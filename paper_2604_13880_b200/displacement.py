@@ -55,13 +55,28 @@ class DisplacementField:
         return float(np.hypot(self.u[..., 0], self.u[..., 1]).max())
 
 
+def _channel_stack(ii: IntegralImageSet) -> np.ndarray:
+    return np.stack(ii.straight_channels() + ii.tilted_channels())
+
+
 def mapping_grid(ii: IntegralImageSet, device: int = 0) -> np.ndarray:
-    """t(d) at every pixel centre, (n, n, 2) (displacement.py:102-131)."""
+    """t(d) at every pixel centre, (n, n, 2), from the set's eight channels (displacement.py:102-131).
+
+    ``k_map_grid`` evaluates the reference's corner-lattice average and anchor combination with
+    its float64 op order, so any IntegralImageSet -- a hand-built one included -- maps exactly as
+    the reference maps it."""
     if ii.total <= 0:
         raise NumericError("mapping undefined for zero total density")
-    if ii.source is None:
-        raise ValueError("IntegralImageSet has no source texture; build it with integral_images()")
-    return get_context(_k_of(ii.size), device).mapping(ii.source)
+    return get_context(_k_of(ii.size), device).mapping_channels(_channel_stack(ii), ii.total)
+
+
+def mapping_point(x: float, y: float, ii: IntegralImageSet, device: int = 0) -> np.ndarray:
+    """The anchor mapping at one continuous location (displacement.py:150-170): straight channels
+    sampled on the corner lattice, tilted channels between pixel centres (``k_map_points``)."""
+    if ii.total <= 0:
+        raise NumericError("mapping undefined for zero total density")
+    ctx = get_context(_k_of(ii.size), device)
+    return ctx.mapping_points(_channel_stack(ii), ii.total, np.array([[x, y]], dtype=np.float64))[0]
 
 
 @functools.lru_cache(maxsize=8)
@@ -73,14 +88,25 @@ def base_mapping(n: int) -> np.ndarray:
 
 
 def residual_field(ii_d: IntegralImageSet, base: np.ndarray | None = None, device: int = 0) -> DisplacementField:
+    """u = t(d) - base at every pixel centre (displacement.py:198-206).
+
+    With ``base=None`` and a set built by :func:`integral_images` (which keeps its texture), u is
+    evaluated by the engine's band kernels in residual-density form, which avoids the cancellation
+    of t(d) - t(1) (agrees with the reference's subtraction to ~1e-13).  Otherwise u is the
+    channel mapping minus ``base`` (``base_mapping(n)`` when None), exactly the reference's
+    expression."""
     n = ii_d.size
     if base is not None and base.shape[0] != n:
         raise ValueError(f"base grid size {base.shape[0]} does not match texture size {n}")
     if ii_d.total <= 0:
         raise NumericError("mapping undefined for zero total density")
-    if ii_d.source is None:
-        raise ValueError("IntegralImageSet has no source texture; build it with integral_images()")
-    u, _, _ = get_context(_k_of(n), device).field(ii_d.source)
+    ctx = get_context(_k_of(n), device)
+    if base is None and ii_d.source is not None:
+        u, _, _ = ctx.field(ii_d.source)
+        return DisplacementField(size=n, u=u, base=base_mapping(n))
+    if base is None:
+        base = base_mapping(n)
+    u = ctx.mapping_channels(_channel_stack(ii_d), ii_d.total, base)
     return DisplacementField(size=n, u=u, base=base)
 
 

@@ -35,6 +35,19 @@ def shoelace_area(ring: np.ndarray) -> float:
     return 0.5 * float(np.sum(xs * np.roll(ys, -1) - np.roll(xs, -1) * ys))
 
 
+def ring_centroid(ring: np.ndarray) -> np.ndarray:
+    """Area-weighted centroid of one ring from its shoelace moments (geomodel.py:34-47); the
+    vertex mean for a degenerate ring."""
+    r = np.asarray(ring, dtype=float)
+    xs, ys = r[:, 0], r[:, 1]
+    xn, yn = np.roll(xs, -1), np.roll(ys, -1)
+    cross = xs * yn - xn * ys
+    a = 0.5 * float(np.sum(cross))
+    if a == 0.0:
+        return r.mean(axis=0)
+    return np.array([float(np.sum((xs + xn) * cross)) / (6.0 * a), float(np.sum((ys + yn) * cross)) / (6.0 * a)])
+
+
 @dataclass(frozen=True)
 class Region:
     """One statistical region (geomodel.py:50-80)."""
@@ -46,6 +59,17 @@ class Region:
 
     def area(self) -> float:
         return sum(shoelace_area(r) for r in self.rings)
+
+    def centroid(self) -> np.ndarray:
+        """Area-weighted centroid over all rings, holes subtracting (geomodel.py:67-77)."""
+        total, acc = 0.0, np.zeros(2)
+        for ring in self.rings:
+            a = shoelace_area(ring)
+            acc += a * ring_centroid(ring)
+            total += a
+        if total == 0.0:
+            return np.vstack(self.rings).mean(axis=0)
+        return acc / total
 
     def vertex_count(self) -> int:
         return sum(int(np.asarray(r).shape[0]) for r in self.rings)

@@ -142,3 +142,23 @@ def build_density(statistics: np.ndarray, labels: LabelTexture, bdv: float, devi
         raise DetError(rc, ctx.lib.det_last_error(ctx.h).decode())
     m = labels.size * labels.size
     return DensityTexture(size=labels.size, d=d, d0=float(d.sum()) / m, bdv=float(bdv), pixel_counts=cnt[:-1])
+
+
+def write_pgm16(path, array: np.ndarray) -> None:
+    """Debug dump as a 16-bit binary PGM, values min-max scaled to [0, 65535] (raster.py:187-196)."""
+    a = np.asarray(array, dtype=float)
+    lo, hi = float(a.min()), float(a.max())
+    scaled = np.zeros_like(a) if hi == lo else (a - lo) / (hi - lo)
+    with open(path, "wb") as fh:
+        fh.write(f"P5\n{a.shape[1]} {a.shape[0]}\n65535\n".encode())
+        fh.write((scaled * 65535).round().astype(">u2").tobytes())
+
+
+def write_raw_f32(path, array: np.ndarray) -> None:
+    """Headerless little-endian float32 row-major dump (raster.py:199-201)."""
+    np.asarray(array, dtype="<f4").tofile(path)
+
+
+def write_raw_f64(path, array: np.ndarray) -> None:
+    """Headerless little-endian float64 row-major dump (raster.py:204-206)."""
+    np.asarray(array, dtype="<f8").tofile(path)

@@ -83,3 +83,32 @@ def unpack_map(z, prefix="") -> MapModel:
         rings[int(rr[q])].append(np.array(xy[rs[q] : rs[q + 1]], dtype=float))
     names = [str(s) for s in z[prefix + "names"]] if (prefix + "names") in z else ids
     return MapModel(regions=tuple(Region(i, nm, tuple(rg), float(s)) for i, nm, rg, s in zip(ids, names, rings, stats)))
+
+
+def many_holes(n_holes=200, y0=0.47, y1=0.53) -> MapModel:
+    """A square region pierced by `n_holes` thin triangular holes along one horizontal band, so a
+    scanline through the band crosses 2*n_holes + 2 of its edges (raster.py:80-89 has no limit
+    on crossings per row); a second region beside it and an island inside one hole."""
+    outer = _sq(0.05, 0.05, 0.9, 0.95)
+    holes = []
+    xs = np.linspace(0.07, 0.88, n_holes, endpoint=False)
+    w = 0.45 * (xs[1] - xs[0])
+    for x in xs:
+        holes.append(np.array([[x, y0], [x + 0.5 * w, y1], [x + w, y0 + 0.002]]))  # CW in y-down: a hole
+    a = Region("A", "holed", (outer, *holes), 5.0)
+    b = Region("B", "side", (_sq(0.91, 0.3, 0.98, 0.7),), 1.0)
+    x = xs[n_holes // 2]
+    isl = Region("C", "island", (np.array([[x + 0.2 * w, y0 + 0.01], [x + 0.8 * w, y0 + 0.01],
+                                           [x + 0.5 * w, y0 + 0.02]]),), 0.5)
+    return MapModel(regions=(a, b, isl))
+
+
+def needle_rings(n_rings=150) -> MapModel:
+    """A square region with `n_rings` two-vertex rings crossing the same scanlines: each adds two
+    coincident toggles per scanline (they cancel), so a row carries > 256 toggles while the
+    region keeps <= 384 rows (the shared-memory path of k_region)."""
+    outer = _sq(0.1, 0.1, 0.9, 0.9)
+    xs = np.linspace(0.15, 0.85, n_rings)
+    rings = [np.array([[x, 0.3], [x + 0.001, 0.7]]) for x in xs]
+    return MapModel(regions=(Region("A", "needles", (outer, *rings), 2.0),
+                             Region("B", "other", (_sq(0.91, 0.3, 0.98, 0.6),), 1.0)))

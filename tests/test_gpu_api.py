@@ -1,0 +1,129 @@
+"""Stage API members on reference-typed inputs, against fixtures made by the real reference
+(tests/golden/make_golden_api.py): mapping_grid / mapping_point / residual_field(ii, base) of a
+channel set (including a hand-built IntegralImageSet with no texture behind it), and the
+float32-field step == run identity."""
+
+import os
+
+import numpy as np
+import pytest
+
+import fixture_maps as fm
+from conftest import cuda_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not cuda_available(), reason="needs a CUDA device")]
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2604_13880_b200 as P
+
+    return P
+
+
+@pytest.fixture(scope="module")
+def api(golden_dir):
+    return np.load(os.path.join(golden_dir, "api.npz"))
+
+
+@pytest.fixture(scope="module")
+def stage(golden_dir):
+    return np.load(os.path.join(golden_dir, "stage_k6.npz"))
+
+
+def _ii(P, ch, total, source=None):
+    return P.IntegralImageSet(*[np.asarray(ch[i]) for i in range(8)], total=float(total), source=source)
+
+
+def test_mapping_grid_of_channels_bit_exact(P, api, stage):
+    # k_map_grid follows displacement.py:102-131's float64 op order: bit-identical
+    g = P.mapping_grid(_ii(P, stage["channels"], stage["total"]))
+    assert np.array_equal(g, api["mapping_grid"])
+
+
+def test_mapping_grid_hand_built_set(P, api):
+    g = P.mapping_grid(_ii(P, api["h_channels"], api["h_total"]))
+    assert np.array_equal(g, api["h_grid"])
+
+
+def test_mapping_point_bit_exact(P, api, stage):
+    ii = _ii(P, stage["channels"], stage["total"])
+    got = np.array([P.mapping_point(float(x), float(y), ii) for x, y in api["pts"]])
+    np.testing.assert_allclose(got, api["mapping_point"], rtol=0, atol=1e-15)
+    hii = _ii(P, api["h_channels"], api["h_total"])
+    got = np.array([P.mapping_point(float(x), float(y), hii) for x, y in api["h_pts"]])
+    np.testing.assert_allclose(got, api["h_mapping_point"], rtol=0, atol=1e-15)
+
+
+def test_residual_field_honours_base(P, api, stage):
+    ii = _ii(P, stage["channels"], stage["total"])
+    fld = P.residual_field(ii, api["base2"])
+    assert np.array_equal(fld.u, api["u_base2"])
+    assert fld.base is not None and np.array_equal(fld.base, api["base2"])
+
+
+def test_residual_field_without_source(P, api, stage):
+    # no texture behind the set: the reference's t(d) - base_mapping(n) from the channels
+    fld = P.residual_field(_ii(P, stage["channels"], stage["total"]))
+    np.testing.assert_allclose(fld.u, api["u_none"], rtol=0, atol=1e-13)
+
+
+def test_residual_field_fused_path_matches(P, api, stage):
+    # set built from the texture: band kernels in residual-density form (no t(d) - t(1) cancellation)
+    ii = P.integral_images(stage["d"])
+    fld = P.residual_field(ii)
+    np.testing.assert_allclose(fld.u, api["u_none"], rtol=0, atol=1e-12)
+
+
+def test_mapping_rejects_zero_total(P, api):
+    ii = _ii(P, np.zeros((8, 16, 16)), 0.0)
+    with pytest.raises(P.NumericError):
+        P.mapping_grid(ii)
+    with pytest.raises(P.NumericError):
+        P.mapping_point(0.5, 0.5, ii)
+
+
+def test_residual_field_base_size_mismatch(P, stage):
+    with pytest.raises(ValueError):
+        P.residual_field(_ii(P, stage["channels"], stage["total"]), np.zeros((32, 32, 2)))
+
+
+@pytest.mark.parametrize("field", ["float64", "mixed", "float32"])
+def test_step_equals_run(P, field):
+    # CartogramEngine.step from the returned state reproduces run() iteration by iteration in every
+    # precision mode (the float32 state is exactly representable after the first step)
+    m = fm.config1()
+    crit = P.StoppingCriteria(error_threshold=1e-300, stagnation_window=10**9, max_iterations=6)
+    eng = P.CartogramEngine(m, criteria=crit, k=8, bdv_multiplier=0.5, field_dtype=field)
+    full = eng.run()
+    st = eng.evaluate(eng.initial_map, 0)
+    for _ in range(6):
+        st = eng.step(st)
+    assert st.iteration == full.state.iteration
+    assert np.array_equal(st.pixel_counts, full.state.pixel_counts)
+    assert np.array_equal(st.mapmodel.vertex_array(), full.state.mapmodel.vertex_array())
+
+
+# ---------------------------------------------------------------- crossings per scanline
+@pytest.mark.parametrize("maker,k", [("many_holes", 12), ("many_holes", 10), ("needle_rings", 9),
+                                     ("needle_rings", 12)])
+def test_many_crossings_per_scanline_bit_exact(P, maker, k):
+    # > 256 toggles on one scanline of one region (the parity-bitmap window of k_region)
+    from oracle import det_oracle as O
+
+    m = getattr(fm, maker)()
+    tex = P.rasterize_labels(m, k, check_collapse=False)
+    ref = O.FlatMap.from_mapmodel(m).labels(k)
+    assert np.array_equal(tex.labels, ref), f"{(tex.labels != ref).sum()} pixels differ"
+    assert np.array_equal(tex.pixel_counts(), np.bincount(ref[ref >= 0], minlength=len(m.regions)))
+
+
+def test_many_holes_engine_vs_oracle(P):
+    from oracle import det_oracle as O
+
+    m = fm.many_holes()
+    crit = P.StoppingCriteria(error_threshold=1e-300, stagnation_window=10**9, max_iterations=3)
+    res = P.CartogramEngine(m, criteria=crit, k=10).run()
+    ref = O.OracleEngine(O.FlatMap.from_mapmodel(m), k=10).run(1e-300, 10**9, 3)
+    assert np.array_equal(res.state.pixel_counts, ref.counts)
+    np.testing.assert_allclose(res.state.mapmodel.vertex_array(), ref.rows, rtol=0, atol=1e-9)

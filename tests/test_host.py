@@ -135,3 +135,29 @@ def test_shard_bounds_cover():
             cov = [shard_bounds(n, r, w) for r in range(w)]
             assert cov[0][0] == 0 and cov[-1][1] == n
             assert all(cov[i][1] == cov[i + 1][0] for i in range(w - 1))
+
+
+def test_region_centroid_matches_reference(golden_dir):
+    import numpy as np
+    import fixture_maps as fm
+
+    z = np.load(os.path.join(golden_dir, "api.npz"))
+    m = fm.overlap_holes_multi()
+    assert np.array_equal(np.array([r.centroid() for r in m.regions]), z["centroids_overlap"])
+    v = fm.small_voronoi(seed=0, r=24, target=600, shuffle_ids=True)
+    assert np.array_equal(np.array([r.centroid() for r in v.regions]), z["centroids_vor"])
+
+
+def test_raster_debug_dumps(tmp_path):
+    import numpy as np
+    from paper_2604_13880_b200.raster import write_pgm16, write_raw_f32, write_raw_f64
+
+    a = np.arange(12, dtype=float).reshape(3, 4)
+    write_pgm16(tmp_path / "a.pgm", a)
+    data = (tmp_path / "a.pgm").read_bytes()
+    assert data.startswith(b"P5\n4 3\n65535\n") and len(data) == len(b"P5\n4 3\n65535\n") + 24
+    assert np.frombuffer(data[-24:], dtype=">u2")[-1] == 65535
+    write_raw_f32(tmp_path / "a.f32", a)
+    write_raw_f64(tmp_path / "a.f64", a)
+    assert np.array_equal(np.fromfile(tmp_path / "a.f32", dtype="<f4"), a.ravel().astype(np.float32))
+    assert np.array_equal(np.fromfile(tmp_path / "a.f64", dtype="<f8"), a.ravel())
