@@ -59,6 +59,7 @@ constexpr int kGraphIters = 16;
 
 struct det_ctx {
     int device = 0, k = 10, n = 1024, f64 = 0, s64 = 0, H = 8;  // f64: float64 field; s64: float64 vertex state
+    bool bitmap_raster = false;  // k_region<..., true>: scanlines with more crossings than its toggle window
     cudaStream_t stream = nullptr;
     std::string err;
     // topology
@@ -274,6 +275,12 @@ static void launch_sat(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S
 static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, int gate, int src,
                           bool f64_rows = false) {
     const dim3 g((c->R + RW_WARPS - 1) / RW_WARPS, c->B);
+    if (c->bitmap_raster) {  // a scanline overflowed the toggle window: the parity-bitmap instantiation
+        if (c->f64) k_region<double, double, true><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
+        else if (c->s64 || f64_rows) k_region<float, double, true><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
+        else k_region<float, float, true><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
+        return;
+    }
     if (c->f64) k_region<double, double><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
     else if (c->s64 || f64_rows) k_region<float, double><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
     else k_region<float, float><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
@@ -481,10 +488,17 @@ static int raster_start(det_ctx* ctx) {
         CK(cudaMemcpyAsync(ms.data(), ctx->maxspan.p, ctx->B * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
         int mx = 0;
-        bool ovf = false;
+        bool ovf = false, tog = false;
         for (int b = 0; b < ctx->B; ++b) {
             mx = std::max(mx, ms[b]);
             ovf |= (hs[b].err & E_SPAN_OVF) != 0;
+            tog |= (hs[b].err & E_TOGGLE_OVF) != 0;
+        }
+        if (tog) {  // > RW_TCAP crossings on one scanline of a region: redo with the bitmap raster
+            if (ctx->bitmap_raster) return fail(ctx, DET_E_STATE, "toggle overflow in the bitmap raster");
+            ctx->bitmap_raster = true;
+            invalidate_graph(ctx);
+            continue;
         }
         const int want = std::max(64, 2 * mx + 32);  // headroom for deformation
         if (!ovf) {
@@ -708,8 +722,10 @@ int det_set_params(det_ctx* ctx, const det_params* params, const double* weights
     return DET_OK;
 }
 
-static int run_once(det_ctx* ctx, const det_criteria* crit, bool* overflow) {
-    *overflow = false;
+// *overflow: bit 0 = a row's spans overflowed the span buffer (grow and redo), bit 1 = a scanline
+// overflowed k_region's toggle window (redo with the bitmap raster)
+static int run_once(det_ctx* ctx, const det_criteria* crit, int* overflow) {
+    *overflow = 0;
     const int B = ctx->B;
     const int tc = crit->max_iterations + 1;
     if (tc > ctx->trace_cap || ctx->trace.n < (size_t)B * ctx->trace_cap * 4) {
@@ -747,7 +763,11 @@ static int run_once(det_ctx* ctx, const det_criteria* crit, bool* overflow) {
         CK(cudaStreamSynchronize(ctx->stream));
         bool any = false;
         for (int b = 0; b < B; ++b) {
-            if (ctx->h_st[b].err & E_SPAN_OVF) { *overflow = true; return DET_OK; }
+            if (ctx->h_st[b].err & (E_SPAN_OVF | E_TOGGLE_OVF)) {
+                for (int q = 0; q < B; ++q)
+                    *overflow |= ((ctx->h_st[q].err & E_SPAN_OVF) ? 1 : 0) | ((ctx->h_st[q].err & E_TOGGLE_OVF) ? 2 : 0);
+                return DET_OK;
+            }
             any |= ctx->h_st[b].active != 0;
         }
         if (!any) break;
@@ -764,7 +784,7 @@ static int run_once(det_ctx* ctx, const det_criteria* crit, bool* overflow) {
     CK(cudaMemcpyAsync(ctx->h_st.data(), ctx->st.p, B * sizeof(Carto), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     for (int b = 0; b < B; ++b)
-        if (ctx->h_st[b].err & E_SPAN_OVF) *overflow = true;
+        *overflow |= ((ctx->h_st[b].err & E_SPAN_OVF) ? 1 : 0) | ((ctx->h_st[b].err & E_TOGGLE_OVF) ? 2 : 0);
     return DET_OK;
 }
 
@@ -775,7 +795,7 @@ int det_run(det_ctx* ctx, const det_criteria* crit) {
         return fail(ctx, DET_E_ARG, "stopping criteria must all be positive");
     cudaSetDevice(ctx->device);
     for (int attempt = 0; attempt < 6; ++attempt) {
-        bool ovf = false;
+        int ovf = 0;
         ctx->bench_mode = false;
         int rc = run_once(ctx, crit, &ovf);
         if (rc) return rc;
@@ -783,9 +803,18 @@ int det_run(det_ctx* ctx, const det_criteria* crit) {
             ctx->ran = true;
             return DET_OK;
         }
-        ctx->cap *= 2;  // a row collected more spans than the buffer holds: grow and redo
-        rc = alloc_spans(ctx);
-        if (rc) return rc;
+        if (ovf & 2) {  // a scanline collected more crossings than k_region's window: bitmap raster
+            if (ctx->bitmap_raster) return fail(ctx, DET_E_STATE, "toggle overflow in the bitmap raster");
+            ctx->bitmap_raster = true;
+            invalidate_graph(ctx);
+        }
+        if (ovf & 1) {
+            ctx->cap *= 2;  // a row collected more spans than the buffer holds: grow and redo
+            rc = alloc_spans(ctx);
+            if (rc) return rc;
+        } else {
+            CK(cudaMemsetAsync(ctx->rowcnt.p, 0, (size_t)ctx->B * ctx->n * sizeof(int), ctx->stream));
+        }
     }
     return fail(ctx, DET_E_STATE, "span capacity did not converge");
 }

@@ -17,7 +17,7 @@ constexpr int CTRL_SEPARATE = -2;  // k_row ctrl_mode: leave the control step to
 enum Mode { M_ADVECT = 1, M_RASTER = 2, M_POSTADV = 4 };
 enum Gate { G_ALWAYS = 0, G_ACTIVE = 1, G_FINAL = 2 };
 enum Stop { S_RUNNING = 0, S_CONVERGED = 1, S_STAGNATION = 2, S_MAXITER = 3, S_COLLAPSED = 4, S_BDV = 5, S_NEGINDEX = 6 };
-enum Err { E_SPAN_OVF = 1, E_NEGIDX = 2 };
+enum Err { E_SPAN_OVF = 1, E_NEGIDX = 2, E_TOGGLE_OVF = 4 };
 enum Src { SRC_LABELS = 0, SRC_DENSE = 1 };
 enum Out { OUT_U = 0, OUT_CH8 = 1 };
 

@@ -195,70 +195,10 @@ __device__ __forceinline__ int warp_excl_scan_int(int v, int lane, int* total) {
     return x - v;
 }
 
-// Spans of one scanline from the parity bitmap of its toggle columns (bit c = parity of the
-// toggles at crop column c): pixel c is inside iff the inclusive prefix XOR at c is 1 (the
-// even-odd cumsum & 1 of raster.py:86-89).  Runs of inside pixels become spans, split at 32-column
-// word boundaries (painting and counts are per pixel, so the split is invisible).  Slots are
-// reserved with one atomic per row; returns this lane's share of the inside-pixel count.
-__device__ __noinline__ int bitmap_spans(const uint32_t* words, int cols, int i_off, unsigned long long rank,
-                                         int* rowcnt, unsigned long long* spans, int cap, int* err, int lane) {
-    const int nw = (cols + 31) >> 5;
-    auto inside_word = [&](int q, int& carry, int& nsp) -> uint32_t {
-        // q = word index of this lane in the current round; carry = parity left of the round
-        const uint32_t x = q < nw ? words[q] : 0u;
-        uint32_t p = x;
-        p ^= p << 1; p ^= p << 2; p ^= p << 4; p ^= p << 8; p ^= p << 16;  // inclusive prefix XOR
-        const unsigned par = __ballot_sync(FULL, __popc(x) & 1);
-        const int pre = (carry + __popc(par & ((1u << lane) - 1u))) & 1;
-        carry = (carry + __popc(par)) & 1;
-        uint32_t in = pre ? ~p : p;
-        const int lo = q * 32;
-        if (q >= nw) in = 0u;
-        else if (cols - lo < 32) in &= (1u << (cols - lo)) - 1u;
-        nsp = __popc(in & ~(in << 1));
-        return in;
-    };
-    int total = 0, carry = 0;
-    for (int q0 = 0; q0 < nw; q0 += 32) {
-        int nsp;
-        inside_word(q0 + lane, carry, nsp);
-        total += nsp;
-    }
-    total = warp_sum(total);
-    int slot = 0;
-    if (lane == 0 && total) slot = atomicAdd(rowcnt, total);
-    slot = __shfl_sync(FULL, slot, 0);
-    int area = 0;
-    carry = 0;
-    for (int q0 = 0; q0 < nw; q0 += 32) {
-        int nsp;
-        const int q = q0 + lane;
-        uint32_t in = inside_word(q, carry, nsp);
-        int chunk;
-        const int ex = warp_excl_scan_int(nsp, lane, &chunk);
-        int s = slot + ex;
-        slot += chunk;
-        area += __popc(in);
-        while (in) {
-            const int a = __ffs(in) - 1;
-            const uint32_t rest = ~(in | ((1u << a) - 1u));  // first clear bit at or above a
-            const int e = rest ? __ffs(rest) - 1 : 32;
-            in = e < 32 ? in & ~((1u << e) - 1u) : 0u;
-            const int col = i_off + q * 32 + a, end = i_off + q * 32 + e;
-            if (s < cap)
-                spans[s] = (rank << 32) | ((unsigned long long)end << 16) | (unsigned long long)col;
-            else
-                atomicOr(err, (int)E_SPAN_OVF);
-            ++s;
-        }
-    }
-    return area;
-}
-
 // UT: field element type (float / double); ST: vertex-state element type.  <float, float> is the
 // float32 path, <double, double> the float64 path, <float, double> the mixed path (float32 field,
 // float64 state and position update).
-template <typename UT, typename ST = UT>
+template <typename UT, typename ST = UT, bool BM = false>
 #ifndef DET_RW_MINB
 #define DET_RW_MINB (32 / DET_RW_WARPS)  // 32 resident warps per SM (64 registers)
 #endif
@@ -495,17 +435,96 @@ __global__ void __launch_bounds__(RW_WARPS * 32, sizeof(ST) == 8 ? DET_RW_MINB64
     const int back = i_off / (cols + 1) + 1;  // max rows a negative column moves a toggle up
     int area = 0;
 
+    // BM: one scanline j of this region rasterised through a parity bitmap of its crop columns
+    // (keys[] reused: RW_TCAP words = 8192 bits >= cols), for any number of crossings -- the
+    // bincount of raster.py:80-89 has no limit.  Every edge is re-scanned from the global rows
+    // with emit()'s exact arithmetic; a column's bit is the parity of its toggles, pixel c is
+    // inside iff the inclusive prefix XOR at c is 1 (cumsum & 1, raster.py:86-89), and runs of
+    // inside pixels become spans (split at 32-column words; painting and counts are per pixel).
+    auto bitmap_row = [&](int jrow) -> int {
+        for (int q = lane; q < RW_TCAP; q += 32) keys[q] = 0u;
+        __syncwarp();
+        for (int e = row0 + lane; e < row1; e += 32) {
+            const int en = next_row(e);
+            double2 a = to_d2(gpos[e]), c = to_d2(gpos[en]);
+            const int ja = min(max(ceil_to_int(__dsub_rn(__dmul_rn(a.y, nd), 0.5)), 0), n);
+            const int jb2 = min(max(ceil_to_int(__dsub_rn(__dmul_rn(c.y, nd), 0.5)), 0), n);
+            const int js = max(min(ja, jb2), jrow), je = min(max(ja, jb2), jrow + 1 + back);
+            if (je <= js) continue;
+            a = make_double2(__dmul_rn(a.x, nd), __dmul_rn(a.y, nd));
+            c = make_double2(__dmul_rn(c.x, nd), __dmul_rn(c.y, nd));
+            const double slope = __ddiv_rn(__dsub_rn(c.x, a.x), __dsub_rn(c.y, a.y));
+            double yc = (double)js + 0.5;
+            for (int j = js; j < je; ++j, yc += 1.0) {
+                const double xc = __dadd_rn(a.x, __dmul_rn(__dsub_rn(yc, a.y), slope));
+                const int i0 = min(max(ceil_to_int(__dsub_rn(xc, 0.5)), 0), n);
+                int dest = j, cc = min(i0 - i_off, cols);
+                if (cc < 0) {
+                    const long long f = (long long)(j - j_off) * width + (long long)cc;
+                    if (f < 0) continue;  // flagged (E_NEGIDX) by the windowed pass already
+                    const long long dr = f / width;
+                    cc = (int)(f - dr * width);
+                    dest = j_off + (int)dr;
+                }
+                if (cc == cols || dest != jrow) continue;
+                atomicXor(&keys[cc >> 5], 1u << (cc & 31));
+            }
+        }
+        __syncwarp();
+        const int nw = (cols + 31) >> 5;
+        const size_t rb = (size_t)b * n + jrow;
+        int px = 0, carry = 0, slot = 0;
+        for (int pass = 0; pass < 2; ++pass) {  // pass 0 counts spans, pass 1 writes them
+            int nsp_all = 0;
+            carry = 0;
+            for (int q0 = 0; q0 < nw; q0 += 32) {
+                const int q = q0 + lane;
+                const uint32_t x = q < nw ? keys[q] : 0u;
+                uint32_t pfx = x;
+                pfx ^= pfx << 1; pfx ^= pfx << 2; pfx ^= pfx << 4; pfx ^= pfx << 8; pfx ^= pfx << 16;
+                const unsigned par = __ballot_sync(FULL, __popc(x) & 1);
+                const int pre = (carry + __popc(par & ((1u << lane) - 1u))) & 1;
+                carry = (carry + __popc(par)) & 1;
+                uint32_t in = pre ? ~pfx : pfx;
+                if (q >= nw) in = 0u;
+                else if (cols - q * 32 < 32) in &= (1u << (cols - q * 32)) - 1u;
+                const int nsp = __popc(in & ~(in << 1));
+                if (pass == 0) {
+                    nsp_all += nsp;
+                    continue;
+                }
+                int chunk;
+                int sl = slot + warp_excl_scan_int(nsp, lane, &chunk);
+                slot += chunk;
+                px += __popc(in);
+                while (in) {
+                    const int lo = __ffs(in) - 1;
+                    const uint32_t rest = ~(in | ((1u << lo) - 1u));
+                    const int hi = rest ? __ffs(rest) - 1 : 32;
+                    in = hi < 32 ? (in & ~((1u << hi) - 1u)) : 0u;
+                    if (sl < D.cap)
+                        D.spans[rb * D.cap + sl] = (rank << 32) | ((unsigned long long)(i_off + q * 32 + hi) << 16) |
+                                                   (unsigned long long)(i_off + q * 32 + lo);
+                    else
+                        atomicOr(&st->err, (int)E_SPAN_OVF);
+                    ++sl;
+                }
+            }
+            if (pass == 0) {
+                nsp_all = warp_sum(nsp_all);
+                int base = 0;
+                if (lane == 0 && nsp_all) base = atomicAdd(&D.rowcnt[rb], nsp_all);
+                slot = __shfl_sync(FULL, base, 0);
+            }
+        }
+        __syncwarp();
+        return px;
+    };
     int w0 = j_off, wh = min(rows, RW_WROWS);
-    // `bits`: a one-row window whose toggles overflow the key buffer is redone as a parity bitmap
-    // of its columns (keys[] reused: 256 words = 8192 bits >= cols), so any number of crossings
-    // per scanline rasterises, as raster.py:80-89's bincount does
-    bool bits = false;
     while (w0 < j_end) {
         const int w1 = min(w0 + wh, j_end);
         const int W = w1 - w0;
         for (int q = lane; q <= W; q += 32) rc[q] = 0;
-        if (bits)
-            for (int q = lane; q < RW_TCAP; q += 32) keys[q] = 0u;
         __syncwarp();
         // ---- crossings of every ring edge (raster.py:30-61, flattening :86-89) ----
         if (lane == 0) s_tot[wid] = 0;
@@ -532,10 +551,6 @@ __global__ void __launch_bounds__(RW_WARPS * 32, sizeof(ST) == 8 ? DET_RW_MINB64
                     dest = j_off + (int)dr;
                 }
                 if (cc == cols || dest < w0 || dest >= w1) continue;  // absorber column / other window
-                if (bits) {  // one-row window: toggle the column's parity bit
-                    atomicXor(&keys[cc >> 5], 1u << (cc & 31));
-                    continue;
-                }
                 const int slot = atomicAdd(&s_tot[wid], 1);
                 if (slot < RW_TCAP) {
                     keys[slot] = ((uint32_t)(dest - w0) << 16) | (uint32_t)(i_off + cc);
@@ -586,19 +601,23 @@ __global__ void __launch_bounds__(RW_WARPS * 32, sizeof(ST) == 8 ? DET_RW_MINB64
             }
         }
         __syncwarp();
-        if (bits) {
-            const size_t rb = (size_t)b * n + w0;
-            area += bitmap_spans(keys, cols, i_off, rank, D.rowcnt + rb, D.spans + rb * D.cap, D.cap, &st->err, lane);
-            bits = false;
-            w0 = w1;
-            __syncwarp();
-            continue;
-        }
         const int tot = s_tot[wid];
         __syncwarp();
         if (tot > RW_TCAP) {
-            if (W == 1) bits = true;  // redo this row as a parity bitmap
-            else wh = max(1, W >> 1);
+            if (W == 1) {
+                if constexpr (BM) {
+                    // more toggles on scanline w0 than the key buffer holds: the parity-bitmap
+                    // slow path (only in the BM instantiation the host switches to on overflow)
+                    area += bitmap_row(w0);
+                    w0 = w1;
+                    __syncwarp();
+                    continue;
+                } else {
+                    if (lane == 0) atomicOr(&st->err, (int)E_TOGGLE_OVF);
+                    return;
+                }
+            }
+            wh = max(1, W >> 1);
             __syncwarp();
             continue;
         }

@@ -19,7 +19,9 @@ float64 expressions so the target weights are bit-identical.
 
 from __future__ import annotations
 
+import functools
 import itertools
+import os
 import time
 from dataclasses import dataclass, field, replace
 
@@ -30,6 +32,7 @@ from ._lib import PRECISIONS, STOP_BDV, STOP_COLLAPSED, STOP_NAMES, STOP_NEGINDE
 from .errors import NumericError, RasterizationError, RegionCollapsedError
 from .geomodel import deferred_rebuild, densify, rebuild, ring_layout
 from .raster import LabelTexture, _LazyLabels, rasterize_labels
+from .shard import run_sharded
 
 DENSIFY_EDGE_PIXELS = 4.0
 
@@ -121,9 +124,18 @@ class BatchEngine:
 
     def __init__(self, mapmodel, statistics, criteria=None, k: int = 10, bdv_multiplier=1.0,
                  background_mass=None, bdv_mode: str = "fixed-mass", apply_densify: bool = True,
-                 start_vertices=None, *, device: int = 0, field_dtype: str = "float64"):
+                 start_vertices=None, *, device: int = 0, field_dtype: str = "float64", devices=None,
+                 distributed: bool = False):
         if bdv_mode not in ("fixed-mass", "rederive"):
             raise ValueError("bdv_mode must be 'fixed-mass' or 'rederive'")
+        # sharded runs (shard.run_sharded): one process per GPU, a contiguous block of the
+        # cartograms each, results gathered at the end; set-up here runs on the local device
+        self.devices = None if devices is None else [int(d) for d in devices]
+        self.distributed = bool(distributed)
+        if self.distributed:
+            device = int(os.environ.get("LOCAL_RANK", "0")) if self.devices is None else device
+        elif self.devices:
+            device = self.devices[0]
         if field_dtype not in PRECISIONS:
             raise ValueError("field_dtype must be 'float64', 'mixed' or 'float32'")
         if not (4 <= k <= 13):
@@ -213,8 +225,16 @@ class BatchEngine:
         ctx.run(c.error_threshold, c.stagnation_window, c.max_iterations)
         return ctx
 
+    def _sharded(self) -> bool:
+        return self.distributed or (self.devices is not None and len(self.devices) > 1)
+
     def run_all(self, criteria=None, iteration_offset: int = 0, clamp_offset: int = 0):
         """List of RunResult (or the CartomorphError/ValueError instance a cartogram raised)."""
+        if self._sharded():
+            task = functools.partial(_batch_shard, self.initial_map, self.statistics, criteria or self.criteria,
+                                     self.k, self.bdv_multiplier, self.background_mass, self.bdv_mode, self._start,
+                                     self.field_dtype, iteration_offset, clamp_offset)
+            return run_sharded(self.B, task, devices=self.devices, distributed=self.distributed)
         t0 = time.perf_counter()
         ctx = self.launch(criteria)
         t1 = time.perf_counter()
@@ -248,7 +268,7 @@ class BatchEngine:
         records = trace_records(tr, it_off)
         clamps = int(r.clamp_events) + (cl_off if r.stop_reason != 2 else 0)
         result_map = deferred_rebuild(self.initial_map, verts, self.statistics[b], self._sizes)
-        lazy = _LazyLabels(ctx, b, getattr(ctx, "generation", None), lambda: result_map, self.k, self.device)
+        lazy = _LazyLabels(ctx, b, getattr(ctx, "generation", None), result_map, self.k, self.device)
         labels = LabelTexture(size=self.n, labels=lazy, region_ids=tuple(self.region_ids), _counts=counts)
         state = CartogramState(mapmodel=result_map, iteration=int(r.iteration) + it_off,
                                labels=labels, pixel_counts=counts[:-1].copy(),
@@ -260,6 +280,17 @@ class BatchEngine:
     def areas(self, b: int = 0) -> np.ndarray:
         """Per-region shoelace areas of cartogram b's last state, on the device (Region.area())."""
         return self._ctx().areas(b)
+
+
+def _batch_shard(mapmodel, stats, criteria, k, mult, masses, bdv_mode, start, field_dtype, it_off, cl_off, lo, hi,
+                 device):
+    """Cartograms [lo, hi) of a sharded BatchEngine on `device` (runs in that GPU's process); the
+    map is already densified and the background masses are the parent's, so every cartogram is
+    exactly the one the unsharded batch would run."""
+    be = BatchEngine(mapmodel, stats[lo:hi], criteria=criteria, k=k, bdv_multiplier=mult[lo:hi],
+                     background_mass=masses[lo:hi], bdv_mode=bdv_mode, apply_densify=False,
+                     start_vertices=None if start is None else start[lo:hi], device=device, field_dtype=field_dtype)
+    return be.run_all(criteria, it_off, cl_off)
 
 
 class CartogramEngine:

@@ -23,15 +23,19 @@ BACKGROUND = -1
 class _LazyLabels:
     """Deferred label texture of a run result: read back from the device while the context
     still holds it, otherwise re-rasterised from the result's own vertices (the raster is
-    deterministic, so both give the same array)."""
+    deterministic, so both give the same array).  Pickles without its context (a result sent
+    from a per-GPU worker process re-rasterises on first access)."""
 
-    def __init__(self, ctx, b, generation, mapmodel_fn, k, device):
-        self.ctx, self.b, self.gen, self.mapmodel_fn, self.k, self.device = ctx, b, generation, mapmodel_fn, k, device
+    def __init__(self, ctx, b, generation, mapmodel, k, device):
+        self.ctx, self.b, self.gen, self.mapmodel, self.k, self.device = ctx, b, generation, mapmodel, k, device
+
+    def __getstate__(self):
+        return dict(self.__dict__, ctx=None, gen=None, device=0)
 
     def materialize(self) -> np.ndarray:
-        if getattr(self.ctx, "generation", None) == self.gen:
+        if self.ctx is not None and getattr(self.ctx, "generation", None) == self.gen:
             return self.ctx.labels(self.b)
-        return rasterize_labels(self.mapmodel_fn(), self.k, check_collapse=False, device=self.device).labels
+        return rasterize_labels(self.mapmodel, self.k, check_collapse=False, device=self.device).labels
 
 
 @dataclass(frozen=True)

@@ -10,6 +10,7 @@ text, row for row.  Argument parsing and file output belong to the CLI and stay 
 
 from __future__ import annotations
 
+import functools
 import time
 
 import numpy as np
@@ -18,14 +19,18 @@ from .engine import BatchEngine, StoppingCriteria
 from .errors import CartomorphError, IngestionError
 from .geomodel import ring_layout
 from .metrics import frame_reports
+from .shard import run_sharded
 
 SWEEP_HEADER = "multiplier,stop_reason,iterations,xi,epsilon,tau,hamming_avg,hamming_max,position_error,wall_ms,error"
 
 
 def sweep_bdv(mapmodel, multipliers, criteria: StoppingCriteria | None = None, k: int = 10, hamming_k: int = 7, *,
-              device: int = 0, field_dtype: str = "float64"):
+              device: int = 0, field_dtype: str = "float64", devices=None, distributed: bool = False):
     """``(csv_text, results)`` for the sorted multipliers (cli.py:265-300); ``results[i]`` is the
-    RunResult (or the CartomorphError) of the i-th sorted multiplier."""
+    RunResult (or the CartomorphError) of the i-th sorted multiplier.
+
+    ``devices=[...]`` / ``distributed=True`` shard the multipliers over one process per GPU
+    (shard.run_sharded); each process runs its block as one batch with its reports."""
     mults = sorted(float(m) for m in multipliers)
     if any(not (0.5 <= m <= 2.0) for m in mults):
         raise IngestionError("multipliers must lie in [0.5, 2]")
@@ -33,6 +38,19 @@ def sweep_bdv(mapmodel, multipliers, criteria: StoppingCriteria | None = None, k
     rows = [SWEEP_HEADER]
     if not mults:
         return "\n".join(rows) + "\n", []
+    task = functools.partial(_sweep_block, mapmodel, mults, criteria, k, hamming_k, field_dtype)
+    if devices is None and not distributed:
+        parts = task(0, len(mults), device)
+    else:
+        parts = run_sharded(len(mults), task, devices=devices, distributed=distributed)
+    rows += [p[0] for p in parts]
+    return "\n".join(rows) + "\n", [p[1] for p in parts]
+
+
+def _sweep_block(mapmodel, all_mults, criteria, k, hamming_k, field_dtype, lo, hi, device):
+    """[(csv row, result)] of multipliers [lo, hi) as one device batch on `device`."""
+    mults = all_mults[lo:hi]
+    rows = []
     began = time.perf_counter()
     stats = mapmodel.statistics() if hasattr(mapmodel, "statistics") else np.array([r.statistic for r in mapmodel.regions])
     try:
@@ -41,8 +59,7 @@ def sweep_bdv(mapmodel, multipliers, criteria: StoppingCriteria | None = None, k
         results = be.run_all()
     except CartomorphError as exc:  # a start-map problem fails every multiplier alike
         wall_ms = (time.perf_counter() - began) * 1e3 / len(mults)
-        rows += [f"{m:.6g},failed,,,,,,,,{wall_ms:.3f},{exc}" for m in mults]
-        return "\n".join(rows) + "\n", [exc] * len(mults)
+        return [(f"{m:.6g},failed,,,,,,,,{wall_ms:.3f},{exc}", exc) for m in mults]
     wall_ms = (time.perf_counter() - began) * 1e3 / len(mults)
     ok = [i for i, r in enumerate(results) if not isinstance(r, Exception)]
     reports = {}
@@ -68,4 +85,4 @@ def sweep_bdv(mapmodel, multipliers, criteria: StoppingCriteria | None = None, k
         rows.append(f"{m:.6g},{res.stop_reason},{st.iteration},{st.xi:.9g},{st.epsilon:.9g},{rep.tau:.9g},"
                     f"{rep.hamming_avg:.9g},{rep.hamming_max:.9g},{rep.position_error:.9g},{wall_ms:.3f},")
         out.append(res)
-    return "\n".join(rows) + "\n", out
+    return list(zip(rows, out))

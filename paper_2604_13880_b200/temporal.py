@@ -19,6 +19,7 @@ temporal.py:203-209) computed on the GPU for all frames at once
 
 from __future__ import annotations
 
+import functools
 import logging
 import time
 from dataclasses import dataclass, field
@@ -32,6 +33,7 @@ from .errors import CartomorphError, IngestionError, RasterizationError, RegionC
 from .geomodel import deferred_rebuild, densify, ring_layout
 from .metrics import frame_reports
 from .raster import LabelTexture, _LazyLabels, rasterize_labels
+from .shard import run_sharded
 
 log = logging.getLogger(__name__)
 
@@ -154,62 +156,82 @@ def _masses(dataset, policy, k, bdv_multiplier):
 def run_direct(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None = None,
                policy: AreaFractionPolicy | None = None, k: int = 10, bdv_multiplier: float = 1.0,
                watchdog_ceiling: float = DEFAULT_WATCHDOG_CEILING, report_raster_k: int = 7, *,
-               device: int = 0, field_dtype: str = "float64") -> FrameSequence:
-    """Every frame deformed independently from the original map -- all frames in one GPU batch."""
+               device: int = 0, field_dtype: str = "float64", devices=None,
+               distributed: bool = False) -> FrameSequence:
+    """Every frame deformed independently from the original map -- all frames in one GPU batch.
+
+    ``devices=[...]`` shards the frames over one worker process per GPU, ``distributed=True`` over
+    the ranks of an initialised torch.distributed job (shard.run_sharded); the frames are
+    independent, so the only exchange is the final gather."""
     criteria = criteria or StoppingCriteria()
     masses, fractions = _masses(dataset, policy, k, bdv_multiplier)
     base_map = densify(dataset.mapmodel, DENSIFY_EDGE_PIXELS / (1 << k))
     seq = FrameSequence(strategy="direct", dataset=dataset, base_map=base_map)
-    began = time.perf_counter()
-    try:
-        # engines are built with the reference's per-frame arguments (temporal.py:190-196):
-        # bdv_multiplier defaults to 1.0 there, the masses carry the user's multiplier
-        be = BatchEngine(base_map, dataset.statistics, criteria=criteria, k=k,
-                         background_mass=np.asarray(masses, dtype=float), apply_densify=False,
-                         device=device, field_dtype=field_dtype)
-        results = be.run_all()
-    except CartomorphError as exc:  # a start-map problem fails every frame alike
-        results = [exc] * dataset.step_count
-    wall_ms = (time.perf_counter() - began) * 1e3 / max(dataset.step_count, 1)
-    ok = [t for t, res in enumerate(results) if not isinstance(res, Exception)]
-    reports = _reports(base_map, dataset, masses, [results[t].state.mapmodel for t in ok], ok, report_raster_k,
-                       wall_ms, device)
-    rep_of = dict(zip(ok, reports))
-    for t, res in enumerate(results):
-        frac = None if fractions[t] is None else float(fractions[t])
-        if isinstance(res, CartomorphError):
-            log.error("direct frame %d failed: %s", t, res)
-            seq.frames.append(Frame(t, dataset.times[t], None, None, None, float(masses[t]), frac, wall_ms,
-                                    error=str(res)))
-        elif isinstance(res, Exception):
-            raise res
-        else:
-            seq.frames.append(_frame(seq, t, dataset, res, rep_of[t], float(masses[t]), frac, wall_ms,
-                                     watchdog_ceiling))
+    task = functools.partial(_direct_block, base_map, dataset.times, dataset.statistics, criteria,
+                             np.asarray(masses, dtype=float), fractions, k, watchdog_ceiling, report_raster_k,
+                             field_dtype)
+    if devices is None and not distributed:
+        seq.frames.extend(task(0, dataset.step_count, device))
+    else:
+        seq.frames.extend(run_sharded(dataset.step_count, task, devices=devices, distributed=distributed))
     return seq
 
 
-def _reports(base_map, dataset, masses, cartos, times, raster_k, wall_ms, device):
+def _direct_block(base_map, times, statistics, criteria, masses, fractions, k, watchdog_ceiling, report_raster_k,
+                  field_dtype, lo, hi, device):
+    """Frames [lo, hi) of a direct-mode sequence as one device batch on `device`, with their
+    reports (temporal.py:185-246 per frame)."""
+    began = time.perf_counter()
+    idx = list(range(lo, hi))
+    try:
+        # engines are built with the reference's per-frame arguments (temporal.py:190-196):
+        # bdv_multiplier defaults to 1.0 there, the masses carry the user's multiplier
+        be = BatchEngine(base_map, statistics[lo:hi], criteria=criteria, k=k, background_mass=masses[lo:hi],
+                         apply_densify=False, device=device, field_dtype=field_dtype)
+        results = be.run_all()
+    except CartomorphError as exc:  # a start-map problem fails every frame alike
+        results = [exc] * len(idx)
+    wall_ms = (time.perf_counter() - began) * 1e3 / max(len(idx), 1)
+    ok = [i for i, res in enumerate(results) if not isinstance(res, Exception)]
+    reports = _reports(base_map, statistics, masses, [results[i].state.mapmodel for i in ok], [lo + i for i in ok],
+                       report_raster_k, wall_ms, device)
+    rep_of = dict(zip(ok, reports))
+    frames = []
+    for i, res in enumerate(results):
+        t = lo + i
+        frac = None if fractions[t] is None else float(fractions[t])
+        if isinstance(res, CartomorphError):
+            log.error("direct frame %d failed: %s", t, res)
+            frames.append(Frame(t, times[t], None, None, None, float(masses[t]), frac, wall_ms, error=str(res)))
+        elif isinstance(res, Exception):
+            raise res
+        else:
+            frames.append(_frame("direct", t, times, res, rep_of[i], float(masses[t]), frac, wall_ms,
+                                 watchdog_ceiling))
+    return frames
+
+
+def _reports(base_map, statistics, masses, cartos, times, raster_k, wall_ms, device):
     """full_report of each successful frame (temporal.py:200-209), all frames in one GPU pass."""
     if not times:
         return []
     _, rs, rr, ids, _ = ring_layout(base_map)
     xy = np.stack([c.vertex_array() for c in cartos])
-    stats = dataset.statistics[times]
-    weights = [dataset.statistics[t] / float(dataset.statistics[t].sum() + masses[t]) for t in times]
+    stats = statistics[times]
+    weights = [statistics[t] / float(statistics[t].sum() + masses[t]) for t in times]
     return frame_reports(base_map, (None, rs, rr, len(ids)), xy, stats, weights, raster_k,
                          [wall_ms] * len(times), device=device)
 
 
-def _frame(seq, t, dataset, res, report, mb, frac, wall_ms, ceiling):
+def _frame(strategy, t, times, res, report, mb, frac, wall_ms, ceiling):
     """A successful deformation plus its report; a report error fails the frame (temporal.py:231-244)."""
     if isinstance(report, Exception):
-        log.error("%s frame %d failed: %s", seq.strategy, t, report)
-        return Frame(t, dataset.times[t], None, None, None, mb, frac, wall_ms, error=str(report))
-    fr = Frame(t, dataset.times[t], res.state.mapmodel, res, report, mb, frac, wall_ms,
+        log.error("%s frame %d failed: %s", strategy, t, report)
+        return Frame(t, times[t], None, None, None, mb, frac, wall_ms, error=str(report))
+    fr = Frame(t, times[t], res.state.mapmodel, res, report, mb, frac, wall_ms,
                watchdog=report.hamming_avg > ceiling)
     if fr.watchdog:
-        log.warning("%s frame %d: average shape distortion %.3f exceeds ceiling %.3f", seq.strategy, t,
+        log.warning("%s frame %d: average shape distortion %.3f exceeds ceiling %.3f", strategy, t,
                     report.hamming_avg, ceiling)
     return fr
 
@@ -263,7 +285,8 @@ def run_cumulative(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None
             results[t] = _chain_result(ctx, base_map, ids, sizes, dataset.statistics[t], totals[t], masses[t],
                                        out_xy[i], r, cnt[i], trace[i], n, k, device)
         ok = [t for t in sorted(results) if not isinstance(results[t], Exception)]
-        reports = _reports(base_map, dataset, masses, [results[t].state.mapmodel for t in ok], ok, report_raster_k,
+        reports = _reports(base_map, dataset.statistics, masses, [results[t].state.mapmodel for t in ok], ok,
+                           report_raster_k,
                            wall_ms, device)
         rep_of = dict(zip(ok, reports))
         restart = None
@@ -275,7 +298,7 @@ def run_cumulative(dataset: TimeSeriesDataset, criteria: StoppingCriteria | None
                 log.error("cumulative frame %d failed: %s", t, res_t)
                 frames[t] = Frame(t, dataset.times[t], None, None, None, mb, frac, wall_ms, error=str(res_t))
                 continue
-            frames[t] = _frame(seq, t, dataset, res_t, rep_of[t], mb, frac, wall_ms, watchdog_ceiling)
+            frames[t] = _frame("cumulative", t, dataset.times, res_t, rep_of[t], mb, frac, wall_ms, watchdog_ceiling)
             if frames[t].error is not None:
                 restart = t
                 break
@@ -292,7 +315,7 @@ def _chain_result(ctx, base_map, ids, sizes, stats_t, total_t, mb, xy_t, r, coun
     total_mass = float(total_t) + float(mb)
     weights = stats_t / total_mass * (n * n)
     records = trace_records(trace_t[: r.trace_len])
-    labels = LabelTexture(size=n, labels=_LazyLabels(ctx, 0, -1, (lambda c=carto: c), k, device),
+    labels = LabelTexture(size=n, labels=_LazyLabels(ctx, 0, -1, carto, k, device),
                           region_ids=tuple(ids), _counts=counts)
     per_region = np.abs(counts[:-1] - weights) / np.maximum(counts[:-1].astype(float), weights)
     state = CartogramState(mapmodel=carto, iteration=int(r.iteration), labels=labels,

@@ -1,11 +1,12 @@
-"""world_size-2 gloo test of the multi-process path: shard frames, compute per rank, final gather.
+"""world_size-2 gloo tests of the multi-process path: shard frames, compute per rank, final gather.
 
-Runs on CPU.  Each rank runs the oracle engine (the checker) on its shard of a
-tiny direct-mode job; the gathered results must equal a single-process run.
-This covers the host-side logic the GPU bench uses (shard_bounds +
-gather_frame_results), which is identical regardless of the compute backend.
+Runs on CPU.  The product's sharding entry point (``shard.run_sharded``, used by
+``run_direct`` / ``sweep_bdv`` / ``BatchEngine`` with ``distributed=True`` or ``devices=[...]``)
+drives a block task; here the task runs the oracle engine (the checker) on its block of a tiny
+direct-mode job, since there is no GPU.  The gathered results must equal a single-process run.
 """
 
+import functools
 import os
 import socket
 
@@ -38,6 +39,11 @@ def _frame(m, stats):
     return r.rows, r.xi
 
 
+def _block(n_frames, lo, hi, device):
+    m, walk = _job(n_frames)
+    return [(t, device) + _frame(m, walk[t]) for t in range(lo, hi)]
+
+
 def _worker(rank, world, port, n_frames, q):
     import sys
 
@@ -58,6 +64,11 @@ def _worker(rank, world, port, n_frames, q):
         rows.append(r)
         xi.append(x)
     out = gather_frame_results({"rows": np.stack(rows), "xi": np.array(xi)}, dist)
+    # the product's entry point: every rank gets every unit's result, in unit order
+    from paper_2604_13880_b200.shard import run_sharded
+
+    objs = run_sharded(n_frames, functools.partial(_block, n_frames), distributed=True)
+    out["objs"] = objs
     if rank == 0:
         q.put(out)
     dist.barrier()
@@ -77,7 +88,38 @@ def test_gloo_two_ranks_shard_and_gather():
         p.join(timeout=120)
         assert p.exitcode == 0
     m, walk = _job(n_frames)
+    assert [o[0] for o in out["objs"]] == list(range(n_frames))
+    assert [o[1] for o in out["objs"]] == [0] * n_frames  # LOCAL_RANK unset: device 0 on every rank
     for t in range(n_frames):
         r, x = _frame(m, walk[t])
         np.testing.assert_array_equal(out["rows"][t], r)
         assert out["xi"][t] == x
+        np.testing.assert_array_equal(out["objs"][t][2], r)
+        assert out["objs"][t][3] == x
+
+
+def test_run_sharded_worker_processes():
+    # devices=[...]: one spawned worker process per device id, blocks gathered in unit order
+    from paper_2604_13880_b200.shard import run_sharded, shutdown_workers
+
+    n_frames = 5
+    try:
+        objs = run_sharded(n_frames, functools.partial(_block_mod, n_frames), devices=[3, 7])
+    finally:
+        shutdown_workers()
+    assert [o[0] for o in objs] == list(range(n_frames))
+    assert [o[1] for o in objs] == [3, 3, 3, 7, 7]
+    m, walk = _job(n_frames)
+    for t in range(n_frames):
+        r, x = _frame(m, walk[t])
+        np.testing.assert_array_equal(objs[t][2], r)
+
+
+def _block_mod(n_frames, lo, hi, device):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for p in (root, os.path.join(root, "tests")):
+        if p not in sys.path:
+            sys.path.insert(0, p)
+    return _block(n_frames, lo, hi, device)

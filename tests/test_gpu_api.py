@@ -127,3 +127,58 @@ def test_many_holes_engine_vs_oracle(P):
     ref = O.OracleEngine(O.FlatMap.from_mapmodel(m), k=10).run(1e-300, 10**9, 3)
     assert np.array_equal(res.state.pixel_counts, ref.counts)
     np.testing.assert_allclose(res.state.mapmodel.vertex_array(), ref.rows, rtol=0, atol=1e-9)
+
+
+# ---------------------------------------------------------------- multi-GPU drop-in (1 GPU here)
+def test_run_direct_sharded_equals_single(P):
+    # devices=[0, 0]: two blocks through the per-GPU worker process, gathered in frame order
+    from paper_2604_13880_b200.shard import shutdown_workers
+
+    m = fm.small_voronoi(seed=5, r=16, target=400, shuffle_ids=True)
+    walk = np.stack([m.statistics() * np.exp(0.1 * t * np.sin(np.arange(16))) for t in range(5)])
+    ds = P.TimeSeriesDataset(m, tuple(f"t{t}" for t in range(5)), walk)
+    crit = P.StoppingCriteria(1e-300, 10**9, 6)
+    one = P.run_direct(ds, crit, k=7)
+    try:
+        two = P.run_direct(ds, crit, k=7, devices=[0, 0])
+        csv1, res1 = P.sweep_bdv(m, [0.5, 0.8, 1.1, 1.4, 1.7], crit, k=7)
+        csv2, res2 = P.sweep_bdv(m, [0.5, 0.8, 1.1, 1.4, 1.7], crit, k=7, devices=[0, 0])
+        be = P.BatchEngine(m, walk, criteria=crit, k=7, devices=[0, 0])
+        bres = be.run_all()
+    finally:
+        shutdown_workers()
+    assert len(two.frames) == len(one.frames) == 5
+    for a, b in zip(one.frames, two.frames):
+        assert a.time_index == b.time_index and a.error == b.error
+        assert np.array_equal(a.mapmodel.vertex_array(), b.mapmodel.vertex_array())
+        assert np.array_equal(a.result.state.pixel_counts, b.result.state.pixel_counts)
+        assert a.report.hamming_avg == b.report.hamming_avg
+    strip = lambda c: [",".join(r.split(",")[:-2]) for r in c.splitlines()]  # drop wall_ms, error
+    assert strip(csv1) == strip(csv2)
+    for a, b, r in zip(one.frames, bres, range(5)):
+        assert np.array_equal(a.mapmodel.vertex_array(), b.state.mapmodel.vertex_array())
+        assert np.array_equal(b.state.labels.labels, a.result.state.labels.labels)  # re-rasterised after pickling
+
+
+@pytest.mark.parametrize("field", ["float64", "float32"])
+def test_run_is_deterministic_and_prefix_stable(P, field):
+    # the same run twice is bit-identical, and a shorter run's trace is a prefix of a longer one's
+    m = fm.config1()
+    runs = []
+    for T in (5, 9, 9):
+        crit = P.StoppingCriteria(error_threshold=1e-300, stagnation_window=10**9, max_iterations=T)
+        runs.append(P.CartogramEngine(m, criteria=crit, k=8, bdv_multiplier=0.5, field_dtype=field).run())
+    a, b, c = runs
+    assert [t.xi for t in b.trace] == [t.xi for t in c.trace]
+    assert np.array_equal(b.state.mapmodel.vertex_array(), c.state.mapmodel.vertex_array())
+    assert [t.xi for t in a.trace] == [t.xi for t in b.trace][:6]
+
+
+def test_bitmap_raster_engine_deterministic(P):
+    # the parity-bitmap k_region instantiation (switched to on toggle overflow) is deterministic
+    m = fm.many_holes()
+    crit = P.StoppingCriteria(error_threshold=1e-300, stagnation_window=10**9, max_iterations=4)
+    r1 = P.CartogramEngine(m, criteria=crit, k=10).run()
+    r2 = P.CartogramEngine(m, criteria=crit, k=10).run()
+    assert np.array_equal(r1.state.mapmodel.vertex_array(), r2.state.mapmodel.vertex_array())
+    assert np.array_equal(r1.state.pixel_counts, r2.state.pixel_counts)
