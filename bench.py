@@ -4,8 +4,9 @@ Workload ("headline"): the 3000-region seeded Voronoi map with ~200k unique
 vertices (synthetic), 1024^2 texture, run as direct-mode time
 steps: every GPU holds a batch of B independent frames (statistics = a seeded
 lognormal random walk over time) and one bench "step" is one DET iteration of
-every frame in the batch.  Inputs are device-resident before timing; the batch
-working set (~35 MB per frame) is larger than the 126 MB L2 for B >= 4.
+every frame in the batch (B = 32 by default).  Inputs are device-resident before
+timing; the batch working set (~45 MB per frame with the float64 field) is larger than
+the 126 MB L2 for B >= 3.
 
     python bench.py [--gpus N --steps K --warmup W --batch B]
     torchrun --nproc-per-node N bench.py --gpus N ...        (one process per GPU)
@@ -40,14 +41,17 @@ def algorithmic_bytes_per_iteration(n: int, n_unique: int) -> float:
     return 28.0 * n * n + 32.0 * n_unique + min(100.0 * n_unique, 20.0 * n * n)
 
 
-def phase_bytes(n: int, n_unique: int, n_rows: int, n_regions: int) -> dict:
-    """Algorithmic bytes per iteration of each phase."""
+def phase_bytes(n: int, n_unique: int, n_rows: int, n_regions: int, field: str = "float64") -> dict:
+    """Algorithmic bytes per iteration of each phase, in the run's field dtype:
+    fb = bytes per field component (8 float64, 4 float32), sb = bytes per state coordinate."""
+    fb = 8 if field == "float64" else 4
+    sb = 4 if field == "float32" else 8
     return {
-        # integral images -> field: read labels (4 n^2), write the float32 field (8 n^2)
-        "integral_images": 12.0 * n * n,
-        # advect + crossings: per unique vertex read 8 B + write 8 B (float32 state) + 4 float2
-        # field texels (32 B)
-        "region": 48.0 * n_unique,
+        # integral images -> field: read labels (4 n^2), write the two-component field (2 fb n^2)
+        "integral_images": (4.0 + 2 * fb) * n * n,
+        # advect + crossings: per unique vertex read + write of the state (4 sb) and the four
+        # two-component field texels of its bilinear tap (8 fb)
+        "region": (4.0 * sb + 8.0 * fb) * n_unique,
         # paint: write labels (4 n^2)
         "row": 4.0 * n * n,
         "ctrl": 0.0,
@@ -55,9 +59,9 @@ def phase_bytes(n: int, n_unique: int, n_rows: int, n_regions: int) -> dict:
 
 
 def kernels_per_iteration(field: str) -> int:
-    """k_sat1/2/3, k_region, k_row, k_ctrl, plus k_advect_rows on the float32 path (advect as its
-    own kernel when DET_SPLIT_ADVECT=1; fused into k_region by default)."""
-    split = field == "float32" and os.environ.get("DET_SPLIT_ADVECT", "0") == "1"
+    """k_sat1w, k_sat2p, k_sat3, k_region, k_row, k_ctrl, plus k_advect_rows(64) on the float32 and
+    float64 paths when DET_SPLIT_ADVECT=1 (advect fused into k_region by default)."""
+    split = field != "mixed" and os.environ.get("DET_SPLIT_ADVECT", "0") == "1"
     return 7 if split else 6
 
 
@@ -231,7 +235,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=64)
     ap.add_argument("--warmup", type=int, default=8)
-    ap.add_argument("--batch", type=int, default=16, help="frames per GPU")
+    ap.add_argument("--batch", type=int, default=32, help="frames per GPU (32: best of 16-128, DESIGN.md §5)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--band", type=int, default=0, help="band height of the integral-image kernels (0 = auto)")
     ap.add_argument("--field", default="float64", choices=["float64", "mixed", "float32"])
@@ -315,7 +319,7 @@ def main():
     names = ["integral_images", "region", "row", "ctrl"]
     per_iter_ms = {k: v / 8 for k, v in zip(names, ph)}
     dom = max(per_iter_ms, key=per_iter_ms.get)
-    pbytes = phase_bytes(n, n_unique, n_rows, len(m.regions))
+    pbytes = phase_bytes(n, n_unique, n_rows, len(m.regions), args.field)
     peak, peak_kind = load_peaks()
     dom_achieved = pbytes[dom] * args.batch / (per_iter_ms[dom] * 1e-3) / 1e9
     step_bytes = algorithmic_bytes_per_iteration(n, n_unique) * args.batch
@@ -393,7 +397,7 @@ def main():
                                    "gc.collect() before each; pinned result buffer reserved at BatchEngine "
                                    "construction",
                        "l2": "inputs larger than L2 (~%d MB working set per GPU vs 126 MB L2)"
-                             % int(args.batch * 35), "iterations_per_time_step": prm["iterations"],
+                             % int(args.batch * (45 if args.field != "float32" else 35)), "iterations_per_time_step": prm["iterations"],
                        "time_steps_per_s": value / prm["iterations"]},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": dom_achieved, "peak": peak, "unit": "GB/s",
                          "frac": dom_achieved / peak, "traffic": traffic_for(dom, args.batch),

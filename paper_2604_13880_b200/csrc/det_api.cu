@@ -165,6 +165,14 @@ static void smem_optin(F fn) {
 #ifndef DET_SAT3_CPT
 #define DET_SAT3_CPT 4  // k_sat3 columns per thread on the float32 path
 #endif
+// Diagnostics only (timing experiments, results invalid): DET_SKIP bit mask of iteration stages
+// left out of the captured graph -- 1 band sums + carries (k_sat1w, k_sat2p), 2 k_sat3,
+// 4 advect + raster (k_region), 8 paint + control step (k_row, k_ctrl).
+static int skip_mask() {
+    static const int m = [] { const char* e = getenv("DET_SKIP"); return e ? atoi(e) : 0; }();
+    return m;
+}
+
 template <int CPT, int NT>
 static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S, int gate, int src, int out,
                            bool u64, int B) {
@@ -191,7 +199,10 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     // where the band kernels use 4)
     constexpr int CPT1 = (CPT == 4 && NT * 4 / DET_SAT1W_CPT <= 1024 && NT * 4 / DET_SAT1W_CPT >= 32) ? DET_SAT1W_CPT : CPT;
     constexpr int NT1 = NT * CPT / CPT1;
-    if (src == SRC_LABELS && out == OUT_U && c->sat1w && n % (32 * CPT1) == 0 && (f32 || n <= 4096)) {
+    const bool skip12 = src == SRC_LABELS && out == OUT_U && (skip_mask() & 1);
+    const bool skip3 = src == SRC_LABELS && out == OUT_U && (skip_mask() & 2);
+    if (skip12) {
+    } else if (src == SRC_LABELS && out == OUT_U && c->sat1w && n % (32 * CPT1) == 0 && (f32 || n <= 4096)) {
         // barrier-free band sums in the field's arithmetic type (float32 or float64)
         constexpr int NW = NT1 / 32, KP = lab_kp1(CPT1 * NT1);
         size_t smem1w = ((size_t)2 * (n + H - 1) + (size_t)3 * H * NW) * sa + 16 +
@@ -216,7 +227,8 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     }
 #undef DET_SAT1
     const int lanes = n + 2 * (2 * n - 1);
-    if (src == SRC_LABELS && out == OUT_U)  // band carries split over the warps of a CTA (one memory round trip)
+    if (skip12) {
+    } else if (src == SRC_LABELS && out == OUT_U)  // band carries split over the warps of a CTA (one memory round trip)
         k_sat2p<<<dim3((lanes + 31) / 32 + 1, B), 32 * SAT2_PARTS, 0, c->stream>>>(D, gate);
     else
         k_sat2<<<dim3((lanes + SAT2_THREADS - 1) / SAT2_THREADS + 1, B), SAT2_THREADS, 0, c->stream>>>(D, gate);
@@ -227,7 +239,8 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
         smem_optin(fn);                                                                                      \
         fn<<<gb, NT, smem, c->stream>>>(T, D, S, gate);                                                      \
     } while (0)
-    if (out == OUT_CH8) {
+    if (skip3) {
+    } else if (out == OUT_CH8) {
         if (src == SRC_LABELS) {
             if (luts) DET_SAT3(SRC_LABELS, double, OUT_CH8, true);
             else DET_SAT3(SRC_LABELS, double, OUT_CH8, false);
@@ -289,9 +302,10 @@ static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, in
 // One iteration's advect + raster: the flat advect kernel then a raster-only k_region (float32
 // state), or k_region's fused advect phase.  Returns the number of kernels launched.
 static int launch_advect_raster(det_ctx* c, const Topo& T, const Bufs& D, int gate, int region_mode) {
-    if (!c->s64 && c->split_adv && (region_mode & M_ADVECT)) {
+    if ((!c->s64 || c->f64) && c->split_adv && (region_mode & M_ADVECT)) {
         const int per = ADV_THREADS * ADV_RPT;
-        k_advect_rows<<<dim3((T.n_rows + per - 1) / per, c->B), ADV_THREADS, 0, c->stream>>>(T, D, gate);
+        if (c->f64) k_advect_rows64<<<dim3((T.n_rows + per - 1) / per, c->B), ADV_THREADS, 0, c->stream>>>(T, D, gate);
+        else k_advect_rows<<<dim3((T.n_rows + per - 1) / per, c->B), ADV_THREADS, 0, c->stream>>>(T, D, gate);
         if (region_mode & M_RASTER) launch_region(c, T, D, M_RASTER | M_POSTADV, gate, 0);
         return (region_mode & M_RASTER) ? 2 : 1;
     }
@@ -332,9 +346,9 @@ static void enqueue_iteration(det_ctx* c, int b0 = 0, int Bg = -1, cudaStream_t 
     c->B = Bg;  // grid.y of every launch below
     SatSrc S;
     memset(&S, 0, sizeof(S));
-    launch_sat(c, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, c->f64 != 0, Bg);
-    launch_advect_raster(c, T, D, G_ACTIVE, M_ADVECT | M_RASTER);
-    launch_row_ctrl(c, T, D, G_ACTIVE, 0);
+    if ((skip_mask() & 3) != 3) launch_sat(c, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, c->f64 != 0, Bg);
+    if (!(skip_mask() & 4)) launch_advect_raster(c, T, D, G_ACTIVE, M_ADVECT | M_RASTER);
+    if (!(skip_mask() & 8)) launch_row_ctrl(c, T, D, G_ACTIVE, 0);
     c->B = Bsave;
     c->stream = keep;
 }

@@ -736,6 +736,50 @@ __global__ void __launch_bounds__(ADV_THREADS) k_advect_rows(Topo T, Bufs D, int
     if ((threadIdx.x & 31) == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
 }
 
+// Advect as its own flat kernel, float64 field and state (DET_SPLIT_ADVECT=1 on the float64 path):
+// k_region's phase A arithmetic (displacement.py:209-238 op order) at full occupancy, ADV_RPT rows
+// per thread; k_region then rasterises the rows written here (M_POSTADV).
+__global__ void __launch_bounds__(ADV_THREADS) k_advect_rows64(Topo T, Bufs D, int gate) {
+    const int b = blockIdx.y + D.b0;
+    Carto* st = D.st + b;
+    if (!gate_open(st, gate)) return;
+    const int n = D.n;
+    const size_t ub = (size_t)b * T.n_rows;
+    double2* const pin = reinterpret_cast<double2*>(D.pos0) + ub;  // advected in place (see k_region)
+    double2* __restrict__ pbest = reinterpret_cast<double2*>(D.best) + ub;
+    const bool bestcopy = st->best_pending != 0;
+    const double* uf = reinterpret_cast<const double*>(D.uf) + (size_t)b * D.nn * 2;
+    const int v0 = blockIdx.x * (ADV_THREADS * ADV_RPT) + threadIdx.x;
+    double2 p[ADV_RPT];
+    Tap tp[ADV_RPT];
+    Texels<double> tx[ADV_RPT];
+#pragma unroll
+    for (int q = 0; q < ADV_RPT; ++q) {
+        const int v = v0 + q * ADV_THREADS;
+        p[q] = v < T.n_rows ? pin[v] : make_double2(0.5, 0.5);
+    }
+#pragma unroll
+    for (int q = 0; q < ADV_RPT; ++q) {
+        tp[q] = field_tap(n, p[q].x, p[q].y);
+        tx[q] = field_load<double, Tap>(uf, tp[q]);
+    }
+    int ncl = 0;
+#pragma unroll
+    for (int q = 0; q < ADV_RPT; ++q) {
+        const int v = v0 + q * ADV_THREADS;
+        if (v >= T.n_rows) continue;
+        const double2 sm = field_blend<double, Tap>(tx[q], tp[q]);
+        const double mx = p[q].x + sm.x, my = p[q].y + sm.y;
+        const double cx = mx < 0.0 ? 0.0 : (mx > 1.0 ? 1.0 : mx);  // np.clip (no NaNs here)
+        const double cy = my < 0.0 ? 0.0 : (my > 1.0 ? 1.0 : my);
+        ncl += (cx != mx) + (cy != my);
+        pin[v] = make_double2(cx, cy);
+        if (bestcopy) pbest[v] = p[q];
+    }
+    ncl = warp_sum(ncl);
+    if ((threadIdx.x & 31) == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
+}
+
 #ifndef DET_ROW_RED
 #define DET_ROW_RED 0  // 1: non-returning atomics + clash check + exact repaint (53.3k vs 54.7k: clashes are common)
 #endif
