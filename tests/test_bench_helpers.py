@@ -27,8 +27,10 @@ def test_algorithmic_bytes_match_survey_table(bench):
     # 55.8 MB per iteration at 1024^2 / 200k unique vertices, 601.8 MB at config 5
     assert bench.algorithmic_bytes_per_iteration(1024, 200_000) == pytest.approx(55.8e6, rel=2e-3)
     assert bench.algorithmic_bytes_per_iteration(4096, 1_000_000) == pytest.approx(601.8e6, rel=2e-3)
-    ph = bench.phase_bytes(1024, 200_000, 400_000, 3000)
+    ph = bench.phase_bytes(1024, 200_000, 400_000, 3000, "float32")
     assert ph["integral_images"] == 12 * 1024 * 1024 and ph["region"] == 48 * 200_000
+    ph = bench.phase_bytes(1024, 200_000, 400_000, 3000, "float64")  # float64 field and state
+    assert ph["integral_images"] == 20 * 1024 * 1024 and ph["region"] == 96 * 200_000
 
 
 def test_traffic_lookup_reads_committed_capture(bench):
