@@ -939,9 +939,10 @@ int det_bench_kernel_times(det_ctx* ctx, int iters, float* ms_out) {
     cudaEvent_t ev[5];
     for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&ev[i]));
     for (int i = 0; i < 4; ++i) ms_out[i] = 0.f;
-    // diagnostics: DET_KT_REGION_MODE=1 times k_region's advect phase alone (raster skipped)
+    // diagnostics: DET_KT_REGION_MODE=1 times k_region's advect phase alone (raster skipped),
+    // =2 its raster alone (the rows are not advected)
     const char* km = getenv("DET_KT_REGION_MODE");
-    const int region_mode = (km && km[0] == '1') ? M_ADVECT : (M_ADVECT | M_RASTER);
+    const int region_mode = (km && km[0] == '1') ? M_ADVECT : (km && km[0] == '2') ? M_RASTER : (M_ADVECT | M_RASTER);
     // DET_KT_ROW_MODE=-1 times k_row without the evaluation / LUT part of the control step
     const char* rm = getenv("DET_KT_ROW_MODE");
     const int row_mode = (rm && rm[0] == '-') ? -1 : 0;

@@ -29,7 +29,8 @@
 //   k_sat3  per band: load the carries, then one top-down sweep computing A,
 //           alpha, UL and the in-band up-right ray URin (DL = DLtot - URin), and
 //           the displacement u at every pixel centre (or the 8 channels).
-// All accumulation is float64; only the stored field may be float32.
+// In-band arithmetic follows the field mode: float64 for the float64 field (the default) and the
+// stage-level channel dumps, float32 for the float32/mixed fields; band carries are float64 always.
 #pragma once
 #include <type_traits>
 #include "det_common.cuh"
