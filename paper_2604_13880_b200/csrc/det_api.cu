@@ -66,7 +66,7 @@ struct det_ctx {
     int R = 0, n_rows = 0, n_rings = 0;
     std::vector<int> h_ring_start, h_region_ring0;
     DVec<double2> xy_rows;  // the loaded vertex rows, device resident (start geometry of every batch)
-    DVec<int> region_row0, region_rank, rank_region, ring_start, region_ring0;
+    DVec<int> region_row0, region_rank, rank_region, ring_start, region_ring0, row_next;
     // batch
     int B = 0, cap = 64, nb = 0, trace_cap = 0;
     // pos0 (the state rows, advected in place) and best hold float2 rows on the float32-field
@@ -124,6 +124,7 @@ static Topo make_topo(det_ctx* c) {
     t.region_ring0 = c->region_ring0.p;
     t.region_rank = c->region_rank.p;
     t.rank_region = c->rank_region.p;
+    t.row_next = c->row_next.p;
     return t;
 }
 
@@ -551,6 +552,13 @@ int det_host_free(void* p) {
     return cudaFreeHost(p) == cudaSuccess ? DET_OK : DET_E_CUDA;
 }
 
+// Synchronous copies on the context's own stream (never the legacy default stream, which a
+// cudaStreamNonBlocking context stream does not order against).
+static cudaError_t copy_sync(det_ctx* ctx, void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+    cudaError_t e = cudaMemcpyAsync(dst, src, bytes, kind, ctx->stream);
+    return e != cudaSuccess ? e : cudaStreamSynchronize(ctx->stream);
+}
+
 const char* det_last_error(const det_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
 
 int det_device_info(int device, char* buf, int buflen) {
@@ -660,11 +668,18 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
     CK(ctx->ring_start.alloc(n_rings + 1));
     CK(ctx->region_rank.alloc(n_regions));
     CK(ctx->rank_region.alloc(n_regions));
-    CK(cudaMemcpy(ctx->region_row0.p, reg_row0.data(), (n_regions + 1) * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->region_ring0.p, reg_ring0.data(), (n_regions + 1) * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->ring_start.p, ring_start, (n_rings + 1) * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->region_rank.p, region_rank, n_regions * sizeof(int), cudaMemcpyHostToDevice));
-    CK(cudaMemcpy(ctx->rank_region.p, rank_reg.data(), n_regions * sizeof(int), cudaMemcpyHostToDevice));
+    CK(copy_sync(ctx, ctx->region_row0.p, reg_row0.data(), (n_regions + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    CK(copy_sync(ctx, ctx->region_ring0.p, reg_ring0.data(), (n_regions + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    CK(copy_sync(ctx, ctx->ring_start.p, ring_start, (n_rings + 1) * sizeof(int), cudaMemcpyHostToDevice));
+    CK(copy_sync(ctx, ctx->region_rank.p, region_rank, n_regions * sizeof(int), cudaMemcpyHostToDevice));
+    CK(copy_sync(ctx, ctx->rank_region.p, rank_reg.data(), n_regions * sizeof(int), cudaMemcpyHostToDevice));
+    {  // ring successor of every row: O(1) for regions with many rings (holes, islands)
+        std::vector<int> nxt(n_rows);
+        for (int q = 0; q < n_rings; ++q)
+            for (int v = ring_start[q]; v < ring_start[q + 1]; ++v) nxt[v] = v + 1 < ring_start[q + 1] ? v + 1 : ring_start[q];
+        CK(ctx->row_next.alloc(n_rows));
+        CK(copy_sync(ctx, ctx->row_next.p, nxt.data(), (size_t)n_rows * sizeof(int), cudaMemcpyHostToDevice));
+    }
     ctx->B = 0;
     ctx->params_set = false;
     return DET_OK;
@@ -700,7 +715,7 @@ int det_rasterize(det_ctx* ctx, int b, int32_t* labels_out, int64_t* counts_out)
     int rc = raster_start(ctx);
     if (rc) return rc;
     Carto hs;
-    CK(cudaMemcpy(&hs, ctx->st.p + b, sizeof(Carto), cudaMemcpyDeviceToHost));
+    CK(copy_sync(ctx, &hs, ctx->st.p + b, sizeof(Carto), cudaMemcpyDeviceToHost));
     if (hs.err & E_NEGIDX) return fail(ctx, DET_E_VALUE, "'list' argument must have no negative elements");
     if (labels_out) {
         const int rc2 = labels_to_host(ctx, b, labels_out);
@@ -708,10 +723,10 @@ int det_rasterize(det_ctx* ctx, int b, int32_t* labels_out, int64_t* counts_out)
     }
     if (counts_out) {
         std::vector<int> c(ctx->R + 1);
-        CK(cudaMemcpy(c.data(), ctx->cnt_acc.p + (size_t)b * (ctx->R + 1), (ctx->R + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+        CK(copy_sync(ctx, c.data(), ctx->cnt_acc.p + (size_t)b * (ctx->R + 1), (ctx->R + 1) * sizeof(int), cudaMemcpyDeviceToHost));
         for (int r = 0; r <= ctx->R; ++r) counts_out[r] = c[r];
     }
-    CK(cudaMemset(ctx->cnt_acc.p, 0, (size_t)ctx->B * (ctx->R + 1) * sizeof(int)));
+    CK(cudaMemsetAsync(ctx->cnt_acc.p, 0, (size_t)ctx->B * (ctx->R + 1) * sizeof(int), ctx->stream));
     ctx->ran = false;
     return DET_OK;
 }
@@ -758,7 +773,7 @@ static int run_once(det_ctx* ctx, const det_criteria* crit, int* overflow) {
     {
         Carto hs;
         for (int b = 0; b < B; ++b) {
-            CK(cudaMemcpy(&hs, ctx->st.p + b, sizeof(Carto), cudaMemcpyDeviceToHost));
+            CK(copy_sync(ctx, &hs, ctx->st.p + b, sizeof(Carto), cudaMemcpyDeviceToHost));
             if (hs.err & E_NEGIDX) return fail(ctx, DET_E_VALUE, "'list' argument must have no negative elements");
         }
     }
@@ -858,8 +873,8 @@ int det_run_chain(det_ctx* ctx, int T, const double* stats, const double* S, con
         int rc = raster_start(ctx);  // frame start raster (engine.py:128, check_collapse=True)
         if (rc) return rc;
         Carto hs;
-        CK(cudaMemcpy(&hs, ctx->st.p, sizeof(Carto), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(c0.data(), ctx->cnt_acc.p, (R + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+        CK(copy_sync(ctx, &hs, ctx->st.p, sizeof(Carto), cudaMemcpyDeviceToHost));
+        CK(copy_sync(ctx, c0.data(), ctx->cnt_acc.p, (R + 1) * sizeof(int), cudaMemcpyDeviceToHost));
         for (int r = 0; r <= R; ++r) counts_out[(size_t)t * (R + 1) + r] = c0[r];
         if (hs.err & E_NEGIDX) {
             res.status = DET_E_VALUE;
@@ -1075,7 +1090,7 @@ int det_get_counts(det_ctx* ctx, int b, int64_t* out) {
     if (!ctx || !out || b < 0 || b >= ctx->B || !ctx->ran) return fail(ctx, DET_E_STATE, "no result");
     cudaSetDevice(ctx->device);
     std::vector<int> c(ctx->R + 1);
-    CK(cudaMemcpy(c.data(), ctx->cnt_state.p + (size_t)b * (ctx->R + 1), (ctx->R + 1) * sizeof(int), cudaMemcpyDeviceToHost));
+    CK(copy_sync(ctx, c.data(), ctx->cnt_state.p + (size_t)b * (ctx->R + 1), (ctx->R + 1) * sizeof(int), cudaMemcpyDeviceToHost));
     for (int r = 0; r <= ctx->R; ++r) out[r] = c[r];
     return DET_OK;
 }
@@ -1083,7 +1098,7 @@ int det_get_counts(det_ctx* ctx, int b, int64_t* out) {
 int det_get_region_error(det_ctx* ctx, int b, double* out) {
     if (!ctx || !out || b < 0 || b >= ctx->B || !ctx->ran) return fail(ctx, DET_E_STATE, "no result");
     cudaSetDevice(ctx->device);
-    CK(cudaMemcpy(out, ctx->rerr.p + (size_t)b * ctx->R, ctx->R * sizeof(double), cudaMemcpyDeviceToHost));
+    CK(copy_sync(ctx, out, ctx->rerr.p + (size_t)b * ctx->R, ctx->R * sizeof(double), cudaMemcpyDeviceToHost));
     return DET_OK;
 }
 
@@ -1092,7 +1107,7 @@ int det_get_trace(det_ctx* ctx, int b, double* out) {
     cudaSetDevice(ctx->device);
     const int len = ctx->h_st[b].trace_len;
     if (len > 0)
-        CK(cudaMemcpy(out, ctx->trace.p + (size_t)b * ctx->trace_cap * 4, (size_t)len * 4 * sizeof(double),
+        CK(copy_sync(ctx, out, ctx->trace.p + (size_t)b * ctx->trace_cap * 4, (size_t)len * 4 * sizeof(double),
                       cudaMemcpyDeviceToHost));
     return DET_OK;
 }
@@ -1178,7 +1193,7 @@ static int field_impl(det_ctx* ctx, const double* d, double* u_out, double* chan
     CK(cudaMemcpyAsync(&C, ctx->rowfull.p + ctx->n, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CK(cudaStreamSynchronize(ctx->stream));
     if (total_out) *total_out = C;
-    if (channels_out) CK(cudaMemcpy(channels_out, ctx->ch8.p, nn * 8 * sizeof(double), cudaMemcpyDeviceToHost));
+    if (channels_out) CK(copy_sync(ctx, channels_out, ctx->ch8.p, nn * 8 * sizeof(double), cudaMemcpyDeviceToHost));
     if (u_out) {
         if (!(C > 0)) return fail(ctx, DET_E_NUMERIC, "mapping undefined for zero total density");
         if (full_mapping) {  // t(d) itself (displacement.py:102-131)

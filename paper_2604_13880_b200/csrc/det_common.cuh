@@ -57,6 +57,7 @@ struct Topo {
     const int* region_ring0;  // R+1: first ring of each region (a region's rings are contiguous)
     const int* region_rank;   // R: rank of region in ascending region_id order
     const int* rank_region;   // R: inverse
+    const int* row_next;      // n_rows: next row of the same ring (wraps) -- multi-ring regions
 };
 
 struct Bufs {

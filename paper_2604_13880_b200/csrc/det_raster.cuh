@@ -237,6 +237,9 @@ __global__ void __launch_bounds__(RW_WARPS * 32, sizeof(ST) == 8 ? DET_RW_MINB64
     // next row of the same ring (wraps): from the region's ring boundaries, no per-row table
     auto next_row = [&](int v) -> int {
         if (rq1 - rq0 == 1) return v + 1 < row1 ? v + 1 : row0;
+        // a multi-ring region too large for shared memory (its edge scan repeats per toggle
+        // window): the static successor table, O(1) per edge; smaller ones walk their rings once
+        if (!in_smem) return __ldg(T.row_next + v);
         int q = rq0;
         while (T.ring_start[q + 1] <= v) ++q;
         const int e = T.ring_start[q + 1];
@@ -445,7 +448,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, sizeof(ST) == 8 ? DET_RW_MINB64
         for (int q = lane; q < RW_TCAP; q += 32) keys[q] = 0u;
         __syncwarp();
         for (int e = row0 + lane; e < row1; e += 32) {
-            const int en = next_row(e);
+            const int en = __ldg(T.row_next + e);
             double2 a = to_d2(gpos[e]), c = to_d2(gpos[en]);
             const int ja = min(max(ceil_to_int(__dsub_rn(__dmul_rn(a.y, nd), 0.5)), 0), n);
             const int jb2 = min(max(ceil_to_int(__dsub_rn(__dmul_rn(c.y, nd), 0.5)), 0), n);
@@ -939,14 +942,15 @@ __global__ void __launch_bounds__(256) k_row(Topo T, Bufs D, int gate, int ctrl_
 #if DET_ROW_TMA
         // the row leaves shared memory as one 1-D TMA bulk store issued by lane 0 (SENT == -1
         // bitwise); the generic-proxy paint is fenced for the async proxy first, and lane 0 waits
-        // for the store to complete before the warp's shared row can go away
+        // until the store has READ the shared row (wait_group.read) before the row can go away --
+        // the global write itself completes asynchronously, before the grid does
         if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(lab_g),
                          "r"((unsigned)__cvta_generic_to_shared(lab_s)), "r"((unsigned)n * 4u)
                          : "memory");
             asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
-            asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+            asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
         }
         __syncwarp();
 #else
