@@ -773,6 +773,9 @@ __global__ void __launch_bounds__(32 * SAT2_PARTS) k_sat2p(Bufs D, int gate) {
 #ifndef DET_SAT3_F2
 #define DET_SAT3_F2 1
 #endif
+#ifndef DET_SAT3_ABS
+#define DET_SAT3_ABS 1  // float64 field: anchor case splits as |e|, |d| terms (no compares/selects)
+#endif
 #ifndef DET_SAT3_MINB
 #define DET_SAT3_MINB 4  // 64 registers, no spills: 512 band CTAs fit one wave (3 and 5 measured slower)
 #endif
@@ -939,6 +942,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? (sizeof(A) == 8 ? DET_SAT3_MI
             const A yc = (A)j * inv_n + half_n;  // (j + 0.5) / n, exact in A
             // PF row constants: y - 1, (1 - 2y) / 4, ravg - C
             const A ycm1 = yc - (A)1, c1y = (A)0.25 - (A)0.5 * yc, rmc = ravg - Cr;
+            const A hravg = (A)0.5 * ravg, hC = (A)0.5 * Cr;  // float64 branch-free form
             const int wi0 = j + x0 - (jt - 1);
             A dlw[CPT + 1];  // DLtot(j + x - 1 + q), sliding window over this thread's columns
             A tuw[CPT];      // Tu(j + x - 1 + q)
@@ -1017,6 +1021,33 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? (sizeof(A) == 8 ? DET_SAT3_MI
                     vy = fmaf(yc, Cr - t, vy);
                     uy[k] = (vy + at) * inv2m;
 #endif
+                } else if constexpr (OUT == OUT_U && sizeof(A) == 8 && DET_SAT3_ABS) {
+                    // float64 field, branch-free: with e = x + y - 1 and d = x - y the case splits
+                    // of displacement.py:62,67 are q2x = q4y = 1 + (e - |e|)/2, q2y = q4x = (e + |e|)/2,
+                    // q3 = ((d + |d|)/2, (|d| - d)/2), so the combination below needs no compares or
+                    // selects: ux*2m = a(1-2y) + cavg + hs e + hd |e| - hK (d + |d|) + x t + bt,
+                    // uy*2m = a(1-2x) + ravg + hs e - hd |e| + hK (d - |d|) + at + y (C - t) with
+                    // hs = (cavg + ravg)/2, hd = (ravg - cavg)/2, hK = (cavg + ravg - C)/2
+                    const A a4 = apm1 + al[k] + anm1 + an[k];  // 4a
+                    const A cavg = cc[k];
+                    const A xc = xc0 + (A)k * inv_n;
+                    const A e = xc + ycm1, d = xc - yc;
+                    const A ae = fabs(e), ad = fabs(d);
+                    const A hs = fma((A)0.5, cavg, hravg), hd = fma((A)-0.5, cavg, hravg);
+                    const A hK = hs - hC;
+                    const A t = at + gt;
+                    A vx = fma(a4, c1y, cavg);
+                    vx = fma(hs, e, vx);
+                    vx = fma(hd, ae, vx);
+                    vx = fma(-hK, d + ad, vx);
+                    vx = fma(xc, t, vx);
+                    ux[k] = (vx + bt) * inv2m;
+                    A vy = fma(a4, fma(xc, (A)-0.5, (A)0.25), ravg);
+                    vy = fma(hs, e, vy);
+                    vy = fma(-hd, ae, vy);
+                    vy = fma(hK, d - ad, vy);
+                    vy = fma(yc, Cr - t, vy);
+                    uy[k] = (vy + at) * inv2m;
                 } else {
                     // anchor combination (displacement.py:128-130) with b = cavg-a, d = ravg-a,
                     // g = C-cavg-ravg+a, delta_t = C-at-bt-gt; since q1+q3 = (1+x-y, 1-x+y) and
