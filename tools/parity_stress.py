@@ -7,6 +7,11 @@ k = 4..9:
   * engine: 4 float64-field iterations vs the oracle engine (counts and trace bit-exact,
     vertices within 1e-9).
 Prints one JSON line with the case counts and the first mismatch (if any).
+
+PARITY_FIELD=float32 (or mixed) runs the engine / temporal sections in that field mode and holds
+them to the north-star bars instead of trajectory identity: vertices within 1e-4, per-region
+shoelace areas within 1e-3 relative (runs whose stop reason or collapse differs from the oracle's
+are counted, not failed -- a float32 trajectory may cross a threshold one iteration apart).
 """
 import json
 import os
@@ -19,6 +24,31 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402
 
 import fixture_maps as fm  # noqa: E402
+
+FIELD = os.environ.get("PARITY_FIELD", "float64")
+
+
+def _areas(rows, m):
+    from paper_2604_13880_b200.geomodel import ring_layout
+
+    _, rs, rr, ids, _ = ring_layout(m)
+    out = np.zeros(len(ids))
+    for q in range(len(rs) - 1):
+        p = rows[rs[q] : rs[q + 1]]
+        if p.shape[0] >= 3:
+            nx = np.roll(p, -1, axis=0)
+            out[rr[q]] += 0.5 * float(np.sum(p[:, 0] * nx[:, 1] - nx[:, 0] * p[:, 1]))
+    return out
+
+
+def _within_bars(rows, ref_rows, m, out):
+    """float32/mixed: the north-star bars on one final state; tracks the worst deviations."""
+    dv = float(np.abs(rows - ref_rows).max())
+    a, ar = _areas(rows, m), _areas(ref_rows, m)
+    da = float((np.abs(a - ar) / np.maximum(np.abs(ar), 1e-300)).max())
+    out["max_vertex_dev"] = max(out.get("max_vertex_dev", 0.0), dv)
+    out["max_area_rel"] = max(out.get("max_area_rel", 0.0), da)
+    return dv <= 1e-4 and da <= 1e-3
 import paper_2604_13880_b200 as P  # noqa: E402
 from oracle import det_oracle as O  # noqa: E402
 
@@ -83,7 +113,7 @@ def engine_stress(budget, seed0):
         crit = P.StoppingCriteria(thr, win, its)
         try:
             res = P.CartogramEngine(m, criteria=crit, k=k, bdv_multiplier=mult, bdv_mode=mode,
-                                    field_dtype="float64").run()
+                                    field_dtype=FIELD).run()
             got = ("ok", res.stop_reason, res.state.iteration, res.state.pixel_counts, res.state.mapmodel.vertex_array())
         except P.RegionCollapsedError as exc:
             got = ("collapse", exc.region_id, exc.iteration, None, None)
@@ -100,8 +130,15 @@ def engine_stress(budget, seed0):
         out["engine_runs"] += 1
         key = got[0] + ":" + str(got[1])
         out["stops"][key] = out["stops"].get(key, 0) + 1
-        same = got[:3] == want[:3] if got[0] != "ok" else (
-            got[:3] == want[:3] and np.array_equal(got[3], want[3]) and np.abs(got[4] - want[4]).max() <= 1e-9)
+        if FIELD != "float64":
+            if got[0] == "ok" and want[0] == "ok" and got[1:3] == want[1:3]:
+                same = _within_bars(got[4], want[4], m, out)
+            else:
+                out["divergent_stops"] = out.get("divergent_stops", 0) + (got[:3] != want[:3])
+                same = True
+        else:
+            same = got[:3] == want[:3] if got[0] != "ok" else (
+                got[:3] == want[:3] and np.array_equal(got[3], want[3]) and np.abs(got[4] - want[4]).max() <= 1e-9)
         if not same:
             out["engine_mismatch"] = {"case": i, "got": [str(x)[:80] for x in got[:3]],
                                       "want": [str(x)[:80] for x in want[:3]], "k": k, "mode": mode,
@@ -128,7 +165,7 @@ def temporal_stress(budget, seed0):
         crit = P.StoppingCriteria(1e-300, 10**9, 6)
         ds = P.TimeSeriesDataset(m, tuple(f"t{q}" for q in range(T)), walk)
         fn = P.run_cumulative if cumulative else P.run_direct
-        seq = fn(ds, crit, k=k, field_dtype="float64")
+        seq = fn(ds, crit, k=k, field_dtype=FIELD)
         ref = O.run_frames(O.FlatMap.from_mapmodel(m), walk, k, cumulative, error_threshold=1e-300,
                            stagnation_window=10**9, max_iterations=6)
         out["sequences"] += 1
@@ -146,8 +183,11 @@ def temporal_stress(budget, seed0):
                     break
                 out["temporal_mismatch"] = {"case": i, "t": t, "ours": fr.error[:120], "oracle": "ok"}
                 break
-            ok = (np.array_equal(fr.result.state.pixel_counts, rf.counts) and
-                  np.abs(fr.mapmodel.vertex_array() - rf.rows).max() <= 1e-9)
+            if FIELD != "float64":
+                ok = _within_bars(fr.mapmodel.vertex_array(), rf.rows, m, out)
+            else:
+                ok = (np.array_equal(fr.result.state.pixel_counts, rf.counts) and
+                      np.abs(fr.mapmodel.vertex_array() - rf.rows).max() <= 1e-9)
             if not ok:
                 out["temporal_mismatch"] = {"case": i, "t": t, "kind": "state", "cumulative": cumulative, "k": k}
                 break
@@ -201,7 +241,7 @@ def main():
     rng = np.random.default_rng(int(time.time()) % 100000)
     seed0 = int(rng.integers(1 << 30))
     t0 = time.perf_counter()
-    stats = {"seed0": seed0, "raster_cases": 0, "engine_cases": 0, "mismatch": None}
+    stats = {"seed0": seed0, "field": FIELD, "raster_cases": 0, "engine_cases": 0, "mismatch": None}
     i = 0
     while time.perf_counter() - t0 < budget and stats["mismatch"] is None:
         r = np.random.default_rng(seed0 + i)
@@ -231,14 +271,17 @@ def main():
         if jit == 0.0 and k >= 5:  # engine trajectories on clean partitions
             crit = P.StoppingCriteria(1e-300, 10**9, 4)
             try:
-                res = P.CartogramEngine(m, criteria=crit, k=k, field_dtype="float64").run()
+                res = P.CartogramEngine(m, criteria=crit, k=k, field_dtype=FIELD).run()
             except P.CartomorphError:
                 continue
             eng = O.OracleEngine(O.FlatMap.from_mapmodel(m), k=k)
             ores = eng.run(error_threshold=1e-300, stagnation_window=10**9, max_iterations=4)
             stats["engine_cases"] += 1
-            ok = (np.array_equal(res.state.pixel_counts, ores.counts) and
-                  np.abs(res.state.mapmodel.vertex_array() - ores.rows).max() <= 1e-9)
+            if FIELD != "float64":
+                ok = _within_bars(res.state.mapmodel.vertex_array(), ores.rows, m, stats)
+            else:
+                ok = (np.array_equal(res.state.pixel_counts, ores.counts) and
+                      np.abs(res.state.mapmodel.vertex_array() - ores.rows).max() <= 1e-9)
             if not ok:
                 stats["mismatch"] = {"case": i, "kind": "engine", "k": k, "regions": nreg}
     stats["seconds"] = time.perf_counter() - t0
