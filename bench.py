@@ -59,9 +59,13 @@ def phase_bytes(n: int, n_unique: int, n_rows: int, n_regions: int, field: str =
 
 
 def kernels_per_iteration(field: str) -> int:
-    """k_sat1w, k_sat2p, k_sat3, k_region, k_row, k_ctrl, plus k_advect_rows(64) on the float32 and
-    float64 paths when DET_SPLIT_ADVECT=1 (advect fused into k_region by default)."""
-    split = field != "mixed" and os.environ.get("DET_SPLIT_ADVECT", "0") == "1"
+    """k_sat1w, k_sat2p, k_sat3, k_region, k_row, k_ctrl, plus the advect as its own kernel:
+    k_advect_uniq64 on the float64 path (one thread per unique vertex; DET_UNIQ_ADVECT=0 fuses it
+    back into k_region), k_advect_rows on the float32 path when DET_SPLIT_ADVECT=1."""
+    if field == "float64":
+        split = os.environ.get("DET_UNIQ_ADVECT", "1") != "0" or os.environ.get("DET_SPLIT_ADVECT", "0") == "1"
+    else:
+        split = field == "float32" and os.environ.get("DET_SPLIT_ADVECT", "0") == "1"
     return 7 if split else 6
 
 

@@ -60,6 +60,7 @@ constexpr int kGraphIters = 16;
 struct det_ctx {
     int device = 0, k = 10, n = 1024, f64 = 0, s64 = 0, H = 8;  // f64: float64 field; s64: float64 vertex state
     bool bitmap_raster = false;  // k_region<..., true>: scanlines with more crossings than its toggle window
+    bool raster_ro = true;       // launches without advect use k_region<..., ADV=false> (DET_RASTER_RO=0: off)
     cudaStream_t stream = nullptr;
     std::string err;
     // topology
@@ -93,6 +94,14 @@ struct det_ctx {
     bool sep_ctrl = true;  // control step as its own kernel (DET_SEP_CTRL=0: k_row's last CTA)
     bool sat1w = true;  // float32 field: barrier-free k_sat1w (DET_SAT1W=0: k_sat1)
     bool split_adv = false;  // float32 state: advect as the flat k_advect_rows (DET_SPLIT_ADVECT=1); 48.6k vs 51.4k fused
+    // float64: advect once per unique vertex (k_advect_uniq64) + the raster-only k_region; valid while
+    // every frame's start rows keep the loaded map's shared vertices bit-identical (ua_ok)
+    bool uniq_adv = true;
+    bool ua_ok = false;
+    int n_uniq = 0;
+    DVec<int> uq_row0, uq_off, uq_rows;
+    std::vector<int> h_uq_off, h_uq_rows;
+    bool g_ua = false;
     Topo g_topo;  // launch signature the graph was captured with
     Bufs g_bufs;
     int g_groups = 0;
@@ -295,6 +304,12 @@ static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, in
         else k_region<float, float, true><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
         return;
     }
+    if (!(mode & M_ADVECT) && c->raster_ro) {  // no advect: the raster-only instantiation
+        if (c->f64) k_region<double, double, false, false><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
+        else if (c->s64 || f64_rows) k_region<float, double, false, false><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
+        else k_region<float, float, false, false><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
+        return;
+    }
     if (c->f64) k_region<double, double><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
     else if (c->s64 || f64_rows) k_region<float, double><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
     else k_region<float, float><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, mode, gate, src);
@@ -303,6 +318,12 @@ static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, in
 // One iteration's advect + raster: the flat advect kernel then a raster-only k_region (float32
 // state), or k_region's fused advect phase.  Returns the number of kernels launched.
 static int launch_advect_raster(det_ctx* c, const Topo& T, const Bufs& D, int gate, int region_mode) {
+    if (c->f64 && c->uniq_adv && c->ua_ok && (region_mode & M_ADVECT)) {
+        k_advect_uniq64<<<dim3((c->n_uniq + ADV_THREADS - 1) / ADV_THREADS, c->B), ADV_THREADS, 0, c->stream>>>(
+            T, D, gate, c->uq_row0.p, c->uq_off.p, c->uq_rows.p, c->n_uniq);
+        if (region_mode & M_RASTER) launch_region(c, T, D, M_RASTER | M_POSTADV, gate, 0);
+        return (region_mode & M_RASTER) ? 2 : 1;
+    }
     if ((!c->s64 || c->f64) && c->split_adv && (region_mode & M_ADVECT)) {
         const int per = ADV_THREADS * ADV_RPT;
         if (c->f64) k_advect_rows64<<<dim3((T.n_rows + per - 1) / per, c->B), ADV_THREADS, 0, c->stream>>>(T, D, gate);
@@ -368,12 +389,14 @@ static int ensure_graph(det_ctx* c) {
         // re-capture only when a pointer, shape or the grouping the graph bakes in changed
         const Topo t = make_topo(c);
         const Bufs d = make_bufs(c);
-        if (c->g_valid && c->g_groups == c->groups && !memcmp(&t, &c->g_topo, sizeof(t)) &&
+        if (c->g_valid && c->g_groups == c->groups && c->g_ua == (c->uniq_adv && c->ua_ok) &&
+            !memcmp(&t, &c->g_topo, sizeof(t)) &&
             !memcmp(&d, &c->g_bufs, sizeof(d)))
             return DET_OK;
         c->g_topo = t;
         c->g_bufs = d;
         c->g_groups = c->groups;
+        c->g_ua = c->uniq_adv && c->ua_ok;
     }
     invalidate_graph(c);
     const int G = std::max(1, std::min(c->groups, c->B));
@@ -580,6 +603,8 @@ int det_ctx_create(int device, int k, int precision, det_ctx** out) {
     det_ctx* ctx = new det_ctx();
     if (const char* e = getenv("DET_SEP_CTRL")) ctx->sep_ctrl = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SPLIT_ADVECT")) ctx->split_adv = atoi(e) != 0;  // A/B switch (diagnostics)
+    if (const char* e = getenv("DET_RASTER_RO")) ctx->raster_ro = atoi(e) != 0;    // A/B switch (diagnostics)
+    if (const char* e = getenv("DET_UNIQ_ADVECT")) ctx->uniq_adv = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SAT1W")) ctx->sat1w = atoi(e) != 0;  // A/B switch (diagnostics)
     ctx->device = device;
     ctx->k = k;
@@ -673,6 +698,41 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
     CK(copy_sync(ctx, ctx->ring_start.p, ring_start, (n_rings + 1) * sizeof(int), cudaMemcpyHostToDevice));
     CK(copy_sync(ctx, ctx->region_rank.p, region_rank, n_regions * sizeof(int), cudaMemcpyHostToDevice));
     CK(copy_sync(ctx, ctx->rank_region.p, rank_reg.data(), n_regions * sizeof(int), cudaMemcpyHostToDevice));
+    {  // unique vertices: rows with bit-identical coordinates, numbered by first occurrence
+        std::vector<int> idx(n_rows);
+        for (int v = 0; v < n_rows; ++v) idx[v] = v;
+        const uint64_t* bits = reinterpret_cast<const uint64_t*>(xy);
+        std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) {
+            return bits[2 * a] != bits[2 * b] ? bits[2 * a] < bits[2 * b] : bits[2 * a + 1] < bits[2 * b + 1];
+        });
+        std::vector<int> grp(n_rows);
+        int ng = 0;
+        for (int i = 0; i < n_rows; ++i) {
+            if (i > 0 && (bits[2 * idx[i]] != bits[2 * idx[i - 1]] || bits[2 * idx[i] + 1] != bits[2 * idx[i - 1] + 1])) ++ng;
+            grp[idx[i]] = ng;
+        }
+        ++ng;
+        // renumber groups by first occurrence (representative rows ascend: near-coalesced reads)
+        std::vector<int> ren(ng, -1), row0;
+        int U = 0;
+        for (int v = 0; v < n_rows; ++v)
+            if (ren[grp[v]] < 0) { ren[grp[v]] = U++; row0.push_back(v); }
+        std::vector<int> off(U + 1, 0), rows(n_rows);
+        for (int v = 0; v < n_rows; ++v) ++off[ren[grp[v]] + 1];
+        for (int u = 0; u < U; ++u) off[u + 1] += off[u];
+        std::vector<int> cur(off.begin(), off.end() - 1);
+        for (int v = 0; v < n_rows; ++v) rows[cur[ren[grp[v]]]++] = v;
+        ctx->n_uniq = U;
+        ctx->h_uq_off = off;
+        ctx->h_uq_rows = rows;
+        CK(ctx->uq_row0.alloc(U));
+        CK(ctx->uq_off.alloc(U + 1));
+        CK(ctx->uq_rows.alloc(n_rows));
+        CK(copy_sync(ctx, ctx->uq_row0.p, row0.data(), (size_t)U * sizeof(int), cudaMemcpyHostToDevice));
+        CK(copy_sync(ctx, ctx->uq_off.p, off.data(), (size_t)(U + 1) * sizeof(int), cudaMemcpyHostToDevice));
+        CK(copy_sync(ctx, ctx->uq_rows.p, rows.data(), (size_t)n_rows * sizeof(int), cudaMemcpyHostToDevice));
+        ctx->ua_ok = false;
+    }
     {  // ring successor of every row: O(1) for regions with many rings (holes, islands)
         std::vector<int> nxt(n_rows);
         for (int q = 0; q < n_rings; ++q)
@@ -694,6 +754,23 @@ int det_set_batch(det_ctx* ctx, int batch, const double* xy, const double* stats
         if (rc) return rc;
     }
     const size_t rowb = (size_t)ctx->n_rows * sizeof(double2);
+    // the unique-vertex advect needs every frame's start rows to keep the map's shared vertices
+    // bit-identical (the loaded rows do; caller-given rows are checked)
+    ctx->ua_ok = true;
+    if (xy) {
+        const uint64_t* bits = reinterpret_cast<const uint64_t*>(xy);
+        for (int b = 0; b < batch && ctx->ua_ok; ++b) {
+            const uint64_t* fb = bits + (size_t)b * ctx->n_rows * 2;
+            for (int u = 0; u < ctx->n_uniq && ctx->ua_ok; ++u) {
+                const int o0 = ctx->h_uq_off[u], o1 = ctx->h_uq_off[u + 1];
+                const int r0 = ctx->h_uq_rows[o0];
+                for (int i = o0 + 1; i < o1; ++i) {
+                    const int v = ctx->h_uq_rows[i];
+                    if (fb[2 * v] != fb[2 * r0] || fb[2 * v + 1] != fb[2 * r0 + 1]) { ctx->ua_ok = false; break; }
+                }
+            }
+        }
+    }
     if (xy) {
         CK(cudaMemcpyAsync(ctx->pos_init.p, xy, (size_t)batch * rowb, cudaMemcpyHostToDevice, ctx->stream));
     } else {  // one upload of the loaded rows, replicated on the device

@@ -198,14 +198,21 @@ __device__ __forceinline__ int warp_excl_scan_int(int v, int lane, int* total) {
 // UT: field element type (float / double); ST: vertex-state element type.  <float, float> is the
 // float32 path, <double, double> the float64 path, <float, double> the mixed path (float32 field,
 // float64 state and position update).
-template <typename UT, typename ST = UT, bool BM = false>
+template <typename UT, typename ST = UT, bool BM = false, bool ADV = true>
 #ifndef DET_RW_MINB
 #define DET_RW_MINB (32 / DET_RW_WARPS)  // 32 resident warps per SM (64 registers)
 #endif
 #ifndef DET_RW_MINB64
 #define DET_RW_MINB64 (24 / DET_RW_WARPS)  // float64 state: 24 warps per SM (80 registers)
 #endif
-__global__ void __launch_bounds__(RW_WARPS * 32, sizeof(ST) == 8 ? DET_RW_MINB64 : DET_RW_MINB) k_region(Topo T, Bufs D, int mode, int gate, int src) {
+#ifndef DET_RW_MINB_RO
+#define DET_RW_MINB_RO (32 / DET_RW_WARPS)  // raster-only instantiation: 64 registers, 32 warps per SM
+#endif
+// ADV = false: the raster-only instantiation (the advect phase compiled out, fewer registers, more
+// warps per SM) for launches without M_ADVECT: start / final rasters and the split advect path.
+__global__ void __launch_bounds__(RW_WARPS * 32, ADV ? (sizeof(ST) == 8 ? DET_RW_MINB64 : DET_RW_MINB) : DET_RW_MINB_RO)
+    k_region(Topo T, Bufs D, int mode_in, int gate, int src) {
+    const int mode = ADV ? mode_in : (mode_in & ~(int)M_ADVECT);
     // per row: ceil(y*n - 0.5) clipped to [0, n] (low 16 bits) | next row of the same ring,
     // region-local (high 16 bits) -- one load per edge end
     __shared__ uint32_t s_jn[RW_WARPS][RW_ROWCAP];
@@ -778,6 +785,46 @@ __global__ void __launch_bounds__(ADV_THREADS) k_advect_rows64(Topo T, Bufs D, i
         ncl += (cx != mx) + (cy != my);
         pin[v] = make_double2(cx, cy);
         if (bestcopy) pbest[v] = p[q];
+    }
+    ncl = warp_sum(ncl);
+    if ((threadIdx.x & 31) == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
+}
+
+// Advect once per UNIQUE vertex (float64 field and state): rows duplicating a shared vertex start
+// bit-identical and evolve bit-identically (the update is a function of the position alone), so
+// one thread advects the vertex from its first row and writes the result to every row of the
+// vertex (CSR uq_off / uq_rows) -- half the taps and texel gathers of the per-row advect.  The
+// clamp count is per row, as the reference counts it over the full vertex array
+// (displacement.py:229-238): a vertex's clamped coordinates count once per row.
+__global__ void __launch_bounds__(ADV_THREADS) k_advect_uniq64(Topo T, Bufs D, int gate, const int* __restrict__ uq_row0,
+                                                             const int* __restrict__ uq_off,
+                                                             const int* __restrict__ uq_rows, int n_uniq) {
+    const int b = blockIdx.y + D.b0;
+    Carto* st = D.st + b;
+    if (!gate_open(st, gate)) return;
+    const int n = D.n;
+    const size_t ub = (size_t)b * T.n_rows;
+    double2* const pin = reinterpret_cast<double2*>(D.pos0) + ub;  // advected in place (see k_region)
+    double2* __restrict__ pbest = reinterpret_cast<double2*>(D.best) + ub;
+    const bool bestcopy = st->best_pending != 0;
+    const double* uf = reinterpret_cast<const double*>(D.uf) + (size_t)b * D.nn * 2;
+    const int u = blockIdx.x * ADV_THREADS + threadIdx.x;
+    int ncl = 0;
+    if (u < n_uniq) {
+        const int o0 = uq_off[u], o1 = uq_off[u + 1];
+        const double2 p = pin[uq_row0[u]];
+        const Tap tp = field_tap(n, p.x, p.y);
+        const double2 sm = field_blend<double, Tap>(field_load<double, Tap>(uf, tp), tp);
+        const double mx = p.x + sm.x, my = p.y + sm.y;
+        const double cx = mx < 0.0 ? 0.0 : (mx > 1.0 ? 1.0 : mx);  // np.clip (no NaNs here)
+        const double cy = my < 0.0 ? 0.0 : (my > 1.0 ? 1.0 : my);
+        ncl = ((cx != mx) + (cy != my)) * (o1 - o0);
+        const double2 c = make_double2(cx, cy);
+        for (int i = o0; i < o1; ++i) {
+            const int v = uq_rows[i];
+            pin[v] = c;
+            if (bestcopy) pbest[v] = p;
+        }
     }
     ncl = warp_sum(ncl);
     if ((threadIdx.x & 31) == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
