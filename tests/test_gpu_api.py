@@ -182,3 +182,52 @@ def test_bitmap_raster_engine_deterministic(P):
     r2 = P.CartogramEngine(m, criteria=crit, k=10).run()
     assert np.array_equal(r1.state.mapmodel.vertex_array(), r2.state.mapmodel.vertex_array())
     assert np.array_equal(r1.state.pixel_counts, r2.state.pixel_counts)
+
+
+# ---------------------------------------------------------------- float64 advect variants
+_ADV_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2604_13880_b200 as P
+from paper_2604_13880_b200.synthetic import voronoi_map
+m = voronoi_map(200, seed=7, target_unique=20000, sigma=0.8)
+res = P.run(m, P.StoppingCriteria(1e-300, 10**9, 25), k=10)
+np.save({out!r}, np.concatenate([res.state.mapmodel.vertex_array().ravel(),
+                                 res.state.pixel_counts.astype(np.float64), [res.state.clamp_events]]))
+"""
+
+
+def test_unique_vertex_advect_equals_per_row(tmp_path):
+    # k_advect_uniq64 + raster-only k_region (default) vs the fused per-row advect (DET_UNIQ_ADVECT=0):
+    # the same float64 arithmetic per vertex, so the trajectories are bit-identical
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for i, e in enumerate([{}, {"DET_UNIQ_ADVECT": "0"}]):
+        out = str(tmp_path / f"a{i}.npy")
+        r = subprocess.run([sys.executable, "-c", _ADV_SCRIPT.format(root=root, out=out)],
+                           env=dict(os.environ, **e), capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_start_rows_breaking_shared_vertices(P):
+    # caller-given start rows where one copy of a shared vertex differs from the other: the batch
+    # falls back to the per-row advect, and the run still equals the oracle's
+    from oracle import det_oracle as O
+
+    m = fm.small_voronoi(seed=11, r=16, target=500, shuffle_ids=False)
+    xy = m.vertex_array().copy()
+    rounded = np.round(xy, 12)
+    _, first, counts = np.unique(rounded.view(np.complex128).ravel(), return_index=True, return_counts=True)
+    dup = first[np.argmax(counts >= 2)]  # a row whose vertex is shared
+    xy[dup] += 1e-4
+    crit = P.StoppingCriteria(1e-300, 10**9, 5)
+    be = P.BatchEngine(m, m.statistics()[None], criteria=crit, k=7, start_vertices=xy[None], apply_densify=False)
+    res = be.run_all()[0]
+    ref = O.OracleEngine(O.FlatMap.from_mapmodel(m.with_vertex_array(xy)), k=7, apply_densify=False).run(1e-300, 10**9, 5)
+    assert np.array_equal(res.state.pixel_counts, ref.counts)
+    np.testing.assert_allclose(res.state.mapmodel.vertex_array(), ref.rows, rtol=0, atol=1e-9)
