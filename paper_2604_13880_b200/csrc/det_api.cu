@@ -102,6 +102,9 @@ struct det_ctx {
     DVec<int> uq_row0, uq_off, uq_rows;
     std::vector<int> h_uq_off, h_uq_rows;
     bool g_ua = false;
+    int g_nuniq = 0;
+    const void* g_uq = nullptr;  // the unique-vertex arrays and count are kernel arguments the graph bakes in
+    const void* g_uq0 = nullptr;
     Topo g_topo;  // launch signature the graph was captured with
     Bufs g_bufs;
     int g_groups = 0;
@@ -390,6 +393,7 @@ static int ensure_graph(det_ctx* c) {
         const Topo t = make_topo(c);
         const Bufs d = make_bufs(c);
         if (c->g_valid && c->g_groups == c->groups && c->g_ua == (c->uniq_adv && c->ua_ok) &&
+            c->g_nuniq == c->n_uniq && c->g_uq == c->uq_rows.p && c->g_uq0 == c->uq_row0.p &&
             !memcmp(&t, &c->g_topo, sizeof(t)) &&
             !memcmp(&d, &c->g_bufs, sizeof(d)))
             return DET_OK;
@@ -397,6 +401,9 @@ static int ensure_graph(det_ctx* c) {
         c->g_bufs = d;
         c->g_groups = c->groups;
         c->g_ua = c->uniq_adv && c->ua_ok;
+        c->g_nuniq = c->n_uniq;
+        c->g_uq = c->uq_rows.p;
+        c->g_uq0 = c->uq_row0.p;
     }
     invalidate_graph(c);
     const int G = std::max(1, std::min(c->groups, c->B));
