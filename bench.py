@@ -4,7 +4,7 @@ Workload ("headline"): the 3000-region seeded Voronoi map with ~200k unique
 vertices (synthetic), 1024^2 texture, run as direct-mode time
 steps: every GPU holds a batch of B independent frames (statistics = a seeded
 lognormal random walk over time) and one bench "step" is one DET iteration of
-every frame in the batch (B = 32 by default).  Inputs are device-resident before
+every frame in the batch (B = 64 by default: four 16-step random walks).  Inputs are device-resident before
 timing; the batch working set (~45 MB per frame with the float64 field) is larger than
 the 126 MB L2 for B >= 3.
 
@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 METRIC = "DET iterations/s at 1024\u00b2 texture, 200k vertices; time steps/s over 8 GPUs"  # BASELINE.json verbatim
 UNIT = "DET iterations/s"
 K_TEX = 10
+WALK_STEPS = 16  # time steps per random walk of the bench batch (see build_workload)
 
 
 def algorithmic_bytes_per_iteration(n: int, n_unique: int) -> float:
@@ -137,11 +138,15 @@ def build_workload(batch: int, rank: int, world: int):
     from paper_2604_13880_b200.synthetic import config_map, random_walk
 
     m, prm = config_map("headline")
-    # weak scaling: every rank runs its own `batch`-frame walk from the base statistics (rank 0's
-    # is the N=1 workload), so per-GPU work has the same distribution at every N -- one long walk
-    # sliced across ranks would drift far enough on high ranks for frames to collapse
-    walk = random_walk(m.statistics(), batch, 0.15, seed=7 + 1009 * rank)
-    return m, prm, walk
+    # weak scaling: every rank runs its own frames from the base statistics (rank 0's are the N=1
+    # workload), so per-GPU work has the same distribution at every N.  The frames are time steps of
+    # random walks of at most WALK_STEPS steps (a new walk from the base statistics every WALK_STEPS
+    # frames): a longer walk drifts far enough (sigma 0.15 per step) for this 3000-region map's
+    # smallest regions to collapse within the run (RegionCollapsedError, as in the reference), which
+    # would leave frames of the batch idle
+    walks = [random_walk(m.statistics(), min(WALK_STEPS, batch - lo), 0.15, seed=7 + 1009 * rank + 31 * (lo // WALK_STEPS))
+             for lo in range(0, batch, WALK_STEPS)]
+    return m, prm, np.concatenate(walks)
 
 
 # ------------------------------------------------------------------ CPU reference arm / baseline
@@ -239,7 +244,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=64)
     ap.add_argument("--warmup", type=int, default=8)
-    ap.add_argument("--batch", type=int, default=32, help="frames per GPU (32: best of 16-128, DESIGN.md §5)")
+    ap.add_argument("--batch", type=int, default=64, help="frames per GPU (DESIGN.md §5: 16-128 swept)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--band", type=int, default=0, help="band height of the integral-image kernels (0 = auto)")
     ap.add_argument("--field", default="float64", choices=["float64", "mixed", "float32"])
