@@ -239,6 +239,43 @@ def traffic_for(phase, batch):
         return None
 
 
+def paper_units(P, m, walk, field, device):
+    """One headline cartogram alone (B = 1, 200 iterations through CartogramEngine.run) and the
+    config-2 cumulative chain (run_cumulative, 12 steps x 100 iterations), wall-clock around the
+    public calls after a warm-up call (results read back included)."""
+    import gc
+
+    from paper_2604_13880_b200.synthetic import config_map, random_walk
+
+    out = {}
+    crit = P.StoppingCriteria(error_threshold=1e-300, stagnation_window=10**9, max_iterations=200)
+    eng = P.CartogramEngine(m.with_statistics(walk[0]), criteria=crit, k=K_TEX, device=device, field_dtype=field)
+    eng.run()
+    gc.collect()
+    t0 = time.perf_counter()
+    res = eng.run()
+    dt = time.perf_counter() - t0
+    out["single_cartogram"] = {"iterations": res.state.iteration, "seconds": dt,
+                               "it_per_s": res.state.iteration / dt, "ms_per_iteration": 1e3 * dt / res.state.iteration,
+                               "note": "one headline frame (3000 regions, 1024^2) through CartogramEngine.run, "
+                                       "host map in and results out"}
+    m2, prm2 = config_map("c2")
+    w2 = random_walk(m2.statistics(), prm2["steps"], prm2["walk_sigma"], seed=21)
+    ds = P.TimeSeriesDataset(m2, tuple(f"t{i}" for i in range(prm2["steps"])), w2)
+    crit2 = P.StoppingCriteria(error_threshold=1e-300, stagnation_window=10**9, max_iterations=prm2["iterations"])
+    P.run_cumulative(ds, crit2, k=prm2["k"], device=device, field_dtype=field)
+    gc.collect()
+    t0 = time.perf_counter()
+    seq = P.run_cumulative(ds, crit2, k=prm2["k"], device=device, field_dtype=field)
+    dt = time.perf_counter() - t0
+    ok = sum(fr.error is None for fr in seq.frames)
+    out["cumulative_chain_c2"] = {"time_steps": len(seq.frames), "ok_steps": ok, "iterations_per_step": prm2["iterations"],
+                                  "seconds": dt, "time_steps_per_s": len(seq.frames) / dt,
+                                  "note": "BASELINE config 2: 500 regions, ~40k vertices, 1024^2, 12 warm-started "
+                                          "steps x 100 iterations, per-frame quality reports included"}
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -251,6 +288,7 @@ def main():
     ap.add_argument("--groups", type=int, default=8, help="frame groups run as parallel graph branches")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--e2e-steps", type=int, default=0)
+    ap.add_argument("--no-extra", action="store_true", help="skip the single-cartogram / chain measurements")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -375,6 +413,13 @@ def main():
     # fetched lazily (only when a caller reads RunResult.state.labels), so it is not counted
     d2h = (n_rows * 16 + (len(m.regions) + 1) * 4 + len(m.regions) * 8 + (e2e_steps + 1) * 32 + 64) * args.batch
 
+    # ---- the paper's own units (rank 0, after the timed regions): one cartogram's latency per
+    # iteration (PAPER.md:318-327 quotes ms per iteration at 1024^2) and a cumulative chain
+    # (config 2: 12 warm-started time steps x 100 iterations) in time steps per second ----
+    extra = {}
+    if rank == 0 and not args.no_extra:
+        extra = paper_units(P, m, walk, args.field, local)
+
     # ---- final gather of per-frame results (the only collective) ----
     xi = torch.tensor([r.state.xi if not isinstance(r, Exception) else -1.0 for r in res], device="cuda",
                       dtype=torch.float64)
@@ -424,6 +469,7 @@ def main():
             "clocks": clk.summary(),
             "device": device_info(local),
             "final_gather": {"frames": int(xi.numel()), "xi_mean": float(xi.mean().item())},
+            **extra,
         }
         print(json.dumps(line))
     if dist is not None:
