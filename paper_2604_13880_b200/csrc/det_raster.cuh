@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, ADV ? (sizeof(ST) == 8 ? DET_RW
     __shared__ int s_tot[RW_WARPS];
     __shared__ uint32_t s_key[RW_WARPS][RW_TCAP];
     __shared__ uint16_t s_col[RW_WARPS][RW_TCAP];
-    __shared__ int s_rc[RW_WARPS][RW_WROWS + 1];
+    __shared__ __align__(16) int s_rc[RW_WARPS][RW_WROWS + 4];  // 16-byte rows: zeroed as int4
     __shared__ uint32_t s_q[RW_WARPS][64];  // compacted crossing edges (ring buffer)
 
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -442,7 +442,16 @@ __global__ void __launch_bounds__(RW_WARPS * 32, ADV ? (sizeof(ST) == 8 ? DET_RW
     }
     const long long width = (long long)cols + 1;  // absorber column (raster.py:79-80)
     const unsigned long long rank = (unsigned long long)T.region_rank[r];
-    const int back = i_off / (cols + 1) + 1;  // max rows a negative column moves a toggle up
+    // max rows a negative column moves a toggle up: i_off / (cols + 1) + 1, the quotient from a
+    // float reciprocal (exact to +-1 for these magnitudes) corrected with one integer product
+    int back;
+    {
+        const int w1 = cols + 1;
+        int q = (int)((float)i_off * __frcp_rn((float)w1));
+        q -= q * w1 > i_off;
+        q += (q + 1) * w1 <= i_off;
+        back = q + 1;
+    }
     int area = 0;
 
     // BM: one scanline j of this region rasterised through a parity bitmap of its crop columns
@@ -534,7 +543,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, ADV ? (sizeof(ST) == 8 ? DET_RW
     while (w0 < j_end) {
         const int w1 = min(w0 + wh, j_end);
         const int W = w1 - w0;
-        for (int q = lane; q <= W; q += 32) rc[q] = 0;
+        for (int q = lane; q <= (W >> 2); q += 32) reinterpret_cast<int4*>(rc)[q] = make_int4(0, 0, 0, 0);
         __syncwarp();
         // ---- crossings of every ring edge (raster.py:30-61, flattening :86-89) ----
         if (lane == 0) s_tot[wid] = 0;
