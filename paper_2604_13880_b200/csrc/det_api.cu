@@ -323,7 +323,8 @@ static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, in
 // state), or k_region's fused advect phase.  Returns the number of kernels launched.
 static int launch_advect_raster(det_ctx* c, const Topo& T, const Bufs& D, int gate, int region_mode) {
     if (c->f64 && c->uniq_adv && c->ua_ok && (region_mode & M_ADVECT)) {
-        k_advect_uniq64<<<dim3((c->n_uniq + ADV_THREADS - 1) / ADV_THREADS, c->B), ADV_THREADS, 0, c->stream>>>(
+        k_advect_uniq64<<<dim3((c->n_uniq + ADV_THREADS * UQ_PT - 1) / (ADV_THREADS * UQ_PT), c->B), ADV_THREADS, 0,
+                          c->stream>>>(
             T, D, gate, c->uq_row0.p, c->uq_off.p, c->uq_rows.p, c->n_uniq);
         if (region_mode & M_RASTER) launch_region(c, T, D, M_RASTER | M_POSTADV, gate, 0);
         return (region_mode & M_RASTER) ? 2 : 1;

@@ -805,6 +805,10 @@ __global__ void __launch_bounds__(ADV_THREADS) k_advect_rows64(Topo T, Bufs D, i
 // vertex (CSR uq_off / uq_rows) -- half the taps and texel gathers of the per-row advect.  The
 // clamp count is per row, as the reference counts it over the full vertex array
 // (displacement.py:229-238): a vertex's clamped coordinates count once per row.
+#ifndef DET_UQ_PER_THREAD
+#define DET_UQ_PER_THREAD 1  // unique vertices per thread (1: 46.4k, 2: 46.0k, 4: 44.6k it/s)
+#endif
+constexpr int UQ_PT = DET_UQ_PER_THREAD;
 __global__ void __launch_bounds__(ADV_THREADS) k_advect_uniq64(Topo T, Bufs D, int gate, const int* __restrict__ uq_row0,
                                                              const int* __restrict__ uq_off,
                                                              const int* __restrict__ uq_rows, int n_uniq) {
@@ -817,26 +821,43 @@ __global__ void __launch_bounds__(ADV_THREADS) k_advect_uniq64(Topo T, Bufs D, i
     double2* __restrict__ pbest = reinterpret_cast<double2*>(D.best) + ub;
     const bool bestcopy = st->best_pending != 0;
     const double* uf = reinterpret_cast<const double*>(D.uf) + (size_t)b * D.nn * 2;
-    const int u = blockIdx.x * ADV_THREADS + threadIdx.x;
+    const int u0 = blockIdx.x * (ADV_THREADS * UQ_PT) + threadIdx.x;
+    int o[UQ_PT + 1 > 2 ? UQ_PT + 1 : 2][2];
+    double2 p[UQ_PT];
+    Tap tp[UQ_PT];
+    Texels<double> tx[UQ_PT];
+#pragma unroll
+    for (int q = 0; q < UQ_PT; ++q) {
+        const int u = u0 + q * ADV_THREADS;
+        o[q][0] = u < n_uniq ? uq_off[u] : 0;
+        o[q][1] = u < n_uniq ? uq_off[u + 1] : 0;
+        p[q] = u < n_uniq ? pin[uq_row0[u]] : make_double2(0.5, 0.5);
+    }
+#pragma unroll
+    for (int q = 0; q < UQ_PT; ++q) {
+        tp[q] = field_tap(n, p[q].x, p[q].y);
+        tx[q] = field_load<double, Tap>(uf, tp[q]);
+    }
     int ncl = 0;
-    if (u < n_uniq) {
-        const int o0 = uq_off[u], o1 = uq_off[u + 1];
-        const double2 p = pin[uq_row0[u]];
-        const Tap tp = field_tap(n, p.x, p.y);
-        const double2 sm = field_blend<double, Tap>(field_load<double, Tap>(uf, tp), tp);
-        const double mx = p.x + sm.x, my = p.y + sm.y;
+#pragma unroll
+    for (int q = 0; q < UQ_PT; ++q) {
+        const double2 sm = field_blend<double, Tap>(tx[q], tp[q]);
+        const double mx = p[q].x + sm.x, my = p[q].y + sm.y;
         const double cx = mx < 0.0 ? 0.0 : (mx > 1.0 ? 1.0 : mx);  // np.clip (no NaNs here)
         const double cy = my < 0.0 ? 0.0 : (my > 1.0 ? 1.0 : my);
-        ncl = ((cx != mx) + (cy != my)) * (o1 - o0);
+        const int o0 = o[q][0], o1 = o[q][1];
+        ncl += ((cx != mx) + (cy != my)) * (o1 - o0);
         const double2 c = make_double2(cx, cy);
         for (int i = o0; i < o1; ++i) {
             const int v = uq_rows[i];
             pin[v] = c;
-            if (bestcopy) pbest[v] = p;
+            if (bestcopy) pbest[v] = p[q];
         }
     }
-    ncl = warp_sum(ncl);
-    if ((threadIdx.x & 31) == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
+    if (__any_sync(FULL, ncl != 0)) {  // clamping is rare (the map's border)
+        ncl = warp_sum(ncl);
+        if ((threadIdx.x & 31) == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
+    }
 }
 
 #ifndef DET_ROW_RED
