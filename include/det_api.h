@@ -81,6 +81,10 @@ int det_abi_version(void);
 int det_host_alloc(size_t bytes, void **out);
 int det_host_free(void *p);
 const char *det_last_error(const det_ctx *ctx);
+/* Debug mode (environment DET_GUARD=1 at library load; no reference counterpart): device buffers
+ * carry 4 KB guard zones and are poisoned when allocated.  Reports the live guarded buffers and
+ * how many guard zones (live or already released) were overwritten; DET_E_STATE when the mode is off. */
+int det_debug_guard_check(long long *n_live, long long *n_bad);
 /* device info string (name, SMs, L2) for reports */
 int det_device_info(int device, char *buf, int buflen);
 

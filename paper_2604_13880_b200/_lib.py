@@ -48,6 +48,7 @@ class DetResult(ctypes.Structure):
 
 EXPORTS = {
     "det_abi_version": (ctypes.c_int, []),
+    "det_debug_guard_check": (ctypes.c_int, [ctypes.POINTER(ctypes.c_longlong), ctypes.POINTER(ctypes.c_longlong)]),
     "det_host_alloc": (ctypes.c_int, [ctypes.c_size_t, ctypes.POINTER(ctypes.c_void_p)]),
     "det_host_free": (ctypes.c_int, [ctypes.c_void_p]),
     "det_last_error": (ctypes.c_char_p, [ctypes.c_void_p]),

@@ -38,3 +38,20 @@ def pytest_collection_modifyitems(config, items):
 @pytest.fixture(scope="session")
 def golden_dir():
     return GOLDEN
+
+
+@pytest.fixture(autouse=True)
+def _device_guard_zones(request):
+    """Under DET_GUARD=1 (the library's guard-zone debug mode) every GPU test ends with a check that
+    no device buffer's guard zone was overwritten (compute-sanitizer is not available on the pool)."""
+    yield
+    if os.environ.get("DET_GUARD", "0") == "0" or "gpu" not in request.keywords:
+        return
+    import ctypes
+
+    from paper_2604_13880_b200 import _lib
+
+    live, bad = ctypes.c_longlong(0), ctypes.c_longlong(0)
+    rc = _lib.load_library().det_debug_guard_check(ctypes.byref(live), ctypes.byref(bad))
+    assert rc == 0, "DET_GUARD set but the library's guard mode is off"
+    assert bad.value == 0, f"{bad.value} device guard zone(s) overwritten ({live.value} live buffers)"
