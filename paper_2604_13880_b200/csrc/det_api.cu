@@ -149,7 +149,7 @@ struct det_ctx {
     DVec<int> labels, cnt_acc, cnt_state, rowcnt, maxspan, rowdone;
     DVec<unsigned long long> spans;
     DVec<float> lutf;
-    DVec<double> lut, stats, weights, rerr, cs, dgc, adc, rt, csX, dgXc, adSc, csT, dgT, adT, rowfull, trace;
+    DVec<double> lut, stats, weights, rerr, cs, dgc, adc, rt, csX, dgXc, adSc, csT, dgT, adT, rowfull, tab, trace;
     DVec<char> uf;
     DVec<Carto> st;
     DVec<Params> prm;
@@ -165,6 +165,7 @@ struct det_ctx {
     int groups = 8;  // graph branches (clamped to the batch); 1/2/4/8 measured 41.5/42.4/43.9/44.2k it/s
     bool sep_ctrl = true;  // control step as its own kernel (DET_SEP_CTRL=0: k_row's last CTA)
     bool sat1w = true;  // float32 field: barrier-free k_sat1w (DET_SAT1W=0: k_sat1)
+    bool sat3w = true;  // float64 field: barrier-free k_sat3w with k_sat1w's slice tables (DET_SAT3W=0: k_sat3)
     bool split_adv = false;  // float32 state: advect as the flat k_advect_rows (DET_SPLIT_ADVECT=1); 48.6k vs 51.4k fused
     // float64: advect once per unique vertex (k_advect_uniq64) + the raster-only k_region; valid while
     // every frame's start rows keep the loaded map's shared vertices bit-identical (ua_ok)
@@ -225,7 +226,7 @@ static Bufs make_bufs(det_ctx* c) {
     d.uf = c->uf.p;
     d.cs = c->cs.p; d.dgc = c->dgc.p; d.adc = c->adc.p; d.rt = c->rt.p;
     d.csX = c->csX.p; d.dgXc = c->dgXc.p; d.adSc = c->adSc.p;
-    d.csT = c->csT.p; d.dgT = c->dgT.p; d.adT = c->adT.p; d.rowfull = c->rowfull.p;
+    d.csT = c->csT.p; d.dgT = c->dgT.p; d.adT = c->adT.p; d.rowfull = c->rowfull.p; d.tab = c->tab.p;
     d.st = c->st.p; d.prm = c->prm.p; d.trace = c->trace.p; d.trace_cap = c->trace_cap;
     return d;
 }
@@ -287,8 +288,21 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
     constexpr int NT1 = NT * CPT / CPT1;
     const bool skip12 = src == SRC_LABELS && out == OUT_U && (skip_mask() & 1);
     const bool skip3 = src == SRC_LABELS && out == OUT_U && (skip_mask() & 2);
+    const bool sat1w_ok = src == SRC_LABELS && out == OUT_U && c->sat1w && n % (32 * CPT1) == 0 && (f32 || n <= 4096);
+    // float64 field: the barrier-free k_sat3w (128-column warp slices, band height below the slice
+    // width) fed by k_sat1w's slice tables
+    const bool w3 = sat1w_ok && !f32 && c->sat3w && CPT1 == 4 && n >= 512 && H < 32 * CPT1;
     if (skip12) {
-    } else if (src == SRC_LABELS && out == OUT_U && c->sat1w && n % (32 * CPT1) == 0 && (f32 || n <= 4096)) {
+    } else if (w3) {
+        constexpr int NW = NT1 / 32, KP = lab_kp1(CPT1 * NT1);
+        size_t smem1w = ((size_t)2 * (n + H - 1) + (size_t)4 * H * NW) * sa + 16 +
+                        (size_t)NW * KP * 32 * CPT1 * sizeof(int);
+        const bool l1 = DET_SAT1W_LUTS && (size_t)lut_smem_len(R) * sa <= 48 * 1024;
+        if (l1) smem1w += (size_t)lut_smem_len(R) * sa;
+        auto fn = l1 ? k_sat1w<CPT1, NT1, true, double, true> : k_sat1w<CPT1, NT1, false, double, true>;
+        smem_optin(fn);
+        fn<<<gb, NT1, smem1w, c->stream>>>(T, D, gate);
+    } else if (sat1w_ok) {
         // barrier-free band sums in the field's arithmetic type (float32 or float64)
         constexpr int NW = NT1 / 32, KP = lab_kp1(CPT1 * NT1);
         size_t smem1w = ((size_t)2 * (n + H - 1) + (size_t)3 * H * NW) * sa + 16 +
@@ -326,6 +340,18 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
         fn<<<gb, NT, smem, c->stream>>>(T, D, S, gate);                                                      \
     } while (0)
     if (skip3) {
+    } else if (w3) {
+        // CTAs of up to 8 warp slices (1024 columns) per band
+        constexpr int NTW = NT * CPT >= 1024 ? 256 : NT;
+        constexpr int NWC = NTW / 32, W = 32 * CPT;
+        constexpr int KPW = lab_kp(W * NWC) > 4 ? 4 : lab_kp(W * NWC);
+        const int WN = NWC * W + H, PW = (WN + 3) / 4 + 1;  // phase-split windows (k_sat3w)
+        const size_t smemw = ((size_t)3 * 4 * PW + 3 * H + (H & 1) + (size_t)4 * (NWC + 2) * H +
+                              (size_t)NWC * (H + 1) + ((NWC * (H + 1)) & 1)) * sizeof(double) +
+                             lut_b + (size_t)NWC * KPW * W * sizeof(int) + 16;
+        auto fn = luts ? k_sat3w<CPT, NTW, true> : k_sat3w<CPT, NTW, false>;
+        smem_optin(fn);
+        fn<<<dim3(c->nb, B, n / (NWC * W)), NTW, smemw, c->stream>>>(T, D, gate);
     } else if (out == OUT_CH8) {
         if (src == SRC_LABELS) {
             if (luts) DET_SAT3(SRC_LABELS, double, OUT_CH8, true);
@@ -531,6 +557,7 @@ static int alloc_sat(det_ctx* ctx, int B) {
     CK(ctx->dgT.alloc(B * M));
     CK(ctx->adT.alloc(B * M));
     CK(ctx->rowfull.alloc(B * (n + 1)));
+    CK(ctx->tab.alloc(B * 4 * n * std::max<size_t>(1, n / 128)));  // nb * 4 * (n/128) slices * H rows
     return DET_OK;
 }
 
@@ -697,6 +724,7 @@ int det_ctx_create(int device, int k, int precision, det_ctx** out) {
     if (const char* e = getenv("DET_RASTER_RO")) ctx->raster_ro = atoi(e) != 0;    // A/B switch (diagnostics)
     if (const char* e = getenv("DET_UNIQ_ADVECT")) ctx->uniq_adv = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SAT1W")) ctx->sat1w = atoi(e) != 0;  // A/B switch (diagnostics)
+    if (const char* e = getenv("DET_SAT3W")) ctx->sat3w = atoi(e) != 0;  // A/B switch (diagnostics)
     ctx->device = device;
     ctx->k = k;
     ctx->n = 1 << k;

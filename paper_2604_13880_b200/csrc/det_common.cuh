@@ -93,6 +93,7 @@ struct Bufs {
     double* dgT;   // B*(2n-1)
     double* adT;   // B*(2n-1)
     double* rowfull;  // B*(n+1)
+    double* tab;      // B*nb*4*(n/W)*H: k_sat1w's per-row slice tables for k_sat3w (W = slice width)
     Carto* st;
     const Params* prm;
     double* trace;

@@ -451,10 +451,16 @@ struct WarpRing {
 #ifndef DET_SAT1W_CPT
 #define DET_SAT1W_CPT 4  // columns per thread of k_sat1w at CPT=4 configs (2: 49.7k, 4: 52.6k it/s)
 #endif
-template <int CPT, int NT, bool LUTS, typename A = float>
+//
+// TAB (float64 field, for k_sat3w): also record, per band row r and slice w, the slice table
+//   tab[0][w][r] = off(r, w): the row prefix left of the slice, sum_{w' < w} slice total(r, w')
+//   tab[1][w][r] = E1(r, w):  sum over the slice of the diagonal partials pd(jt + r, .)
+//   tab[2][w][r] = pd at the slice's last column, tab[3][w][r] = pa at its first column
+// (D.tab + band * 4 * NW * H), from which k_sat3w's warps form every value crossing a slice edge.
+template <int CPT, int NT, bool LUTS, typename A = float, bool TAB = false>
 __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
     constexpr int NW = NT / 32, W = 32 * CPT, KP = lab_kp1(CPT * NT);
-    // dg[L] | ad[L] | row partials [H][NW] | exitD [NW][H] | exitA [NW][H] | rings (16-B aligned)
+    // dg[L] | ad[L] | row partials [H][NW] | exitD [NW][H] | exitA [NW][H] | (TAB) E1 [NW][H] | rings (16-B aligned)
     extern __shared__ unsigned char s_raw1[];
     __shared__ uint64_t s_bar[NW * KP];
     __shared__ double s_red[33];
@@ -470,15 +476,17 @@ __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
     A* s_rows = ad + L;
     A* exD = s_rows + H * NW;
     A* exA = exD + NW * H;
+    A* exE = exA + NW * H;  // TAB only
     const A* glut = sizeof(A) == 4 ? reinterpret_cast<const A*>(D.lutf + (size_t)b * (R + 1))
                                    : reinterpret_cast<const A*>(D.lut + (size_t)b * (R + 1));
     // LUTS: the LUT staged in shared memory after the rings
-    A* s_lut = reinterpret_cast<A*>(align16(exA + NW * H) + NW * KP * W);
+    A* ring_base = exA + NW * H * (TAB ? 2 : 1);
+    A* s_lut = reinterpret_cast<A*>(align16(ring_base) + NW * KP * W);
     if (LUTS)  // background-first (see band_lut): labels index s_lut + 1 directly
         for (int i = t; i <= R; i += NT) s_lut[i] = __ldg(glut + (i == 0 ? R : i - 1));
     const A* lut = LUTS ? s_lut + 1 : glut;
     WarpRing<CPT, KP> ring;
-    ring.q = align16(exA + NW * H) + w * KP * W;
+    ring.q = align16(ring_base) + w * KP * W;
     ring.bar = s_bar + w * KP;
     ring.lab = D.labels + (size_t)b * D.nn + c0;
     ring.n = n;
@@ -494,6 +502,7 @@ __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
     for (int k = 0; k < CPT; ++k) cs[k] = pd[k] = pa[k] = (A)0;
     A rho_n[CPT];
     A ts_even = (A)0;  // the even row's partial, reduced together with the odd row (H is even)
+    A ps_even = (A)0;  // TAB: the even row's diagonal-partial sum
     ring.template take<A, LUTS>(jt, lane, active, lut, R, rho_n);
     for (int j = jt; j <= jb; ++j) {
         A rho[CPT];
@@ -505,7 +514,8 @@ __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
         for (int k = 0; k < CPT; ++k) ts += rho[k];
         // slice row totals, two rows per butterfly: after one exchange the lower half-warp holds
         // the even row's partials and the upper half the odd row's, so 5 shuffles serve 2 rows
-        if (((j - jt) & 1) == 0) {
+        if (TAB) {
+        } else if (((j - jt) & 1) == 0) {
             ts_even = ts;
             if (j == jb) {  // odd band height (H = 1): the last row is reduced alone
                 const A t1 = warp_sum(ts);
@@ -533,6 +543,38 @@ __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
         for (int k = 0; k < CPT; ++k) cs[k] += rho[k];
         if (lane == 31) exD[w * H + (j - jt)] = pd[CPT - 1];  // diagonal leaving the slice's right edge
         if (lane == 0) exA[w * H + (j - jt)] = pa[0];  // anti-diagonal leaving the slice's left edge
+        if constexpr (TAB) {
+            // slice row total and E1 (the slice's sum of this row's diagonal partials), two rows per
+            // butterfly: the half-warps take the even / odd row, then the quarter-warps the total /
+            // E1, so 6 shuffles serve 4 sums (lanes 0, 8, 16, 24 end with them)
+            A ps = (A)0;
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) ps += pd[k];
+            const int r = j - jt;
+            if ((r & 1) == 0 && j < jb) {
+                ts_even = ts;
+                ps_even = ps;
+            } else {
+                const bool odd = (r & 1) != 0;
+                const bool up = (lane & 16) != 0, qp = (lane & 8) != 0;
+                A kt, kp;
+                if (odd) {
+                    kt = (up ? ts : ts_even) + __shfl_xor_sync(FULL, up ? ts_even : ts, 16);
+                    kp = (up ? ps : ps_even) + __shfl_xor_sync(FULL, up ? ps_even : ps, 16);
+                } else {  // odd band height: the last row alone (both half-warps hold it)
+                    kt = ts + __shfl_xor_sync(FULL, ts, 16);
+                    kp = ps + __shfl_xor_sync(FULL, ps, 16);
+                }
+                A v = (qp ? kp : kt) + __shfl_xor_sync(FULL, qp ? kt : kp, 8);
+#pragma unroll
+                for (int o = 4; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+                const int r0 = odd ? r - 1 : r;
+                if (lane == 0) s_rows[r0 * NW + w] = v;
+                if (lane == 8) exE[w * H + r0] = v;
+                if (odd && lane == 16) s_rows[r * NW + w] = v;
+                if (odd && lane == 24) exE[w * H + r] = v;
+            }
+        }
     }
     __syncthreads();  // exits, row partials published
     // band-bottom entries + the neighbour slice's part of each crossing diagonal
@@ -561,9 +603,21 @@ __global__ void __launch_bounds__(NT) k_sat1w(Topo T, Bufs D, int gate) {
     double run = block_excl_scan(csum, s_red, &tot);  // (its barriers also publish dg/ad)
     if (t < H) {  // row totals in float64, warp order
         double s = 0.0;
+        double* tab = TAB ? D.tab + bb * 4 * NW * H : nullptr;
 #pragma unroll
-        for (int q = 0; q < NW; ++q) s += (double)s_rows[t * NW + q];
+        for (int q = 0; q < NW; ++q) {
+            if (TAB) tab[q * H + t] = s;  // off(t, q): the slice totals left of slice q
+            s += (double)s_rows[t * NW + q];
+        }
         D.rt[(size_t)b * n + jt + t] = s;
+    }
+    if constexpr (TAB) {
+        double* tab = D.tab + bb * 4 * NW * H;
+        for (int i = t; i < NW * H; i += NT) {
+            tab[NW * H + i] = (double)exE[i];
+            tab[2 * NW * H + i] = (double)exD[i];
+            tab[3 * NW * H + i] = (double)exA[i];
+        }
     }
 #pragma unroll
     for (int k = 0; k < CPT; ++k) {
@@ -1099,6 +1153,236 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? (sizeof(A) == 8 ? DET_SAT3_MI
         for (int k = 0; k < CPT; ++k) { al[k] = an[k]; ul[k] = uln[k]; ur[k] = urn[k]; }
         ps = slot;
         slot = slot == 2 ? 0 : slot + 1;
+    }
+}
+
+
+// ---------------------------------------------------------------------------------
+// k_sat3w: k_sat3 for the float64 field with independent warps and no CTA barrier in the sweep.
+// A CTA covers a band and up to 32*CPT*NT/32 columns (cb = its first column); each warp owns a
+// W = 32*CPT column slice and streams it through its own TMA ring.  What crosses a slice edge in
+// row j = jt + r is formed from k_sat1w's slice tables (off, E1, exD, exA; see k_sat1w TAB) instead
+// of being exchanged between warps:
+//   A(j, c0-1)       = off(r, w)
+//   alpha(j-1, c0-1) = csX(c0-1) + sum_{r'<r} off(r', w)
+//   UL(j-1, c0-1)    = dgXc(c0-1-r) + sum_{r'<r} off(r', w-1) + E1(r-1, w-1)
+//   UL(j-1, c0-2)    = dgXc(c0-2-r) + sum_{r'<r} off(r', w-1) + E1(r-1, w-1) - exD(r-1, w-1)
+//   URin(j-1, c0+W)  = sum_{r'<r} (off(r', w+1) + exA(r', w+1))
+// (H <= W - 1: every diagonal / anti-diagonal through a band crosses at most one slice edge, so its
+// in-band sum left / right of the edge is the neighbour slice's in-slice partial.)  The per-pixel
+// arithmetic is k_sat3's float64 anchor combination (displacement.py:102-131 in residual form).
+template <int CPT, int NT, bool LUTS>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3w(Topo T, Bufs D, int gate) {
+    using A = double;
+    extern __shared__ unsigned char s_raw3w[];
+    constexpr int NWC = NT / 32, W = 32 * CPT, KP = lab_kp(W * NWC) > 4 ? 4 : lab_kp(W * NWC);
+    __shared__ uint64_t s_bar[NWC * KP];
+    const int band = blockIdx.x, b = blockIdx.y + D.b0, t = threadIdx.x;
+    const int lane = t & 31, wl = t >> 5;
+    if (!gate_open(D.st + b, gate)) return;
+    const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, M = 2 * n - 1, R = T.R;
+    const int NW = n / W;                   // slices per band row
+    const int cb = blockIdx.z * NWC * W;    // this CTA's first column
+    const int w = blockIdx.z * NWC + wl;    // slice index in the band row
+    const int c0 = w * W, x0 = c0 + lane * CPT;
+    const size_t bb = (size_t)b * D.nb + band;
+    const int WN = NWC * W + H;
+    // The windows are stored phase-split, element e at [e % 4][e / 4] (P entries per phase): lane l
+    // reads elements e0 + 4l + q, so every load of a warp touches consecutive words of one phase
+    // (bank-conflict-free) instead of a 4-element stride (16-way conflicts on 16-byte loads).
+    const int P = (WN + 3) / 4 + 1;
+    using A2 = double2;
+    A2* win_dt = reinterpret_cast<A2*>(s_raw3w);  // DLtot(w), Tu(w) for w in [cb+jt-1, cb+jb+NWC*W-1]
+    A* win_tv = reinterpret_cast<A*>(win_dt + 4 * P);  // Tv(v), v in [cb-jb, cb+NWC*W-1-jt]
+    A* s_rc = win_tv + 4 * P;                       // per band row: ravg, rowfull(j+1), right boundary
+    A* s_tab = s_rc + 3 * H + (H & 1);              // [4][NWC + 2][H]: slices cb/W - 1 .. cb/W + NWC
+    A* s_cw = s_tab + 4 * (NWC + 2) * H;            // [NWC][H + 1]: dgXc(c0 - 1 - m)
+    A* s_lut = s_cw + NWC * (H + 1) + ((NWC * (H + 1)) & 1);
+    const double* rowfull = D.rowfull + (size_t)b * (n + 1);
+    const double* adT = D.adT + (size_t)b * M;
+    const double* dgT = D.dgT + (size_t)b * M;
+    const double* csT = D.csT + (size_t)b * n;
+    const double* tabg = D.tab + bb * 4 * NW * H;
+
+    // ---- carries (k_sat2p), slice tables, row constants, LUT ----
+    for (int q = t; q < WN; q += NT) {
+        const int wq = cb + jt - 1 + q;
+        const int ps = (q & 3) * P + (q >> 2);
+        win_dt[ps].x = (wq < 0) ? 0.0 : D.adSc[bb * (n + H) + (q + cb)];  // DLtot(-1) = 0
+        win_dt[ps].y = (wq >= 0 && wq < M) ? adT[wq] : 0.0;
+        const int iv = q + cb - jb + n - 1;  // Tv index of v = q + cb - jb
+        win_tv[ps] = (iv >= 0 && iv < M) ? dgT[iv] : 0.0;
+    }
+    for (int i = t; i < 4 * (NWC + 2) * H; i += NT) {
+        const int f = i / ((NWC + 2) * H), rem = i - f * (NWC + 2) * H, sl = rem / H, r = rem - sl * H;
+        const int ws = cb / W - 1 + sl;
+        s_tab[i] = (ws >= 0 && ws < NW) ? tabg[(f * NW + ws) * H + r] : 0.0;
+    }
+    for (int i = t; i < NWC * (H + 1); i += NT) {
+        const int sl = i / (H + 1), m = i - sl * (H + 1);
+        const int x = cb + sl * W - 1 - m;
+        s_cw[i] = x >= 0 ? D.dgXc[bb * n + x] : 0.0;
+    }
+    const double rf_top = rowfull[jt];
+    for (int q = t; q < H; q += NT) {
+        const double r0 = rowfull[jt + q], r1 = rowfull[jt + q + 1];
+        s_rc[q] = 0.5 * (r0 + r1);
+        s_rc[H + q] = r1;
+        s_rc[2 * H + q] = r0 - rf_top;
+    }
+    const A* lut = band_lut<A, LUTS, LUTS>(D, R, b, s_lut);
+    A ul[CPT], al[CPT], cc[CPT], ur[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int x = x0 + k;
+        al[k] = D.csX[bb * n + x];
+        ul[k] = D.dgXc[bb * n + x];
+        const double cfi = csT[x], cfe = x > 0 ? csT[x - 1] : 0.0;
+        cc[k] = 0.5 * (cfe + cfi);
+        ur[k] = 0.0;
+    }
+    A aL = c0 > 0 ? D.csX[bb * n + c0 - 1] : 0.0;  // alpha(j-1, c0-1), advanced per row
+    A sL = 0.0, sR = 0.0;                            // running sums of the neighbour tables
+    const A Cr = rowfull[n];
+    const double inv_nd = 1.0 / (double)n;  // exact: n is a power of two
+    const A inv_n = inv_nd, half_n = 0.5 * inv_nd;
+    const A inv2m = 0.5 * inv_nd * inv_nd;
+    const A xc0 = ((double)x0 + 0.5) * inv_nd;  // pixel-centre x of column x0 (displacement.py:59)
+    double* uf = reinterpret_cast<double*>(D.uf) + (size_t)b * D.nn * 2;
+    WarpRing<CPT, KP> ring;
+    ring.q = align16(s_lut + (LUTS ? lut_smem_len(R) : 0)) + wl * KP * W;
+    ring.bar = s_bar + wl * KP;
+    ring.lab = D.labels + (size_t)b * D.nn + c0;
+    ring.n = n;
+    ring.jt = jt;
+    ring.j_last = jb;
+    ring.bytes = (unsigned)(W * 4);
+    ring.init(lane);
+    ring.prologue(lane);
+    __syncthreads();  // windows, tables, row constants and LUT published (the only CTA barrier)
+    const A* tO = s_tab + (wl + 1) * H;                // own slice: off
+    const A* tOL = s_tab + wl * H;                     // left slice: off, E1 (+ (NWC+2)H), exD (+ 2(NWC+2)H)
+    const A* tOR = s_tab + (wl + 2) * H;               // right slice: off, exA (+ 3(NWC+2)H)
+    constexpr int dummy = 0;
+    (void)dummy;
+    const int FS = (NWC + 2) * H;
+    const A* cw = s_cw + wl * (H + 1);
+    const bool first = w == 0, last = w == NW - 1;
+
+    for (int j = jt; j <= jb; ++j) {
+        const int r = j - jt;
+        A rho[CPT];
+        ring.template take<A, LUTS>(j, lane, true, lut, R, rho);
+        // edge values of row j-1 from the tables (running sums advanced by row r-1)
+        A e1 = 0.0, exd = 0.0;
+        if (r > 0) {
+            aL += tO[r - 1];
+            sL += tOL[r - 1];
+            sR += tOR[r - 1];
+            sR += tOR[3 * FS + r - 1];
+            e1 = tOL[FS + r - 1];
+            exd = tOL[2 * FS + r - 1];
+        }
+        const A base = first ? 0.0 : tO[r];  // A(j, c0-1)
+        A loc[CPT];
+        A run = 0.0;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) { run += rho[k]; loc[k] = run; }
+        const A tsum = run;
+        const A winc = warp_incl_scan_t<A>(tsum);
+        const A excl = base + (winc - tsum);
+        A ap_m1 = __shfl_up_sync(FULL, al[CPT - 1], 1);
+        A ul_m1 = __shfl_up_sync(FULL, ul[CPT - 1], 1);
+        A ul_m2 = __shfl_up_sync(FULL, ul[CPT - 2], 1);
+        A ur_p = __shfl_down_sync(FULL, ur[0], 1);
+        if (lane == 0) {
+            if (first) { ap_m1 = 0.0; ul_m1 = 0.0; ul_m2 = 0.0; }
+            else {
+                const A le = sL + e1;
+                ap_m1 = aL;
+                ul_m1 = cw[r] + le;
+                ul_m2 = cw[r + 1] + (le - exd);
+            }
+        }
+        if (lane == 31) ur_p = last ? s_rc[2 * H + r] : sR;
+        A Av[CPT], an[CPT], uln[CPT], urn[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) Av[k] = excl + loc[k];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            an[k] = al[k] + Av[k];
+            uln[k] = Av[k] + (k == 0 ? ul_m1 : ul[k - 1]);
+            urn[k] = Av[k] + (k == CPT - 1 ? ur_p : ur[k + 1]);
+        }
+        {
+            const A ravg = s_rc[r];
+            const A yc = (A)j * inv_n + half_n;  // (j + 0.5) / n, exact
+            const A ycm1 = yc - 1.0, c1y = 0.25 - 0.5 * yc;
+            const A hravg = 0.5 * ravg, hC = 0.5 * Cr;
+            const int e0 = j - jt + c0 - cb;  // window element of lane 0's dlw[0]: e0 + CPT*lane + q
+            const int f0 = c0 - cb - j + jb;  // win_tv element of lane 0's column c0: f0 + CPT*lane + k
+            A dlw[CPT + 1];
+            A tuw[CPT], tvw[CPT];
+#pragma unroll
+            for (int q = 0; q <= CPT; ++q) {
+                const int e = e0 + q;
+                const A2 v = win_dt[(e & 3) * P + (e >> 2) + lane];
+                dlw[q] = v.x;
+                if (q < CPT) tuw[q] = v.y;
+            }
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) {
+                const int e = f0 + k;
+                tvw[k] = win_tv[(e & 3) * P + (e >> 2) + lane];
+            }
+            A ux[CPT], uy[CPT];
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) {
+                const int x = x0 + k;
+                const A apm1 = k == 0 ? ap_m1 : al[k - 1];
+                const A anm1 = k == 0 ? (ap_m1 + excl) : an[k - 1];
+                const A ulnm1 = k == 0 ? (excl + ul_m2) : uln[k - 1];
+                const A ulpm1 = k == 0 ? ul_m1 : ul[k - 1];
+                const A ulpm2 = k == 0 ? ul_m2 : (k == 1 ? ul_m1 : ul[k - 2]);
+                const A urp1 = k == CPT - 1 ? ur_p : ur[k + 1];
+                const A Dw = dlw[k + 1], Dwm1 = dlw[k];
+                const A Tu = tuw[k];
+                const A Tv = tvw[k];
+                const A R_UV = ulpm1 + (Dw - urp1);
+                A R_UVm1 = ulnm1 + (Dw - urn[k]);
+                A R_Um1Vm1 = ulpm2 + (Dwm1 - ur[k]);
+                if (k == 0 && x0 == 0) { R_UVm1 = 0.0; R_Um1Vm1 = 0.0; }
+                const A bt = R_UVm1;
+                const A at = Tu - R_Um1Vm1 + rho[k];
+                const A gt = Tv - R_UV;
+                // branch-free anchor combination (see k_sat3, DET_SAT3_ABS)
+                const A a4 = apm1 + al[k] + anm1 + an[k];  // 4a
+                const A cavg = cc[k];
+                const A xc = xc0 + (A)k * inv_n;
+                const A e = xc + ycm1, d = xc - yc;
+                const A ae = fabs(e), ad = fabs(d);
+                const A hs = fma(0.5, cavg, hravg), hd = fma(-0.5, cavg, hravg);
+                const A hK = hs - hC;
+                const A tt = at + gt;
+                A vx = fma(a4, c1y, cavg);
+                vx = fma(hs, e, vx);
+                vx = fma(hd, ae, vx);
+                vx = fma(-hK, d + ad, vx);
+                vx = fma(xc, tt, vx);
+                ux[k] = (vx + bt) * inv2m;
+                A vy = fma(a4, fma(xc, -0.5, 0.25), ravg);
+                vy = fma(hs, e, vy);
+                vy = fma(-hd, ae, vy);
+                vy = fma(hK, d - ad, vy);
+                vy = fma(yc, Cr - tt, vy);
+                uy[k] = (vy + at) * inv2m;
+            }
+            double* o = uf + ((size_t)j * n + x0) * 2;
+#pragma unroll
+            for (int k = 0; k < CPT; k += 2) st_global_v4f64(o + 2 * k, ux[k], uy[k], ux[k + 1], uy[k + 1]);
+        }
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) { al[k] = an[k]; ul[k] = uln[k]; ur[k] = urn[k]; }
     }
 }
 
