@@ -8,5 +8,5 @@ python bench.py $* > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 DET_PROFILE_RANGE=2 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none -k regex:k_ -c 768 --csv \
   --log-file gpurun_out/${TAG}_launches.csv $A > gpurun_out/${TAG}_ncu.log 2>&1
 DET_PROFILE_RANGE=1 ncu --set full --clock-control none --import-source on --profile-from-start off \
-  -k regex:'k_sat|k_region|k_row|k_ctrl' -c 6 -o gpurun_out/${TAG}_full $A > gpurun_out/${TAG}_ncufull.log 2>&1
+  -k regex:'k_sat|k_region|k_row|k_ctrl|k_advect' -c 7 -o gpurun_out/${TAG}_full $A > gpurun_out/${TAG}_ncufull.log 2>&1
 echo done
