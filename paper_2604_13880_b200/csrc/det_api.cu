@@ -166,6 +166,7 @@ struct det_ctx {
     bool sep_ctrl = true;  // control step as its own kernel (DET_SEP_CTRL=0: k_row's last CTA)
     bool sat1w = true;  // float32 field: barrier-free k_sat1w (DET_SAT1W=0: k_sat1)
     bool sat3w = true;  // float64 field: barrier-free k_sat3w with k_sat1w's slice tables (DET_SAT3W=0: k_sat3)
+    bool sat3x = true;  // k_sat3w as k_sat3x (edge records prefixed per band, rows unrolled 4x; DET_SAT3X=0: k_sat3w)
     bool split_adv = false;  // float32 state: advect as the flat k_advect_rows (DET_SPLIT_ADVECT=1); 48.6k vs 51.4k fused
     // float64: advect once per unique vertex (k_advect_uniq64) + the raster-only k_region; valid while
     // every frame's start rows keep the loaded map's shared vertices bit-identical (ua_ok)
@@ -349,6 +350,16 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
         const size_t smemw = ((size_t)3 * 4 * PW + 3 * H + (H & 1) + (size_t)4 * (NWC + 2) * H +
                               (size_t)NWC * (H + 1) + ((NWC * (H + 1)) & 1)) * sizeof(double) +
                              lut_b + (size_t)NWC * KPW * W * sizeof(int) + 16;
+        if constexpr (CPT == 4) {
+            if (c->sat3x) {  // loop-invariant edge records + 4x unrolled rows (DET_SAT3X=0: k_sat3w)
+                const size_t smemx = ((size_t)3 * 4 * sat3x_phase_len(NWC) + (size_t)NWC * H * 6) * sizeof(double) +
+                                     lut_b + (size_t)NWC * 4 * W * sizeof(int) + 16;
+                auto fx = luts ? k_sat3x<NTW, true> : k_sat3x<NTW, false>;
+                smem_optin(fx);
+                fx<<<dim3(c->nb, B, n / (NWC * W)), NTW, smemx, c->stream>>>(T, D, gate);
+                return;
+            }
+        }
         auto fn = luts ? k_sat3w<CPT, NTW, true> : k_sat3w<CPT, NTW, false>;
         smem_optin(fn);
         fn<<<dim3(c->nb, B, n / (NWC * W)), NTW, smemw, c->stream>>>(T, D, gate);
@@ -725,6 +736,7 @@ int det_ctx_create(int device, int k, int precision, det_ctx** out) {
     if (const char* e = getenv("DET_UNIQ_ADVECT")) ctx->uniq_adv = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SAT1W")) ctx->sat1w = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SAT3W")) ctx->sat3w = atoi(e) != 0;  // A/B switch (diagnostics)
+    if (const char* e = getenv("DET_SAT3X")) ctx->sat3x = atoi(e) != 0;  // A/B switch (diagnostics)
     ctx->device = device;
     ctx->k = k;
     ctx->n = 1 << k;

@@ -116,6 +116,10 @@ __host__ __device__ constexpr int lab_kp(int cols) { return cols >= 8192 ? 2 : (
 #endif
 __host__ __device__ constexpr int lab_kp1(int cols) { return cols >= 8192 ? 2 : (cols >= 4096 ? 4 : DET_KP1); }
 
+// k_sat3x: entries per phase of its phase-split carry windows for CTAs of NWC 128-column slices
+// (compile-time: the band height is below the slice width)
+__host__ __device__ constexpr int sat3x_phase_len(int NWC) { return (NWC * 128 + 128 + 6) / 4 + 2; }
+
 // first 16-byte aligned int slot at or after p (cp.async 16-byte copies and int4 reads)
 // (offset arithmetic on the pointer itself, so the compiler keeps it in the shared window: LDS,
 // not generic LD, for the ring reads)
@@ -1383,6 +1387,275 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3w
         }
 #pragma unroll
         for (int k = 0; k < CPT; ++k) { al[k] = an[k]; ul[k] = uln[k]; ur[k] = urn[k]; }
+    }
+}
+
+// ---------------------------------------------------------------------------------
+// k_sat3x: k_sat3w with everything that does not depend on the pixel taken out of the row loop.
+//  * The values crossing a slice edge (k_sat3w's running sums over k_sat1w's slice tables) are
+//    prefixed once per band by the warp itself (a warp scan over the band rows) into a 6-double
+//    record per row -- A(j, c0-1), alpha(j-1, c0-1), UL(j-1, c0-1), UL(j-1, c0-2), URin(j-1, c0+W)
+//    and the row-total average -- which the row reads as three broadcast 16-byte loads.
+//  * The row loop is unrolled four times, so the phase of the phase-split carry windows, the ring
+//    slot and the record offset are compile-time: every shared load of a row is [pointer + immediate],
+//    the pointers advance once per four rows, and the carries rotate by register renaming.
+// The per-pixel arithmetic is k_sat3w's, in the same operation order (the edge prefixes are summed
+// in warp-scan order instead of row order).  CPT = 4 only (KP = 4 ring slots = the unroll).
+template <int NT, bool LUTS>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x(Topo T, Bufs D, int gate) {
+    using A = double;
+    using A2 = double2;
+    constexpr int CPT = 4, NWC = NT / 32, W = 32 * CPT, KP = 4;
+    constexpr int P = sat3x_phase_len(NWC);  // entries per window phase (compile-time: H < W)
+    extern __shared__ __align__(16) unsigned char s_raw3x[];
+    __shared__ uint64_t s_bar[NWC * KP];
+    const int band = blockIdx.x, b = blockIdx.y + D.b0, t = threadIdx.x;
+    const int lane = t & 31, wl = t >> 5;
+    if (!gate_open(D.st + b, gate)) return;
+    const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, M = 2 * n - 1, R = T.R;
+    const int NW = n / W;                   // slices per band row
+    const int cb = blockIdx.z * NWC * W;    // this CTA's first column
+    const int w = blockIdx.z * NWC + wl;    // slice index in the band row
+    const int c0 = w * W, x0 = c0 + lane * CPT;
+    const size_t bb = (size_t)b * D.nb + band;
+    const int WN = NWC * W + H;
+    const int pad = (3 - (H - 1)) & 3;      // win_tv storage shift: row r reads phase (3 - r + k) & 3
+    const int Hq = (H - 1 + pad) >> 2;
+    A2* win_dt = reinterpret_cast<A2*>(s_raw3x);       // [4][P]: DLtot(w), Tu(w), w from cb+jt-1, element e at [e&3][e>>2]
+    A* win_tv = reinterpret_cast<A*>(win_dt + 4 * P);  // [4][P]: Tv(v), v from cb-jb, element e+pad at [..&3][..>>2]
+    A* s_rec = win_tv + 4 * P;                         // [NWC][H][6] edge records
+    A* s_lut = s_rec + (size_t)NWC * H * 6;
+    const double* rowfull = D.rowfull + (size_t)b * (n + 1);
+    const double* adT = D.adT + (size_t)b * M;
+    const double* dgT = D.dgT + (size_t)b * M;
+    const double* csT = D.csT + (size_t)b * n;
+    const double* tabg = D.tab + bb * 4 * NW * H;
+
+    // ---- carries (k_sat2p) into the phase-split windows, LUT ----
+    for (int q = t; q < WN; q += NT) {
+        const int wq = cb + jt - 1 + q;
+        A2 v;
+        v.x = (wq < 0) ? 0.0 : D.adSc[bb * (n + H) + (q + cb)];  // DLtot(-1) = 0
+        v.y = (wq >= 0 && wq < M) ? adT[wq] : 0.0;
+        win_dt[(q & 3) * P + (q >> 2)] = v;
+        const int iv = q + cb - jb + n - 1;  // Tv index of v = q + cb - jb
+        const int qp = q + pad;
+        win_tv[(qp & 3) * P + (qp >> 2)] = (iv >= 0 && iv < M) ? dgT[iv] : 0.0;
+    }
+    const A* lut = band_lut<A, LUTS, LUTS>(D, R, b, s_lut);
+    // ---- this warp's edge records: exclusive prefixes over the band rows of the slice tables ----
+    {
+        const bool first = w == 0, last = w == NW - 1;
+        const double rf_top = rowfull[jt];
+        A cA = c0 > 0 ? D.csX[bb * n + c0 - 1] : 0.0;  // alpha(jt-1, c0-1)
+        A cL = 0.0, cR = 0.0;
+        A* rec = s_rec + (size_t)wl * H * 6;
+        for (int r0 = 0; r0 < H; r0 += 32) {
+            const int r = r0 + lane;
+            const bool in = r < H;
+            const A offw = (in && !first) ? tabg[(0 * NW + w) * H + r] : 0.0;
+            const A offl = (in && !first) ? tabg[(0 * NW + w - 1) * H + r] : 0.0;
+            const A offr = (in && !last) ? tabg[(0 * NW + w + 1) * H + r] + tabg[(3 * NW + w + 1) * H + r] : 0.0;
+            const A sA = warp_incl_scan_t<A>(offw), sL = warp_incl_scan_t<A>(offl), sR = warp_incl_scan_t<A>(offr);
+            if (in) {
+                const A e1 = (!first && r > 0) ? tabg[(1 * NW + w - 1) * H + r - 1] : 0.0;
+                const A exd = (!first && r > 0) ? tabg[(2 * NW + w - 1) * H + r - 1] : 0.0;
+                const int xa = c0 - 1 - r;
+                const A cw0 = xa >= 0 ? D.dgXc[bb * n + xa] : 0.0;
+                const A cw1 = xa >= 1 ? D.dgXc[bb * n + xa - 1] : 0.0;
+                const A le = (cL + (sL - offl)) + e1;
+                const double rf0 = rowfull[jt + r], rf1 = rowfull[jt + r + 1];
+                A* o = rec + r * 6;
+                o[0] = offw;                                         // A(j, c0-1)
+                o[1] = first ? 0.0 : cA + (sA - offw);               // alpha(j-1, c0-1)
+                o[2] = first ? 0.0 : cw0 + le;                       // UL(j-1, c0-1)
+                o[3] = first ? 0.0 : cw1 + (le - exd);               // UL(j-1, c0-2)
+                o[4] = last ? rf0 - rf_top : cR + (sR - offr);       // URin(j-1, c0+W)
+                o[5] = 0.5 * (rf0 + rf1);                            // row-total average
+            }
+            cA += __shfl_sync(FULL, sA, 31);
+            cL += __shfl_sync(FULL, sL, 31);
+            cR += __shfl_sync(FULL, sR, 31);
+        }
+    }
+    A ul[CPT], al[CPT], cc[CPT], ur[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int x = x0 + k;
+        al[k] = D.csX[bb * n + x];
+        ul[k] = D.dgXc[bb * n + x];
+        const double cfi = csT[x], cfe = x > 0 ? csT[x - 1] : 0.0;
+        cc[k] = 0.5 * (cfe + cfi);
+        ur[k] = 0.0;
+    }
+    const A Cr = rowfull[n];
+    const double inv_nd = 1.0 / (double)n;  // exact: n is a power of two
+    const A inv_n = inv_nd;
+    const A inv2m = 0.5 * inv_nd * inv_nd;
+    const A xc0 = ((double)x0 + 0.5) * inv_nd;  // pixel-centre x of column x0 (displacement.py:59)
+    const A hC = 0.5 * Cr;
+    const bool zero0 = x0 == 0;
+    // ---- the warp's label ring (KP = 4 slots of W ints; row r sits in slot r & 3) ----
+    int* rq = align16(s_lut + (LUTS ? lut_smem_len(R) : 0)) + wl * KP * W;
+    const unsigned rq_s = (unsigned)__cvta_generic_to_shared(rq);
+    const unsigned bar_s = (unsigned)__cvta_generic_to_shared(s_bar + wl * KP);
+    const int* glab = D.labels + (size_t)b * D.nn + (size_t)jt * n + c0;  // row jt of the slice
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < KP; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s + 8u * s));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+#pragma unroll
+        for (int p = 0; p < KP - 1; ++p)
+            if (p < H) {
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s + 8u * p), "r"(W * 4)
+                             : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+                                 "r"(rq_s + (unsigned)(p * W * 4)), "l"(glab + (size_t)p * n), "r"(W * 4), "r"(bar_s + 8u * p)
+                             : "memory");
+            }
+    }
+    const int* gnext = glab + (size_t)(KP - 1) * n;  // the row the next refill fetches
+    __syncthreads();  // windows, LUT and (for its own warp) records published: the only CTA barrier
+
+    const A2* pdt = win_dt + ((c0 - cb) >> 2) + lane;
+    const A* ptv = win_tv + ((c0 - cb) >> 2) + lane + Hq;
+    const A2* prec = reinterpret_cast<const A2*>(s_rec + (size_t)wl * H * 6);
+    const int* rsrc = rq + lane * CPT;
+    double* o = reinterpret_cast<double*>(D.uf) + (size_t)b * D.nn * 2 + ((size_t)jt * n + x0) * 2;
+    const size_t ostep = (size_t)n * 2;
+    A yc = ((double)jt + 0.5) * inv_nd;  // (j + 0.5) / n, advanced exactly by 1/n per row
+    int rows_left = H;                   // rows not yet fetched beyond the prologue's KP - 1
+    unsigned parity = 0;
+
+    auto row = [&](auto rr_c) {
+        constexpr int RR = decltype(rr_c)::value;
+        // ---- labels of this row -> residual densities; refill the slot row r-1 used ----
+        __syncwarp();
+        if (lane == 0 && rows_left > KP - 1) {
+            constexpr int SL = (RR + KP - 1) & 3;
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s + 8u * SL), "r"(W * 4)
+                         : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+                             "r"(rq_s + (unsigned)(SL * W * 4)), "l"(gnext), "r"(W * 4), "r"(bar_s + 8u * SL)
+                         : "memory");
+        }
+        gnext += n;
+        --rows_left;
+        {
+            unsigned done = 0;
+            while (!done) {
+                asm volatile(
+                    "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                    : "=r"(done)
+                    : "r"(bar_s + 8u * RR), "r"(parity)
+                    : "memory");
+            }
+        }
+        const int4 Lv = *reinterpret_cast<const int4*>(rsrc + RR * W);
+        A rho[CPT];
+        rho[0] = LUTS ? lut[Lv.x] : lut[Lv.x < 0 ? R : Lv.x];
+        rho[1] = LUTS ? lut[Lv.y] : lut[Lv.y < 0 ? R : Lv.y];
+        rho[2] = LUTS ? lut[Lv.z] : lut[Lv.z < 0 ? R : Lv.z];
+        rho[3] = LUTS ? lut[Lv.w] : lut[Lv.w < 0 ? R : Lv.w];
+        // ---- edge record of the row (broadcast loads) ----
+        const A2 e01 = prec[RR * 3 + 0], e23 = prec[RR * 3 + 1], e45 = prec[RR * 3 + 2];
+        A loc[CPT];
+        A run = 0.0;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) { run += rho[k]; loc[k] = run; }
+        const A tsum = run;
+        const A winc = warp_incl_scan_t<A>(tsum);
+        const A excl = e01.x + (winc - tsum);
+        A ap_m1 = __shfl_up_sync(FULL, al[CPT - 1], 1);
+        A ul_m1 = __shfl_up_sync(FULL, ul[CPT - 1], 1);
+        A ul_m2 = __shfl_up_sync(FULL, ul[CPT - 2], 1);
+        A ur_p = __shfl_down_sync(FULL, ur[0], 1);
+        if (lane == 0) { ap_m1 = e01.y; ul_m1 = e23.x; ul_m2 = e23.y; }
+        if (lane == 31) ur_p = e45.x;
+        A Av[CPT], an[CPT], uln[CPT], urn[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) Av[k] = excl + loc[k];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            an[k] = al[k] + Av[k];
+            uln[k] = Av[k] + (k == 0 ? ul_m1 : ul[k - 1]);
+            urn[k] = Av[k] + (k == CPT - 1 ? ur_p : ur[k + 1]);
+        }
+        const A ravg = e45.y;
+        const A ycm1 = yc - 1.0, c1y = 0.25 - 0.5 * yc;
+        const A hravg = 0.5 * ravg;
+        A dlw[CPT + 1], tuw[CPT], tvw[CPT];
+#pragma unroll
+        for (int q = 0; q <= CPT; ++q) {
+            const A2 v = pdt[((RR + q) & 3) * P + ((RR + q) >> 2)];
+            dlw[q] = v.x;
+            if (q < CPT) tuw[q] = v.y;
+        }
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) tvw[k] = ptv[((3 - RR + k) & 3) * P + ((3 - RR + k) >> 2)];
+        A ux[CPT], uy[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) {
+            const A apm1 = k == 0 ? ap_m1 : al[k - 1];
+            const A anm1 = k == 0 ? (ap_m1 + excl) : an[k - 1];
+            const A ulnm1 = k == 0 ? (excl + ul_m2) : uln[k - 1];
+            const A ulpm1 = k == 0 ? ul_m1 : ul[k - 1];
+            const A ulpm2 = k == 0 ? ul_m2 : (k == 1 ? ul_m1 : ul[k - 2]);
+            const A urp1 = k == CPT - 1 ? ur_p : ur[k + 1];
+            const A Dw = dlw[k + 1], Dwm1 = dlw[k];
+            const A R_UV = ulpm1 + (Dw - urp1);
+            A R_UVm1 = ulnm1 + (Dw - urn[k]);
+            A R_Um1Vm1 = ulpm2 + (Dwm1 - ur[k]);
+            if (k == 0 && zero0) { R_UVm1 = 0.0; R_Um1Vm1 = 0.0; }
+            const A bt = R_UVm1;
+            const A at = tuw[k] - R_Um1Vm1 + rho[k];
+            const A gt = tvw[k] - R_UV;
+            // branch-free anchor combination (see k_sat3, DET_SAT3_ABS)
+            const A a4 = apm1 + al[k] + anm1 + an[k];  // 4a
+            const A cavg = cc[k];
+            const A xc = xc0 + (A)k * inv_n;
+            const A e = xc + ycm1, d = xc - yc;
+            const A ae = fabs(e), ad = fabs(d);
+            const A hs = fma(0.5, cavg, hravg), hd = fma(-0.5, cavg, hravg);
+            const A hK = hs - hC;
+            const A tt = at + gt;
+            A vx = fma(a4, c1y, cavg);
+            vx = fma(hs, e, vx);
+            vx = fma(hd, ae, vx);
+            vx = fma(-hK, d + ad, vx);
+            vx = fma(xc, tt, vx);
+            ux[k] = (vx + bt) * inv2m;
+            A vy = fma(a4, fma(xc, -0.5, 0.25), ravg);
+            vy = fma(hs, e, vy);
+            vy = fma(-hd, ae, vy);
+            vy = fma(hK, d - ad, vy);
+            vy = fma(yc, Cr - tt, vy);
+            uy[k] = (vy + at) * inv2m;
+        }
+#pragma unroll
+        for (int k = 0; k < CPT; k += 2) st_global_v4f64(o + 2 * k, ux[k], uy[k], ux[k + 1], uy[k + 1]);
+        o += ostep;
+        yc += inv_n;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) { al[k] = an[k]; ul[k] = uln[k]; ur[k] = urn[k]; }
+    };
+
+    int r = 0;
+    for (; r + 4 <= H; r += 4) {
+        row(std::integral_constant<int, 0>{});
+        row(std::integral_constant<int, 1>{});
+        row(std::integral_constant<int, 2>{});
+        row(std::integral_constant<int, 3>{});
+        pdt += 1;
+        ptv -= 1;
+        prec += 12;
+        parity ^= 1u;
+    }
+    if (r < H) {  // band heights that are not a multiple of four
+        row(std::integral_constant<int, 0>{});
+        if (r + 1 < H) row(std::integral_constant<int, 1>{});
+        if (r + 2 < H) row(std::integral_constant<int, 2>{});
     }
 }
 

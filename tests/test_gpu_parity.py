@@ -454,3 +454,57 @@ def test_band_height_independence(P):
         outs.append(be.run_all(crit)[0].state.mapmodel.vertex_array())
         ctx.set_band_height(0)  # back to the automatic height for the shared per-thread context
     assert max(np.abs(o - outs[0]).max() for o in outs) <= 1e-5
+
+
+_VARIANT64_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, {root!r})
+import paper_2604_13880_b200 as P
+from paper_2604_13880_b200.synthetic import voronoi_map
+m = voronoi_map(200, seed=7, target_unique=20000, sigma=0.8)
+res = P.run(m, P.StoppingCriteria(1e-300, 10**9, 30), k={k}, field_dtype="float64")
+np.save({out!r}, np.concatenate([res.state.mapmodel.vertex_array().ravel(),
+                                 res.state.pixel_counts.astype(np.float64)]))
+"""
+
+
+@pytest.mark.parametrize("k", [9, 10])
+@pytest.mark.parametrize("env", [{"DET_SAT3X": "0"}, {"DET_SAT3W": "0"}])
+def test_float64_band_kernel_variants_agree(P, tmp_path, env, k):
+    """The float64 field's sweep kernels -- k_sat3x (edge records, rows unrolled four times), k_sat3w
+    (running edge sums) and the barrier-per-row k_sat3 -- give the same cartogram after 30
+    iterations: vertices within 1e-10 (only the grouping of the edge sums differs), identical counts."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for i, e in enumerate([{}, env]):
+        out = str(tmp_path / f"w{i}.npy")
+        code = _VARIANT64_SCRIPT.format(root=root, out=out, k=k)
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **e), capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    nv = outs[0].size - 200
+    dv = np.abs(outs[0][:nv] - outs[1][:nv]).max()
+    assert dv <= 1e-10, dv
+    assert np.array_equal(outs[0][nv:], outs[1][nv:])
+
+
+def test_float64_band_height_independence(P):
+    """k_sat3x / k_sat1w(TAB) at 1024^2 for band heights 1, 2 (the unroll's tail rows), 32 and 64 (two
+    record chunks per warp): the same cartogram as the automatic height within 1e-10."""
+    from paper_2604_13880_b200.synthetic import voronoi_map
+
+    m = voronoi_map(120, seed=5, target_unique=12000, sigma=0.6)
+    crit = P.StoppingCriteria(1e-300, 10**9, 6)
+    outs = []
+    for h in (0, 1, 2, 32, 64):
+        be = P.BatchEngine(m, np.atleast_2d(m.statistics()), criteria=crit, k=10, bdv_multiplier=1.0,
+                           field_dtype="float64")
+        ctx = be._ctx()
+        if h:
+            ctx.set_band_height(h)
+        outs.append(be.run_all(crit)[0].state.mapmodel.vertex_array())
+        ctx.set_band_height(0)
+    assert max(np.abs(o - outs[0]).max() for o in outs) <= 1e-10
