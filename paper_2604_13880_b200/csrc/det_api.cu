@@ -167,6 +167,7 @@ struct det_ctx {
     bool sat1w = true;  // float32 field: barrier-free k_sat1w (DET_SAT1W=0: k_sat1)
     bool sat3w = true;  // float64 field: barrier-free k_sat3w with k_sat1w's slice tables (DET_SAT3W=0: k_sat3)
     bool sat3x = true;  // k_sat3w as k_sat3x (edge records prefixed per band, rows unrolled 4x; DET_SAT3X=0: k_sat3w)
+    bool sat1x = true;  // k_sat1w (float64, slice tables) as k_sat1x (DET_SAT1X=0: k_sat1w)
     bool split_adv = false;  // float32 state: advect as the flat k_advect_rows (DET_SPLIT_ADVECT=1); 48.6k vs 51.4k fused
     // float64: advect once per unique vertex (k_advect_uniq64) + the raster-only k_region; valid while
     // every frame's start rows keep the loaded map's shared vertices bit-identical (ua_ok)
@@ -300,9 +301,22 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
                         (size_t)NW * KP * 32 * CPT1 * sizeof(int);
         const bool l1 = DET_SAT1W_LUTS && (size_t)lut_smem_len(R) * sa <= 48 * 1024;
         if (l1) smem1w += (size_t)lut_smem_len(R) * sa;
-        auto fn = l1 ? k_sat1w<CPT1, NT1, true, double, true> : k_sat1w<CPT1, NT1, false, double, true>;
-        smem_optin(fn);
-        fn<<<gb, NT1, smem1w, c->stream>>>(T, D, gate);
+        bool done1 = false;
+        if constexpr (CPT1 == 4 && NT1 <= 512) {
+            if (c->sat1x) {  // rows unrolled 4x over an 8-slot ring, dg/ad aliased (DET_SAT1X=0: k_sat1w)
+                const size_t smem1x = (size_t)4 * H * NW * sa + (size_t)NW * 8 * 32 * CPT1 * sizeof(int) +
+                                      (l1 ? (size_t)lut_smem_len(R) * sa : 0);
+                auto fx = l1 ? k_sat1x<NT1, true> : k_sat1x<NT1, false>;
+                smem_optin(fx);
+                fx<<<gb, NT1, smem1x, c->stream>>>(T, D, gate);
+                done1 = true;
+            }
+        }
+        if (!done1) {
+            auto fn = l1 ? k_sat1w<CPT1, NT1, true, double, true> : k_sat1w<CPT1, NT1, false, double, true>;
+            smem_optin(fn);
+            fn<<<gb, NT1, smem1w, c->stream>>>(T, D, gate);
+        }
     } else if (sat1w_ok) {
         // barrier-free band sums in the field's arithmetic type (float32 or float64)
         constexpr int NW = NT1 / 32, KP = lab_kp1(CPT1 * NT1);
@@ -737,6 +751,7 @@ int det_ctx_create(int device, int k, int precision, det_ctx** out) {
     if (const char* e = getenv("DET_SAT1W")) ctx->sat1w = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SAT3W")) ctx->sat3w = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SAT3X")) ctx->sat3x = atoi(e) != 0;  // A/B switch (diagnostics)
+    if (const char* e = getenv("DET_SAT1X")) ctx->sat1x = atoi(e) != 0;  // A/B switch (diagnostics)
     ctx->device = device;
     ctx->k = k;
     ctx->n = 1 << k;

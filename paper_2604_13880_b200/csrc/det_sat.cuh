@@ -1401,6 +1401,9 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3w
 //    the pointers advance once per four rows, and the carries rotate by register renaming.
 // The per-pixel arithmetic is k_sat3w's, in the same operation order (the edge prefixes are summed
 // in warp-scan order instead of row order).  CPT = 4 only (KP = 4 ring slots = the unroll).
+#ifndef DET_SAT3X_PIPE
+#define DET_SAT3X_PIPE 0  // 1: the next row's labels, LUT reads and row-prefix scan issued ahead of this row's field arithmetic (spills at 128 registers: 49.6k vs 51.6k it/s)
+#endif
 template <int NT, bool LUTS>
 __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x(Topo T, Bufs D, int gate) {
     using A = double;
@@ -1500,12 +1503,13 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x
     const unsigned rq_s = (unsigned)__cvta_generic_to_shared(rq);
     const unsigned bar_s = (unsigned)__cvta_generic_to_shared(s_bar + wl * KP);
     const int* glab = D.labels + (size_t)b * D.nn + (size_t)jt * n + c0;  // row jt of the slice
+    constexpr int PF = DET_SAT3X_PIPE ? KP : KP - 1;  // rows fetched by the prologue
     if (lane == 0) {
 #pragma unroll
         for (int s = 0; s < KP; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s + 8u * s));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
 #pragma unroll
-        for (int p = 0; p < KP - 1; ++p)
+        for (int p = 0; p < PF; ++p)
             if (p < H) {
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s + 8u * p), "r"(W * 4)
                              : "memory");
@@ -1514,7 +1518,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x
                              : "memory");
             }
     }
-    const int* gnext = glab + (size_t)(KP - 1) * n;  // the row the next refill fetches
+    const int* gnext = glab + (size_t)PF * n;  // the row the next refill fetches
     __syncthreads();  // windows, LUT and (for its own warp) records published: the only CTA barrier
 
     const A2* pdt = win_dt + ((c0 - cb) >> 2) + lane;
@@ -1524,15 +1528,39 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x
     double* o = reinterpret_cast<double*>(D.uf) + (size_t)b * D.nn * 2 + ((size_t)jt * n + x0) * 2;
     const size_t ostep = (size_t)n * 2;
     A yc = ((double)jt + 0.5) * inv_nd;  // (j + 0.5) / n, advanced exactly by 1/n per row
-    int rows_left = H;                   // rows not yet fetched beyond the prologue's KP - 1
+    int rows_left = H;                   // rows from this one to the band end
     unsigned parity = 0;
+
+    // labels in ring slot SL (phase parity par) -> residual densities and the lane's exclusive
+    // in-slice row prefix
+    A rho_n[CPT], pre_n = 0.0;
+    auto take = [&](auto sl_c, unsigned par) {
+        constexpr int SL = decltype(sl_c)::value;
+        unsigned done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(bar_s + 8u * SL), "r"(par)
+                : "memory");
+        }
+        const int4 Lv = *reinterpret_cast<const int4*>(rsrc + SL * W);
+        rho_n[0] = LUTS ? lut[Lv.x] : lut[Lv.x < 0 ? R : Lv.x];
+        rho_n[1] = LUTS ? lut[Lv.y] : lut[Lv.y < 0 ? R : Lv.y];
+        rho_n[2] = LUTS ? lut[Lv.z] : lut[Lv.z < 0 ? R : Lv.z];
+        rho_n[3] = LUTS ? lut[Lv.w] : lut[Lv.w < 0 ? R : Lv.w];
+        const A tsum = ((rho_n[0] + rho_n[1]) + rho_n[2]) + rho_n[3];
+        pre_n = warp_incl_scan_t<A>(tsum) - tsum;
+    };
+    if (DET_SAT3X_PIPE) take(std::integral_constant<int, 0>{}, 0u);
 
     auto row = [&](auto rr_c) {
         constexpr int RR = decltype(rr_c)::value;
-        // ---- labels of this row -> residual densities; refill the slot row r-1 used ----
+        // ---- labels -> residual densities; refill a consumed slot ----
         __syncwarp();
-        if (lane == 0 && rows_left > KP - 1) {
-            constexpr int SL = (RR + KP - 1) & 3;
+        if (lane == 0 && rows_left > PF) {
+            // PIPE: row r's slot (read one row ago) takes row r + 4; else row r-1's slot takes row r + 3
+            constexpr int SL = DET_SAT3X_PIPE ? RR : ((RR + KP - 1) & 3);
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s + 8u * SL), "r"(W * 4)
                          : "memory");
@@ -1541,32 +1569,26 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x
                          : "memory");
         }
         gnext += n;
-        --rows_left;
-        {
-            unsigned done = 0;
-            while (!done) {
-                asm volatile(
-                    "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-                    : "=r"(done)
-                    : "r"(bar_s + 8u * RR), "r"(parity)
-                    : "memory");
-            }
+        A rho[CPT], pre;
+        if (DET_SAT3X_PIPE) {
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
+            pre = pre_n;
+            if (rows_left > 1) take(std::integral_constant<int, (RR + 1) & 3>{}, RR == 3 ? parity ^ 1u : parity);
+        } else {
+            take(rr_c, parity);
+#pragma unroll
+            for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
+            pre = pre_n;
         }
-        const int4 Lv = *reinterpret_cast<const int4*>(rsrc + RR * W);
-        A rho[CPT];
-        rho[0] = LUTS ? lut[Lv.x] : lut[Lv.x < 0 ? R : Lv.x];
-        rho[1] = LUTS ? lut[Lv.y] : lut[Lv.y < 0 ? R : Lv.y];
-        rho[2] = LUTS ? lut[Lv.z] : lut[Lv.z < 0 ? R : Lv.z];
-        rho[3] = LUTS ? lut[Lv.w] : lut[Lv.w < 0 ? R : Lv.w];
+        --rows_left;
         // ---- edge record of the row (broadcast loads) ----
         const A2 e01 = prec[RR * 3 + 0], e23 = prec[RR * 3 + 1], e45 = prec[RR * 3 + 2];
         A loc[CPT];
         A run = 0.0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) { run += rho[k]; loc[k] = run; }
-        const A tsum = run;
-        const A winc = warp_incl_scan_t<A>(tsum);
-        const A excl = e01.x + (winc - tsum);
+        const A excl = e01.x + pre;
         A ap_m1 = __shfl_up_sync(FULL, al[CPT - 1], 1);
         A ul_m1 = __shfl_up_sync(FULL, ul[CPT - 1], 1);
         A ul_m2 = __shfl_up_sync(FULL, ul[CPT - 2], 1);
@@ -1657,6 +1679,219 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x
         if (r + 1 < H) row(std::integral_constant<int, 1>{});
         if (r + 2 < H) row(std::integral_constant<int, 2>{});
     }
+}
+
+// ---------------------------------------------------------------------------------
+// k_sat1x: k_sat1w<4, NT, LUTS, double, TAB> (the float64 field's band sums and slice tables) with the
+// row loop unrolled four times over an 8-slot warp ring (two halves of four compile-time slots,
+// prefetch distance 6 rows), the slice exports written through advancing pointers, and the band-end
+// dg / ad staging aliased onto the ring and LUT area (free once the sweep is over).  Same sums in
+// the same order as k_sat1w.
+#ifndef DET_SAT1X_MINB
+#define DET_SAT1X_MINB 2  // 90 registers, no spill (3 CTAs/SM at 80 registers spills: 46.9k vs 51.7k it/s)
+#endif
+template <int NT, bool LUTS>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT1X_MINB : 1)) k_sat1x(Topo T, Bufs D, int gate) {
+    using A = double;
+    constexpr int CPT = 4, NW = NT / 32, W = 32 * CPT, KP = 8;
+    // row partials [H][NW] | exitD [NW][H] | exitA [NW][H] | E1 [NW][H] | { rings, LUT } aliased by { dg[L] | ad[L] }
+    extern __shared__ __align__(16) unsigned char s_raw1x[];
+    __shared__ uint64_t s_bar[NW * KP];
+    __shared__ double s_red[33];
+    const int band = blockIdx.x, b = blockIdx.y + D.b0, t = threadIdx.x;
+    const int lane = t & 31, w = t >> 5;
+    if (!gate_open(D.st + b, gate)) return;
+    const int n = D.n, H = D.H, jt = band * H, jb = jt + H - 1, L = n + H - 1, R = T.R;
+    const int x0 = t * CPT, c0 = w * W;
+    const size_t bb = (size_t)b * D.nb + band;
+    A* s_rows = reinterpret_cast<A*>(s_raw1x);
+    A* exD = s_rows + H * NW;
+    A* exA = exD + NW * H;
+    A* exE = exA + NW * H;
+    int* ring_base = reinterpret_cast<int*>(exE + NW * H);  // 16-byte aligned: 4*H*NW doubles
+    A* s_lut = reinterpret_cast<A*>(ring_base + NW * KP * W);
+    A* dg = reinterpret_cast<A*>(ring_base);                // band end only
+    A* ad = dg + L;
+    const A* glut = reinterpret_cast<const A*>(D.lut + (size_t)b * (R + 1));
+    if (LUTS)  // background-first (see band_lut): labels index s_lut + 1 directly
+        for (int i = t; i <= R; i += NT) s_lut[i] = __ldg(glut + (i == 0 ? R : i - 1));
+    const A* lut = LUTS ? s_lut + 1 : glut;
+    int* rq = ring_base + w * KP * W;
+    const unsigned rq_s = (unsigned)__cvta_generic_to_shared(rq);
+    const unsigned bar_s = (unsigned)__cvta_generic_to_shared(s_bar + w * KP);
+    const int* glab = D.labels + (size_t)b * D.nn + (size_t)jt * n + c0;
+    auto fetch = [&](const int* src, unsigned slot) {  // lane 0: one 512-byte slice row into a slot
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s + 8u * slot), "r"(W * 4)
+                     : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::
+                         "r"(rq_s + slot * (unsigned)(W * 4)), "l"(src), "r"(W * 4), "r"(bar_s + 8u * slot)
+                     : "memory");
+    };
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < KP; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s + 8u * s));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+#pragma unroll
+        for (int p = 0; p < KP - 1; ++p)
+            if (p < H) fetch(glab + (size_t)p * n, (unsigned)p);
+    }
+    __syncwarp();
+    if (LUTS) __syncthreads();  // LUT published
+
+    A cs[CPT], pd[CPT], pa[CPT];
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) cs[k] = pd[k] = pa[k] = 0.0;
+    A rho_n[CPT];
+    A ts_even = 0.0, ps_even = 0.0;
+    const int* gnext = glab + (size_t)(KP - 1) * n;  // the row the next refill fetches
+    int fetch_left = H - (KP - 1);                   // rows still to fetch
+    unsigned half = 0, parity = 0;                   // ring half (slots 4*half ..), its phase parity
+    const int* rsrc = rq + lane * CPT;
+    A* pxd = exD + w * H;
+    A* pxa = exA + w * H;
+    A* pxe = exE + w * H;
+    A* prow = s_rows + w;
+
+    // labels of the row in slot SL of ring half hf -> rho_n (waits for the slot's copy)
+    auto take = [&](auto sl_c, unsigned hf, unsigned par) {
+        constexpr int SL = decltype(sl_c)::value;
+        unsigned done = 0;
+        while (!done) {
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(done)
+                : "r"(bar_s + 8u * SL + 32u * hf), "r"(par)
+                : "memory");
+        }
+        const int4 Lv = *reinterpret_cast<const int4*>(rsrc + SL * W + hf * (4 * W));
+        rho_n[0] = LUTS ? lut[Lv.x] : __ldg(lut + (Lv.x < 0 ? R : Lv.x));
+        rho_n[1] = LUTS ? lut[Lv.y] : __ldg(lut + (Lv.y < 0 ? R : Lv.y));
+        rho_n[2] = LUTS ? lut[Lv.z] : __ldg(lut + (Lv.z < 0 ? R : Lv.z));
+        rho_n[3] = LUTS ? lut[Lv.w] : __ldg(lut + (Lv.w < 0 ? R : Lv.w));
+    };
+    take(std::integral_constant<int, 0>{}, 0u, 0u);
+
+    // one band row; RR = r & 3, `more`: a next row exists (its labels are taken one row early)
+    auto row = [&](auto rr_c, bool more, bool last_row) {
+        constexpr int RR = decltype(rr_c)::value;
+        A rho[CPT];
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
+        // the slot of row r-1 (read one row ago by every lane) takes row r + KP - 1
+        __syncwarp();
+        if (lane == 0 && fetch_left > 0) {
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            fetch(gnext, (unsigned)((RR + 3) & 3) + 4u * (RR == 0 ? (half ^ 1u) : half));
+        }
+        gnext += n;
+        --fetch_left;
+        if (more) {
+            if constexpr (RR == 3) take(std::integral_constant<int, 0>{}, half ^ 1u, half ? parity ^ 1u : parity);
+            else take(std::integral_constant<int, RR + 1>{}, half, parity);
+        }
+        A ts = 0.0;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) ts += rho[k];
+        A left = __shfl_up_sync(FULL, pd[CPT - 1], 1);
+        A right = __shfl_down_sync(FULL, pa[0], 1);
+        if (lane == 0) left = 0.0;    // partials restart at the slice edge
+        if (lane == 31) right = 0.0;
+#pragma unroll
+        for (int k = CPT - 1; k >= 0; --k) pd[k] = rho[k] + (k == 0 ? left : pd[k - 1]);
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) pa[k] = rho[k] + (k == CPT - 1 ? right : pa[k + 1]);
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) cs[k] += rho[k];
+        if (lane == 31) pxd[RR] = pd[CPT - 1];  // diagonal leaving the slice's right edge
+        if (lane == 0) pxa[RR] = pa[0];         // anti-diagonal leaving the slice's left edge
+        A ps = 0.0;
+#pragma unroll
+        for (int k = 0; k < CPT; ++k) ps += pd[k];
+        // slice row total and E1, two rows per butterfly (see k_sat1w)
+        if ((RR & 1) == 0 && !last_row) {
+            ts_even = ts;
+            ps_even = ps;
+        } else {
+            constexpr bool odd = (RR & 1) != 0;
+            const bool up = (lane & 16) != 0, qp = (lane & 8) != 0;
+            A kt, kp;
+            if (odd) {
+                kt = (up ? ts : ts_even) + __shfl_xor_sync(FULL, up ? ts_even : ts, 16);
+                kp = (up ? ps : ps_even) + __shfl_xor_sync(FULL, up ? ps_even : ps, 16);
+            } else {  // odd band height: the last row alone (both half-warps hold it)
+                kt = ts + __shfl_xor_sync(FULL, ts, 16);
+                kp = ps + __shfl_xor_sync(FULL, ps, 16);
+            }
+            A v = (qp ? kp : kt) + __shfl_xor_sync(FULL, qp ? kt : kp, 8);
+#pragma unroll
+            for (int o = 4; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+            constexpr int R0 = odd ? RR - 1 : RR;
+            if (lane == 0) prow[R0 * NW] = v;
+            if (lane == 8) pxe[R0] = v;
+            if (odd && lane == 16) prow[RR * NW] = v;
+            if (odd && lane == 24) pxe[RR] = v;
+        }
+    };
+    int r = 0;
+    for (; r + 4 <= H; r += 4) {
+        const bool more = r + 4 < H;
+        row(std::integral_constant<int, 0>{}, true, false);
+        row(std::integral_constant<int, 1>{}, true, false);
+        row(std::integral_constant<int, 2>{}, true, false);
+        row(std::integral_constant<int, 3>{}, more, false);
+        pxd += 4; pxa += 4; pxe += 4; prow += 4 * NW;
+        if (half) parity ^= 1u;
+        half ^= 1u;
+    }
+    if (r < H) {  // band heights 1 and 2
+        row(std::integral_constant<int, 0>{}, r + 1 < H, r + 1 == H);
+        if (r + 1 < H) row(std::integral_constant<int, 1>{}, r + 2 < H, r + 2 == H);
+        if (r + 2 < H) row(std::integral_constant<int, 2>{}, false, true);
+    }
+    __syncthreads();  // exits, row partials published; ring and LUT free (dg / ad alias them)
+    // band-bottom entries + the neighbour slice's part of each crossing diagonal
+    double csum = 0.0;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        const int x = x0 + k;
+        const int xi = x - c0;                       // column inside the slice
+        A vd = pd[k], va = pa[k];
+        if (w > 0 && xi <= H - 2) vd += exD[(w - 1) * H + (H - 2 - xi)];
+        const int xr = W - 1 - xi;                   // columns to the slice's right edge
+        if (w < NW - 1 && xr <= H - 2) va += exA[(w + 1) * H + (H - 2 - xr)];
+        dg[x] = vd;
+        ad[H - 1 + x] = va;
+        csum += cs[k];
+    }
+    // diagonals leaving the texture's right edge / anti-diagonals leaving its left edge (j < jb)
+    if (t < H - 1) {
+        dg[n - 1 - (jt + t) + jb] = exD[(NW - 1) * H + t];
+        ad[t] = exA[t];
+    }
+    double tot;
+    double run = block_excl_scan(csum, s_red, &tot);  // (its barriers also publish dg/ad)
+    double* tab = D.tab + bb * 4 * NW * H;
+    if (t < H) {  // row totals in float64, warp order
+        double s = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) {
+            tab[q * H + t] = s;  // off(t, q): the slice totals left of slice q
+            s += s_rows[t * NW + q];
+        }
+        D.rt[(size_t)b * n + jt + t] = s;
+    }
+    for (int i = t; i < NW * H; i += NT) {
+        tab[NW * H + i] = exE[i];
+        tab[2 * NW * H + i] = exD[i];
+        tab[3 * NW * H + i] = exA[i];
+    }
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) {
+        run += cs[k];
+        D.cs[bb * n + x0 + k] = run;
+    }
+    block_prefix_smem<A>(dg, D.dgc + bb * L, L, s_red);
+    block_prefix_smem<A>(ad, D.adc + bb * L, L, s_red);
 }
 
 }  // namespace det
