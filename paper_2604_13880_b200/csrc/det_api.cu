@@ -174,8 +174,11 @@ struct det_ctx {
     bool uniq_adv = true;
     bool ua_ok = false;
     int n_uniq = 0;
-    DVec<int> uq_row0, uq_off, uq_rows;
-    std::vector<int> h_uq_off, h_uq_rows, h_uq_row0;
+    DVec<int> uq_row0, uq_off, uq_rows, row_uniq, uq_flag;
+    DVec<double2> upos, ubest;  // unique-vertex state of the graph iterations (see k_uq_gather)
+    bool uq_state = true;       // DET_UQ_STATE=0: the graph iterations advect the rows (k_advect_uniq64)
+    bool g_uqs = false;
+    std::vector<int> h_uq_off, h_uq_rows, h_uq_row0, h_row_uniq;
     std::vector<double> h_xy_prev;  // the rows the unique-vertex table was built from
     bool g_ua = false;
     int g_nuniq = 0;
@@ -213,6 +216,7 @@ static Topo make_topo(det_ctx* c) {
     t.region_rank = c->region_rank.p;
     t.rank_region = c->rank_region.p;
     t.row_next = c->row_next.p;
+    t.row_uniq = c->row_uniq.p;
     return t;
 }
 
@@ -222,6 +226,7 @@ static Bufs make_bufs(det_ctx* c) {
     d.B = c->B; d.n = c->n; d.k = c->k; d.cap = c->cap; d.H = c->H; d.nb = c->nb;
     d.nn = (size_t)c->n * c->n;
     d.pos0 = c->pos0.p; d.best = c->best.p;
+    d.upos = c->upos.p; d.ubest = c->ubest.p; d.uq_flag = c->uq_flag.p; d.n_uniq = c->n_uniq;
     d.labels = c->labels.p; d.cnt_acc = c->cnt_acc.p; d.cnt_state = c->cnt_state.p;
     d.spans = c->spans.p; d.rowcnt = c->rowcnt.p; d.maxspan = c->maxspan.p; d.rowdone = c->rowdone.p;
     d.lut = c->lut.p; d.lutf = c->lutf.p; d.stats = c->stats.p; d.weights = c->weights.p; d.rerr = c->rerr.p;
@@ -254,6 +259,13 @@ static void smem_optin(F fn) {
 #ifndef DET_SAT3_CPT
 #define DET_SAT3_CPT 4  // k_sat3 columns per thread on the float32 path
 #endif
+static int skip_mask();
+// graph iterations on the unique-vertex state: float64, every shared vertex bit-identical in the
+// start rows, the plain (non-bitmap) raster
+static bool uqs_on(const det_ctx* c) {
+    return c->f64 && c->uniq_adv && c->ua_ok && c->uq_state && !c->bitmap_raster && !(skip_mask() & 4);
+}
+
 // Diagnostics only (timing experiments, results invalid): DET_SKIP bit mask of iteration stages
 // left out of the captured graph -- 1 band sums + carries (k_sat1w, k_sat2p), 2 k_sat3,
 // 4 advect + raster (k_region), 8 paint + control step (k_row, k_ctrl).
@@ -444,7 +456,14 @@ static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, in
 
 // One iteration's advect + raster: the flat advect kernel then a raster-only k_region (float32
 // state), or k_region's fused advect phase.  Returns the number of kernels launched.
-static int launch_advect_raster(det_ctx* c, const Topo& T, const Bufs& D, int gate, int region_mode) {
+static int launch_advect_raster(det_ctx* c, const Topo& T, const Bufs& D, int gate, int region_mode, bool uqs = false) {
+    if (uqs) {  // unique-vertex state (inside a graph launch): coalesced advect, raster through row_uniq
+        k_advect_uniq64s<<<dim3((c->n_uniq + ADV_THREADS - 1) / ADV_THREADS, c->B), ADV_THREADS, 0, c->stream>>>(
+            T, D, gate, c->uq_off.p);
+        const dim3 g((c->R + RW_WARPS - 1) / RW_WARPS, c->B);
+        k_region<double, double, false, false, true><<<g, RW_WARPS * 32, 0, c->stream>>>(T, D, M_RASTER | M_POSTADV, gate, 0);
+        return 2;
+    }
     if (c->f64 && c->uniq_adv && c->ua_ok && (region_mode & M_ADVECT)) {
         k_advect_uniq64<<<dim3((c->n_uniq + ADV_THREADS * UQ_PT - 1) / (ADV_THREADS * UQ_PT), c->B), ADV_THREADS, 0,
                           c->stream>>>(
@@ -485,7 +504,7 @@ static void launch_row_ctrl(det_ctx* c, const Topo& T, const Bufs& D, int gate, 
     }
 }
 
-static void enqueue_iteration(det_ctx* c, int b0 = 0, int Bg = -1, cudaStream_t s = nullptr) {
+static void enqueue_iteration(det_ctx* c, int b0 = 0, int Bg = -1, cudaStream_t s = nullptr, int uqs = 0) {
     if (Bg < 0) Bg = c->B;
     cudaStream_t keep = c->stream;
     if (s) c->stream = s;
@@ -497,8 +516,12 @@ static void enqueue_iteration(det_ctx* c, int b0 = 0, int Bg = -1, cudaStream_t 
     SatSrc S;
     memset(&S, 0, sizeof(S));
     if ((skip_mask() & 3) != 3) launch_sat(c, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, c->f64 != 0, Bg);
-    if (!(skip_mask() & 4)) launch_advect_raster(c, T, D, G_ACTIVE, M_ADVECT | M_RASTER);
+    if (uqs & 1)  // first iteration of a graph launch: rows -> unique-vertex state
+        k_uq_gather<<<dim3(std::min((c->n_uniq + 255) / 256, 1024), Bg), 256, 0, c->stream>>>(T, D, G_ACTIVE, c->uq_row0.p);
+    if (!(skip_mask() & 4)) launch_advect_raster(c, T, D, G_ACTIVE, M_ADVECT | M_RASTER, uqs != 0);
     if (!(skip_mask() & 8)) launch_row_ctrl(c, T, D, G_ACTIVE, 0);
+    if (uqs & 4)  // last iteration of a graph launch: unique-vertex state -> rows (+ best rows)
+        k_uq_expand<<<dim3(std::min((c->n_rows + 255) / 256, 1024), Bg), 256, 0, c->stream>>>(T, D);
     c->B = Bsave;
     c->stream = keep;
 }
@@ -517,7 +540,7 @@ static int ensure_graph(det_ctx* c) {
         // re-capture only when a pointer, shape or the grouping the graph bakes in changed
         const Topo t = make_topo(c);
         const Bufs d = make_bufs(c);
-        if (c->g_valid && c->g_groups == c->groups && c->g_ua == (c->uniq_adv && c->ua_ok) &&
+        if (c->g_valid && c->g_groups == c->groups && c->g_ua == (c->uniq_adv && c->ua_ok) && c->g_uqs == uqs_on(c) &&
             c->g_nuniq == c->n_uniq && c->g_uq == c->uq_rows.p && c->g_uq0 == c->uq_row0.p &&
             !memcmp(&t, &c->g_topo, sizeof(t)) &&
             !memcmp(&d, &c->g_bufs, sizeof(d)))
@@ -526,6 +549,7 @@ static int ensure_graph(det_ctx* c) {
         c->g_bufs = d;
         c->g_groups = c->groups;
         c->g_ua = c->uniq_adv && c->ua_ok;
+        c->g_uqs = uqs_on(c);
         c->g_nuniq = c->n_uniq;
         c->g_uq = c->uq_rows.p;
         c->g_uq0 = c->uq_row0.p;
@@ -547,7 +571,9 @@ static int ensure_graph(det_ctx* c) {
         const int b0 = (int)((long long)c->B * g / G), b1 = (int)((long long)c->B * (g + 1) / G);
         cudaStream_t s = c->gstreams[g];
         CK(cudaStreamWaitEvent(s, fork, 0));
-        for (int i = 0; i < kGraphIters; ++i) enqueue_iteration(c, b0, b1 - b0, s);
+        const bool uqs = uqs_on(c);
+        for (int i = 0; i < kGraphIters; ++i)
+            enqueue_iteration(c, b0, b1 - b0, s, uqs ? (2 | (i == 0 ? 1 : 0) | (i == kGraphIters - 1 ? 4 : 0)) : 0);
         CK(cudaEventRecord(join[g], s));
         CK(cudaStreamWaitEvent(c->stream, join[g], 0));
     }
@@ -604,6 +630,12 @@ static int alloc_batch(det_ctx* ctx, int B) {
     CK(ctx->pos_init.alloc((size_t)B * ctx->n_rows));
     CK(ctx->pos0.alloc((size_t)B * ctx->n_rows));
     CK(ctx->best.alloc((size_t)B * ctx->n_rows));
+    if (ctx->f64) {
+        CK(ctx->upos.alloc((size_t)B * ctx->n_uniq));
+        CK(ctx->ubest.alloc((size_t)B * ctx->n_uniq));
+        CK(ctx->uq_flag.alloc(B));
+        CK(cudaMemsetAsync(ctx->uq_flag.p, 0, (size_t)B * sizeof(int), ctx->stream));
+    }
     if (!ctx->s64) CK(ctx->rows64.alloc((size_t)B * ctx->n_rows));
     CK(ctx->labels.alloc((size_t)B * nn));
     CK(ctx->cnt_acc.alloc((size_t)B * (ctx->R + 1)));
@@ -751,6 +783,7 @@ int det_ctx_create(int device, int k, int precision, det_ctx** out) {
     if (const char* e = getenv("DET_SAT1W")) ctx->sat1w = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SAT3W")) ctx->sat3w = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SAT3X")) ctx->sat3x = atoi(e) != 0;  // A/B switch (diagnostics)
+    if (const char* e = getenv("DET_UQ_STATE")) ctx->uq_state = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SAT1X")) ctx->sat1x = atoi(e) != 0;  // A/B switch (diagnostics)
     ctx->device = device;
     ctx->k = k;
@@ -884,6 +917,7 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
         ctx->h_uq_off = off;
         ctx->h_uq_rows = rows;
         ctx->h_uq_row0 = row0;
+        ctx->h_row_uniq = uid;
     }
     if (!same_rows) {  // (unchanged rows: the device tables still hold this map's)
         const int U = ctx->n_uniq;
@@ -896,6 +930,8 @@ int det_load_map(det_ctx* ctx, const double* xy, int n_rows, const int32_t* ring
         CK(copy_sync(ctx, ctx->uq_row0.p, row0.data(), (size_t)U * sizeof(int), cudaMemcpyHostToDevice));
         CK(copy_sync(ctx, ctx->uq_off.p, off.data(), (size_t)(U + 1) * sizeof(int), cudaMemcpyHostToDevice));
         CK(copy_sync(ctx, ctx->uq_rows.p, rows.data(), (size_t)n_rows * sizeof(int), cudaMemcpyHostToDevice));
+        CK(ctx->row_uniq.alloc(n_rows));
+        CK(copy_sync(ctx, ctx->row_uniq.p, ctx->h_row_uniq.data(), (size_t)n_rows * sizeof(int), cudaMemcpyHostToDevice));
     }
     ctx->ua_ok = false;
     {  // ring successor of every row: O(1) for regions with many rings (holes, islands)

@@ -58,6 +58,7 @@ struct Topo {
     const int* region_rank;   // R: rank of region in ascending region_id order
     const int* rank_region;   // R: inverse
     const int* row_next;      // n_rows: next row of the same ring (wraps) -- multi-ring regions
+    const int* row_uniq;      // n_rows: unique-vertex index of each row (unique-vertex state, k_region<.., UQ>)
 };
 
 struct Bufs {
@@ -68,6 +69,13 @@ struct Bufs {
     // float2 on the float32-field path (k_region<UT> reads them as Vec2<UT>)
     void* pos0;
     void* best;
+    // unique-vertex state of the float64 graph iterations (one double2 per unique vertex and cartogram;
+    // gathered from / expanded to the rows at the ends of each graph launch), its best copy, and a
+    // per-cartogram flag word: 2 = gathered by this launch, 1 = ubest written
+    double2* upos;
+    double2* ubest;
+    int* uq_flag;
+    int n_uniq;
     int* labels;
     int* cnt_acc;
     int* cnt_state;

@@ -198,7 +198,7 @@ __device__ __forceinline__ int warp_excl_scan_int(int v, int lane, int* total) {
 // UT: field element type (float / double); ST: vertex-state element type.  <float, float> is the
 // float32 path, <double, double> the float64 path, <float, double> the mixed path (float32 field,
 // float64 state and position update).
-template <typename UT, typename ST = UT, bool BM = false, bool ADV = true>
+template <typename UT, typename ST = UT, bool BM = false, bool ADV = true, bool UQ = false>
 #ifndef DET_RW_MINB
 #define DET_RW_MINB (32 / DET_RW_WARPS)  // 32 resident warps per SM (64 registers)
 #endif
@@ -263,7 +263,17 @@ __global__ void __launch_bounds__(RW_WARPS * 32, ADV ? (sizeof(ST) == 8 ? DET_RW
     const bool bestcopy = (mode & M_ADVECT) && sth.w != 0;
     PT* const pin = reinterpret_cast<PT*>((mode & (M_ADVECT | M_POSTADV)) || src == 0 ? D.pos0 : D.best) + ub;
     PT* const pout = pin;
-    const PT* gpos = pin;  // row positions for huge regions
+    // UQ (raster-only, float64): the rows' positions come from the unique-vertex state through the
+    // static row -> unique-vertex table (the rows themselves are stale inside a graph launch)
+    const double2* upos = UQ ? D.upos + (size_t)b * D.n_uniq : nullptr;
+    auto rowpos = [&](int v) -> PT {
+        if constexpr (UQ) {
+            const double2 q = upos[__ldg(T.row_uniq + v)];
+            return PT{(ST)q.x, (ST)q.y};
+        } else {
+            return pin[v];
+        }
+    };
     const UT* uf = reinterpret_cast<const UT*>(D.uf) + (size_t)b * D.nn * 2;
 
     // ---- phase A: advect every vertex row (Q rows in flight per lane); per-row scaled
@@ -301,7 +311,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, ADV ? (sizeof(ST) == 8 ? DET_RW
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             const int v = base + q * 32 + lane;
-            p[q] = v < row1 ? pin[v] : PT{0.5, 0.5};
+            p[q] = v < row1 ? rowpos(v) : PT{0.5, 0.5};
         }
         PT nq[Q];
         if (mode & M_ADVECT) {
@@ -465,7 +475,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, ADV ? (sizeof(ST) == 8 ? DET_RW
         __syncwarp();
         for (int e = row0 + lane; e < row1; e += 32) {
             const int en = __ldg(T.row_next + e);
-            double2 a = to_d2(gpos[e]), c = to_d2(gpos[en]);
+            double2 a = to_d2(rowpos(e)), c = to_d2(rowpos(en));
             const int ja = min(max(ceil_to_int(__dsub_rn(__dmul_rn(a.y, nd), 0.5)), 0), n);
             const int jb2 = min(max(ceil_to_int(__dsub_rn(__dmul_rn(c.y, nd), 0.5)), 0), n);
             const int js = max(min(ja, jb2), jrow), je = min(max(ja, jb2), jrow + 1 + back);
@@ -585,7 +595,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, ADV ? (sizeof(ST) == 8 ? DET_RW
             auto run = [&](uint32_t ent) {
                 const int el = (int)(ent & 0xFFFFu), en = (int)(ent >> 16);
                 const int ja = (int)(sjn[el] & 0xFFFFu), jb2 = (int)(sjn[en] & 0xFFFFu);
-                emit(to_d2(gpos[row0 + el]), to_d2(gpos[row0 + en]), max(min(ja, jb2), w0), min(max(ja, jb2), w1 + back));
+                emit(to_d2(rowpos(row0 + el)), to_d2(rowpos(row0 + en)), max(min(ja, jb2), w0), min(max(ja, jb2), w1 + back));
             };
             for (int e0 = 0; e0 < nrows; e0 += 32) {
                 const int el = e0 + lane;
@@ -611,7 +621,7 @@ __global__ void __launch_bounds__(RW_WARPS * 32, ADV ? (sizeof(ST) == 8 ? DET_RW
         } else {
             for (int e = row0 + lane; e < row1; e += 32) {
                 const int en = next_row(e) - row0;
-                const double2 a = to_d2(gpos[e]), c = to_d2(gpos[row0 + en]);
+                const double2 a = to_d2(rowpos(e)), c = to_d2(rowpos(row0 + en));
                 const int ja = min(max(ceil_to_int(__dsub_rn(__dmul_rn(a.y, nd), 0.5)), 0), n);
                 const int jb2 = min(max(ceil_to_int(__dsub_rn(__dmul_rn(c.y, nd), 0.5)), 0), n);
                 const int js = max(min(ja, jb2), w0);  // scanlines j in [jlo, jhi) are crossed
@@ -854,6 +864,70 @@ __global__ void __launch_bounds__(ADV_THREADS) k_advect_uniq64(Topo T, Bufs D, i
             if (bestcopy) pbest[v] = p[q];
         }
     }
+    if (__any_sync(FULL, ncl != 0)) {  // clamping is rare (the map's border)
+        ncl = warp_sum(ncl);
+        if ((threadIdx.x & 31) == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
+    }
+}
+
+// Unique-vertex STATE (float64 graph iterations): inside a graph launch the cartogram's positions
+// live in D.upos, one double2 per unique vertex -- k_uq_gather fills it from the rows at the
+// launch's start, k_advect_uniq64s advects it in place (coalesced reads and writes, no row
+// scatter), k_region<.., UQ> rasterises through Topo::row_uniq, and k_uq_expand writes the rows
+// (and the best rows, when a best copy was taken) back at the launch's end.  Same arithmetic as
+// k_advect_uniq64: bit-identical rows.
+__global__ void __launch_bounds__(256) k_uq_gather(Topo T, Bufs D, int gate, const int* __restrict__ uq_row0) {
+    const int b = blockIdx.y + D.b0;
+    const bool open = gate_open(D.st + b, gate);
+    if (blockIdx.x == 0 && threadIdx.x == 0) D.uq_flag[b] = open ? 2 : 0;
+    if (!open) return;
+    const double2* pin = reinterpret_cast<const double2*>(D.pos0) + (size_t)b * T.n_rows;
+    double2* up = D.upos + (size_t)b * D.n_uniq;
+    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < D.n_uniq; u += gridDim.x * blockDim.x)
+        up[u] = pin[uq_row0[u]];
+}
+
+__global__ void __launch_bounds__(256) k_uq_expand(Topo T, Bufs D) {
+    const int b = blockIdx.y + D.b0;
+    const int fl = D.uq_flag[b];
+    if (!(fl & 2)) return;
+    double2* pin = reinterpret_cast<double2*>(D.pos0) + (size_t)b * T.n_rows;
+    double2* pbest = reinterpret_cast<double2*>(D.best) + (size_t)b * T.n_rows;
+    const double2* up = D.upos + (size_t)b * D.n_uniq;
+    const double2* ub = D.ubest + (size_t)b * D.n_uniq;
+    const bool wb = (fl & 1) != 0;
+    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < T.n_rows; v += gridDim.x * blockDim.x) {
+        const int u = __ldg(T.row_uniq + v);
+        pin[v] = up[u];
+        if (wb) pbest[v] = ub[u];
+    }
+}
+
+__global__ void __launch_bounds__(ADV_THREADS) k_advect_uniq64s(Topo T, Bufs D, int gate, const int* __restrict__ uq_off) {
+    const int b = blockIdx.y + D.b0;
+    Carto* st = D.st + b;
+    if (!gate_open(st, gate)) return;
+    const int n = D.n, n_uniq = D.n_uniq;
+    double2* const up = D.upos + (size_t)b * n_uniq;  // advected in place
+    double2* __restrict__ ub = D.ubest + (size_t)b * n_uniq;
+    const bool bestcopy = st->best_pending != 0;
+    const double* uf = reinterpret_cast<const double*>(D.uf) + (size_t)b * D.nn * 2;
+    const int u = blockIdx.x * ADV_THREADS + threadIdx.x;
+    const bool in = u < n_uniq;
+    const int o0 = in ? uq_off[u] : 0, o1 = in ? uq_off[u + 1] : 0;
+    const double2 p = in ? up[u] : make_double2(0.5, 0.5);
+    const Tap tp = field_tap(n, p.x, p.y);
+    const Texels<double> tx = field_load<double, Tap>(uf, tp);
+    const double2 sm = field_blend<double, Tap>(tx, tp);
+    const double mx = p.x + sm.x, my = p.y + sm.y;
+    const double cx = mx < 0.0 ? 0.0 : (mx > 1.0 ? 1.0 : mx);  // np.clip (no NaNs here)
+    const double cy = my < 0.0 ? 0.0 : (my > 1.0 ? 1.0 : my);
+    int ncl = ((cx != mx) + (cy != my)) * (o1 - o0);  // counted once per row (displacement.py:229-238)
+    if (in) {
+        up[u] = make_double2(cx, cy);
+        if (bestcopy) ub[u] = p;
+    }
+    if (bestcopy && blockIdx.x == 0 && threadIdx.x == 0) D.uq_flag[b] = 3;
     if (__any_sync(FULL, ncl != 0)) {  // clamping is rare (the map's border)
         ncl = warp_sum(ncl);
         if ((threadIdx.x & 31) == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
