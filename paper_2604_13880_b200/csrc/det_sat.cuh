@@ -1742,7 +1742,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT1X_MINB : 1)) k_sat1x(
 #pragma unroll
     for (int k = 0; k < CPT; ++k) cs[k] = pd[k] = pa[k] = 0.0;
     A rho_n[CPT];
-    A ts_even = 0.0, ps_even = 0.0;
     const int* gnext = glab + (size_t)(KP - 1) * n;  // the row the next refill fetches
     int fetch_left = H - (KP - 1);                   // rows still to fetch
     unsigned half = 0, parity = 0;                   // ring half (slots 4*half ..), its phase parity
@@ -1771,8 +1770,34 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT1X_MINB : 1)) k_sat1x(
     };
     take(std::integral_constant<int, 0>{}, 0u, 0u);
 
-    // one band row; RR = r & 3, `more`: a next row exists (its labels are taken one row early)
-    auto row = [&](auto rr_c, bool more, bool last_row) {
+    // Slice row totals and E1 (the slice's sum of a row's diagonal partials) of four rows in one
+    // butterfly: the half-warps take rows {0,1} / {2,3}, the quarter-warps one row of the pair, the
+    // eighth-warps the total / E1, then two steps inside each group of four lanes -- 9 double
+    // shuffles in 5 dependent steps for 8 sums (lanes 0, 4, .., 28 end with them).  Issued inside the
+    // NEXT group's first row, so its shuffle chain overlaps that row's arithmetic.
+    A tsv[4], psv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tsv[q] = psv[q] = 0.0;
+    auto flush4 = [&](A* prow_g, A* pxe_g, int nv) {
+        const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0, b2 = (lane & 4) != 0;
+        const A k0t = (b4 ? tsv[2] : tsv[0]) + __shfl_xor_sync(FULL, b4 ? tsv[0] : tsv[2], 16);
+        const A k1t = (b4 ? tsv[3] : tsv[1]) + __shfl_xor_sync(FULL, b4 ? tsv[1] : tsv[3], 16);
+        const A k0p = (b4 ? psv[2] : psv[0]) + __shfl_xor_sync(FULL, b4 ? psv[0] : psv[2], 16);
+        const A k1p = (b4 ? psv[3] : psv[1]) + __shfl_xor_sync(FULL, b4 ? psv[1] : psv[3], 16);
+        const A mt = (b3 ? k1t : k0t) + __shfl_xor_sync(FULL, b3 ? k0t : k1t, 8);
+        const A mp = (b3 ? k1p : k0p) + __shfl_xor_sync(FULL, b3 ? k0p : k1p, 8);
+        A v = (b2 ? mp : mt) + __shfl_xor_sync(FULL, b2 ? mt : mp, 4);
+        v += __shfl_xor_sync(FULL, v, 2);
+        v += __shfl_xor_sync(FULL, v, 1);
+        const int row = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
+        if ((lane & 3) == 0 && row < nv) {
+            if (b2) pxe_g[row] = v;
+            else prow_g[row * NW] = v;
+        }
+    };
+    // one band row; RR = r & 3, `more`: a next row exists (its labels are taken one row early);
+    // `flush`: the previous group's four row sums are reduced here
+    auto row = [&](auto rr_c, bool more, bool flush) {
         constexpr int RR = decltype(rr_c)::value;
         A rho[CPT];
 #pragma unroll
@@ -1789,6 +1814,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT1X_MINB : 1)) k_sat1x(
             if constexpr (RR == 3) take(std::integral_constant<int, 0>{}, half ^ 1u, half ? parity ^ 1u : parity);
             else take(std::integral_constant<int, RR + 1>{}, half, parity);
         }
+        if (RR == 0 && flush) flush4(prow - 4 * NW, pxe - 4, 4);
         A ts = 0.0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) ts += rho[k];
@@ -1807,35 +1833,13 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT1X_MINB : 1)) k_sat1x(
         A ps = 0.0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) ps += pd[k];
-        // slice row total and E1, two rows per butterfly (see k_sat1w)
-        if ((RR & 1) == 0 && !last_row) {
-            ts_even = ts;
-            ps_even = ps;
-        } else {
-            constexpr bool odd = (RR & 1) != 0;
-            const bool up = (lane & 16) != 0, qp = (lane & 8) != 0;
-            A kt, kp;
-            if (odd) {
-                kt = (up ? ts : ts_even) + __shfl_xor_sync(FULL, up ? ts_even : ts, 16);
-                kp = (up ? ps : ps_even) + __shfl_xor_sync(FULL, up ? ps_even : ps, 16);
-            } else {  // odd band height: the last row alone (both half-warps hold it)
-                kt = ts + __shfl_xor_sync(FULL, ts, 16);
-                kp = ps + __shfl_xor_sync(FULL, ps, 16);
-            }
-            A v = (qp ? kp : kt) + __shfl_xor_sync(FULL, qp ? kt : kp, 8);
-#pragma unroll
-            for (int o = 4; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-            constexpr int R0 = odd ? RR - 1 : RR;
-            if (lane == 0) prow[R0 * NW] = v;
-            if (lane == 8) pxe[R0] = v;
-            if (odd && lane == 16) prow[RR * NW] = v;
-            if (odd && lane == 24) pxe[RR] = v;
-        }
+        tsv[RR] = ts;
+        psv[RR] = ps;
     };
     int r = 0;
     for (; r + 4 <= H; r += 4) {
         const bool more = r + 4 < H;
-        row(std::integral_constant<int, 0>{}, true, false);
+        row(std::integral_constant<int, 0>{}, true, r > 0);
         row(std::integral_constant<int, 1>{}, true, false);
         row(std::integral_constant<int, 2>{}, true, false);
         row(std::integral_constant<int, 3>{}, more, false);
@@ -1843,10 +1847,12 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT1X_MINB : 1)) k_sat1x(
         if (half) parity ^= 1u;
         half ^= 1u;
     }
-    if (r < H) {  // band heights 1 and 2
-        row(std::integral_constant<int, 0>{}, r + 1 < H, r + 1 == H);
-        if (r + 1 < H) row(std::integral_constant<int, 1>{}, r + 2 < H, r + 2 == H);
-        if (r + 2 < H) row(std::integral_constant<int, 2>{}, false, true);
+    if (r > 0) {
+        flush4(prow - 4 * NW, pxe - 4, 4);
+    } else {  // band heights 1 and 2
+        row(std::integral_constant<int, 0>{}, H > 1, false);
+        if (H > 1) row(std::integral_constant<int, 1>{}, false, false);
+        flush4(prow, pxe, H);
     }
     __syncthreads();  // exits, row partials published; ring and LUT free (dg / ad alias them)
     // band-bottom entries + the neighbour slice's part of each crossing diagonal
