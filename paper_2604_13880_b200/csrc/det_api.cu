@@ -1243,11 +1243,16 @@ int det_bench_kernel_times(det_ctx* ctx, int iters, float* ms_out) {
     const Bufs D = make_bufs(ctx);
     SatSrc S;
     memset(&S, 0, sizeof(S));
+    // the graph's own kernels: on the unique-vertex state when the graph runs on it (gathered before
+    // and expanded after the timed iterations, as at the ends of a graph launch)
+    const bool uqs = uqs_on(ctx) && region_mode == (M_ADVECT | M_RASTER);
+    if (uqs)
+        k_uq_gather<<<dim3(std::min((ctx->n_uniq + 255) / 256, 1024), ctx->B), 256, 0, ctx->stream>>>(T, D, G_ACTIVE, ctx->uq_row0.p);
     for (int it = 0; it < iters; ++it) {
         CK(cudaEventRecord(ev[0], ctx->stream));
         launch_sat(ctx, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, ctx->f64 != 0, ctx->B);
         CK(cudaEventRecord(ev[1], ctx->stream));
-        launch_advect_raster(ctx, T, D, G_ACTIVE, region_mode);
+        launch_advect_raster(ctx, T, D, G_ACTIVE, region_mode, uqs);
         CK(cudaEventRecord(ev[2], ctx->stream));
         launch_row_ctrl(ctx, T, D, G_ACTIVE, row_mode);  // includes the control step
         CK(cudaEventRecord(ev[3], ctx->stream));
@@ -1259,6 +1264,8 @@ int det_bench_kernel_times(det_ctx* ctx, int iters, float* ms_out) {
             ms_out[q] += t;
         }
     }
+    if (uqs) k_uq_expand<<<dim3(std::min((ctx->n_rows + 255) / 256, 1024), ctx->B), 256, 0, ctx->stream>>>(T, D);
+    CK(cudaGetLastError());
     for (int i = 0; i < 5; ++i) cudaEventDestroy(ev[i]);
     return DET_OK;
 }

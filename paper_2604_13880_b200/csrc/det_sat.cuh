@@ -1402,7 +1402,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3w
 // The per-pixel arithmetic is k_sat3w's, in the same operation order (the edge prefixes are summed
 // in warp-scan order instead of row order).  CPT = 4 only (KP = 4 ring slots = the unroll).
 #ifndef DET_SAT3X_PIPE
-#define DET_SAT3X_PIPE 0  // 1: the next row's labels, LUT reads and row-prefix scan issued ahead of this row's field arithmetic (spills at 128 registers: 49.6k vs 51.6k it/s)
+#define DET_SAT3X_PIPE 0  // 2: the next row's row-prefix scan issued ahead of this row's field arithmetic, densities re-read (54.3k vs 55.4k it/s); 1: the next row's labels, LUT reads and row-prefix scan issued ahead of this row's field arithmetic (spills at 128 registers: 49.6k vs 51.6k it/s)
 #endif
 template <int NT, bool LUTS>
 __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x(Topo T, Bufs D, int gate) {
@@ -1503,7 +1503,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x
     const unsigned rq_s = (unsigned)__cvta_generic_to_shared(rq);
     const unsigned bar_s = (unsigned)__cvta_generic_to_shared(s_bar + wl * KP);
     const int* glab = D.labels + (size_t)b * D.nn + (size_t)jt * n + c0;  // row jt of the slice
-    constexpr int PF = DET_SAT3X_PIPE ? KP : KP - 1;  // rows fetched by the prologue
+    constexpr int PF = DET_SAT3X_PIPE == 1 ? KP : KP - 1;  // rows fetched by the prologue
     if (lane == 0) {
 #pragma unroll
         for (int s = 0; s < KP; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar_s + 8u * s));
@@ -1560,7 +1560,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x
         __syncwarp();
         if (lane == 0 && rows_left > PF) {
             // PIPE: row r's slot (read one row ago) takes row r + 4; else row r-1's slot takes row r + 3
-            constexpr int SL = DET_SAT3X_PIPE ? RR : ((RR + KP - 1) & 3);
+            constexpr int SL = DET_SAT3X_PIPE == 1 ? RR : ((RR + KP - 1) & 3);
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar_s + 8u * SL), "r"(W * 4)
                          : "memory");
@@ -1570,7 +1570,18 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x
         }
         gnext += n;
         A rho[CPT], pre;
-        if (DET_SAT3X_PIPE) {
+        if (DET_SAT3X_PIPE == 2) {
+            // the NEXT row's labels -> row-prefix scan first (only the prefix is carried over), then
+            // this row's densities re-read from its slot: the scan's shuffle chain overlaps this
+            // row's field arithmetic at the cost of one more label / LUT read per pixel
+            pre = pre_n;
+            if (rows_left > 1) take(std::integral_constant<int, (RR + 1) & 3>{}, RR == 3 ? parity ^ 1u : parity);
+            const int4 Lv = *reinterpret_cast<const int4*>(rsrc + RR * W);
+            rho[0] = LUTS ? lut[Lv.x] : lut[Lv.x < 0 ? R : Lv.x];
+            rho[1] = LUTS ? lut[Lv.y] : lut[Lv.y < 0 ? R : Lv.y];
+            rho[2] = LUTS ? lut[Lv.z] : lut[Lv.z < 0 ? R : Lv.z];
+            rho[3] = LUTS ? lut[Lv.w] : lut[Lv.w < 0 ? R : Lv.w];
+        } else if (DET_SAT3X_PIPE == 1) {
 #pragma unroll
             for (int k = 0; k < CPT; ++k) rho[k] = rho_n[k];
             pre = pre_n;
