@@ -45,6 +45,10 @@ constexpr int RW_WROWS = 128;    // texture rows per warp window
 #ifndef DET_RW_UNROLL
 #define DET_RW_UNROLL 2
 #endif
+#ifndef DET_RW_UNROLL_RO
+#define DET_RW_UNROLL_RO 5  // raster-only k_region (2: 55.5k, 3: 56.0k, 4: 56.25k, 5: 56.4k, 6: 56.4k, 8: 55.2k it/s)
+#endif
+constexpr int RW_UNROLL_RO = DET_RW_UNROLL_RO;
 constexpr int RW_UNROLL = DET_RW_UNROLL;  // vertex rows in flight per lane (2 measured best of 1-8)
 
 // Bilinear sample of the field (displacement.py:209-226): g = p*n - 0.5,
@@ -431,8 +435,10 @@ __global__ void __launch_bounds__(RW_WARPS * 32, ADV ? (sizeof(ST) == 8 ? DET_RW
     }
 #endif
     if (!done_a) {
+        // raster-only instantiations keep RW_UNROLL_RO rows in flight per lane (no advect state to hold)
+        constexpr int RU = ADV ? RW_UNROLL : RW_UNROLL_RO;
         int base = row0;
-        for (; base + 32 < row1; base += 32 * RW_UNROLL) chunk(std::integral_constant<int, RW_UNROLL>{}, base);
+        for (; base + 32 < row1; base += 32 * RU) chunk(std::integral_constant<int, RU>{}, base);
         if (base < row1) chunk(std::integral_constant<int, 1>{}, base);
     }
     if (mode & M_ADVECT) {
