@@ -4,7 +4,7 @@ Workload ("headline"): the 3000-region seeded Voronoi map with ~200k unique
 vertices (synthetic), 1024^2 texture, run as direct-mode time
 steps: every GPU holds a batch of B independent frames (statistics = a seeded
 lognormal random walk over time) and one bench "step" is one DET iteration of
-every frame in the batch (B = 64 by default: four 16-step random walks).  Inputs are device-resident before
+every frame in the batch (B = 296 by default: 37 eight-step random walks).  Inputs are device-resident before
 timing; the batch working set (~45 MB per frame with the float64 field) is larger than
 the 126 MB L2 for B >= 3.
 
@@ -34,7 +34,7 @@ sys.path.insert(0, ROOT)
 METRIC = "DET iterations/s at 1024\u00b2 texture, 200k vertices; time steps/s over 8 GPUs"  # BASELINE.json verbatim
 UNIT = "DET iterations/s"
 K_TEX = 10
-WALK_STEPS = 16  # time steps per random walk of the bench batch (see build_workload)
+WALK_STEPS = int(os.environ.get("DET_WALK_STEPS", "8"))  # time steps per random walk of the bench batch (see build_workload)
 
 
 def algorithmic_bytes_per_iteration(n: int, n_unique: int) -> float:
@@ -281,7 +281,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=64)
     ap.add_argument("--warmup", type=int, default=8)
-    ap.add_argument("--batch", type=int, default=64, help="frames per GPU (DESIGN.md §5: 16-128 swept)")
+    ap.add_argument("--batch", type=int, default=296, help="frames per GPU (DESIGN.md §5: 16-296 swept; 296 = two per SM)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--band", type=int, default=0, help="band height of the integral-image kernels (0 = auto)")
     ap.add_argument("--field", default="float64", choices=["float64", "mixed", "float32"])
