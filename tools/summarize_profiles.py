@@ -39,7 +39,7 @@ reps = args[2:]
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 PHASE = {"k_sat1": "integral_images", "k_sat2": "integral_images", "k_sat3": "integral_images",
          "k_sat1w": "integral_images", "k_sat2p": "integral_images", "k_sat3w": "integral_images",
-         "k_sat3x": "integral_images", "k_sat1x": "integral_images", "k_advect_uniq64": "region",
+         "k_sat3x": "integral_images", "k_sat1x": "integral_images", "k_advect_uniq64": "region", "k_advect_uniq64s": "region",
          "k_region": "region", "k_row": "row"}
 lines = [f"# ncu summary {tag}", "", "## Launch list (gpu__time_duration.sum, --clock-control none, serialised)", "",
          "| kernel | launches | mean (us) | share |", "|---|---|---|---|"]
