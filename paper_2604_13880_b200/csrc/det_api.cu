@@ -504,7 +504,8 @@ static void launch_row_ctrl(det_ctx* c, const Topo& T, const Bufs& D, int gate, 
     }
 }
 
-static void enqueue_iteration(det_ctx* c, int b0 = 0, int Bg = -1, cudaStream_t s = nullptr, int uqs = 0) {
+static void enqueue_iteration(det_ctx* c, int b0 = 0, int Bg = -1, cudaStream_t s = nullptr, int uqs = 0,
+                              cudaEvent_t after_sat = nullptr) {
     if (Bg < 0) Bg = c->B;
     cudaStream_t keep = c->stream;
     if (s) c->stream = s;
@@ -516,6 +517,7 @@ static void enqueue_iteration(det_ctx* c, int b0 = 0, int Bg = -1, cudaStream_t 
     SatSrc S;
     memset(&S, 0, sizeof(S));
     if ((skip_mask() & 3) != 3) launch_sat(c, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, c->f64 != 0, Bg);
+    if (after_sat) cudaEventRecord(after_sat, c->stream);  // (capture) the staggered neighbour branch starts here
     if (uqs & 1)  // first iteration of a graph launch: rows -> unique-vertex state
         k_uq_gather<<<dim3(std::min((c->n_uniq + 255) / 256, 1024), Bg), 256, 0, c->stream>>>(T, D, G_ACTIVE, c->uq_row0.p);
     if (!(skip_mask() & 4)) launch_advect_raster(c, T, D, G_ACTIVE, M_ADVECT | M_RASTER, uqs != 0);
@@ -564,6 +566,9 @@ static int ensure_graph(det_ctx* c) {
     cudaEvent_t fork, join[16];
     CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     for (int g = 0; g < G; ++g) CK(cudaEventCreateWithFlags(&join[g], cudaEventDisableTiming));
+    static const bool stagger = [] { const char* e = getenv("DET_STAGGER"); return e && atoi(e) != 0; }();
+    cudaEvent_t stag[16];
+    for (int g = 0; g < G; ++g) CK(cudaEventCreateWithFlags(&stag[g], cudaEventDisableTiming));
     cudaGraph_t graph;
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     CK(cudaEventRecord(fork, c->stream));
@@ -572,8 +577,14 @@ static int ensure_graph(det_ctx* c) {
         cudaStream_t s = c->gstreams[g];
         CK(cudaStreamWaitEvent(s, fork, 0));
         const bool uqs = uqs_on(c);
+        // DET_STAGGER=1 (experiment): odd branches start when their even neighbour has finished its
+        // first iteration's band kernels, so the two run out of phase (DRAM-bound kernels of one
+        // next to issue-bound kernels of the other)
+        const bool lead = stagger && (g % 2 == 0) && g + 1 < G;
+        if (stagger && (g % 2 == 1)) CK(cudaStreamWaitEvent(s, stag[g - 1], 0));
         for (int i = 0; i < kGraphIters; ++i)
-            enqueue_iteration(c, b0, b1 - b0, s, uqs ? (2 | (i == 0 ? 1 : 0) | (i == kGraphIters - 1 ? 4 : 0)) : 0);
+            enqueue_iteration(c, b0, b1 - b0, s, uqs ? (2 | (i == 0 ? 1 : 0) | (i == kGraphIters - 1 ? 4 : 0)) : 0,
+                              (lead && i == 0) ? stag[g] : nullptr);
         CK(cudaEventRecord(join[g], s));
         CK(cudaStreamWaitEvent(c->stream, join[g], 0));
     }
@@ -582,6 +593,7 @@ static int ensure_graph(det_ctx* c) {
     cudaGraphDestroy(graph);
     cudaEventDestroy(fork);
     for (int g = 0; g < G; ++g) cudaEventDestroy(join[g]);
+    for (int g = 0; g < G; ++g) cudaEventDestroy(stag[g]);
     CK(e);
     c->g_valid = true;
     return DET_OK;

@@ -1667,7 +1667,11 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x
             uy[k] = (vy + at) * inv2m;
         }
 #pragma unroll
-        for (int k = 0; k < CPT; k += 2) st_global_v4f64(o + 2 * k, ux[k], uy[k], ux[k + 1], uy[k + 1]);
+        for (int k = 0; k < CPT; k += 2)
+#ifdef DET_SAT3X_SKIPTEST  // timing experiment only (invalid field): half of the sector stores dropped
+            if (((RR + lane + (k >> 1)) & 1) == 0)
+#endif
+            st_global_v4f64(o + 2 * k, ux[k], uy[k], ux[k + 1], uy[k + 1]);
         o += ostep;
         yc += inv_n;
 #pragma unroll

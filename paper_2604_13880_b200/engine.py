@@ -20,6 +20,7 @@ float64 expressions so the target weights are bit-identical.
 from __future__ import annotations
 
 import functools
+from collections.abc import Sequence as _Sequence
 import itertools
 import os
 import time
@@ -66,6 +67,54 @@ def trace_records(tr: np.ndarray, it_off: int = 0) -> tuple:
         rec.__dict__.update(iteration=int(it) + it_off, epsilon=eps, xi=xi, millis=ms)
         out.append(rec)
     return tuple(out)
+
+
+class TraceView(_Sequence):
+    """A run's trace as a read-only sequence of IterationRecord (engine.py:38-43, 189-195) that
+    builds the records on first access: a 296-frame batch returns 59k records, most of them never
+    read.  Length is known without building; pickles and compares as the plain tuple."""
+
+    __slots__ = ("_rows", "_off", "_recs")
+
+    def __init__(self, rows: np.ndarray, it_off: int = 0):
+        self._rows, self._off, self._recs = rows, it_off, None
+
+    def _mat(self) -> tuple:
+        if self._recs is None:
+            self._recs = trace_records(self._rows, self._off)
+            self._rows = None
+        return self._recs
+
+    def __len__(self):
+        return len(self._rows) if self._recs is None else len(self._recs)
+
+    def __getitem__(self, i):
+        return self._mat()[i]
+
+    def __iter__(self):
+        return iter(self._mat())
+
+    def __eq__(self, other):
+        if isinstance(other, TraceView):
+            other = other._mat()
+        return self._mat() == (tuple(other) if isinstance(other, list) else other)
+
+    def __ne__(self, other):
+        return not self.__eq__(other)
+
+    __hash__ = None
+
+    def __repr__(self):
+        return repr(self._mat())
+
+    def __add__(self, other):
+        return self._mat() + tuple(other)
+
+    def __radd__(self, other):
+        return tuple(other) + self._mat()
+
+    def __reduce__(self):
+        return (tuple, (self._mat(),))
 
 
 @dataclass(frozen=True)
@@ -265,7 +314,7 @@ class BatchEngine:
         else:
             tr = fetched[3][: r.trace_len]
             verts, counts, rerr = verts_out, fetched[1], fetched[2]
-        records = trace_records(tr, it_off)
+        records = TraceView(np.array(tr, dtype=np.float64), it_off)  # (copy: the batch block is reused)
         clamps = int(r.clamp_events) + (cl_off if r.stop_reason != 2 else 0)
         result_map = deferred_rebuild(self.initial_map, verts, self.statistics[b], self._sizes)
         lazy = _LazyLabels(ctx, b, getattr(ctx, "generation", None), result_map, self.k, self.device)

@@ -161,3 +161,22 @@ def test_raster_debug_dumps(tmp_path):
     write_raw_f64(tmp_path / "a.f64", a)
     assert np.array_equal(np.fromfile(tmp_path / "a.f32", dtype="<f4"), a.ravel().astype(np.float32))
     assert np.array_equal(np.fromfile(tmp_path / "a.f64", dtype="<f8"), a.ravel())
+
+
+def test_trace_view_is_a_lazy_tuple_of_records():
+    """RunResult.trace builds its IterationRecord objects on first access (engine.py:38-43 records,
+    :189-195 bookkeeping): same length, items, equality and pickle as the plain tuple."""
+    import pickle
+
+    from paper_2604_13880_b200.engine import TraceView, trace_records
+
+    tr = np.random.default_rng(0).random((7, 4))
+    tr[:, 0] = np.arange(7)
+    ref = trace_records(tr, 5)
+    v = TraceView(tr.copy(), 5)
+    assert len(v) == 7 and v._recs is None            # the length needs no records
+    assert v[0] == ref[0] and v[-1].iteration == 11
+    assert v == ref and list(v) == list(ref) and v == TraceView(tr.copy(), 5)
+    w = pickle.loads(pickle.dumps(v))
+    assert isinstance(w, tuple) and w == ref
+    assert [t.xi for t in v] == [t.xi for t in ref]
