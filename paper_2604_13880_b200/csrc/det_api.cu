@@ -46,6 +46,10 @@ struct GuardAlloc {
     int device;
 };
 static std::mutex g_guard_mu;
+// guard mode only: its allocations poison memory through the legacy stream and synchronise the
+// device, which would invalidate a graph capture running on another thread (one context per
+// steering session) -- captures and guard allocations exclude each other
+static std::recursive_mutex g_guard_capture_mu;
 static std::vector<GuardAlloc> g_guard_live;
 static long long g_guard_bad_freed = 0;  // corrupted guards found when a buffer was released
 static bool guard_mode() {
@@ -69,6 +73,7 @@ static bool guard_intact(const GuardAlloc& g) {
 }
 static cudaError_t dev_alloc(void** out, size_t bytes) {
     if (!guard_mode()) return cudaMalloc(out, bytes);
+    std::lock_guard<std::recursive_mutex> cap(g_guard_capture_mu);
     char* raw = nullptr;
     cudaError_t e = cudaMalloc(&raw, bytes + 2 * kGuard);
     if (e != cudaSuccess) return e;
@@ -89,6 +94,7 @@ static void dev_free(void* p) {
         return;
     }
     char* raw = static_cast<char*>(p) - kGuard;
+    std::lock_guard<std::recursive_mutex> cap(g_guard_capture_mu);
     std::lock_guard<std::mutex> lk(g_guard_mu);
     for (size_t i = 0; i < g_guard_live.size(); ++i) {
         if (g_guard_live[i].raw != raw) continue;
@@ -570,6 +576,8 @@ static int ensure_graph(det_ctx* c) {
     cudaEvent_t stag[16];
     for (int g = 0; g < G; ++g) CK(cudaEventCreateWithFlags(&stag[g], cudaEventDisableTiming));
     cudaGraph_t graph;
+    std::unique_lock<std::recursive_mutex> cap(g_guard_capture_mu, std::defer_lock);
+    if (guard_mode()) cap.lock();  // (released when this function returns, after EndCapture)
     CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
     CK(cudaEventRecord(fork, c->stream));
     for (int g = 0; g < G; ++g) {
@@ -742,6 +750,7 @@ int det_abi_version(void) { return 1; }
 
 int det_debug_guard_check(long long* n_live, long long* n_bad) {
     if (!n_live || !n_bad) return DET_E_ARG;
+    std::lock_guard<std::recursive_mutex> cap(g_guard_capture_mu);
     std::lock_guard<std::mutex> lk(g_guard_mu);
     long long bad = g_guard_bad_freed;
     for (const GuardAlloc& g : g_guard_live) bad += guard_intact(g) ? 0 : 1;

@@ -1763,7 +1763,6 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT1X_MINB : 1)) k_sat1x(
     const int* rsrc = rq + lane * CPT;
     A* pxd = exD + w * H;
     A* pxa = exA + w * H;
-    A* pxe = exE + w * H;
     A* prow = s_rows + w;
 
     // labels of the row in slot SL of ring half hf -> rho_n (waits for the slot's copy)
@@ -1785,30 +1784,27 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT1X_MINB : 1)) k_sat1x(
     };
     take(std::integral_constant<int, 0>{}, 0u, 0u);
 
-    // Slice row totals and E1 (the slice's sum of a row's diagonal partials) of four rows in one
-    // butterfly: the half-warps take rows {0,1} / {2,3}, the quarter-warps one row of the pair, the
-    // eighth-warps the total / E1, then two steps inside each group of four lanes -- 9 double
-    // shuffles in 5 dependent steps for 8 sums (lanes 0, 4, .., 28 end with them).  Issued inside the
-    // NEXT group's first row, so its shuffle chain overlaps that row's arithmetic.
-    A tsv[4], psv[4];
+    // Slice row totals of four rows in one butterfly: the half-warps take rows {0,1} / {2,3}, the
+    // quarter-warps one row of the pair, then three steps inside each group of eight lanes -- 6
+    // double shuffles in 5 dependent steps for 4 sums (lanes 0, 8, 16, 24 end with them).  Issued
+    // inside the NEXT group's first row, so its shuffle chain overlaps that row's arithmetic.
+    // E1 (the slice's sum of a row's diagonal partials) needs no per-lane work: summing the
+    // recurrence pd(r, x) = rho(r, x) + pd(r-1, x-1) over the slice gives
+    //   E1(r) = total(r) + E1(r-1) - pd(r-1, last column) = sum_{r'<=r} total(r') - sum_{r'<r} exitD(r'),
+    // two warp scans per slice at the band end.
+    A tsv[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) tsv[q] = psv[q] = 0.0;
-    auto flush4 = [&](A* prow_g, A* pxe_g, int nv) {
-        const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0, b2 = (lane & 4) != 0;
-        const A k0t = (b4 ? tsv[2] : tsv[0]) + __shfl_xor_sync(FULL, b4 ? tsv[0] : tsv[2], 16);
-        const A k1t = (b4 ? tsv[3] : tsv[1]) + __shfl_xor_sync(FULL, b4 ? tsv[1] : tsv[3], 16);
-        const A k0p = (b4 ? psv[2] : psv[0]) + __shfl_xor_sync(FULL, b4 ? psv[0] : psv[2], 16);
-        const A k1p = (b4 ? psv[3] : psv[1]) + __shfl_xor_sync(FULL, b4 ? psv[1] : psv[3], 16);
-        const A mt = (b3 ? k1t : k0t) + __shfl_xor_sync(FULL, b3 ? k0t : k1t, 8);
-        const A mp = (b3 ? k1p : k0p) + __shfl_xor_sync(FULL, b3 ? k0p : k1p, 8);
-        A v = (b2 ? mp : mt) + __shfl_xor_sync(FULL, b2 ? mt : mp, 4);
+    for (int q = 0; q < 4; ++q) tsv[q] = 0.0;
+    auto flush4 = [&](A* prow_g, int nv) {
+        const bool b4 = (lane & 16) != 0, b3 = (lane & 8) != 0;
+        const A k0 = (b4 ? tsv[2] : tsv[0]) + __shfl_xor_sync(FULL, b4 ? tsv[0] : tsv[2], 16);
+        const A k1 = (b4 ? tsv[3] : tsv[1]) + __shfl_xor_sync(FULL, b4 ? tsv[1] : tsv[3], 16);
+        A v = (b3 ? k1 : k0) + __shfl_xor_sync(FULL, b3 ? k0 : k1, 8);
+        v += __shfl_xor_sync(FULL, v, 4);
         v += __shfl_xor_sync(FULL, v, 2);
         v += __shfl_xor_sync(FULL, v, 1);
         const int row = ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1);
-        if ((lane & 3) == 0 && row < nv) {
-            if (b2) pxe_g[row] = v;
-            else prow_g[row * NW] = v;
-        }
+        if ((lane & 7) == 0 && row < nv) prow_g[row * NW] = v;
     };
     // one band row; RR = r & 3, `more`: a next row exists (its labels are taken one row early);
     // `flush`: the previous group's four row sums are reduced here
@@ -1829,7 +1825,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT1X_MINB : 1)) k_sat1x(
             if constexpr (RR == 3) take(std::integral_constant<int, 0>{}, half ^ 1u, half ? parity ^ 1u : parity);
             else take(std::integral_constant<int, RR + 1>{}, half, parity);
         }
-        if (RR == 0 && flush) flush4(prow - 4 * NW, pxe - 4, 4);
+        if (RR == 0 && flush) flush4(prow - 4 * NW, 4);
         A ts = 0.0;
 #pragma unroll
         for (int k = 0; k < CPT; ++k) ts += rho[k];
@@ -1845,11 +1841,7 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT1X_MINB : 1)) k_sat1x(
         for (int k = 0; k < CPT; ++k) cs[k] += rho[k];
         if (lane == 31) pxd[RR] = pd[CPT - 1];  // diagonal leaving the slice's right edge
         if (lane == 0) pxa[RR] = pa[0];         // anti-diagonal leaving the slice's left edge
-        A ps = 0.0;
-#pragma unroll
-        for (int k = 0; k < CPT; ++k) ps += pd[k];
         tsv[RR] = ts;
-        psv[RR] = ps;
     };
     int r = 0;
     for (; r + 4 <= H; r += 4) {
@@ -1858,18 +1850,29 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT1X_MINB : 1)) k_sat1x(
         row(std::integral_constant<int, 1>{}, true, false);
         row(std::integral_constant<int, 2>{}, true, false);
         row(std::integral_constant<int, 3>{}, more, false);
-        pxd += 4; pxa += 4; pxe += 4; prow += 4 * NW;
+        pxd += 4; pxa += 4; prow += 4 * NW;
         if (half) parity ^= 1u;
         half ^= 1u;
     }
     if (r > 0) {
-        flush4(prow - 4 * NW, pxe - 4, 4);
+        flush4(prow - 4 * NW, 4);
     } else {  // band heights 1 and 2
         row(std::integral_constant<int, 0>{}, H > 1, false);
         if (H > 1) row(std::integral_constant<int, 1>{}, false, false);
-        flush4(prow, pxe, H);
+        flush4(prow, H);
     }
     __syncthreads();  // exits, row partials published; ring and LUT free (dg / ad alias them)
+    {   // E1 of this warp's slice from its row totals and diagonal exits (published by the barriers below)
+        A ct = 0.0, cd = 0.0;
+        for (int r0 = 0; r0 < H; r0 += 32) {
+            const int rr = r0 + lane;
+            const A tv = rr < H ? s_rows[rr * NW + w] : 0.0, dv = rr < H ? exD[w * H + rr] : 0.0;
+            const A st = warp_incl_scan_t<A>(tv), sd = warp_incl_scan_t<A>(dv);
+            if (rr < H) exE[w * H + rr] = (ct + st) - (cd + (sd - dv));
+            ct += __shfl_sync(FULL, st, 31);
+            cd += __shfl_sync(FULL, sd, 31);
+        }
+    }
     // band-bottom entries + the neighbour slice's part of each crossing diagonal
     double csum = 0.0;
 #pragma unroll
