@@ -60,8 +60,9 @@ def phase_bytes(n: int, n_unique: int, n_rows: int, n_regions: int, field: str =
 
 
 def kernels_per_iteration(field: str) -> int:
-    """k_sat1w, k_sat2p, k_sat3, k_region, k_row, k_ctrl, plus the advect as its own kernel:
-    k_advect_uniq64 on the float64 path (one thread per unique vertex; DET_UNIQ_ADVECT=0 fuses it
+    """Band sums, carries, sweep (k_sat1x, k_sat2p, k_sat3x on the float64 path), k_region, k_row, k_ctrl, plus the
+    advect as its own kernel:
+    k_advect_uniq64s on the float64 path (one thread per unique vertex; DET_UNIQ_ADVECT=0 fuses it
     back into k_region), k_advect_rows on the float32 path when DET_SPLIT_ADVECT=1."""
     if field == "float64":
         split = os.environ.get("DET_UNIQ_ADVECT", "1") != "0" or os.environ.get("DET_SPLIT_ADVECT", "0") == "1"
@@ -70,11 +71,13 @@ def kernels_per_iteration(field: str) -> int:
     return 7 if split else 6
 
 
-def timed_launches(steps: int, groups: int, batch: int, per_iter: int = 7) -> int:
+def timed_launches(steps: int, groups: int, batch: int, per_iter: int = 7, per_graph: int = 0) -> int:
     """Our kernel launches in the timed region: per_iter kernels per frame group per iteration;
-    full 16-iteration chunks run as a CUDA graph with min(groups, batch) branches, the remainder
-    eagerly over the whole batch."""
-    return per_iter * (min(groups, batch) * 16 * (steps // 16) + steps % 16)
+    full 16-iteration chunks run as a CUDA graph with min(groups, batch) branches (plus per_graph
+    kernels per branch and graph launch: the float64 path's k_uq_gather / k_uq_expand), the
+    remainder eagerly over the whole batch."""
+    g = min(groups, batch)
+    return per_iter * (g * 16 * (steps // 16) + steps % 16) + per_graph * g * (steps // 16)
 
 
 def load_peaks():
@@ -464,7 +467,8 @@ def main():
                     "d2h_bytes_per_step": d2h / e2e_steps, "steps": e2e_steps,
                     "runs_it_per_s": [e2e_steps * args.batch * world / t for t in e2e_runs],
                     "host_split": getattr(be, "last_timing", {})},
-            "gpu_launches": timed_launches(args.steps, args.groups, args.batch, kernels_per_iteration(args.field)),
+            "gpu_launches": timed_launches(args.steps, args.groups, args.batch, kernels_per_iteration(args.field),
+                                            2 if args.field == "float64" else 0),
             "iterations_executed": iters_total, "frames_active_after": int(act.sum()),
             "clocks": clk.summary(),
             "device": device_info(local),
