@@ -187,6 +187,13 @@ struct det_ctx {
     DVec<double2> upos, ubest;  // unique-vertex state of the graph iterations (see k_uq_gather)
     bool uq_state = true;       // DET_UQ_STATE=0: the graph iterations advect the rows (k_advect_uniq64)
     bool g_uqs = false;
+    DVec<unsigned char> uq_band0, uq_band1;  // band-fused advect: per-vertex band bytes, by iteration parity
+    int uq_bstride = 0;
+    // DET_FUSE_ADVECT=1 (experiment, off): k_sat3x advects a band's vertices after its sweep.  Correct
+    // (bit-identical, tested) but slower: 44.0k vs 61.6k it/s -- with 16 warps per SM the band CTA
+    // serialises the position -> texel round trips that the flat advect hides with 53 warps per SM
+    bool fuse_adv = false;
+    bool g_fa = false;
     std::vector<int> h_uq_off, h_uq_rows, h_uq_row0, h_row_uniq;
     std::vector<double> h_xy_prev;  // the rows the unique-vertex table was built from
     bool g_ua = false;
@@ -236,6 +243,7 @@ static Bufs make_bufs(det_ctx* c) {
     d.nn = (size_t)c->n * c->n;
     d.pos0 = c->pos0.p; d.best = c->best.p;
     d.upos = c->upos.p; d.ubest = c->ubest.p; d.uq_flag = c->uq_flag.p; d.n_uniq = c->n_uniq;
+    d.uq_band[0] = c->uq_band0.p; d.uq_band[1] = c->uq_band1.p; d.uq_bstride = c->uq_bstride;
     d.labels = c->labels.p; d.cnt_acc = c->cnt_acc.p; d.cnt_state = c->cnt_state.p;
     d.spans = c->spans.p; d.rowcnt = c->rowcnt.p; d.maxspan = c->maxspan.p; d.rowdone = c->rowdone.p;
     d.lut = c->lut.p; d.lutf = c->lutf.p; d.stats = c->stats.p; d.weights = c->weights.p; d.rerr = c->rerr.p;
@@ -275,6 +283,13 @@ static bool uqs_on(const det_ctx* c) {
     return c->f64 && c->uniq_adv && c->ua_ok && c->uq_state && !c->bitmap_raster && !(skip_mask() & 4);
 }
 
+// band-fused advect: the unique-vertex state, k_sat3x with one CTA per band row (n = 512 or 1024),
+// band ids in a byte
+static bool fa_on(const det_ctx* c) {
+    return uqs_on(c) && c->fuse_adv && c->sat1w && c->sat3w && c->sat3x && (c->n == 512 || c->n == 1024) &&
+           c->H < 128 && c->nb < 254 && !(skip_mask() & 2);
+}
+
 // Diagnostics only (timing experiments, results invalid): DET_SKIP bit mask of iteration stages
 // left out of the captured graph -- 1 band sums + carries (k_sat1w, k_sat2p), 2 k_sat3,
 // 4 advect + raster (k_region), 8 paint + control step (k_row, k_ctrl).
@@ -285,7 +300,7 @@ static int skip_mask() {
 
 template <int CPT, int NT>
 static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S, int gate, int src, int out,
-                           bool u64, int B) {
+                           bool u64, int B, int fa = -1) {
     const int n = c->n, H = c->H, R = c->R;
     const dim3 gb(c->nb, B);
     // float32 in-band arithmetic only for the float32 field from labels; float64 otherwise
@@ -389,9 +404,15 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
             if (c->sat3x) {  // loop-invariant edge records + 4x unrolled rows (DET_SAT3X=0: k_sat3w)
                 const size_t smemx = ((size_t)3 * 4 * sat3x_phase_len(NWC) + (size_t)NWC * H * 6) * sizeof(double) +
                                      lut_b + (size_t)NWC * 4 * W * sizeof(int) + 16;
+                if (fa >= 0 && n == NWC * W) {  // band-fused advect (one CTA per band row)
+                    auto fa_k = luts ? k_sat3x<NTW, true, true> : k_sat3x<NTW, false, true>;
+                    smem_optin(fa_k);
+                    fa_k<<<dim3(c->nb, B, 1), NTW, smemx, c->stream>>>(T, D, gate, fa, c->uq_off.p);
+                    return;
+                }
                 auto fx = luts ? k_sat3x<NTW, true> : k_sat3x<NTW, false>;
                 smem_optin(fx);
-                fx<<<dim3(c->nb, B, n / (NWC * W)), NTW, smemx, c->stream>>>(T, D, gate);
+                fx<<<dim3(c->nb, B, n / (NWC * W)), NTW, smemx, c->stream>>>(T, D, gate, -1, nullptr);
                 return;
             }
         }
@@ -429,16 +450,16 @@ static void launch_sat_cfg(det_ctx* c, const Topo& T, const Bufs& D, const SatSr
 
 // band kernels: one CTA per band row-set; CPT columns per thread, NT = n/CPT threads (>= 32)
 static void launch_sat(det_ctx* c, const Topo& T, const Bufs& D, const SatSrc& S, int gate, int src, int out, bool u64,
-                       int B) {
+                       int B, int fa = -1) {
     switch (c->n) {
-        case 16: case 32: case 64: launch_sat_cfg<2, 32>(c, T, D, S, gate, src, out, u64, B); break;
-        case 128: launch_sat_cfg<2, 64>(c, T, D, S, gate, src, out, u64, B); break;
-        case 256: launch_sat_cfg<2, 128>(c, T, D, S, gate, src, out, u64, B); break;
-        case 512: launch_sat_cfg<4, 128>(c, T, D, S, gate, src, out, u64, B); break;
-        case 1024: launch_sat_cfg<4, 256>(c, T, D, S, gate, src, out, u64, B); break;
-        case 2048: launch_sat_cfg<4, 512>(c, T, D, S, gate, src, out, u64, B); break;
-        case 4096: launch_sat_cfg<4, 1024>(c, T, D, S, gate, src, out, u64, B); break;
-        default: launch_sat_cfg<8, 1024>(c, T, D, S, gate, src, out, u64, B); break;
+        case 16: case 32: case 64: launch_sat_cfg<2, 32>(c, T, D, S, gate, src, out, u64, B, fa); break;
+        case 128: launch_sat_cfg<2, 64>(c, T, D, S, gate, src, out, u64, B, fa); break;
+        case 256: launch_sat_cfg<2, 128>(c, T, D, S, gate, src, out, u64, B, fa); break;
+        case 512: launch_sat_cfg<4, 128>(c, T, D, S, gate, src, out, u64, B, fa); break;
+        case 1024: launch_sat_cfg<4, 256>(c, T, D, S, gate, src, out, u64, B, fa); break;
+        case 2048: launch_sat_cfg<4, 512>(c, T, D, S, gate, src, out, u64, B, fa); break;
+        case 4096: launch_sat_cfg<4, 1024>(c, T, D, S, gate, src, out, u64, B, fa); break;
+        default: launch_sat_cfg<8, 1024>(c, T, D, S, gate, src, out, u64, B, fa); break;
     }
 }
 
@@ -465,8 +486,13 @@ static void launch_region(det_ctx* c, const Topo& T, const Bufs& D, int mode, in
 
 // One iteration's advect + raster: the flat advect kernel then a raster-only k_region (float32
 // state), or k_region's fused advect phase.  Returns the number of kernels launched.
-static int launch_advect_raster(det_ctx* c, const Topo& T, const Bufs& D, int gate, int region_mode, bool uqs = false) {
+static int launch_advect_raster(det_ctx* c, const Topo& T, const Bufs& D, int gate, int region_mode, bool uqs = false,
+                                int fa = -1) {
     if (uqs) {  // unique-vertex state (inside a graph launch): coalesced advect, raster through row_uniq
+        if (fa >= 0)  // band-fused advect: k_sat3x advected the in-band vertices; the band-straddling ones here
+            k_advect_bnd<<<dim3((c->n_uniq + ADV_THREADS - 1) / ADV_THREADS, c->B), ADV_THREADS, 0, c->stream>>>(
+                T, D, gate, c->uq_off.p, fa);
+        else
         k_advect_uniq64s<<<dim3((c->n_uniq + ADV_THREADS - 1) / ADV_THREADS, c->B), ADV_THREADS, 0, c->stream>>>(
             T, D, gate, c->uq_off.p);
         const dim3 g((c->R + RW_WARPS - 1) / RW_WARPS, c->B);
@@ -525,11 +551,12 @@ static void enqueue_iteration(det_ctx* c, int b0 = 0, int Bg = -1, cudaStream_t 
     c->B = Bg;  // grid.y of every launch below
     SatSrc S;
     memset(&S, 0, sizeof(S));
-    if ((skip_mask() & 3) != 3) launch_sat(c, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, c->f64 != 0, Bg);
-    if (after_sat) cudaEventRecord(after_sat, c->stream);  // (capture) the staggered neighbour branch starts here
-    if (uqs & 1)  // first iteration of a graph launch: rows -> unique-vertex state
+    const int fa = (uqs & 8) ? ((uqs & 16) ? 1 : 0) : -1;  // band-fused advect: iteration parity
+    if (uqs & 1)  // first iteration of a graph launch: rows -> unique-vertex state (+ band bytes)
         k_uq_gather<<<dim3(std::min((c->n_uniq + 255) / 256, 1024), Bg), 256, 0, c->stream>>>(T, D, G_ACTIVE, c->uq_row0.p);
-    if (!(skip_mask() & 4)) launch_advect_raster(c, T, D, G_ACTIVE, M_ADVECT | M_RASTER, uqs != 0);
+    if ((skip_mask() & 3) != 3) launch_sat(c, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, c->f64 != 0, Bg, fa);
+    if (after_sat) cudaEventRecord(after_sat, c->stream);  // (capture) the staggered neighbour branch starts here
+    if (!(skip_mask() & 4)) launch_advect_raster(c, T, D, G_ACTIVE, M_ADVECT | M_RASTER, uqs != 0, fa);
     if (!(skip_mask() & 8)) launch_row_ctrl(c, T, D, G_ACTIVE, 0);
     if (uqs & 4)  // last iteration of a graph launch: unique-vertex state -> rows (+ best rows)
         k_uq_expand<<<dim3(std::min((c->n_rows + 255) / 256, 1024), Bg), 256, 0, c->stream>>>(T, D);
@@ -551,7 +578,7 @@ static int ensure_graph(det_ctx* c) {
         // re-capture only when a pointer, shape or the grouping the graph bakes in changed
         const Topo t = make_topo(c);
         const Bufs d = make_bufs(c);
-        if (c->g_valid && c->g_groups == c->groups && c->g_ua == (c->uniq_adv && c->ua_ok) && c->g_uqs == uqs_on(c) &&
+        if (c->g_valid && c->g_groups == c->groups && c->g_ua == (c->uniq_adv && c->ua_ok) && c->g_uqs == uqs_on(c) && c->g_fa == fa_on(c) &&
             c->g_nuniq == c->n_uniq && c->g_uq == c->uq_rows.p && c->g_uq0 == c->uq_row0.p &&
             !memcmp(&t, &c->g_topo, sizeof(t)) &&
             !memcmp(&d, &c->g_bufs, sizeof(d)))
@@ -561,6 +588,7 @@ static int ensure_graph(det_ctx* c) {
         c->g_groups = c->groups;
         c->g_ua = c->uniq_adv && c->ua_ok;
         c->g_uqs = uqs_on(c);
+        c->g_fa = fa_on(c);
         c->g_nuniq = c->n_uniq;
         c->g_uq = c->uq_rows.p;
         c->g_uq0 = c->uq_row0.p;
@@ -594,7 +622,8 @@ static int ensure_graph(det_ctx* c) {
         const bool lead = stagger && (g % 2 == 0) && g + 1 < G;
         if (stagger && (g % 2 == 1)) CK(cudaStreamWaitEvent(s, stag[g - 1], 0));
         for (int i = 0; i < kGraphIters; ++i)
-            enqueue_iteration(c, b0, b1 - b0, s, uqs ? (2 | (i == 0 ? 1 : 0) | (i == kGraphIters - 1 ? 4 : 0)) : 0,
+            enqueue_iteration(c, b0, b1 - b0, s,
+                              uqs ? (2 | (i == 0 ? 1 : 0) | (i == kGraphIters - 1 ? 4 : 0) | (fa_on(c) ? 8 : 0) | ((i & 1) ? 16 : 0)) : 0,
                               (lead && i == 0) ? stag[g] : nullptr);
         CK(cudaEventRecord(join[g], s));
         CK(cudaStreamWaitEvent(c->stream, join[g], 0));
@@ -657,6 +686,11 @@ static int alloc_batch(det_ctx* ctx, int B) {
         CK(ctx->upos.alloc((size_t)B * ctx->n_uniq));
         CK(ctx->ubest.alloc((size_t)B * ctx->n_uniq));
         CK(ctx->uq_flag.alloc(B));
+        ctx->uq_bstride = (ctx->n_uniq + 15) & ~15;
+        CK(ctx->uq_band0.alloc((size_t)B * ctx->uq_bstride));
+        CK(ctx->uq_band1.alloc((size_t)B * ctx->uq_bstride));
+        CK(cudaMemsetAsync(ctx->uq_band0.p, 254, (size_t)B * ctx->uq_bstride, ctx->stream));  // pad bytes: no band
+        CK(cudaMemsetAsync(ctx->uq_band1.p, 254, (size_t)B * ctx->uq_bstride, ctx->stream));
         CK(cudaMemsetAsync(ctx->uq_flag.p, 0, (size_t)B * sizeof(int), ctx->stream));
     }
     if (!ctx->s64) CK(ctx->rows64.alloc((size_t)B * ctx->n_rows));
@@ -808,6 +842,7 @@ int det_ctx_create(int device, int k, int precision, det_ctx** out) {
     if (const char* e = getenv("DET_SAT3W")) ctx->sat3w = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SAT3X")) ctx->sat3x = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_UQ_STATE")) ctx->uq_state = atoi(e) != 0;  // A/B switch (diagnostics)
+    if (const char* e = getenv("DET_FUSE_ADVECT")) ctx->fuse_adv = atoi(e) != 0;  // A/B switch (diagnostics)
     if (const char* e = getenv("DET_SAT1X")) ctx->sat1x = atoi(e) != 0;  // A/B switch (diagnostics)
     ctx->device = device;
     ctx->k = k;
@@ -1274,9 +1309,10 @@ int det_bench_kernel_times(det_ctx* ctx, int iters, float* ms_out) {
         k_uq_gather<<<dim3(std::min((ctx->n_uniq + 255) / 256, 1024), ctx->B), 256, 0, ctx->stream>>>(T, D, G_ACTIVE, ctx->uq_row0.p);
     for (int it = 0; it < iters; ++it) {
         CK(cudaEventRecord(ev[0], ctx->stream));
-        launch_sat(ctx, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, ctx->f64 != 0, ctx->B);
+        const int fa = (uqs && fa_on(ctx)) ? (it & 1) : -1;  // (an even iteration count leaves buffer 0 current)
+        launch_sat(ctx, T, D, S, G_ACTIVE, SRC_LABELS, OUT_U, ctx->f64 != 0, ctx->B, fa);
         CK(cudaEventRecord(ev[1], ctx->stream));
-        launch_advect_raster(ctx, T, D, G_ACTIVE, region_mode, uqs);
+        launch_advect_raster(ctx, T, D, G_ACTIVE, region_mode, uqs, fa);
         CK(cudaEventRecord(ev[2], ctx->stream));
         launch_row_ctrl(ctx, T, D, G_ACTIVE, row_mode);  // includes the control step
         CK(cudaEventRecord(ev[3], ctx->stream));

@@ -76,6 +76,11 @@ struct Bufs {
     double2* ubest;
     int* uq_flag;
     int n_uniq;
+    // band-fused advect: per unique vertex the band (of H rows) holding both rows of its bilinear tap,
+    // 255 when the tap straddles two bands; double-buffered by iteration parity (read [par], write [par^1]);
+    // uq_bstride = per-cartogram stride (n_uniq rounded up to 16, pad bytes 254)
+    unsigned char* uq_band[2];
+    int uq_bstride;
     int* labels;
     int* cnt_acc;
     int* cnt_state;

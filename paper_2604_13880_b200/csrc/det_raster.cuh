@@ -130,6 +130,31 @@ __device__ __forceinline__ Texels<UT> field_load(const UT* __restrict__ uf, cons
     return x;
 }
 
+// the four texels with plain (coherent) loads: for a field written earlier by this same kernel
+// (band-fused advect), where the read-only path of field_load must not be used
+__device__ __forceinline__ Texels<double> field_load_coherent(const double* uf, const Tap& t) {
+    const double2* u2 = reinterpret_cast<const double2*>(uf);
+    const double2 a = u2[t.o0 >> 1], b = u2[(t.o0 >> 1) + 1];
+    const double2 c = u2[t.o1 >> 1], d = u2[(t.o1 >> 1) + 1];
+    Texels<double> x;
+    x.v[0] = a.x; x.v[1] = a.y; x.v[2] = b.x; x.v[3] = b.y;
+    x.v[4] = c.x; x.v[5] = c.y; x.v[6] = d.x; x.v[7] = d.y;
+    return x;
+}
+
+// Band of H rows (H = 1 << lgH) holding BOTH rows iy, iy + 1 of the bilinear tap of a vertex at
+// height py (field_tap's row: iy = clip(floor(py*n - 0.5), 0, n-2)); 255 when iy is a band's last
+// row, so that the tap straddles two bands.
+__device__ __forceinline__ unsigned char tap_band(int n, int lgH, double py) {
+    const double gy = py * (double)n - 0.5;
+    const double hi = (double)(n - 2);
+    double by = floor_exact(gy);
+    by = by < 0.0 ? 0.0 : (by > hi ? hi : by);
+    const int iy = floor_to_int(by);
+    const int H = 1 << lgH;
+    return (unsigned char)(((iy & (H - 1)) == H - 1) ? 255 : (iy >> lgH));
+}
+
 template <typename UT, typename TP>
 __device__ __forceinline__ double2 field_blend(const Texels<UT>& x, const TP& t) {
     const UT fx = (UT)t.fx, fy = (UT)t.fy;
@@ -889,8 +914,13 @@ __global__ void __launch_bounds__(256) k_uq_gather(Topo T, Bufs D, int gate, con
     if (!open) return;
     const double2* pin = reinterpret_cast<const double2*>(D.pos0) + (size_t)b * T.n_rows;
     double2* up = D.upos + (size_t)b * D.n_uniq;
-    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < D.n_uniq; u += gridDim.x * blockDim.x)
-        up[u] = pin[uq_row0[u]];
+    unsigned char* band0 = D.uq_band[0] ? D.uq_band[0] + (size_t)b * D.uq_bstride : nullptr;
+    const int lgH = __ffs(D.H) - 1;
+    for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < D.n_uniq; u += gridDim.x * blockDim.x) {
+        const double2 p = pin[uq_row0[u]];
+        up[u] = p;
+        if (band0) band0[u] = tap_band(D.n, lgH, p.y);  // band-fused advect: the first iteration reads buffer 0
+    }
 }
 
 __global__ void __launch_bounds__(256) k_uq_expand(Topo T, Bufs D) {
@@ -906,6 +936,98 @@ __global__ void __launch_bounds__(256) k_uq_expand(Topo T, Bufs D) {
         const int u = __ldg(T.row_uniq + v);
         pin[v] = up[u];
         if (wb) pbest[v] = ub[u];
+    }
+}
+
+// One unique vertex advected in place on the unique-vertex state (the arithmetic of
+// k_advect_uniq64s); COH: the field was written by this kernel (coherent loads).  Writes the
+// vertex's band byte for the next iteration when bnext is given.  Returns its clamp count.
+template <bool COH>
+__device__ __forceinline__ int advect_uq_vertex(const Bufs& D, int n, int lgH, const double* uf, double2* up, double2* ub,
+                                                bool bestcopy, const int* __restrict__ uq_off, unsigned char* bnext, int u) {
+    const double2 p = up[u];
+    const Tap tp = field_tap(n, p.x, p.y);
+    const Texels<double> tx = COH ? field_load_coherent(uf, tp) : field_load<double, Tap>(uf, tp);
+    const double2 sm = field_blend<double, Tap>(tx, tp);
+    const double mx = p.x + sm.x, my = p.y + sm.y;
+    const double cx = mx < 0.0 ? 0.0 : (mx > 1.0 ? 1.0 : mx);  // np.clip (no NaNs here)
+    const double cy = my < 0.0 ? 0.0 : (my > 1.0 ? 1.0 : my);
+    up[u] = make_double2(cx, cy);
+    if (bestcopy) ub[u] = p;
+    if (bnext) bnext[u] = tap_band(n, lgH, cy);
+    const int nc = (cx != mx) + (cy != my);
+    return nc ? nc * (uq_off[u + 1] - uq_off[u]) : 0;  // counted once per row (displacement.py:229-238)
+}
+
+// Band-fused advect, second part: the vertices whose tap straddles two bands (band byte 255), after
+// k_sat3x<.., FA> advected all others from inside their band's sweep.
+__global__ void __launch_bounds__(ADV_THREADS) k_advect_bnd(Topo T, Bufs D, int gate, const int* __restrict__ uq_off, int par) {
+    const int b = blockIdx.y + D.b0;
+    Carto* st = D.st + b;
+    if (!gate_open(st, gate)) return;
+    const int n = D.n, n_uniq = D.n_uniq;
+    const bool bestcopy = st->best_pending != 0;
+    const int u = blockIdx.x * ADV_THREADS + threadIdx.x;
+    const unsigned char* bcur = D.uq_band[par] + (size_t)b * D.uq_bstride;
+    int ncl = 0;
+    if (u < n_uniq && bcur[u] == 255)
+        ncl = advect_uq_vertex<false>(D, n, __ffs(D.H) - 1, reinterpret_cast<const double*>(D.uf) + (size_t)b * D.nn * 2,
+                                      D.upos + (size_t)b * n_uniq, D.ubest + (size_t)b * n_uniq, bestcopy, uq_off,
+                                      D.uq_band[par ^ 1] + (size_t)b * D.uq_bstride, u);
+    if (bestcopy && blockIdx.x == 0 && threadIdx.x == 0) D.uq_flag[b] = 3;
+    if (__any_sync(FULL, ncl != 0)) {
+        ncl = warp_sum(ncl);
+        if ((threadIdx.x & 31) == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
+    }
+}
+
+// Band-fused advect, first part (called by every warp of a k_sat3x<.., FA> CTA after the CTA's
+// barrier at the end of its band sweep): scan the cartogram's band bytes for this band, compact the
+// matching vertices into the warp's queue (512 ints of shared memory) and advect them 32 at a time
+// while the band's field rows are still in L2 / L1.
+__device__ __forceinline__ void advect_band_vertices(const Bufs& D, int b, int band, int par, int wl, int nwarps, int lane,
+                                                     int* queue, const int* __restrict__ uq_off) {
+    Carto* st = D.st + b;
+    const int n = D.n, nU = D.n_uniq, lgH = __ffs(D.H) - 1;
+    const bool bestcopy = st->best_pending != 0;
+    const double* uf = reinterpret_cast<const double*>(D.uf) + (size_t)b * D.nn * 2;
+    double2* up = D.upos + (size_t)b * nU;
+    double2* ub = D.ubest + (size_t)b * nU;
+    const unsigned char* bcur = D.uq_band[par] + (size_t)b * D.uq_bstride;
+    unsigned char* bnext = D.uq_band[par ^ 1] + (size_t)b * D.uq_bstride;
+    const unsigned pat = (unsigned)band * 0x01010101u;
+    int qh = 0, qt = 0, ncl = 0;
+    for (int base = wl * 256; base < nU; base += nwarps * 256) {
+        const int u0 = base + lane * 8;
+        uint2 w = make_uint2(0xFEFEFEFEu, 0xFEFEFEFEu);  // 254: no band
+        if (u0 < D.uq_bstride) w = *reinterpret_cast<const uint2*>(bcur + u0);  // (pad bytes are 254)
+        unsigned mlo = __vcmpeq4(w.x, pat), mhi = __vcmpeq4(w.y, pat);  // 0xFF per matching byte
+        const int c = (__popc(mlo) + __popc(mhi)) >> 3;
+        int tot;
+        int pos = qt + warp_excl_scan_int(c, lane, &tot);
+        while (mlo) {
+            const int j = (__ffs(mlo) - 1) >> 3;
+            mlo &= ~(0xFFu << (8 * j));
+            queue[pos++ & 511] = u0 + j;
+        }
+        while (mhi) {
+            const int j = (__ffs(mhi) - 1) >> 3;
+            mhi &= ~(0xFFu << (8 * j));
+            queue[pos++ & 511] = u0 + 4 + j;
+        }
+        qt += tot;
+        __syncwarp();
+        while (qt - qh >= 32) {
+            ncl += advect_uq_vertex<true>(D, n, lgH, uf, up, ub, bestcopy, uq_off, bnext, queue[(qh + lane) & 511]);
+            qh += 32;
+        }
+        __syncwarp();
+    }
+    if (lane < qt - qh)
+        ncl += advect_uq_vertex<true>(D, n, lgH, uf, up, ub, bestcopy, uq_off, bnext, queue[(qh + lane) & 511]);
+    if (__any_sync(FULL, ncl != 0)) {
+        ncl = warp_sum(ncl);
+        if (lane == 0 && ncl) atomicAdd(&st->clamps, (unsigned long long)ncl);
     }
 }
 

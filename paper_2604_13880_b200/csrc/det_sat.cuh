@@ -1404,8 +1404,12 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3w
 #ifndef DET_SAT3X_PIPE
 #define DET_SAT3X_PIPE 0  // 2: the next row's row-prefix scan issued ahead of this row's field arithmetic, densities re-read (54.3k vs 55.4k it/s); 1: the next row's labels, LUT reads and row-prefix scan issued ahead of this row's field arithmetic (spills at 128 registers: 49.6k vs 51.6k it/s)
 #endif
-template <int NT, bool LUTS>
-__global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x(Topo T, Bufs D, int gate) {
+// FA (band-fused advect, fa_par = iteration parity >= 0): after the sweep the CTA advects the unique
+// vertices whose bilinear tap lies inside this band (advect_band_vertices, det_raster.cuh) while the
+// band's field rows are still on chip; the CTA must span the whole band row (gridDim.z == 1).
+template <int NT, bool LUTS, bool FA = false>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x(Topo T, Bufs D, int gate, int fa_par = -1,
+                                                                                 const int* __restrict__ uq_off = nullptr) {
     using A = double;
     using A2 = double2;
     constexpr int CPT = 4, NWC = NT / 32, W = 32 * CPT, KP = 4;
@@ -1693,6 +1697,12 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? DET_SAT3_MINB64 : 1)) k_sat3x
         row(std::integral_constant<int, 0>{});
         if (r + 1 < H) row(std::integral_constant<int, 1>{});
         if (r + 2 < H) row(std::integral_constant<int, 2>{});
+    }
+    if constexpr (FA) {
+        if (fa_par >= 0) {
+            __syncthreads();  // every warp's rows of the band are written; windows and records are dead
+            advect_band_vertices(D, b, band, fa_par, wl, NWC, lane, reinterpret_cast<int*>(s_raw3x) + wl * 512, uq_off);
+        }
     }
 }
 

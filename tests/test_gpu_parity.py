@@ -508,3 +508,23 @@ def test_float64_band_height_independence(P):
         outs.append(be.run_all(crit)[0].state.mapmodel.vertex_array())
         ctx.set_band_height(0)
     assert max(np.abs(o - outs[0]).max() for o in outs) <= 1e-10
+
+
+@pytest.mark.parametrize("k", [9, 10])
+@pytest.mark.parametrize("env", [{"DET_FUSE_ADVECT": "1"}, {"DET_UQ_STATE": "0"}])
+def test_float64_vertex_state_variants_bit_identical(P, tmp_path, env, k):
+    """The three float64 advect forms -- per-row state with k_advect_uniq64, the unique-vertex state
+    with k_advect_uniq64s (the default), and the experimental band-fused advect inside k_sat3x (+ k_advect_bnd) -- evaluate the
+    same expressions on the same field: bit-identical vertices and counts after 30 iterations."""
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for i, e in enumerate([{}, env]):
+        out = str(tmp_path / f"u{i}.npy")
+        code = _VARIANT64_SCRIPT.format(root=root, out=out, k=k)
+        r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, **e), capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
