@@ -243,7 +243,8 @@ static Bufs make_bufs(det_ctx* c) {
     d.nn = (size_t)c->n * c->n;
     d.pos0 = c->pos0.p; d.best = c->best.p;
     d.upos = c->upos.p; d.ubest = c->ubest.p; d.uq_flag = c->uq_flag.p; d.n_uniq = c->n_uniq;
-    d.uq_band[0] = c->uq_band0.p; d.uq_band[1] = c->uq_band1.p; d.uq_bstride = c->uq_bstride;
+    if (c->fuse_adv) { d.uq_band[0] = c->uq_band0.p; d.uq_band[1] = c->uq_band1.p; }  // (null: k_uq_gather skips the band bytes)
+    d.uq_bstride = c->uq_bstride;
     d.labels = c->labels.p; d.cnt_acc = c->cnt_acc.p; d.cnt_state = c->cnt_state.p;
     d.spans = c->spans.p; d.rowcnt = c->rowcnt.p; d.maxspan = c->maxspan.p; d.rowdone = c->rowdone.p;
     d.lut = c->lut.p; d.lutf = c->lutf.p; d.stats = c->stats.p; d.weights = c->weights.p; d.rerr = c->rerr.p;
@@ -687,10 +688,12 @@ static int alloc_batch(det_ctx* ctx, int B) {
         CK(ctx->ubest.alloc((size_t)B * ctx->n_uniq));
         CK(ctx->uq_flag.alloc(B));
         ctx->uq_bstride = (ctx->n_uniq + 15) & ~15;
+        if (ctx->fuse_adv) {
         CK(ctx->uq_band0.alloc((size_t)B * ctx->uq_bstride));
         CK(ctx->uq_band1.alloc((size_t)B * ctx->uq_bstride));
         CK(cudaMemsetAsync(ctx->uq_band0.p, 254, (size_t)B * ctx->uq_bstride, ctx->stream));  // pad bytes: no band
         CK(cudaMemsetAsync(ctx->uq_band1.p, 254, (size_t)B * ctx->uq_bstride, ctx->stream));
+        }
         CK(cudaMemsetAsync(ctx->uq_flag.p, 0, (size_t)B * sizeof(int), ctx->stream));
     }
     if (!ctx->s64) CK(ctx->rows64.alloc((size_t)B * ctx->n_rows));
