@@ -752,7 +752,10 @@ __global__ void __launch_bounds__(RW_WARPS * 32, ADV ? (sizeof(ST) == 8 ? DET_RW
 // Advect as its own flat kernel (float32 state): ADV_RPT rows per thread over the whole row range
 // of each cartogram (grid.y), every lane busy and ~64 warps per SM to cover the position -> texel
 // load chain; the same float arithmetic as k_region's phase A (displacement.py:209-238).
-constexpr int ADV_THREADS = 256;
+#ifndef DET_ADV_THREADS
+#define DET_ADV_THREADS 256
+#endif
+constexpr int ADV_THREADS = DET_ADV_THREADS;
 constexpr int ADV_RPT = 2;
 __global__ void __launch_bounds__(ADV_THREADS) k_advect_rows(Topo T, Bufs D, int gate) {
     const int b = blockIdx.y + D.b0;
