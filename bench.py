@@ -77,7 +77,8 @@ def timed_launches(steps: int, groups: int, batch: int, per_iter: int = 7, per_g
     kernels per branch and graph launch: the float64 path's k_uq_gather / k_uq_expand), the
     remainder eagerly over the whole batch."""
     g = min(groups, batch)
-    return per_iter * (g * 16 * (steps // 16) + steps % 16) + per_graph * g * (steps // 16)
+    return (per_iter * (g * 16 * (steps // 16) + steps % 16) + per_graph * g * (steps // 16)
+            + (per_graph if steps % 16 else 0))  # the eager remainder gathers / expands once over the whole batch
 
 
 def load_peaks():

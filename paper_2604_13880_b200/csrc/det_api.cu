@@ -1280,7 +1280,11 @@ int det_bench_iterations(det_ctx* ctx, int iters) {
     }
     int done = 0;
     for (; done + kGraphIters <= iters; done += kGraphIters) CK(cudaGraphLaunch(ctx->gexec, ctx->stream));
-    for (; done < iters; ++done) enqueue_iteration(ctx);
+    // the remainder runs eagerly over the whole batch, on the unique-vertex state like the graph
+    // (gathered in its first iteration, expanded in its last)
+    const int rem = iters - done;
+    for (int i = 0; i < rem; ++i)
+        enqueue_iteration(ctx, 0, -1, nullptr, uqs_on(ctx) ? (2 | (i == 0 ? 1 : 0) | (i == rem - 1 ? 4 : 0)) : 0);
     CK(cudaGetLastError());
     return DET_OK;
 }

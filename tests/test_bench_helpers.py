@@ -45,6 +45,7 @@ def test_timed_launch_count(bench):
     assert bench.timed_launches(64, 8, 4, 6) == 6 * 4 * 64   # branches clamp to the batch
     assert bench.timed_launches(20, 8, 16, 7) == 7 * (8 * 16 + 4)  # 16 in the graph + 4 eager
     assert bench.timed_launches(64, 8, 296, 7, 2) == 7 * 8 * 64 + 2 * 8 * 4  # + gather / expand per branch and graph launch
+    assert bench.timed_launches(20, 8, 296, 7, 2) == 7 * (8 * 16 + 4) + 2 * 8 + 2  # + one gather / expand around the eager remainder
     assert bench.kernels_per_iteration("float64") == 7  # + k_advect_uniq64
     assert bench.kernels_per_iteration("mixed") == 6
     assert bench.kernels_per_iteration("float32") == 6  # advect fused into k_region by default
