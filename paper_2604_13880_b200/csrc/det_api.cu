@@ -665,11 +665,14 @@ static int alloc_sat(det_ctx* ctx, int B) {
     return DET_OK;
 }
 
+#ifndef DET_BAND_FILL
+#define DET_BAND_FILL 148  // band CTAs wanted per launch before bands grow taller (2 * 148: B=4 31.3k vs 34.5k, B=8 43.5k vs 44.6k it/s)
+#endif
 static int auto_band_height(int n, int B) {
-    // enough band CTAs to fill the 148 SMs twice over, but tall bands amortise the carries
-    // and the per-CTA LUT copy (H = 32 at 1024^2 x 16 frames; 16 and 64 measured slower)
+    // one band CTA per SM before bands grow taller: tall bands amortise the carries and the
+    // per-CTA LUT copy (1024^2: H = 8 for 1-2 frames, 16 for 4, 32 for 8, 64 from 16 frames on)
     int h = 8;
-    while (h < 64 && (long long)(n / (2 * h)) * B >= 2 * 148) h *= 2;
+    while (h < 64 && (long long)(n / (2 * h)) * B >= DET_BAND_FILL) h *= 2;
     return std::min(h, n);
 }
 
