@@ -770,7 +770,15 @@ __global__ void __launch_bounds__(32 * SAT2_PARTS) k_sat2p(Bufs D, int gate) {
         v0[k] = (ok && p0 + k < p1) ? val(p0 + k) : 0.0;
         loc += v0[k];
     }
-    for (int c0 = p0 + SAT2P_CH; c0 < p1; ++c0) loc += ok ? val(c0) : 0.0;
+    // (more bands per part than the register chunk -- short bands, few frames: later chunks are loaded
+    // SAT2P_CH at a time, so their round trips overlap instead of running one band after another)
+    for (int c0 = p0 + SAT2P_CH; c0 < p1; c0 += SAT2P_CH) {
+        double v[SAT2P_CH];
+#pragma unroll
+        for (int k = 0; k < SAT2P_CH; ++k) v[k] = (ok && c0 + k < p1) ? val(c0 + k) : 0.0;
+#pragma unroll
+        for (int k = 0; k < SAT2P_CH; ++k) loc += v[k];
+    }
     s_part[part][lane] = loc;
     __syncthreads();
     if (!ok) return;
@@ -792,10 +800,17 @@ __global__ void __launch_bounds__(32 * SAT2_PARTS) k_sat2p(Bufs D, int gate) {
                 run += v0[k];
             }
         }
-        for (int band = p0 + SAT2P_CH; band < p1; ++band) {
-            const double v = val(band);
-            put(band);
-            run += v;
+        for (int c0 = p0 + SAT2P_CH; c0 < p1; c0 += SAT2P_CH) {
+            double v[SAT2P_CH];
+#pragma unroll
+            for (int k = 0; k < SAT2P_CH; ++k) v[k] = c0 + k < p1 ? val(c0 + k) : 0.0;
+#pragma unroll
+            for (int k = 0; k < SAT2P_CH; ++k) {
+                if (c0 + k < p1) {
+                    put(c0 + k);
+                    run += v[k];
+                }
+            }
         }
         if (part == SAT2_PARTS - 1) {
             if (type == 0) D.csT[(size_t)b * n + idx] = run;
@@ -807,9 +822,17 @@ __global__ void __launch_bounds__(32 * SAT2_PARTS) k_sat2p(Bufs D, int gate) {
             const int q = idx - band * H + 1;  // w - (jt - 1)
             if (q >= 0 && q < L + 1) D.adSc[(base + band) * (L + 1) + q] = run;
         };
-        for (int band = p1 - 1; band >= p0 + SAT2P_CH; --band) {
-            run += val(band);
-            put(band);
+        for (int c1 = p1; c1 > p0 + SAT2P_CH; c1 -= SAT2P_CH) {  // bands c1-1 down to max(c1 - CH, p0 + CH)
+            double v[SAT2P_CH];
+#pragma unroll
+            for (int k = 0; k < SAT2P_CH; ++k) v[k] = c1 - 1 - k >= p0 + SAT2P_CH ? val(c1 - 1 - k) : 0.0;
+#pragma unroll
+            for (int k = 0; k < SAT2P_CH; ++k) {
+                if (c1 - 1 - k >= p0 + SAT2P_CH) {
+                    run += v[k];
+                    put(c1 - 1 - k);
+                }
+            }
         }
 #pragma unroll
         for (int k = SAT2P_CH - 1; k >= 0; --k) {
